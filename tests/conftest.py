@@ -1,0 +1,39 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a) device")
+
+
+@pytest.fixture
+def rng():
+    return np.random.default_rng(1234)
+
+
+def load_golden(name):
+    return np.load(os.path.join(GOLDEN, name), allow_pickle=False)
+
+
+def csr_csc(users, items, vals, n_users, n_items):
+    """Reference RatingMatrix index layout (ratings.py:74-92) in numpy."""
+    users = np.asarray(users, np.int64)
+    items = np.asarray(items, np.int64)
+    vals = np.asarray(vals, np.float64)
+    o = np.lexsort((items, users))
+    row_ptr = np.zeros(n_users + 1, np.int64)
+    np.cumsum(np.bincount(users, minlength=n_users), out=row_ptr[1:])
+    o2 = np.lexsort((users, items))
+    col_ptr = np.zeros(n_items + 1, np.int64)
+    np.cumsum(np.bincount(items, minlength=n_items), out=col_ptr[1:])
+    return ((row_ptr, items[o].astype(np.int32), vals[o]),
+            (col_ptr, users[o2].astype(np.int32), vals[o2]))

@@ -1,0 +1,190 @@
+"""Generate golden fixtures by running the REAL reference package.
+
+Run in the build container only (the reference is not on the GPU box):
+
+    cd /tmp && NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONDONTWRITEBYTECODE=1 \
+        python /root/repo/tests/golden/make_golden.py
+
+The reference is imported read-only from /root/reference/pkg/src; numba's
+cache is redirected to /tmp so nothing is written into the reference tree.
+Outputs (committed): tests/golden/*.npz.  All inputs are fp32-representable
+(float32 arrays upcast to float64) so the same fixtures serve the fp32 GPU
+path: the reference sees exactly the values the GPU sees.
+"""
+
+import os
+import sys
+import warnings
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+sys.dont_write_bytecode = True
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import numpy as np  # noqa: E402
+
+import coreals  # noqa: E402
+from coreals import RatingMatrix, SolverConfig, ces_sketch, fit_core, update_user_core  # noqa: E402
+from coreals.core import sketch_budget  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def f32(a):
+    return np.asarray(a, dtype=np.float32).astype(np.float64)
+
+
+def sketch_cases():
+    """ces_sketch on adversarial columns: Gaussian, 0.1-rounded ties, signed
+    zeros, fp32 denormals, all-equal, sorted (core.py:95-115)."""
+    rng = np.random.default_rng(20250918)
+    Xs, rates, rows, cps = [], [], [], []
+    fams = ["gauss", "round", "zeros", "denorm", "equal", "sorted"]
+    for t in range(240):
+        fam = fams[t % len(fams)]
+        n = int(rng.integers(1, 300))
+        p = int(rng.integers(1, 6))
+        X = rng.normal(size=(n, p))
+        if fam == "round":
+            X = np.round(X, 1)
+        elif fam == "zeros":
+            X[rng.random(size=X.shape) < 0.3] = 0.0
+            X[rng.random(size=X.shape) < 0.2] = -0.0
+        elif fam == "denorm":
+            X = X * 1e-39
+        elif fam == "equal":
+            X = np.sign(X) * 0.5
+        elif fam == "sorted":
+            X = np.sort(np.abs(X), axis=0)
+        X = f32(X)
+        rate = float(rng.choice([0.02, 0.05, 0.1, 0.2, 0.3, 0.5, 0.7, 0.999, 1.0, rng.uniform(0.01, 1)]))
+        sk = ces_sketch(X, rate)
+        Xs.append(X)
+        rates.append(rate)
+        rows.append(sk.rows.astype(np.int32))
+        cps.append(sk.col_ptr)
+    out = {"n_cases": len(Xs)}
+    for i in range(len(Xs)):
+        out[f"X{i}"] = Xs[i]
+        out[f"rate{i}"] = rates[i]
+        out[f"rows{i}"] = rows[i]
+        out[f"colptr{i}"] = cps[i]
+    budgets = [(10, 0.7), (7, 0.01), (3, 0.999), (5, 0.2), (1000, 0.3), (20, 0.05), (99, 0.1 + 0.2)]
+    out["budget_cases"] = np.array([[n, r] for n, r in budgets], dtype=np.float64)
+    out["budget_want"] = np.array([sketch_budget(n, r) for n, r in budgets], dtype=np.int64)
+    np.savez_compressed(os.path.join(OUT, "sketch_cases.npz"), **out)
+
+
+def update_cases():
+    """update_user_core (core.py:134-157) on sketched and complete slices."""
+    rng = np.random.default_rng(7)
+    out = {}
+    n_cases = 120
+    for i in range(n_cases):
+        n = int(rng.integers(1, 60))
+        p = int(rng.integers(1, 9))
+        X = f32(rng.normal(size=(n, p)))
+        y = f32(rng.normal(size=n))
+        rate = float(rng.choice([0.1, 0.3, 0.5, 1.0]))
+        lam = float(rng.choice([0.0, 0.05, 0.2])) if n >= p else 0.2
+        sk = ces_sketch(X, rate)
+        if lam == 0.0:
+            # lam = 0 only where the sketched Gram is well conditioned; a
+            # numerically singular system has no reproducible solution
+            G = sk.to_dense().T @ X
+            if np.linalg.cond(G) > 1e6:
+                lam = 0.05
+        try:
+            w = update_user_core(X, sk, y, lam, n)
+            ok = 1
+        except coreals.NumericalError:
+            w = np.full(p, np.nan)
+            ok = 0
+        out[f"X{i}"] = X
+        out[f"y{i}"] = y
+        out[f"rate{i}"] = rate
+        out[f"lam{i}"] = lam
+        out[f"w{i}"] = w
+        out[f"ok{i}"] = ok
+        out[f"rows{i}"] = sk.rows.astype(np.int32)
+        out[f"colptr{i}"] = sk.col_ptr
+    out["n_cases"] = n_cases
+    np.savez_compressed(os.path.join(OUT, "update_cases.npz"), **out)
+
+
+def make_matrix(seed, n_users, n_items, density, n_f_true, noise, ties=False):
+    rng = np.random.default_rng(seed)
+    mask = rng.random((n_users, n_items)) < density
+    # every user and item keeps >= 1 rating except a couple of deliberate empties
+    users, items = np.nonzero(mask)
+    Ut = rng.normal(size=(n_users, n_f_true))
+    Vt = rng.normal(size=(n_items, n_f_true))
+    vals = np.einsum("ef,ef->e", Ut[users], Vt[items]) + noise * rng.normal(size=users.size)
+    if ties:
+        vals = np.round(vals * 2) / 2
+    return users.astype(np.int64), items.astype(np.int64), f32(vals)
+
+
+def fit_case(name, seed, n_users, n_items, density, n_f, lam, rate, iters, ties=False,
+             drop_user=None, drop_item=None):
+    users, items, vals = make_matrix(seed, n_users, n_items, density, max(2, n_f // 2), 0.5, ties)
+    keep = np.ones(users.size, bool)
+    if drop_user is not None:
+        keep &= users != drop_user
+    if drop_item is not None:
+        keep &= items != drop_item
+    users, items, vals = users[keep], items[keep], vals[keep]
+    R = RatingMatrix(users, items, vals, n_users=n_users, n_items=n_items)
+    rng = np.random.default_rng(seed + 1)
+    M0 = rng.normal(0.0, 0.1, size=(n_items, n_f))
+    if ties:
+        M0 = np.round(M0, 2)
+    M0 = f32(M0)
+    cfg1 = SolverConfig(method="core", n_f=n_f, lam=lam, rate=rate, max_iters=1, tol=1e-15)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        F1, rep1 = fit_core(R, cfg1, init_m=M0)
+        # item half from a fp32 snapshot of U1 (the GPU's input injection)
+        U1 = f32(F1.user_factors)
+        F1b, _ = fit_core(R, cfg1, init_u=U1, items_first=True)
+        cfgN = SolverConfig(method="core", n_f=n_f, lam=lam, rate=rate, max_iters=iters, tol=1e-15)
+        FN, repN = fit_core(R, cfgN, init_m=M0)
+
+    def thr(side_ptr, side_idx, source):
+        T = np.zeros((side_ptr.size - 1, n_f), dtype=np.uint64)
+        for i in range(side_ptr.size - 1):
+            lo, hi = side_ptr[i], side_ptr[i + 1]
+            if hi == lo:
+                continue
+            X = source[side_idx[lo:hi]]
+            sk = ces_sketch(X, rate)
+            for c in range(n_f):
+                r, v = sk.column(c)
+                bits = np.abs(v).astype(np.float32).view(np.uint32).astype(np.uint64) & np.uint64(0x7FFFFFFF)
+                k = (bits << np.uint64(32)) | (np.uint64(0xFFFFFFFF) - r.astype(np.uint64))
+                T[i, c] = k.min()
+        return T
+
+    np.savez_compressed(
+        os.path.join(OUT, f"fit_{name}.npz"),
+        users=users, items=items, vals=vals, n_users=n_users, n_items=n_items,
+        n_f=n_f, lam=lam, rate=rate, iters=iters, M0=M0,
+        U1=F1.user_factors, M1_from_U1=F1b.item_factors, U1_f32=U1,
+        obj1=rep1.objective_trace, rmse1=rep1.rmse_trace,
+        objN=repN.objective_trace, rmseN=repN.rmse_trace, UN=FN.user_factors, MN=FN.item_factors,
+        thr_user=thr(R.row_ptr, R.row_items, M0), thr_item=thr(R.col_ptr, R.col_users, U1),
+        skipped_users=repN.skipped_users, skipped_items=repN.skipped_items,
+    )
+
+
+if __name__ == "__main__":
+    sketch_cases()
+    update_cases()
+    # config-1 shape scaled down (BASELINE configs[0]: n_f=5, lam=0.1, r=0.3)
+    fit_case("small", 0, 300, 240, 0.2, 5, 0.1, 0.3, 5)
+    # medium-like rank (n_f=16, lam=0.05, r=0.2), dense enough for long rows
+    fit_case("medium", 1, 160, 120, 0.5, 16, 0.05, 0.2, 4)
+    # n_f=32 with rows shorter than n_f, empty user/item, ties in data and factors
+    fit_case("ties_wide", 2, 90, 70, 0.15, 32, 0.05, 0.2, 3, ties=True, drop_user=3, drop_item=5)
+    # rate 1: every row takes the exact SPD path
+    fit_case("rate1", 3, 50, 40, 0.4, 4, 0.1, 1.0, 3)
+    print("golden fixtures written to", OUT)
