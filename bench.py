@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark: observed ratings processed per second per core-elements ALS
+iteration (BASELINE.json metric) on 1..8 B200s.
+
+A "step" is one full ALS iteration of fit_core over the workload: the user
+half-sweep, its all-gather (N > 1), the item half-sweep with the fused
+residual, its all-gather, and the objective terms (rss + penalty) read back
+to the host -- exactly what fit_core does per iteration.  value = nnz * K / T
+with T the max over ranks of the CUDA-event time of the K timed steps; inputs
+are device resident and L2 is flushed (a 512 MiB write) before every timed
+step, outside its events.
+
+Extra keys: roofline (dominant kernel, algorithmic bytes / its event-timed
+duration vs the measured HBM copy bandwidth), cpu_baseline (the float64 C
+oracle port on one host core, bounded sample), e2e (fit_core through the
+public API from host numpy arrays, copies included), clocks, gpu_launches.
+
+--impl reference times the reference algorithm's CPU path (the oracle port;
+the reference itself is Python+numba and does not travel to the GPU box) with
+all host threads on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_CONFIG = "medium"
+METRIC = "observed ratings processed/sec per ALS iteration"
+UNIT = "ratings/s/iter"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=DEFAULT_CONFIG)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for s in self.samples for j in range(4) if s[2 + j].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def algorithmic_bytes(counts, n_f):
+    """each observed rating gathers its fp32 factor row plus int32
+    index and fp32 value; each solved row reads its pointer and writes its row."""
+    counts = np.asarray(counts, np.int64)
+    act = counts > 0
+    return float(counts.sum() * (4 * n_f + 8) + act.sum() * (4 * n_f + 8))
+
+
+def tier_bytes(side, n_f):
+    c = side.counts
+    small = algorithmic_bytes(c[side.small_host], n_f) if side.small_host.size else 0.0
+    big = algorithmic_bytes(c[side.big_host], n_f) if side.big_host.size else 0.0
+    return small, big
+
+
+def cpu_baseline_port(data_host, spec, M0, seconds):
+    """The float64 C oracle (a restatement of the reference algorithm) on ONE
+    host core: a row sample of one user half-sweep + one item half-sweep."""
+    import oracle
+
+    n_f, lam, rate = spec["n_f"], spec["lam"], spec["rate"]
+    R = data_host
+    rng = np.random.default_rng(0)
+    U = np.zeros((R.n_users, n_f))
+    M = M0.astype(np.float64)
+    done_ratings, t_used = 0, 0.0
+    for side, ptr, idx, val, src, tgt in (("user", R.row_ptr, R.row_items, R.row_vals, M, U),
+                                          ("item", R.col_ptr, R.col_users, R.col_vals, None, None)):
+        if side == "item":
+            src, tgt = U, M.copy()
+        counts = np.diff(ptr)
+        rows = rng.permutation(np.flatnonzero(counts > 0)).astype(np.int32)
+        budget = seconds / 2.0
+        pos = 0
+        t0 = time.perf_counter()
+        chunk = 64
+        while pos < rows.size and time.perf_counter() - t0 < budget:
+            sl = rows[pos:pos + chunk]
+            oracle.core_half_sweep(ptr, idx, val, src, n_f, lam, rate, tgt, want_rss=(side == "item"), rows=sl,
+                                   threads=1)
+            done_ratings += int(counts[sl].sum())
+            pos += sl.size
+            chunk = min(chunk * 2, 4096)
+        t_used += time.perf_counter() - t0
+    return {"value": done_ratings / t_used / 2.0 if t_used > 0 else 0.0, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"random row sample of one user + one item half-sweep ({done_ratings} slice ratings, "
+                      f"{t_used:.1f} s), float64 C oracle port, 1 thread; ratings/s/iter = sampled ratings / "
+                      f"time / 2 sides"}
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm's CPU path (oracle port) with
+    all host threads, each step = one bounded row sample of a full iteration."""
+    import torch
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from paper_2509_18024_b200 import synth
+
+    spec = dict(synth.CONFIGS[args.config])
+    data = synth.generate(args.config, device="cuda" if torch.cuda.is_available() else "cpu")
+    R = data.rating_matrix()
+    M0 = synth.init_m(R.n_items, spec["n_f"]).astype(np.float64)
+    threads = os.cpu_count() or 1
+    n_f, lam, rate = spec["n_f"], spec["lam"], spec["rate"]
+    rng = np.random.default_rng(1)
+    budget = max(5.0, 60.0 / max(args.steps + args.warmup, 1))
+    U = np.zeros((R.n_users, n_f))
+    M = M0.copy()
+    rates = []
+    for step in range(args.warmup + args.steps):
+        done, t_used = 0, 0.0
+        for side in ("user", "item"):
+            ptr, idx, val = (R.row_ptr, R.row_items, R.row_vals) if side == "user" else (R.col_ptr, R.col_users, R.col_vals)
+            src, tgt = (M, U) if side == "user" else (U, M)
+            counts = np.diff(ptr)
+            rows = rng.permutation(np.flatnonzero(counts > 0)).astype(np.int32)
+            pos, chunk = 0, 256 * threads
+            t0 = time.perf_counter()
+            while pos < rows.size and time.perf_counter() - t0 < budget / 2:
+                sl = rows[pos:pos + chunk]
+                oracle.core_half_sweep(ptr, idx, val, src, n_f, lam, rate, tgt, want_rss=(side == "item"), rows=sl,
+                                       threads=threads)
+                done += int(counts[sl].sum())
+                pos += sl.size
+            t_used += time.perf_counter() - t0
+        if step >= args.warmup:
+            rates.append(done / t_used / 2.0)
+    value = float(np.median(rates))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": data.nnz / value * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "nnz": data.nnz, "n_users": R.n_users, "n_items": R.n_items,
+                   "n_f": n_f, "lam": lam, "rate": rate},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"per step a random row sample of both half-sweeps, {budget:.0f} s of "
+                                   f"{threads}-thread float64 C oracle work; ms_per_step extrapolated to all rows"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2509_18024_b200 import _lib, synth
+    from paper_2509_18024_b200.engine import CoreEngine
+    from paper_2509_18024_b200.shard import ShardedEngine
+
+    spec = dict(synth.CONFIGS[args.config])
+    n_f, lam, rate = spec["n_f"], spec["lam"], spec["rate"]
+    t_gen = time.perf_counter()
+    data = synth.generate(args.config, device=dev, seed=0)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t_gen
+    M0 = synth.init_m(data.n_items, n_f)
+    eng = (ShardedEngine(data, n_f, rate, lam, rank, world, device=dev) if world > 1
+           else CoreEngine(data, n_f, rate, lam, device=dev))
+    eng.set_factors(np.zeros((data.n_users, n_f), np.float32), M0)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    for _ in range(args.warmup):
+        eng.iterate("user")
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream(dev)
+    times = []
+    _lib.profile_enable(True)
+    _lib.profile_collect()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            terms = eng.iterate("user")
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    prof = _lib.profile_collect()
+    _lib.profile_enable(False)
+    total_ms = float(sum(times))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    nnz = data.nnz
+    value = nnz * args.steps / (total_ms / 1e3)
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    hbm, peak_kind = measured_peaks()
+    core = eng.eng if world > 1 else eng
+    sb_u, bb_u = tier_bytes(core.user, n_f)
+    sb_i, bb_i = tier_bytes(core.item, n_f)
+    kbytes = {"small_sweep_kernel": (sb_u + sb_i) * args.steps, "big_gram_kernel": (bb_u + bb_i) * args.steps,
+              "big_scan_kernel": (bb_u + bb_i) * args.steps}
+    dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (0, 0.0))
+    dom_name, (dom_cnt, dom_ms) = dom
+    dom_bytes = kbytes.get(dom_name)
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9 if dom_bytes and dom_ms > 0 else None
+    b_iter = algorithmic_bytes(np.diff(data.row_ptr.cpu().numpy()), n_f) + algorithmic_bytes(
+        np.diff(data.col_ptr.cpu().numpy()), n_f)
+    gpu_launches = sum(c for c, _ in prof.values())
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": {"workload": args.config, "nnz": nnz, "n_users": data.n_users, "n_items": data.n_items,
+                   "n_f": n_f, "lam": lam, "rate": rate, "parallelism": f"row-shard x{world}",
+                   "l2": "512 MiB flush before every timed step (outside its events)",
+                   "init": "M0 ~ N(0, 0.1^2) numpy seed 0, fp32; U0 = 0"},
+        "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": (achieved / hbm) if achieved else None, "traffic": None, "peak_kind": peak_kind,
+                     "launches": dom_cnt, "kernel_ms_total": dom_ms,
+                     "step_alg_bytes": b_iter,
+                     "step_frac": (b_iter / (hbm * 1e9)) / (total_ms / 1e3 / args.steps)},
+        "kernels": {k: {"launches": c, "ms": ms} for k, (c, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
+        "gpu_launches": gpu_launches,
+        "clocks": clk.summary(),
+        "rmse_last": float(np.sqrt(terms.rss / core.ssq)),
+        "setup_s": {"generate": t_gen},
+    }
+    if not args.no_cpu and world == 1:
+        R_host = data.rating_matrix()
+        line["cpu_baseline"] = cpu_baseline_port(R_host, spec, M0, args.cpu_seconds)
+    else:
+        line["cpu_baseline"] = None
+    if not args.no_e2e and world == 1:
+        line["e2e"] = e2e(data, spec, M0, args.steps)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    print(json.dumps(line), flush=True)
+
+
+def e2e(data, spec, M0, steps):
+    """fit_core through the public API from host (numpy) arrays: H2D of both
+    indexes and the init, `steps` iterations, D2H of both factor matrices."""
+    import warnings
+
+    import torch
+
+    import paper_2509_18024_b200 as cb
+
+    R = data.rating_matrix()
+    cfg = cb.SolverConfig(method="core", n_f=spec["n_f"], lam=spec["lam"], rate=spec["rate"], max_iters=steps,
+                          tol=1e-15)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        cb.fit_core(R, cb.SolverConfig(method="core", n_f=spec["n_f"], lam=spec["lam"], rate=spec["rate"],
+                                       max_iters=1, tol=1e-15), init_m=M0)  # warm (allocator, module load)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        F, rep = cb.fit_core(R, cfg, init_m=M0)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    nnz = R.n_entries
+    n_f = spec["n_f"]
+    h2d = (R.row_ptr.nbytes + R.col_ptr.nbytes + 2 * nnz * 4 + 2 * nnz * 4 + (R.n_users + R.n_items) * n_f * 4)
+    d2h = (R.n_users + R.n_items) * n_f * 4 + rep.iters_run * 5 * 8
+    return {"value": nnz * rep.iters_run / wall, "unit": UNIT, "h2d_bytes_per_step": h2d / rep.iters_run,
+            "d2h_bytes_per_step": d2h / rep.iters_run, "wall_s": wall, "iters": rep.iters_run,
+            "how": "paper_2509_18024_b200.fit_core(RatingMatrix of numpy arrays) incl. plan, H2D (pageable), "
+                   "all iterations, D2H of float64 factors; per-step bytes amortised over the fit"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+/*
+ * coreals_b200.h -- C ABI of the B200 (sm_100a) core-elements ALS half-sweep.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ *   coreals.fit_core -> als._alternate -> core._CoreSweeper.row
+ * (/root/reference/pkg/src/coreals/core.py:301-312, als.py:243-323,
+ *  core.py:173-223).  The reference's per-row Python plugin seam
+ * (`sweeper.begin/row`, als.py:281-285) is replaced at half-sweep
+ * granularity: one call updates every row of one side.
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers owned by the caller, unless the
+ *    parameter name ends in `_host`.  Nothing here allocates device memory:
+ *    scratch comes from a caller-provided workspace sized by
+ *    cals_workspace_bytes().
+ *  - Work is enqueued on `stream` (a cudaStream_t passed as void*); calls are
+ *    asynchronous and capturable into CUDA graphs.  One host thread per
+ *    device/stream.
+ *  - Factor matrices are fp32, row-major, leading dimension `ld` >= n_f.
+ *  - Ratings are CSR (user side) or CSC (item side): int64 ptr, int32 idx
+ *    ascending within each row, fp32 values (reference RatingMatrix,
+ *    ratings.py:83-92, with values narrowed to fp32).
+ *  - Return value: CALS_OK or a CALS_ERR_* code; cals_strerror() names it.
+ *    Per-row numerical outcomes go to `row_status` (CALS_ROW_*), which the
+ *    host maps to NumericalError exactly where the reference raises it
+ *    (core.py:131, als.py:197).
+ */
+#ifndef COREALS_B200_H
+#define COREALS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CALS_OK 0
+#define CALS_ERR_ARG 1
+#define CALS_ERR_CUDA 2
+#define CALS_ERR_WORKSPACE 3
+#define CALS_ERR_UNSUPPORTED 4
+
+/* per-row status (core.py:120-131 / als.py:184-197 jitter semantics) */
+#define CALS_ROW_OK 0
+#define CALS_ROW_JITTERED 1
+#define CALS_ROW_SINGULAR 2
+
+#define CALS_MAX_NF 128
+
+/* One side of the rating matrix (CSR over users or CSC over items). */
+typedef struct cals_side {
+    const int64_t* ptr; /* [n_rows + 1] */
+    const int32_t* idx; /* [nnz]  source-row ids, ascending per row */
+    const float* val;   /* [nnz]  ratings */
+    int64_t n_rows;
+    int64_t nnz;
+} cals_side;
+
+/*
+ * Static per-side schedule, built once per (dataset, n_f, rate) on the host
+ * by cals_plan_build(); the caller uploads the arrays and points the struct
+ * at the device copies.  Rows with n_i = 0 are absent (skipped,
+ * als.py:252-259).
+ */
+typedef struct cals_plan {
+    const int32_t* budget;        /* [n_rows] s_i = sketch_budget(n_i, rate), core.py:48-54 */
+    const int32_t* small_rows;    /* rows whose slice is staged whole in shared memory, n desc */
+    int64_t n_small;
+    int64_t small_seg[4];         /* small_rows[seg[g] .. seg[g+1]) have n_i <= small_seg_maxn[g] */
+    int32_t small_seg_maxn[3];
+    const int32_t* big_rows;      /* rows streamed in work items (slice > shared memory), n desc */
+    int64_t n_big;
+    const int64_t* big_tile_ptr;  /* [n_big + 1] prefix of work items per big row */
+    int64_t n_big_tiles;
+    const int64_t* big_cand_ptr;  /* [n_big + 1] candidate-key offsets per big row (n_f equal regions) */
+    int64_t big_cand_total;
+    int32_t item_rows;            /* slice rows per work item of a big row */
+    int32_t n_f;                  /* rank the plan was built for */
+} cals_plan;
+
+/* Host: reference budget rule for every row (core.py:48-54), fp64, no FMA. */
+int cals_budget_host(const int64_t* counts_host, int64_t n_rows, double rate, int32_t* budget_host);
+
+/* Host: build the schedule.  counts_host[i] = n_i.  Output host arrays:
+ * budget_host, small_rows_host, big_rows_host sized n_rows;
+ * big_tile_ptr_host, big_cand_ptr_host sized n_rows + 1.  `meta` receives
+ * the scalar fields (its pointer fields are set to NULL). */
+int cals_plan_build(const int64_t* counts_host, int64_t n_rows, int n_f, double rate,
+                    int32_t* budget_host, int32_t* small_rows_host, int32_t* big_rows_host,
+                    int64_t* big_tile_ptr_host, int64_t* big_cand_ptr_host, cals_plan* meta);
+
+/* Device workspace needed by cals_core_half_sweep for this plan. */
+size_t cals_workspace_bytes(const cals_plan* plan);
+
+/*
+ * One core-estimator half-sweep (the GPU replacement for the per-row loop
+ * als.py:282-288 driving core.py:199-223):
+ *   for every row i with n_i > 0:
+ *     per column c keep the s_i slice rows of largest |source[idx, c]| (ties to
+ *     the smallest row), G = X*^T X + lam*n_i*I, b = X*^T y, solve G w = b by
+ *     LU with partial pivoting (s_i == n_i: the exact SPD ridge row), target[i] = w.
+ *   rss_rows (nullable): fused residual sum_k (y_k - X_k . w)^2 per row, fp64
+ *     (_kernels.py:219-230; the reference fuses it into the item half-sweep).
+ *   thr_keys (nullable): [n_rows, n_f] selection threshold key per (row, column),
+ *     key = (abs_bits(x) << 32) | (0xFFFFFFFF - slice_row); the kept set of column
+ *     c is exactly {k : key(k, c) >= thr_keys[i, c]}.
+ *   row_status: [n_rows] CALS_ROW_*; rows with n_i = 0 are left untouched.
+ *   status_summary (nullable, 1 element, overwritten): max over rows of
+ *     (status << 32) | (0xFFFFFFFF - row) -- 0 when every row is CALS_ROW_OK;
+ *     otherwise the worst status and the first row having it, so the host can
+ *     raise NumericalError with the reference's context after one tiny read.
+ */
+int cals_core_half_sweep(const cals_side* side, const cals_plan* plan, const float* source,
+                         int64_t n_src, int ld_src, int n_f, double lam, float* target,
+                         int ld_tgt, double* rss_rows, uint64_t* thr_keys, int32_t* row_status,
+                         uint64_t* status_summary, void* workspace, size_t ws_bytes, void* stream);
+
+/* Deterministic fp64 sum of an array (fixed reduction tree). out: 1 double. */
+int cals_sum_f64(const double* x, int64_t n, double* out, void* workspace, size_t ws_bytes,
+                 void* stream);
+
+/* Weighted penalty term sum_i counts_i * ||F_i||^2 (als.py:162-167), fp64. */
+int cals_weighted_sqnorm(const float* F, int64_t n_rows, int n_f, int ld, const int64_t* ptr,
+                         double* out, void* workspace, size_t ws_bytes, void* stream);
+
+/* Public subsample entry (core.py:95-115): per column of the dense slice X
+ * (n x p, row-major fp32) keep s rows; rows_out (p*s) slice-local, strict-
+ * then-tied ascending order as the reference emits them; vals_out = X[rows, c]. */
+int cals_ces_sketch(const float* X, int64_t n, int p, int32_t s, int32_t* rows_out,
+                    float* vals_out, void* workspace, size_t ws_bytes, void* stream);
+size_t cals_ces_sketch_workspace_bytes(int64_t n, int p);
+
+/* Same selection for a float64 slice (exact |x| ranks, any values): rows_out
+ * as above.  workspace >= n * p bytes.  For the public API on float64 input. */
+int cals_ces_sketch_f64(const double* X, int64_t n, int p, int32_t s, int32_t* rows_out, void* workspace,
+                        size_t ws_bytes, void* stream);
+
+/* Public single-row sketched update (core.py:134-157): X (n x p) float64,
+ * sketch given as per-column slice-local rows (col_ptr int64[p+1], rows int32),
+ * complete -> exact SPD path; float64 arithmetic.  w_out (p doubles), status_out (1 int32). */
+int cals_update_core(const double* X, int64_t n, int p, const int64_t* col_ptr,
+                     const int32_t* rows, const double* y, double lam_n, int complete,
+                     double* w_out, int32_t* status_out, void* stream);
+
+/* predict_entries (als.py:143-152): out[e] = U[users[e]] . M[items[e]]. */
+int cals_predict_entries(const float* U, const float* M, int n_f, int ld_u, int ld_m,
+                         const int64_t* users, const int64_t* items, int64_t n, double* out,
+                         void* stream);
+
+/* Optional per-kernel timing with CUDA events recorded on the launch stream
+ * (for bench.py's roofline numbers).  collect() synchronises on the recorded
+ * events, writes "name launches total_ms" lines into buf, and resets. */
+void cals_profile_enable(int on);
+int cals_profile_collect(char* buf, size_t len);
+
+const char* cals_strerror(int status);
+const char* cals_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COREALS_B200_H */

@@ -1,0 +1,19 @@
+"""B200-native core-elements ALS (arXiv 2509.18024): a drop-in for the
+reference package's ``core`` method path (``coreals.fit_core`` and its
+sketch / update / predict entry points), running every half-sweep as
+hand-written sm_100a CUDA kernels behind the C ABI in include/coreals_b200.h.
+"""
+
+from .als import FactorPair, FitReport, SolverConfig, init_factors, predict, predict_entries, predict_full
+from .core import SparseSketch, ces_sketch, fit_core, sketch_budget, update_item_core, update_user_core
+from .driver import fit_method
+from .errors import ConfigError, DataError, NumericalError
+from .ratings import RatingMatrix
+
+__all__ = [
+    "FactorPair", "FitReport", "SolverConfig", "init_factors", "predict", "predict_entries", "predict_full",
+    "SparseSketch", "ces_sketch", "fit_core", "sketch_budget", "update_item_core", "update_user_core",
+    "fit_method", "ConfigError", "DataError", "NumericalError", "RatingMatrix",
+]
+
+__version__ = "0.1.0"

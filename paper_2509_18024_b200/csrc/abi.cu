@@ -1,0 +1,515 @@
+// abi.cu -- extern "C" boundary: host planner, workspace sizing, launchers.
+// See include/coreals_b200.h for the contract of every entry point.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <vector>
+
+#include "coreals_b200.h"
+#include "sweep_common.cuh"
+
+
+using namespace cals;
+
+namespace {
+
+constexpr size_t kSmemBudget = 224 * 1024;  // dynamic shared memory per CTA (B200 opt-in max is 227 KB)
+constexpr int kQSsmall = 4096, kQSbig = 8192;
+constexpr int kItemRowsMin = 4096;
+
+thread_local char g_err[256] = "";
+
+// ---- optional per-kernel timing (CUDA events on the launch stream) --------
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+struct Prof {
+    bool on = false;
+    std::vector<ProfRec> live;
+    std::vector<cudaEvent_t> pool;
+    std::mutex mu;
+    cudaEvent_t get() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+};
+Prof& prof() {
+    static Prof p;
+    return p;
+}
+struct ProfScope {
+    const char* name;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    ProfScope(const char* n, cudaStream_t s) : name(n), st(s) {
+        Prof& P = prof();
+        if (!P.on) return;
+        std::lock_guard<std::mutex> lk(P.mu);
+        a = P.get();
+        cudaEventRecord(a, st);
+    }
+    ~ProfScope() {
+        if (!a) return;
+        Prof& P = prof();
+        std::lock_guard<std::mutex> lk(P.mu);
+        cudaEvent_t b = P.get();
+        cudaEventRecord(b, st);
+        P.live.push_back({name, a, b});
+    }
+};
+
+inline float delta_tab_for(int QS) { return 3.0f * 0.5f / std::sqrt((float)QS); }
+
+int small_nmax(int nf) {
+    int lo = 1, hi = 1 << 16;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) / 2;
+        if (T1Layout(mid, nf, kThreads).total <= kSmemBudget) lo = mid; else hi = mid - 1;
+    }
+    return std::min(lo, 65535);
+}
+
+int big_chunk(int nf) {
+    // largest power of two whose staged chunk fits ~96 KB alongside mask/G/scratch
+    const size_t per = (size_t)xs_stride(nf) * 4;
+    int ch = 1024;
+    while (ch > 64 && (size_t)ch * per > 96 * 1024) ch >>= 1;
+    return ch;
+}
+
+size_t big_gram_smem(int nf, int chunk) {
+    const int sx = xs_stride(nf), mw = (nf + 31) / 32;
+    return align16((size_t)chunk * sx * 4) + align16((size_t)chunk * mw * 4) + align16((size_t)nf * (nf + 1) * 4) +
+           (size_t)kThreads * 16 * 4;
+}
+
+int64_t cand_cap(int64_t n, float delta_tab) {
+    const double d = 3.0 * std::sqrt(0.25 / (double)n) + delta_tab + 0.5 / kQ;
+    int64_t cap = (int64_t)std::ceil(3.0 * d * (double)n) + 64;
+    cap = std::max<int64_t>(cap, 64);
+    return std::min<int64_t>(cap, std::max<int64_t>(n, 64));
+}
+
+struct Carve {
+    char* base;
+    size_t off = 0;
+    explicit Carve(void* b) : base((char*)b) {}
+    template <typename T>
+    T* take(size_t count) {
+        off = (off + 255) & ~(size_t)255;
+        T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+        off += count * sizeof(T);
+        return p;
+    }
+};
+
+struct Device {
+    int sms = 148;
+    bool init = false;
+};
+Device& dev() {
+    static Device d;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!d.init) {
+        int id = 0;
+        cudaGetDevice(&id);
+        cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, id);
+        d.init = true;
+    }
+    return d;
+}
+
+template <typename K>
+void allow_smem(K kernel) {
+    static std::mutex mu;
+    static std::vector<const void*> done;
+    std::lock_guard<std::mutex> lk(mu);
+    const void* k = reinterpret_cast<const void*>(kernel);
+    if (std::find(done.begin(), done.end(), k) == done.end()) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
+        done.push_back(k);
+    }
+}
+
+template <typename K>
+int grid_for(K kernel, size_t smem, int64_t work, int cap_per_sm = 8) {
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
+    occ = std::max(1, std::min(occ, cap_per_sm));
+    int64_t g = (int64_t)std::min(dev().sms, 160) * occ;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, work));
+}
+
+int cuda_status(const char* where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        std::snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+        return CALS_ERR_CUDA;
+    }
+    return CALS_OK;
+}
+
+struct Work {
+    uint32_t* qtab;
+    int* cnt;
+    uint64_t* cand;
+    uint64_t* thr;
+    float* part;
+    float* wbig;
+    double* rss_part;
+    double* retry;
+};
+
+constexpr int kMaxGrid = 160 * 8;  // grid_for never exceeds min(SMs, 160) * 8 CTAs
+inline int retry_stride(int nf) { return ((nf * (nf + 1) + nf) + 31) & ~31; }
+
+Work carve(const cals_plan* P, void* ws, size_t* total) {
+    Carve c(ws);
+    Work w{};
+    const int nf = P->n_f;
+    w.qtab = c.take<uint32_t>((size_t)nf * (kQ + 1));
+    w.cnt = c.take<int>((size_t)P->n_big * nf * 2);
+    w.cand = c.take<uint64_t>((size_t)P->big_cand_total);
+    w.thr = c.take<uint64_t>((size_t)P->n_big * nf);
+    w.part = c.take<float>((size_t)P->n_big_tiles * nf * (nf + 1));
+    w.wbig = c.take<float>((size_t)P->n_big * nf);
+    w.rss_part = c.take<double>((size_t)P->n_big_tiles);
+    w.retry = c.take<double>((size_t)kMaxGrid * retry_stride(nf));
+    *total = c.off + 256;
+    return w;
+}
+
+template <int NFP>
+int launch_small(const SweepArgs& A, const cals_plan* P, cudaStream_t st) {
+    allow_smem(small_sweep_kernel<NFP>);
+    for (int g = 0; g < 3; ++g) {
+        const int64_t b = P->small_seg[g], e = P->small_seg[g + 1];
+        if (e <= b) continue;
+        const int N = P->small_seg_maxn[g];
+        const size_t smem = T1Layout(N, A.nf, kThreads).total;
+        const int grid = grid_for(small_sweep_kernel<NFP>, smem, e - b);
+        ProfScope ps("small_sweep_kernel", st);
+        small_sweep_kernel<NFP><<<grid, kThreads, smem, st>>>(A, P->small_rows + b, e - b, N);
+    }
+    return cuda_status("small_sweep_kernel");
+}
+
+template <int NFP>
+int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream_t st) {
+    const int nf = A.nf;
+    BigArgs B{};
+    B.rows = P->big_rows;
+    B.tile_ptr = P->big_tile_ptr;
+    B.cand_ptr = P->big_cand_ptr;
+    B.n_big = P->n_big;
+    B.n_tiles = P->n_big_tiles;
+    B.item_rows = P->item_rows;
+    B.chunk = big_chunk(nf);
+    B.cnt = w.cnt;
+    B.cand = w.cand;
+    B.thr = w.thr;
+    B.part = w.part;
+    B.wbig = w.wbig;
+    B.rss_part = w.rss_part;
+    cudaMemsetAsync(w.cnt, 0, sizeof(int) * (size_t)P->n_big * nf * 2, st);
+    const size_t scan_smem = align16((size_t)B.chunk * xs_stride(nf) * 4);
+    allow_smem(big_scan_kernel);
+    {
+        ProfScope ps("big_scan_kernel", st);
+        big_scan_kernel<<<grid_for(big_scan_kernel, scan_smem, B.n_tiles), kThreads, scan_smem, st>>>(A, B);
+    }
+    {
+        const int64_t warps = B.n_big * nf;
+        const int64_t blocks = std::min<int64_t>((warps + 7) / 8, (int64_t)dev().sms * 8);
+        ProfScope ps("big_resolve_kernel", st);
+        big_resolve_kernel<<<(int)std::max<int64_t>(1, blocks), kThreads, 0, st>>>(A, B);
+    }
+    const size_t gram_smem = big_gram_smem(nf, B.chunk);
+    allow_smem(big_gram_kernel);
+    {
+        ProfScope ps("big_gram_kernel", st);
+        big_gram_kernel<<<grid_for(big_gram_kernel, gram_smem, B.n_tiles), kThreads, gram_smem, st>>>(A, B);
+    }
+    const size_t solve_smem = 2 * align16((size_t)nf * (nf + 1) * 4);
+    allow_smem(big_solve_kernel<NFP>);
+    {
+        ProfScope ps("big_solve_kernel", st);
+        big_solve_kernel<NFP><<<grid_for(big_solve_kernel<NFP>, solve_smem, B.n_big), kThreads, solve_smem, st>>>(A, B);
+    }
+    if (A.rss_rows != nullptr) {
+        ProfScope ps("big_rss_kernel", st);
+        big_rss_kernel<<<grid_for(big_rss_kernel, 0, B.n_tiles), kThreads, 0, st>>>(A, B);
+        const int64_t blocks = (B.n_big + 255) / 256;
+        big_rss_reduce_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 1024)), 256, 0, st>>>(A, B);
+    }
+    return cuda_status("big-row kernels");
+}
+
+}  // namespace
+
+extern "C" {
+
+int cals_budget_host(const int64_t* counts, int64_t n_rows, double rate, int32_t* out) {
+    if (!counts || !out || n_rows < 0 || !(rate > 0.0) || rate > 1.0) return CALS_ERR_ARG;
+    for (int64_t i = 0; i < n_rows; ++i) {
+        const int64_t n = counts[i];
+        volatile double prod = (double)n * rate;  // multiply, then add (core.py:54): no contraction
+        const double f = std::floor(prod + 1e-9);
+        int64_t s = (int64_t)f;
+        if (s < 1) s = 1;
+        if (s > n) s = n;
+        out[i] = (int32_t)s;
+    }
+    return CALS_OK;
+}
+
+int cals_plan_build(const int64_t* counts, int64_t n_rows, int n_f, double rate, int32_t* budget,
+                    int32_t* small_rows, int32_t* big_rows, int64_t* big_tile_ptr, int64_t* big_cand_ptr,
+                    cals_plan* meta) {
+    if (!counts || !budget || !small_rows || !big_rows || !big_tile_ptr || !big_cand_ptr || !meta) return CALS_ERR_ARG;
+    if (n_f < 1 || n_f > CALS_MAX_NF || n_rows < 0 || n_rows > 0x7fffffff) return CALS_ERR_ARG;
+    int rc = cals_budget_host(counts, n_rows, rate, budget);
+    if (rc) return rc;
+    std::memset(meta, 0, sizeof(*meta));
+    meta->n_f = n_f;
+    const int nmax = small_nmax(n_f);
+    std::vector<int32_t> small, big;
+    for (int64_t i = 0; i < n_rows; ++i) {
+        if (counts[i] <= 0) continue;
+        if (counts[i] > 0x7fffffffLL) return CALS_ERR_UNSUPPORTED;
+        (counts[i] <= nmax ? small : big).push_back((int32_t)i);
+    }
+    auto by_len = [counts](int32_t a, int32_t b) { return counts[a] != counts[b] ? counts[a] > counts[b] : a < b; };
+    std::stable_sort(small.begin(), small.end(), by_len);
+    std::stable_sort(big.begin(), big.end(), by_len);
+    std::copy(small.begin(), small.end(), small_rows);
+    std::copy(big.begin(), big.end(), big_rows);
+    meta->n_small = (int64_t)small.size();
+    meta->n_big = (int64_t)big.size();
+    // segments over the descending list: (256, nmax], (64, 256], [1, 64]
+    const int64_t thresholds[3] = {nmax, 256, 64};
+    int64_t pos = 0;
+    for (int g = 0; g < 3; ++g) {
+        const int64_t lo_bound = (g < 2) ? thresholds[g + 1] : 0;
+        meta->small_seg[g] = pos;
+        meta->small_seg_maxn[g] = pos < (int64_t)small.size() ? (int32_t)counts[small[pos]] : 1;
+        while (pos < (int64_t)small.size() && counts[small[pos]] > lo_bound) ++pos;
+    }
+    meta->small_seg[3] = pos;
+    // big rows: work items and candidate buffers
+    const int chunk = big_chunk(n_f);
+    meta->item_rows = std::max(kItemRowsMin, chunk);
+    const float dtab = delta_tab_for(kQSbig);
+    big_tile_ptr[0] = 0;
+    big_cand_ptr[0] = 0;
+    for (size_t r = 0; r < big.size(); ++r) {
+        const int64_t n = counts[big[r]];
+        big_tile_ptr[r + 1] = big_tile_ptr[r] + (n + meta->item_rows - 1) / meta->item_rows;
+        big_cand_ptr[r + 1] = big_cand_ptr[r] + (int64_t)n_f * cand_cap(n, dtab);
+    }
+    meta->n_big_tiles = big_tile_ptr[big.size()];
+    meta->big_cand_total = big_cand_ptr[big.size()];
+    return CALS_OK;
+}
+
+size_t cals_workspace_bytes(const cals_plan* plan) {
+    if (!plan) return 0;
+    size_t total = 0;
+    carve(plan, nullptr, &total);
+    return total;
+}
+
+int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float* source, int64_t n_src, int ld_src,
+                         int n_f, double lam, float* target, int ld_tgt, double* rss_rows, uint64_t* thr_keys,
+                         int32_t* row_status, uint64_t* status_summary, void* ws, size_t ws_bytes, void* stream) {
+    if (!side || !P || !source || !target || !row_status) return CALS_ERR_ARG;
+    if (n_f < 1 || n_f > CALS_MAX_NF || n_f != P->n_f || ld_src < n_f || ld_tgt < n_f || lam < 0) return CALS_ERR_ARG;
+    if ((P->n_small && !P->small_rows) || (P->n_big && (!P->big_rows || !P->big_tile_ptr || !P->big_cand_ptr)) ||
+        !P->budget)
+        return CALS_ERR_ARG;
+    size_t need = 0;
+    Work w = carve(P, ws, &need);
+    if (ws_bytes < need || (!ws && need > 256)) return CALS_ERR_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    (void)dev();
+    if (status_summary) cudaMemsetAsync(status_summary, 0, sizeof(uint64_t), st);
+
+    SweepArgs A{};
+    A.ptr = side->ptr;
+    A.idx = side->idx;
+    A.val = side->val;
+    A.budget = P->budget;
+    A.src = source;
+    A.n_src = n_src;
+    A.ld_src = ld_src;
+    A.nf = n_f;
+    A.tgt = target;
+    A.ld_tgt = ld_tgt;
+    A.lam = lam;
+    A.rss_rows = rss_rows;
+    A.thr_keys = thr_keys;
+    A.status = row_status;
+    A.summary = reinterpret_cast<unsigned long long*>(status_summary);
+    A.qtab = nullptr;
+    A.retry_ws = w.retry;
+    A.retry_stride = retry_stride(n_f);
+
+    const bool long_small = P->n_small > 0 && P->small_seg_maxn[0] > kCap;
+    if ((long_small || P->n_big > 0) && side->nnz > 0) {
+        const int QS = P->n_big > 0 ? kQSbig : kQSsmall;
+        allow_smem(quantile_table_kernel);
+        {
+            ProfScope ps("quantile_table_kernel", st);
+            quantile_table_kernel<<<n_f, 1024, (size_t)QS * 4, st>>>(side->idx, side->nnz, source, ld_src, QS, w.qtab);
+        }
+        A.qtab = w.qtab;
+        A.delta_tab = delta_tab_for(QS);
+        int rc = cuda_status("quantile_table_kernel");
+        if (rc) return rc;
+    }
+    int rc = CALS_OK;
+    if (P->n_small > 0) {
+        if (n_f <= 8) rc = launch_small<8>(A, P, st);
+        else if (n_f <= 16) rc = launch_small<16>(A, P, st);
+        else if (n_f <= 32) rc = launch_small<32>(A, P, st);
+        else rc = launch_small<0>(A, P, st);
+        if (rc) return rc;
+    }
+    if (P->n_big > 0) {
+        if (n_f <= 8) rc = launch_big<8>(A, P, w, st);
+        else if (n_f <= 16) rc = launch_big<16>(A, P, w, st);
+        else if (n_f <= 32) rc = launch_big<32>(A, P, w, st);
+        else rc = launch_big<0>(A, P, w, st);
+    }
+    return rc;
+}
+
+int cals_sum_f64(const double* x, int64_t n, double* out, void* ws, size_t ws_bytes, void* stream) {
+    if (!out || (n > 0 && !x) || !ws || ws_bytes < kRedBlocks * sizeof(double)) return CALS_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    double* partials = (double*)ws;
+    ProfScope ps("sum_f64", st);
+    sum_partial_kernel<<<kRedBlocks, 256, 0, st>>>(x, n, partials);
+    finish_sum_kernel<<<1, 256, 0, st>>>(partials, kRedBlocks, out);
+    return cuda_status("cals_sum_f64");
+}
+
+int cals_weighted_sqnorm(const float* F, int64_t n_rows, int n_f, int ld, const int64_t* ptr, double* out, void* ws,
+                         size_t ws_bytes, void* stream) {
+    if (!F || !ptr || !out || !ws || ws_bytes < kRedBlocks * sizeof(double) || ld < n_f) return CALS_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    double* partials = (double*)ws;
+    ProfScope ps("weighted_sqnorm", st);
+    sqnorm_partial_kernel<<<kRedBlocks, 256, 0, st>>>(F, n_rows, n_f, ld, ptr, partials);
+    finish_sum_kernel<<<1, 256, 0, st>>>(partials, kRedBlocks, out);
+    return cuda_status("cals_weighted_sqnorm");
+}
+
+size_t cals_ces_sketch_workspace_bytes(int64_t n, int p) {
+    return (size_t)p * (size_t)std::max<int64_t>(n, 32) * sizeof(uint64_t) + 256;
+}
+
+int cals_ces_sketch(const float* X, int64_t n, int p, int32_t s, int32_t* rows_out, float* vals_out, void* ws,
+                    size_t ws_bytes, void* stream) {
+    if (!X || !rows_out || !vals_out || n < 1 || p < 1 || s < 1 || s > n || n > 0x7fffffff) return CALS_ERR_ARG;
+    if (!ws || ws_bytes < cals_ces_sketch_workspace_bytes(n, p)) return CALS_ERR_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int blocks = (p * 32 + 255) / 256;
+    ces_sketch_kernel<<<blocks, 256, 0, st>>>(X, (int)n, p, s, rows_out, vals_out, (uint64_t*)ws);
+    return cuda_status("cals_ces_sketch");
+}
+
+int cals_ces_sketch_f64(const double* X, int64_t n, int p, int32_t s, int32_t* rows_out, void* ws, size_t ws_bytes,
+                        void* stream) {
+    if (!X || !rows_out || n < 1 || p < 1 || s < 1 || s > n || n > 0x7fffffff) return CALS_ERR_ARG;
+    if (!ws || ws_bytes < (size_t)n * p) return CALS_ERR_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    dim3 grid((unsigned)((n + 255) / 256), (unsigned)p);
+    ces_rank_f64_kernel<<<grid, 256, 0, st>>>(X, (int)n, p, s, (uint8_t*)ws);
+    ces_emit_f64_kernel<<<(p * 32 + 255) / 256, 256, 0, st>>>(X, (int)n, p, s, (const uint8_t*)ws, rows_out);
+    return cuda_status("cals_ces_sketch_f64");
+}
+
+int cals_update_core(const double* X, int64_t n, int p, const int64_t* col_ptr, const int32_t* rows, const double* y,
+                     double lam_n, int complete, double* w_out, int32_t* status_out, void* stream) {
+    if (!X || !y || !w_out || !status_out || n < 1 || p < 1 || p > CALS_MAX_NF) return CALS_ERR_ARG;
+    if (!complete && (!col_ptr || !rows)) return CALS_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t smem = (size_t)(2 * p * (p + 1) + p) * sizeof(double);
+    allow_smem(update_core_kernel);
+    update_core_kernel<<<1, 256, smem, st>>>(X, (int)n, p, col_ptr, rows, y, lam_n, complete, w_out, status_out);
+    return cuda_status("cals_update_core");
+}
+
+int cals_predict_entries(const float* U, const float* M, int n_f, int ld_u, int ld_m, const int64_t* users,
+                         const int64_t* items, int64_t n, double* out, void* stream) {
+    if (!U || !M || !users || !items || !out || n_f < 1 || ld_u < n_f || ld_m < n_f) return CALS_ERR_ARG;
+    if (n == 0) return CALS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)dev().sms * 16);
+    predict_entries_kernel<<<(int)blocks, 256, 0, st>>>(U, M, n_f, ld_u, ld_m, users, items, n, out);
+    return cuda_status("cals_predict_entries");
+}
+
+void cals_profile_enable(int on) {
+    Prof& P = prof();
+    std::lock_guard<std::mutex> lk(P.mu);
+    P.on = on != 0;
+}
+
+int cals_profile_collect(char* buf, size_t len) {
+    Prof& P = prof();
+    std::lock_guard<std::mutex> lk(P.mu);
+    struct Agg {
+        const char* name;
+        int count;
+        double ms;
+    };
+    std::vector<Agg> agg;
+    for (auto& r : P.live) {
+        cudaEventSynchronize(r.b);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        auto it = std::find_if(agg.begin(), agg.end(), [&](const Agg& g) { return std::strcmp(g.name, r.name) == 0; });
+        if (it == agg.end()) agg.push_back({r.name, 1, (double)ms});
+        else { it->count += 1; it->ms += ms; }
+        P.pool.push_back(r.a);
+        P.pool.push_back(r.b);
+    }
+    P.live.clear();
+    size_t off = 0;
+    if (buf && len) buf[0] = 0;
+    for (auto& g : agg) {
+        if (!buf || off >= len) break;
+        off += (size_t)std::snprintf(buf + off, len - off, "%s %d %.6f\n", g.name, g.count, g.ms);
+    }
+    return (int)agg.size();
+}
+
+const char* cals_strerror(int status) {
+    switch (status) {
+        case CALS_OK: return "ok";
+        case CALS_ERR_ARG: return "invalid argument";
+        case CALS_ERR_CUDA: return g_err[0] ? g_err : "CUDA error";
+        case CALS_ERR_WORKSPACE: return "workspace too small";
+        case CALS_ERR_UNSUPPORTED: return "unsupported shape";
+        default: return "unknown status";
+    }
+}
+
+const char* cals_build_info(void) {
+    return "coreals_b200: sm_100a, nvcc " CALS_NVCC_VERSION ", warp sample-select + masked-dense SIMT Gram v1";
+}
+
+}  // extern "C"

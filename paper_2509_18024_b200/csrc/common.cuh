@@ -1,0 +1,102 @@
+// common.cuh -- shared device helpers for the core-elements ALS kernels (sm_100a).
+//
+// Selection key (bit-exact with the reference's ordering, core.py:26-27,
+// _kernels.py:84-96): |x| descending, then slice-local row ascending.
+//   key(k) = (abs_bits(x) << 32) | (0xFFFFFFFF - k)
+// abs_bits of an fp32 is monotone in |x| for every finite value including
+// denormals (never compiled with -ftz / fast-math) and +-0 collapse to 0.
+// Keys of one column are unique, so "top-s" is exactly {key >= T} for the
+// s-th largest key T.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "coreals_b200.h"
+
+#define CALS_FULL_MASK 0xffffffffu
+
+namespace cals {
+
+__device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7FFFFFFFu; }
+
+__device__ __forceinline__ uint64_t make_key(float x, uint32_t k) {
+    return ((uint64_t)abs_bits(x) << 32) | (uint64_t)(0xFFFFFFFFu - k);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Bitonic sort of one 64-bit key per lane; result descending (lane 0 = max).
+__device__ __forceinline__ uint64_t warp_sort_desc(uint64_t v, int lane) {
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            uint64_t o = __shfl_xor_sync(CALS_FULL_MASK, v, stride);
+            bool lower = (lane & stride) == 0;
+            bool desc_block = (lane & size) == 0;
+            bool keep_max = (lower == desc_block);
+            v = keep_max ? (v > o ? v : o) : (v < o ? v : o);
+        }
+    }
+    return v;
+}
+
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CALS_FULL_MASK, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CALS_FULL_MASK, v, o);
+    return v;
+}
+
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CALS_FULL_MASK, v, o);
+    return v;
+}
+
+// Fixed-order block reduction of one double per thread (deterministic).
+// scratch: >= blockDim.x/32 doubles.  Result valid in thread 0.
+__device__ __forceinline__ double block_sum_d(double v, double* scratch) {
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum_d(v);
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x == 0) {
+        int nw = (blockDim.x + 31) >> 5;
+        for (int w = 0; w < nw; ++w) r += scratch[w];
+    }
+    return r;
+}
+
+__device__ __forceinline__ int block_sum_i(int v, int* scratch) {
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum_i(v);
+    __syncthreads();
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    int r = 0;
+    int nw = (blockDim.x + 31) >> 5;
+    for (int w = 0; w < nw; ++w) r += scratch[w];
+    __syncthreads();
+    return r;  // valid in every thread
+}
+
+// Exact floor division e / d for e < 2^24, d <= 256, via one multiply-high.
+struct FastDiv {
+    uint32_t d, magic;
+    __host__ __device__ FastDiv() : d(1), magic(0) {}
+    __host__ __device__ explicit FastDiv(uint32_t dd) : d(dd), magic((uint32_t)((0x100000000ull + dd - 1) / dd)) {}
+    __device__ __forceinline__ uint32_t div(uint32_t e) const { return d == 1 ? e : __umulhi(e, magic); }
+};
+
+}  // namespace cals

@@ -1,0 +1,5 @@
+// coreals_b200.cu -- unity translation unit for libcoreals_b200.so (sm_100a).
+#include "sweep_small.cu"
+#include "sweep_big.cu"
+#include "misc.cu"
+#include "abi.cu"

@@ -1,0 +1,191 @@
+// solve.cuh -- small dense solves for the sketched normal equations.
+//
+// The sketched Gram X*^T X + lam*n*I is NOT symmetric (only one factor is
+// sketched, core.py:7-14), so it is solved by LU with partial pivoting, as
+// the reference does with LAPACK gesv (_kernels.py:233-236).  Rows whose
+// sketch is complete (s == n) take the exact SPD ridge path (core.py:206-207,
+// als.py:184-205): elimination without pivoting, failing on a non-positive
+// pivot exactly where Cholesky fails.  Either failure triggers the
+// reference's single jitter retry (+1e-10 * tr(G)/n_f on the diagonal,
+// core.py:126-131), done in float64 by the block solver (rare path).
+//
+// Input: augmented matrix G[r * gs + j], j < nf the Gram, j == nf the RHS.
+#pragma once
+#include "common.cuh"
+
+namespace cals {
+
+// One warp, lane r owns row r in registers; NFP >= nf (compile-time bound).
+// Pivot-row values are broadcast with shuffles inside the elimination loop,
+// so the only per-lane state is the row itself.
+// Returns 0 ok, 1 failure (zero / non-finite pivot; non-positive when spd).
+template <int NFP>
+__device__ int warp_lu_solve(const float* G, int gs, int nf, bool spd, float* x_out, int lane) {
+    float a[NFP];
+    float rhs = 0.f;
+#pragma unroll
+    for (int j = 0; j < NFP; ++j) a[j] = (lane < nf && j < nf) ? G[lane * gs + j] : ((lane == j) ? 1.f : 0.f);
+    if (lane < nf) rhs = G[lane * gs + nf];
+#pragma unroll
+    for (int k = 0; k < NFP; ++k) {
+        if (k < nf) {
+            int p = k;
+            if (!spd) {
+                float best = (lane >= k && lane < nf) ? fabsf(a[k]) : -1.f;
+                int bi = lane;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const float ob = __shfl_xor_sync(CALS_FULL_MASK, best, o);
+                    const int oi = __shfl_xor_sync(CALS_FULL_MASK, bi, o);
+                    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+                }
+                if (!(best > 0.f)) return 1;
+                p = bi;
+            }
+            const float d = __shfl_sync(CALS_FULL_MASK, a[k], p);
+            if (spd ? !(d > 0.f) : !(d == d)) return 1;
+            const float rowk_k = __shfl_sync(CALS_FULL_MASK, a[k], k);
+            const float mine = (lane == p) ? rowk_k : a[k];  // column-k entry after the swap
+            const float f = (lane > k && lane < nf) ? mine / d : 0.f;
+#pragma unroll
+            for (int j = 0; j < NFP; ++j) {
+                if (j > k) {
+                    const float vp = __shfl_sync(CALS_FULL_MASK, a[j], p);
+                    const float vk = __shfl_sync(CALS_FULL_MASK, a[j], k);
+                    float v = (lane == k) ? vp : ((lane == p) ? vk : a[j]);
+                    a[j] = fmaf(-f, vp, v);
+                }
+            }
+            if (lane == k) a[k] = d;
+            const float bp = __shfl_sync(CALS_FULL_MASK, rhs, p);
+            const float bk = __shfl_sync(CALS_FULL_MASK, rhs, k);
+            const float bv = (lane == k) ? bp : ((lane == p) ? bk : rhs);
+            rhs = fmaf(-f, bp, bv);
+        }
+    }
+    float x = 0.f;
+#pragma unroll
+    for (int k = NFP - 1; k >= 0; --k) {
+        if (k < nf) {
+            float xk = (lane == k) ? rhs / a[k] : 0.f;
+            xk = __shfl_sync(CALS_FULL_MASK, xk, k);
+            if (lane == k) x = xk;
+            if (lane < k) rhs = fmaf(-a[k], xk, rhs);
+        }
+    }
+    if (lane < nf) x_out[lane] = x;
+    const bool bad = !(x == x) || (x - x != 0.f);
+    return __any_sync(CALS_FULL_MASK, lane < nf && bad) ? 1 : 0;
+}
+
+// Block-wide LU (nf <= 128) in shared memory, in place on W (stride nf+1),
+// working copy of G.  All threads of the block must call it.  Returns 0/1.
+template <typename T>
+__device__ int block_lu_solve(T* W, int nf, bool spd, T* x_out, int* s_piv) {
+    const int gs = nf + 1;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int k = 0; k < nf; ++k) {
+        if (warp == 0) {
+            int p = k;
+            T best = (T)-1;
+            if (!spd) {
+                for (int r = k + lane; r < nf; r += 32) {
+                    T v = W[r * gs + k];
+                    v = v < 0 ? -v : v;
+                    if (v > best) { best = v; p = r; }
+                }
+                int bi = (best >= 0) ? p : 0x7fffffff;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    T ob = __shfl_xor_sync(CALS_FULL_MASK, best, o);
+                    int oi = __shfl_xor_sync(CALS_FULL_MASK, bi, o);
+                    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+                }
+                p = bi;
+                if (lane == 0) s_piv[0] = (best > (T)0) ? p : -1;
+            } else {
+                T d = W[k * gs + k];
+                if (lane == 0) s_piv[0] = (d > (T)0) ? k : -1;
+            }
+        }
+        __syncthreads();
+        int p = s_piv[0];
+        if (p < 0) return 1;
+        if (p != k) {
+            for (int j = tid; j < gs; j += nt) {
+                T t = W[k * gs + j];
+                W[k * gs + j] = W[p * gs + j];
+                W[p * gs + j] = t;
+            }
+            __syncthreads();
+        }
+        T d = W[k * gs + k];
+        int rows = nf - k - 1, cols = nf - k;  // trailing rows, columns k+1..nf (incl. RHS)
+        for (int e = tid; e < rows * cols; e += nt) {
+            int r = k + 1 + e / cols;
+            int j = k + 1 + e % cols;
+            W[r * gs + j] -= (W[r * gs + k] / d) * W[k * gs + j];
+        }
+        __syncthreads();
+    }
+    if (warp == 0) {
+        for (int r = nf - 1; r >= 0; --r) {
+            T acc = 0;
+            for (int j = r + 1 + lane; j < nf; j += 32) acc += W[r * gs + j] * x_out[j];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(CALS_FULL_MASK, acc, o);
+            if (lane == 0) x_out[r] = (W[r * gs + nf] - acc) / W[r * gs + r];
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    int bad = 0;
+    for (int j = tid; j < nf; j += nt) {
+        T v = x_out[j];
+        if (!(v == v) || (v - v != 0)) bad = 1;
+    }
+    return __syncthreads_or(bad);
+}
+
+// Solve one sketched system with the reference's failure semantics.
+// All threads of the block call it.  G: fp32 augmented matrix in shared
+// memory (left intact).  Fast path: warp-register LU (NFP > 0) or block LU in
+// shared memory on Wf (NFP == 0).  On failure: float64 retry with the
+// diagonal jitter 1e-10*tr(G)/nf (core.py:126-131 / als.py:191-197) on Wd
+// (global scratch, nf*(nf+1) + nf doubles per CTA).  Returns CALS_ROW_*.
+template <int NFP>
+__device__ int solve_row(const float* G, int nf, bool spd, float* wv, float* Wf, double* Wd, int* s_piv,
+                         int* s_flag) {
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int gs = nf + 1, nout = nf * gs;
+    if constexpr (NFP > 0) {
+        if (warp == 0) {
+            const int bad = warp_lu_solve<NFP>(G, gs, nf, spd, wv, lane);
+            if (lane == 0) s_flag[0] = bad;
+        }
+        __syncthreads();
+    } else {
+        for (int e = tid; e < nout; e += nt) Wf[e] = G[e];
+        __syncthreads();
+        const int bad = block_lu_solve<float>(Wf, nf, spd, wv, s_piv);
+        if (tid == 0) s_flag[0] = bad;
+        __syncthreads();
+    }
+    if (!s_flag[0]) return CALS_ROW_OK;
+    double tr = 0.0;
+    for (int c = 0; c < nf; ++c) tr += (double)G[c * gs + c];
+    const double jit = 1e-10 * tr / (double)nf;
+    double* xd = Wd + nout;
+    for (int e = tid; e < nout; e += nt) {
+        const int c = e / gs, f = e - c * gs;
+        Wd[e] = (double)G[e] + ((c == f) ? jit : 0.0);
+    }
+    __syncthreads();
+    const int bad = block_lu_solve<double>(Wd, nf, spd, xd, s_piv);
+    for (int f = tid; f < nf; f += nt) wv[f] = (float)xd[f];
+    __syncthreads();
+    return bad ? CALS_ROW_SINGULAR : CALS_ROW_JITTERED;
+}
+
+}  // namespace cals

@@ -1,0 +1,252 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the reference's
+golden fixtures and the float64 CPU oracle on identical fp32 inputs.
+
+Bars (BASELINE.json north_star):
+  * selection: the per-(row, column) threshold key -- hence the kept index set --
+    is bit-exact (integer equality);
+  * factors: per row, max|w_gpu - w_ref| <= 1e-4 * max(max|w_ref|, 1e-2)
+    (fp32 device arithmetic vs the reference's float64), half-sweep by half-sweep
+    with the reference fed the GPU's own input snapshot;
+  * end to end: |rmse_gpu - rmse_ref| <= 1e-3 after the fixed iteration count.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import csr_csc, load_golden
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected only on GPU boxes
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2509_18024_b200 as cb  # noqa: E402
+from paper_2509_18024_b200.engine import CoreEngine  # noqa: E402
+
+FACTOR_TOL = 1e-4
+
+
+def row_rel_err(got, want, rows=None):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    if rows is not None:
+        got, want = got[rows], want[rows]
+    scale = np.maximum(np.abs(want).max(axis=1), 1e-2)
+    return float((np.abs(got - want).max(axis=1) / scale).max())
+
+
+def gpu_half(eng, side, source, init_target=None):
+    """One GPU half-sweep from a given fp32 source; returns (target, thr_keys)."""
+    n_rows = eng.n_users if side == "user" else eng.n_items
+    keys = torch.zeros((n_rows, eng.n_f), dtype=torch.int64, device=eng.device)
+    if side == "user":
+        eng.set_factors(M=source, U=init_target if init_target is not None else np.zeros((eng.n_users, eng.n_f)))
+    else:
+        eng.set_factors(U=source, M=init_target if init_target is not None else np.zeros((eng.n_items, eng.n_f)))
+    eng.half(side, want_rss=(side == "item"), thr_keys=keys)
+    torch.cuda.synchronize()
+    tgt = (eng.U if side == "user" else eng.M).double().cpu().numpy()
+    return tgt, keys.cpu().numpy().view(np.uint64)
+
+
+class _nowarn:
+    def __enter__(self):
+        import warnings
+        self.c = warnings.catch_warnings()
+        self.c.__enter__()
+        warnings.simplefilter("ignore")
+
+    def __exit__(self, *a):
+        self.c.__exit__(*a)
+
+
+def golden_engine(name):
+    g = load_golden(f"fit_{name}.npz")
+    R = cb.RatingMatrix(g["users"], g["items"], g["vals"], n_users=int(g["n_users"]), n_items=int(g["n_items"]))
+    eng = CoreEngine(R, int(g["n_f"]), float(g["rate"]), float(g["lam"]))
+    return g, R, eng
+
+
+@pytest.mark.parametrize("name", ["small", "medium", "ties_wide", "rate1"])
+def test_golden_half_sweeps(name):
+    g, R, eng = golden_engine(name)
+    U, keys = gpu_half(eng, "user", g["M0"])
+    act = np.diff(R.row_ptr) > 0
+    np.testing.assert_array_equal(keys[act], g["thr_user"][act])
+    assert row_rel_err(U, g["U1"], act) <= FACTOR_TOL
+    M, keys = gpu_half(eng, "item", g["U1_f32"], init_target=g["M0"])
+    act = np.diff(R.col_ptr) > 0
+    np.testing.assert_array_equal(keys[act], g["thr_item"][act])
+    assert row_rel_err(M, g["M1_from_U1"], act) <= FACTOR_TOL
+
+
+@pytest.mark.parametrize("name", ["small", "medium", "ties_wide", "rate1"])
+def test_golden_fit_rmse(name):
+    g, R, _ = golden_engine(name)
+    cfg = cb.SolverConfig(method="core", n_f=int(g["n_f"]), lam=float(g["lam"]), rate=float(g["rate"]),
+                          max_iters=int(g["iters"]), tol=1e-15)
+    with _nowarn():
+        F, rep = cb.fit_core(R, cfg, init_m=g["M0"])
+    assert rep.iters_run == int(g["iters"])
+    assert abs(rep.rmse_trace[-1] - g["rmseN"][-1]) <= 1e-3
+    np.testing.assert_allclose(rep.objective_trace, g["objN"], rtol=1e-3)
+    assert rep.skipped_users == int(g["skipped_users"]) and rep.skipped_items == int(g["skipped_items"])
+    assert F.user_factors.dtype == np.float64
+
+
+def random_matrix(seed, n_users, n_items, density, n_f_true=4, heavy_items=0, heavy_density=0.0, ties=False):
+    rng = np.random.default_rng(seed)
+    mask = rng.random((n_users, n_items)) < density
+    if heavy_items:
+        mask[:, :heavy_items] = rng.random((n_users, heavy_items)) < heavy_density
+    u, i = np.nonzero(mask)
+    Ut = rng.normal(size=(n_users, n_f_true))
+    Vt = rng.normal(size=(n_items, n_f_true))
+    v = np.einsum("ef,ef->e", Ut[u], Vt[i]) + 0.3 * rng.normal(size=u.size)
+    if ties:
+        v = np.round(v)
+    return u, i, v.astype(np.float32).astype(np.float64)
+
+
+def check_against_oracle(R, n_f, lam, rate, source_item, seed=0, ties=False):
+    rng = np.random.default_rng(seed)
+    eng = CoreEngine(R, n_f, rate, lam)
+    csr = (R.row_ptr, R.row_items, R.row_vals)
+    csc = (R.col_ptr, R.col_users, R.col_vals)
+    # user half from M0
+    M0 = source_item
+    U, keys = gpu_half(eng, "user", M0)
+    Uo = np.zeros((R.n_users, n_f))
+    _, st, ko = oracle.core_half_sweep(*csr, M0.astype(np.float64), n_f, lam, rate, Uo, want_keys=True, threads=8)
+    act = np.diff(R.row_ptr) > 0
+    np.testing.assert_array_equal(keys[act], ko[act])
+    assert row_rel_err(U, Uo, act) <= FACTOR_TOL
+    # item half from the GPU's own fp32 U (injection)
+    U32 = U.astype(np.float32)
+    M, keys = gpu_half(eng, "item", U32)
+    Mo = np.zeros((R.n_items, n_f))
+    rss_o, st, ko = oracle.core_half_sweep(*csc, U32.astype(np.float64), n_f, lam, rate, Mo, want_rss=True,
+                                           want_keys=True, threads=8)
+    act = np.diff(R.col_ptr) > 0
+    np.testing.assert_array_equal(keys[act], ko[act])
+    assert row_rel_err(M, Mo, act) <= FACTOR_TOL
+    rss_g = eng.item.rss_rows.cpu().numpy()
+    np.testing.assert_allclose(rss_g[act].sum(), rss_o[act].sum(), rtol=1e-4)
+    return eng
+
+
+@pytest.mark.parametrize("n_f", [1, 3, 5, 8, 16, 24, 32, 48, 64, 128])
+def test_oracle_parity_mixed_tiers(n_f):
+    """Short rows (identity lists), table-bracket rows and big tiled rows."""
+    u, i, v = random_matrix(n_f, 3000, 400, 0.04, heavy_items=6, heavy_density=0.9)
+    R = cb.RatingMatrix(u, i, v, n_users=3000, n_items=400)
+    M0 = np.random.default_rng(1).normal(0, 0.1, (400, n_f)).astype(np.float32)
+    eng = check_against_oracle(R, n_f, 0.05, 0.2, M0)
+    assert eng.item.plan.n_big > 0  # the heavy items exercise the tiled tier
+    if n_f <= 32:
+        assert eng.user.plan.n_small > 0
+
+
+@pytest.mark.parametrize("rate", [0.02, 0.1, 0.3, 0.5, 0.999, 1.0])
+def test_oracle_parity_rates(rate):
+    u, i, v = random_matrix(7, 2000, 300, 0.1, heavy_items=3, heavy_density=1.0)
+    R = cb.RatingMatrix(u, i, v, n_users=2000, n_items=300)
+    M0 = np.random.default_rng(2).normal(0, 0.1, (300, 16)).astype(np.float32)
+    check_against_oracle(R, 16, 0.05, rate, M0)
+
+
+def test_oracle_parity_ties_and_zeros():
+    u, i, v = random_matrix(11, 2500, 300, 0.2, heavy_items=2, heavy_density=1.0, ties=True)
+    R = cb.RatingMatrix(u, i, v, n_users=2500, n_items=300)
+    rng = np.random.default_rng(3)
+    M0 = np.round(rng.normal(0, 0.1, (300, 8)), 2).astype(np.float32)  # heavy |x| ties
+    M0[rng.random(M0.shape) < 0.2] = 0.0
+    M0[rng.random(M0.shape) < 0.1] = -0.0
+    check_against_oracle(R, 8, 0.1, 0.25, M0)
+
+
+def test_half_sweep_is_deterministic():
+    u, i, v = random_matrix(5, 3000, 300, 0.1, heavy_items=3, heavy_density=0.8)
+    R = cb.RatingMatrix(u, i, v, n_users=3000, n_items=300)
+    M0 = np.random.default_rng(4).normal(0, 0.1, (300, 32)).astype(np.float32)
+    eng = CoreEngine(R, 32, 0.2, 0.05)
+    a, ka = gpu_half(eng, "user", M0)
+    b, kb = gpu_half(eng, "user", M0)
+    assert np.array_equal(a, b) and np.array_equal(ka, kb)
+    c, _ = gpu_half(eng, "item", a.astype(np.float32))
+    r1 = eng.item.rss_rows.clone()
+    d, _ = gpu_half(eng, "item", a.astype(np.float32))
+    assert np.array_equal(c, d) and torch.equal(r1, eng.item.rss_rows)
+
+
+def test_ces_sketch_matches_reference_rows_exactly():
+    g = load_golden("sketch_cases.npz")
+    for k in range(int(g["n_cases"])):
+        sk = cb.ces_sketch(g[f"X{k}"], float(g[f"rate{k}"]))
+        np.testing.assert_array_equal(sk.rows, g[f"rows{k}"])
+        np.testing.assert_array_equal(sk.col_ptr, g[f"colptr{k}"])
+
+
+def test_ces_sketch_tall_fp32_path_matches_oracle():
+    rng = np.random.default_rng(9)
+    X = np.round(rng.normal(size=(20000, 3)), 2).astype(np.float32).astype(np.float64)
+    sk = cb.ces_sketch(X, 0.1)
+    want = oracle.ces_sketch(X, 0.1)
+    np.testing.assert_array_equal(sk.rows, want.rows)
+
+
+def test_ces_sketch_errors():
+    with pytest.raises(cb.ConfigError):
+        cb.ces_sketch(np.ones((3, 2)), 0.0)
+    with pytest.raises(cb.DataError):
+        cb.ces_sketch(np.ones(3), 0.5)
+
+
+def test_update_core_matches_reference():
+    g = load_golden("update_cases.npz")
+    for k in range(int(g["n_cases"])):
+        X, y = g[f"X{k}"], g[f"y{k}"]
+        sk = cb.SparseSketch(X.shape[0], X.shape[1], g[f"colptr{k}"], g[f"rows{k}"],
+                             X[g[f"rows{k}"], np.repeat(np.arange(X.shape[1]), np.diff(g[f"colptr{k}"]))])
+        if int(g[f"ok{k}"]) == 0:
+            with pytest.raises(cb.NumericalError):
+                cb.update_user_core(X, sk, y, float(g[f"lam{k}"]), X.shape[0])
+            continue
+        w = cb.update_item_core(X, sk, y, float(g[f"lam{k}"]), X.shape[0])
+        want = g[f"w{k}"]
+        assert np.abs(w - want).max() <= 1e-9 * max(1.0, np.abs(want).max()), k
+
+
+def test_predict_entries_and_full():
+    rng = np.random.default_rng(0)
+    F = cb.FactorPair(rng.normal(size=(50, 7)).astype(np.float32), rng.normal(size=(40, 7)).astype(np.float32))
+    us, its = rng.integers(0, 50, 1000), rng.integers(0, 40, 1000)
+    got = cb.predict_entries(F, us, its)
+    want = np.einsum("ef,ef->e", F.user_factors[us], F.item_factors[its])
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12)
+    assert cb.predict(F, 3, 4) == pytest.approx(float(F.user_factors[3] @ F.item_factors[4]))
+    with pytest.raises(IndexError):
+        cb.predict_entries(F, [50], [0])
+
+
+def test_singular_row_raises_with_reference_context():
+    # user 1 rates only item 0 whose factor row is all zeros, lam = 0 -> G = 0
+    users = np.array([0, 0, 1, 2, 2])
+    items = np.array([0, 1, 0, 1, 2])
+    R = cb.RatingMatrix(users, items, np.ones(5), n_users=3, n_items=3)
+    M0 = np.array([[0.0, 0.0], [0.5, 0.1], [0.2, 0.3]])
+    cfg = cb.SolverConfig(method="core", n_f=2, lam=0.0, rate=0.5, max_iters=1, tol=1e-15)
+    with _nowarn():
+        with pytest.raises(cb.NumericalError, match="singular"):
+            cb.fit_core(R, cfg, init_m=M0)
+
+
+def test_fit_method_dispatch_and_zero_iters():
+    g = load_golden("fit_small.npz")
+    R = cb.RatingMatrix(g["users"], g["items"], g["vals"], n_users=int(g["n_users"]), n_items=int(g["n_items"]))
+    cfg = cb.SolverConfig(method="core", n_f=5, lam=0.1, rate=0.3, max_iters=0)
+    F, rep = cb.fit_method(R, cfg, init_m=g["M0"])
+    assert rep.iters_run == 0 and rep.objective_trace.size == 0
+    np.testing.assert_array_equal(F.item_factors, g["M0"])
