@@ -137,7 +137,13 @@ void allow_smem(K kernel) {
     std::lock_guard<std::mutex> lk(mu);
     const void* k = reinterpret_cast<const void*>(kernel);
     if (std::find(done.begin(), done.end(), k) == done.end()) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(227 * 1024));
+        int id = 0, optin = 0;
+        cudaGetDevice(&id);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, id);
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, k);
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+        cudaGetLastError();  // an attribute failure must not masquerade as a launch error
         done.push_back(k);
     }
 }

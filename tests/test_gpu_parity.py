@@ -144,9 +144,19 @@ def test_oracle_parity_mixed_tiers(n_f):
     R = cb.RatingMatrix(u, i, v, n_users=3000, n_items=400)
     M0 = np.random.default_rng(1).normal(0, 0.1, (400, n_f)).astype(np.float32)
     eng = check_against_oracle(R, n_f, 0.05, 0.2, M0)
-    assert eng.item.plan.n_big > 0  # the heavy items exercise the tiled tier
-    if n_f <= 32:
-        assert eng.user.plan.n_small > 0
+    assert eng.user.plan.n_small > 0
+    if n_f >= 16:
+        assert eng.item.plan.n_big > 0  # the heavy items exercise the tiled tier
+
+
+@pytest.mark.parametrize("n_f", [1, 5, 8])
+def test_oracle_parity_tiled_tier_small_rank(n_f):
+    """Rows long enough to leave shared memory even at tiny n_f."""
+    u, i, v = random_matrix(100 + n_f, 20000, 60, 0.01, heavy_items=2, heavy_density=0.97)
+    R = cb.RatingMatrix(u, i, v, n_users=20000, n_items=60)
+    M0 = np.random.default_rng(5).normal(0, 0.1, (60, n_f)).astype(np.float32)
+    eng = check_against_oracle(R, n_f, 0.1, 0.3, M0)
+    assert eng.item.plan.n_big > 0
 
 
 @pytest.mark.parametrize("rate", [0.02, 0.1, 0.3, 0.5, 0.999, 1.0])
