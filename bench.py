@@ -247,7 +247,7 @@ def main():
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     for _ in range(args.warmup):
-        eng.iterate("user")
+        eng.step("user")
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -264,7 +264,8 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            terms = eng.iterate("user")
+            eng.step("user")  # iteration t, its first half fusing the residual of t-1
+            terms = eng.terms(eng.iters_done - 2)  # the host read fit_core does every iteration
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
@@ -288,7 +289,7 @@ def main():
     core = eng.eng if world > 1 else eng
     sb_u, bb_u = tier_bytes(core.user, n_f)
     sb_i, bb_i = tier_bytes(core.item, n_f)
-    kbytes = {"small_sweep_kernel": (sb_u + sb_i) * args.steps, "big_gram_kernel": (bb_u + bb_i) * args.steps,
+    kbytes = {"small_gram_kernel": (sb_u + sb_i) * args.steps, "big_gram_kernel": (bb_u + bb_i) * args.steps,
               "big_scan_kernel": (bb_u + bb_i) * args.steps}
     dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (0, 0.0))
     dom_name, (dom_cnt, dom_ms) = dom
@@ -313,7 +314,7 @@ def main():
         "kernels": {k: {"launches": c, "ms": ms} for k, (c, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
         "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
-        "rmse_last": float(np.sqrt(terms.rss / core.ssq)),
+        "rmse_prev_iter": float(np.sqrt(terms.rss / core.ssq)),
         "setup_s": {"generate": t_gen},
     }
     if not args.no_cpu and world == 1:

@@ -16,7 +16,10 @@
  *  - Work is enqueued on `stream` (a cudaStream_t passed as void*); calls are
  *    asynchronous and capturable into CUDA graphs.  One host thread per
  *    device/stream.
- *  - Factor matrices are fp32, row-major, leading dimension `ld` >= n_f.
+ *  - Factor matrices are fp32, row-major, leading dimension `ld` >= n_f.  The
+ *    SOURCE of a half-sweep must have ld a multiple of 4 (>= n_f rounded up),
+ *    16-byte alignment and zeros in the padding columns: its rows are
+ *    gathered as 16-byte chunks (cp.async).
  *  - Ratings are CSR (user side) or CSC (item side): int64 ptr, int32 idx
  *    ascending within each row, fp32 values (reference RatingMatrix,
  *    ratings.py:83-92, with values narrowed to fp32).
@@ -69,6 +72,7 @@ typedef struct cals_plan {
     int64_t n_small;
     int64_t small_seg[4];         /* small_rows[seg[g] .. seg[g+1]) have n_i <= small_seg_maxn[g] */
     int32_t small_seg_maxn[3];
+    int32_t small_seg_maxs[3];    /* largest budget s_i < n_i in the segment (kept-row lists) */
     const int32_t* big_rows;      /* rows streamed in work items (slice > shared memory), n desc */
     int64_t n_big;
     const int64_t* big_tile_ptr;  /* [n_big + 1] prefix of work items per big row */
@@ -100,8 +104,13 @@ size_t cals_workspace_bytes(const cals_plan* plan);
  *     per column c keep the s_i slice rows of largest |source[idx, c]| (ties to
  *     the smallest row), G = X*^T X + lam*n_i*I, b = X*^T y, solve G w = b by
  *     LU with partial pivoting (s_i == n_i: the exact SPD ridge row), target[i] = w.
- *   rss_rows (nullable): fused residual sum_k (y_k - X_k . w)^2 per row, fp64
- *     (_kernels.py:219-230; the reference fuses it into the item half-sweep).
+ *   target may alias target_old only when rss_rows is NULL.
+ *   rss_rows (nullable; needs target_old): fused residual of the PREVIOUS rows,
+ *     sum_k (y_k - X_k . target_old[i])^2 per row, fp64 (_kernels.py:219-230).
+ *     The reference fuses the residual of iteration t into its item half-sweep;
+ *     here it rides on the first half-sweep of iteration t+1, whose slices
+ *     hold exactly the needed rows, so it costs no extra memory traffic.
+ *   pen_rows (nullable): n_i * |w_i|^2 of every new row, fp64 (als.py:162-167).
  *   thr_keys (nullable): [n_rows, n_f] selection threshold key per (row, column),
  *     key = (abs_bits(x) << 32) | (0xFFFFFFFF - slice_row); the kept set of column
  *     c is exactly {k : key(k, c) >= thr_keys[i, c]}.
@@ -113,8 +122,14 @@ size_t cals_workspace_bytes(const cals_plan* plan);
  */
 int cals_core_half_sweep(const cals_side* side, const cals_plan* plan, const float* source,
                          int64_t n_src, int ld_src, int n_f, double lam, float* target,
-                         int ld_tgt, double* rss_rows, uint64_t* thr_keys, int32_t* row_status,
+                         int ld_tgt, const float* target_old, int ld_old, double* rss_rows,
+                         double* pen_rows, uint64_t* thr_keys, int32_t* row_status,
                          uint64_t* status_summary, void* workspace, size_t ws_bytes, void* stream);
+
+/* Residual only: rss_rows[i] = sum over row i's ratings of (y - source[idx] . rows_w[i])^2,
+ * fp64 (the fused residual of the final iteration, _kernels.py:219-230). */
+int cals_residual(const cals_side* side, const float* source, int ld_src, int n_f, const float* rows_w, int ld_w,
+                  double* rss_rows, void* stream);
 
 /* Deterministic fp64 sum of an array (fixed reduction tree). out: 1 double. */
 int cals_sum_f64(const double* x, int64_t n, double* out, void* workspace, size_t ws_bytes,

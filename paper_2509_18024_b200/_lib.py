@@ -27,7 +27,7 @@ class cals_side(ctypes.Structure):
 class cals_plan(ctypes.Structure):
     _fields_ = [
         ("budget", P), ("small_rows", P), ("n_small", i64),
-        ("small_seg", i64 * 4), ("small_seg_maxn", ctypes.c_int32 * 3),
+        ("small_seg", i64 * 4), ("small_seg_maxn", ctypes.c_int32 * 3), ("small_seg_maxs", ctypes.c_int32 * 3),
         ("big_rows", P), ("n_big", i64), ("big_tile_ptr", P), ("n_big_tiles", i64),
         ("big_cand_ptr", P), ("big_cand_total", i64), ("item_rows", ctypes.c_int32),
         ("n_f", ctypes.c_int32),
@@ -40,7 +40,8 @@ SIGNATURES = {
     "cals_plan_build": (i32, [P, i64, i32, f64, P, P, P, P, P, ctypes.POINTER(cals_plan)]),
     "cals_workspace_bytes": (sz, [ctypes.POINTER(cals_plan)]),
     "cals_core_half_sweep": (i32, [ctypes.POINTER(cals_side), ctypes.POINTER(cals_plan), P, i64, i32, i32, f64,
-                                   P, i32, P, P, P, P, P, sz, P]),
+                                   P, i32, P, i32, P, P, P, P, P, P, sz, P]),
+    "cals_residual": (i32, [ctypes.POINTER(cals_side), P, i32, i32, P, i32, P, P]),
     "cals_sum_f64": (i32, [P, i64, P, P, sz, P]),
     "cals_weighted_sqnorm": (i32, [P, i64, i32, i32, P, P, P, sz, P]),
     "cals_ces_sketch": (i32, [P, i64, i32, ctypes.c_int32, P, P, P, sz, P]),

@@ -212,28 +212,39 @@ def fit_core(R, cfg, *, init_u=None, init_m=None, items_first=False, engine=None
     ssq = eng.ssq
     obj_trace, rmse_trace = [], []
     converged = False
-    iters = 0
-    prev = None
     first = "item" if items_first else "user"
     second = "user" if items_first else "item"
     sides = {"user": eng.user, "item": eng.item}
-    t_loop = 0.0
-    for it in range(cfg.max_iters):
-        t0 = time.perf_counter()
-        terms = eng.iterate(first)
-        t_loop += time.perf_counter() - t0
-        _raise_for(terms.status_first, first, sides[first], it)
-        _raise_for(terms.status_second, second, sides[second], it)
-        obj = terms.rss + (cfg.lam * (terms.pen_u + terms.pen_m) if cfg.lam != 0.0 else 0.0)
+    prev = [None]
+
+    def consume(t):
+        """obj/rmse of iteration t (als.py:299-307); True when converged there."""
+        terms = eng.terms(t)
+        _raise_for(terms.status_first, first, sides[first], t)
+        _raise_for(terms.status_second, second, sides[second], t)
+        obj = terms.rss + (cfg.lam * terms.pen if cfg.lam != 0.0 else 0.0)
         obj_trace.append(obj)
         rmse_trace.append(np.sqrt(terms.rss / ssq) if ssq > 0 else 0.0)
-        iters = it + 1
-        if prev is not None:
-            rel = abs(obj - prev) / max(prev, np.finfo(np.float64).tiny)
-            if rel < cfg.tol:
-                converged = True
-                break
-        prev = obj
+        done = False
+        if prev[0] is not None:
+            rel = abs(obj - prev[0]) / max(prev[0], np.finfo(np.float64).tiny)
+            done = rel < cfg.tol
+        prev[0] = obj
+        return done
+
+    t0 = time.perf_counter()
+    for it in range(cfg.max_iters):
+        eng.step(first)  # iteration it; its first half also yields the residual of it-1
+        if it >= 1 and consume(it - 1):
+            converged = True
+            eng.rewind()  # the factors of iteration it-1 are the result
+            break
+    if not converged and eng.iters_done > 0:
+        eng.finish(first)
+        converged = consume(eng.iters_done - 1)
+    torch.cuda.current_stream().synchronize()
+    t_loop = time.perf_counter() - t0
+    iters = eng.iters_done
     U, M = eng.factors_host()
     report = FitReport(
         method=cfg.method,

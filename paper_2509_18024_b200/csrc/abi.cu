@@ -70,18 +70,26 @@ struct ProfScope {
 
 inline float delta_tab_for(int QS) { return 3.0f * 0.5f / std::sqrt((float)QS); }
 
-int small_nmax(int nf) {
-    int lo = 1, hi = 1 << 16;
+constexpr size_t kSmallSmem = 110 * 1024;  // staged-tier CTA budget: two CTAs per SM
+
+inline int budget_of(int64_t n, double rate) {
+    volatile double prod = (double)n * rate;
+    int64_t s = (int64_t)std::floor(prod + 1e-9);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(s, n));
+}
+
+int small_nmax(int nf, double rate) {
+    int lo = 1, hi = 1 << 15;
     while (lo < hi) {
-        int mid = (lo + hi + 1) / 2;
-        if (T1Layout(mid, nf, kThreads).total <= kSmemBudget) lo = mid; else hi = mid - 1;
+        const int mid = (lo + hi + 1) / 2;
+        if (T1Layout(mid, budget_of(mid, rate), nf, kThreads).total <= kSmallSmem) lo = mid; else hi = mid - 1;
     }
     return std::min(lo, 65535);
 }
 
 int big_chunk(int nf) {
     // largest power of two whose staged chunk fits ~96 KB alongside mask/G/scratch
-    const size_t per = (size_t)xs_stride(nf) * 4;
+    const size_t per = (size_t)xs_stride(nf) * 4 + 4 + (size_t)((nf + 31) / 32) * 4;
     int ch = 1024;
     while (ch > 64 && (size_t)ch * per > 96 * 1024) ch >>= 1;
     return ch;
@@ -89,8 +97,8 @@ int big_chunk(int nf) {
 
 size_t big_gram_smem(int nf, int chunk) {
     const int sx = xs_stride(nf), mw = (nf + 31) / 32;
-    return align16((size_t)chunk * sx * 4) + align16((size_t)chunk * mw * 4) + align16((size_t)nf * (nf + 1) * 4) +
-           (size_t)kThreads * 16 * 4;
+    return align16((size_t)chunk * sx * 4) + align16((size_t)chunk * 4) + align16((size_t)chunk * mw * 4) +
+           align16((size_t)nf * (nf + 1) * 4) + (size_t)kThreads * 16 * 4;
 }
 
 int64_t cand_cap(int64_t n, float delta_tab) {
@@ -149,9 +157,9 @@ void allow_smem(K kernel) {
 }
 
 template <typename K>
-int grid_for(K kernel, size_t smem, int64_t work, int cap_per_sm = 8) {
+int grid_for(K kernel, size_t smem, int64_t work, int cap_per_sm = 8, int threads = kThreads) {
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
     occ = std::max(1, std::min(occ, cap_per_sm));
     int64_t g = (int64_t)std::min(dev().sms, 160) * occ;
     return (int)std::max<int64_t>(1, std::min<int64_t>(g, work));
@@ -172,13 +180,22 @@ struct Work {
     uint64_t* cand;
     uint64_t* thr;
     float* part;
-    float* wbig;
     double* rss_part;
     double* retry;
+    float* gbuf;
+    int64_t gbuf_rows;
 };
 
-constexpr int kMaxGrid = 160 * 8;  // grid_for never exceeds min(SMs, 160) * 8 CTAs
+constexpr int kMaxGrid = 160 * 16;  // grid_for never exceeds min(SMs, 160) * 16 CTAs
 inline int retry_stride(int nf) { return ((nf * (nf + 1) + nf) + 31) & ~31; }
+constexpr int64_t kMaxSolveWarps = 160 * 4 * 8;  // solve_warp_kernel grid cap (4 CTAs of 8 warps per SM)
+
+// Normal-equation batch: rows solved per phase-A/phase-B launch pair (<= ~1 GiB).
+int64_t gbuf_rows_for(int nf, int64_t rows) {
+    const int64_t per = (int64_t)nf * (nf + 1) * 4;
+    const int64_t cap = std::max<int64_t>(4096, ((int64_t)1 << 30) / per);
+    return std::max<int64_t>(1, std::min<int64_t>(cap, rows));
+}
 
 Work carve(const cals_plan* P, void* ws, size_t* total) {
     Carve c(ws);
@@ -189,26 +206,50 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
     w.cand = c.take<uint64_t>((size_t)P->big_cand_total);
     w.thr = c.take<uint64_t>((size_t)P->n_big * nf);
     w.part = c.take<float>((size_t)P->n_big_tiles * nf * (nf + 1));
-    w.wbig = c.take<float>((size_t)P->n_big * nf);
     w.rss_part = c.take<double>((size_t)P->n_big_tiles);
-    w.retry = c.take<double>((size_t)kMaxGrid * retry_stride(nf));
+    w.retry = c.take<double>((size_t)std::max<int64_t>(kMaxGrid, kMaxSolveWarps) * retry_stride(nf));
+    w.gbuf_rows = gbuf_rows_for(nf, P->n_small + P->n_big);
+    w.gbuf = c.take<float>((size_t)w.gbuf_rows * nf * (nf + 1));
     *total = c.off + 256;
     return w;
 }
 
 template <int NFP>
-int launch_small(const SweepArgs& A, const cals_plan* P, cudaStream_t st) {
-    allow_smem(small_sweep_kernel<NFP>);
+void launch_solve(const SweepArgs& A, const int32_t* rows, int64_t count, cudaStream_t st) {
+    if (count <= 0) return;
+    ProfScope ps("solve_kernel", st);
+    if constexpr (NFP > 0) {
+        const int64_t blocks = std::min<int64_t>((count + 7) / 8, kMaxSolveWarps / 8);
+        solve_warp_kernel<NFP><<<(int)blocks, 256, 0, st>>>(A, rows, count);
+    } else {
+        const size_t smem = align16((size_t)A.nf * (A.nf + 1) * 4);
+        allow_smem(solve_block_kernel);
+        const int grid = grid_for(solve_block_kernel, smem, count, 16, 128);
+        solve_block_kernel<<<std::min(grid, kMaxGrid), 128, smem, st>>>(A, rows, count);
+    }
+}
+
+template <int NFP>
+int launch_small(SweepArgs A, const cals_plan* P, const Work& w, cudaStream_t st) {
+    allow_smem(small_gram_kernel);
     for (int g = 0; g < 3; ++g) {
         const int64_t b = P->small_seg[g], e = P->small_seg[g + 1];
         if (e <= b) continue;
         const int N = P->small_seg_maxn[g];
-        const size_t smem = T1Layout(N, A.nf, kThreads).total;
-        const int grid = grid_for(small_sweep_kernel<NFP>, smem, e - b);
-        ProfScope ps("small_sweep_kernel", st);
-        small_sweep_kernel<NFP><<<grid, kThreads, smem, st>>>(A, P->small_rows + b, e - b, N);
+        const int S = P->small_seg_maxs[g];
+        const int threads = N <= 256 ? 128 : 256;
+        const size_t smem = T1Layout(N, S, A.nf, threads).total;
+        for (int64_t b0 = b; b0 < e; b0 += w.gbuf_rows) {
+            const int64_t cnt = std::min<int64_t>(w.gbuf_rows, e - b0);
+            const int grid = grid_for(small_gram_kernel, smem, cnt, 16, threads);
+            {
+                ProfScope ps("small_gram_kernel", st);
+                small_gram_kernel<<<grid, threads, smem, st>>>(A, P->small_rows + b0, cnt, N, S);
+            }
+            launch_solve<NFP>(A, P->small_rows + b0, cnt, st);
+        }
     }
-    return cuda_status("small_sweep_kernel");
+    return cuda_status("small tier");
 }
 
 template <int NFP>
@@ -226,7 +267,6 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
     B.cand = w.cand;
     B.thr = w.thr;
     B.part = w.part;
-    B.wbig = w.wbig;
     B.rss_part = w.rss_part;
     cudaMemsetAsync(w.cnt, 0, sizeof(int) * (size_t)P->n_big * nf * 2, st);
     const size_t scan_smem = align16((size_t)B.chunk * xs_stride(nf) * 4);
@@ -247,17 +287,13 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
         ProfScope ps("big_gram_kernel", st);
         big_gram_kernel<<<grid_for(big_gram_kernel, gram_smem, B.n_tiles), kThreads, gram_smem, st>>>(A, B);
     }
-    const size_t solve_smem = 2 * align16((size_t)nf * (nf + 1) * 4);
-    allow_smem(big_solve_kernel<NFP>);
-    {
-        ProfScope ps("big_solve_kernel", st);
-        big_solve_kernel<NFP><<<grid_for(big_solve_kernel<NFP>, solve_smem, B.n_big), kThreads, solve_smem, st>>>(A, B);
-    }
-    if (A.rss_rows != nullptr) {
-        ProfScope ps("big_rss_kernel", st);
-        big_rss_kernel<<<grid_for(big_rss_kernel, 0, B.n_tiles), kThreads, 0, st>>>(A, B);
-        const int64_t blocks = (B.n_big + 255) / 256;
-        big_rss_reduce_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(blocks, 1024)), 256, 0, st>>>(A, B);
+    for (int64_t r0 = 0; r0 < B.n_big; r0 += w.gbuf_rows) {
+        const int64_t cnt = std::min<int64_t>(w.gbuf_rows, B.n_big - r0);
+        {
+            ProfScope ps("big_reduce_kernel", st);
+            big_reduce_kernel<<<(int)std::min<int64_t>(cnt, (int64_t)dev().sms * 8), kThreads, 0, st>>>(A, B, r0, cnt);
+        }
+        launch_solve<NFP>(A, P->big_rows + r0, cnt, st);
     }
     return cuda_status("big-row kernels");
 }
@@ -289,7 +325,7 @@ int cals_plan_build(const int64_t* counts, int64_t n_rows, int n_f, double rate,
     if (rc) return rc;
     std::memset(meta, 0, sizeof(*meta));
     meta->n_f = n_f;
-    const int nmax = small_nmax(n_f);
+    const int nmax = small_nmax(n_f, rate);
     std::vector<int32_t> small, big;
     for (int64_t i = 0; i < n_rows; ++i) {
         if (counts[i] <= 0) continue;
@@ -310,7 +346,12 @@ int cals_plan_build(const int64_t* counts, int64_t n_rows, int n_f, double rate,
         const int64_t lo_bound = (g < 2) ? thresholds[g + 1] : 0;
         meta->small_seg[g] = pos;
         meta->small_seg_maxn[g] = pos < (int64_t)small.size() ? (int32_t)counts[small[pos]] : 1;
-        while (pos < (int64_t)small.size() && counts[small[pos]] > lo_bound) ++pos;
+        meta->small_seg_maxs[g] = 1;
+        while (pos < (int64_t)small.size() && counts[small[pos]] > lo_bound) {
+            const int32_t sr = budget[small[pos]];
+            if (sr < counts[small[pos]]) meta->small_seg_maxs[g] = std::max(meta->small_seg_maxs[g], sr);
+            ++pos;
+        }
     }
     meta->small_seg[3] = pos;
     // big rows: work items and candidate buffers
@@ -337,10 +378,14 @@ size_t cals_workspace_bytes(const cals_plan* plan) {
 }
 
 int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float* source, int64_t n_src, int ld_src,
-                         int n_f, double lam, float* target, int ld_tgt, double* rss_rows, uint64_t* thr_keys,
-                         int32_t* row_status, uint64_t* status_summary, void* ws, size_t ws_bytes, void* stream) {
+                         int n_f, double lam, float* target, int ld_tgt, const float* target_old, int ld_old,
+                         double* rss_rows, double* pen_rows, uint64_t* thr_keys, int32_t* row_status,
+                         uint64_t* status_summary, void* ws, size_t ws_bytes, void* stream) {
     if (!side || !P || !source || !target || !row_status) return CALS_ERR_ARG;
-    if (n_f < 1 || n_f > CALS_MAX_NF || n_f != P->n_f || ld_src < n_f || ld_tgt < n_f || lam < 0) return CALS_ERR_ARG;
+    if (rss_rows && (!target_old || ld_old < n_f)) return CALS_ERR_ARG;
+    if (n_f < 1 || n_f > CALS_MAX_NF || n_f != P->n_f || ld_src < 4 * xs_chunks(n_f) || (ld_src & 3) || ld_tgt < n_f ||
+        lam < 0 || ((uintptr_t)source & 15))
+        return CALS_ERR_ARG;
     if ((P->n_small && !P->small_rows) || (P->n_big && (!P->big_rows || !P->big_tile_ptr || !P->big_cand_ptr)) ||
         !P->budget)
         return CALS_ERR_ARG;
@@ -363,8 +408,12 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.tgt = target;
     A.ld_tgt = ld_tgt;
     A.lam = lam;
+    A.tgt_old = target_old;
+    A.ld_old = ld_old;
     A.rss_rows = rss_rows;
+    A.pen_rows = pen_rows;
     A.thr_keys = thr_keys;
+    A.gbuf = w.gbuf;
     A.status = row_status;
     A.summary = reinterpret_cast<unsigned long long*>(status_summary);
     A.qtab = nullptr;
@@ -386,10 +435,10 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     }
     int rc = CALS_OK;
     if (P->n_small > 0) {
-        if (n_f <= 8) rc = launch_small<8>(A, P, st);
-        else if (n_f <= 16) rc = launch_small<16>(A, P, st);
-        else if (n_f <= 32) rc = launch_small<32>(A, P, st);
-        else rc = launch_small<0>(A, P, st);
+        if (n_f <= 8) rc = launch_small<8>(A, P, w, st);
+        else if (n_f <= 16) rc = launch_small<16>(A, P, w, st);
+        else if (n_f <= 32) rc = launch_small<32>(A, P, w, st);
+        else rc = launch_small<0>(A, P, w, st);
         if (rc) return rc;
     }
     if (P->n_big > 0) {
@@ -399,6 +448,17 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
         else rc = launch_big<0>(A, P, w, st);
     }
     return rc;
+}
+
+int cals_residual(const cals_side* side, const float* source, int ld_src, int n_f, const float* rows_w, int ld_w,
+                  double* rss_rows, void* stream) {
+    if (!side || !source || !rows_w || !rss_rows || n_f < 1 || ld_src < n_f || ld_w < n_f) return CALS_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((side->n_rows + 7) / 8, (int64_t)dev().sms * 16));
+    ProfScope ps("residual_kernel", st);
+    residual_kernel<<<(int)blocks, 256, 0, st>>>(side->ptr, side->idx, side->val, side->n_rows, source, ld_src, n_f,
+                                                rows_w, ld_w, rss_rows);
+    return cuda_status("cals_residual");
 }
 
 int cals_sum_f64(const double* x, int64_t n, double* out, void* ws, size_t ws_bytes, void* stream) {

@@ -13,42 +13,55 @@
 
 namespace cals {
 
-// Must be called by all threads of the block.  Xs: n rows, stride sx
-// (y in column nf, zero padding up to sx).  mb: n * mw mask words.
+// One 4x4 tile (rows c0..c0+3, columns f0..f0+3 of [X | y]) over k = kbeg, kbeg+kstep, ...
+__device__ __forceinline__ void gram_tile(const float* __restrict__ Xs, int sx, const float* __restrict__ ys,
+                                          const uint32_t* __restrict__ mb, int mw, int n, int nf, int c0, int f0,
+                                          int kbeg, int kstep, float (&acc)[4][4]) {
+    const int wsel = c0 >> 5, sh = c0 & 31;
+    const int yslot = nf - f0;  // component of the B tile that is the response (if in [0, 4))
+    const bool bx = f0 < 4 * xs_chunks(nf);  // staged data chunks only (padding beyond is not staged)
+    (void)sx;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+#pragma unroll 4
+    for (int k = kbeg; k < n; k += kstep) {
+        const float4 av = *reinterpret_cast<const float4*>(Xs + (size_t)k * sx + c0);
+        float4 bv = bx ? *reinterpret_cast<const float4*>(Xs + (size_t)k * sx + f0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (yslot >= 0 && yslot < 4) {
+            const float yk = ys[k];
+            bv.x = yslot == 0 ? yk : bv.x;
+            bv.y = yslot == 1 ? yk : bv.y;
+            bv.z = yslot == 2 ? yk : bv.z;
+            bv.w = yslot == 3 ? yk : bv.w;
+        }
+        const uint32_t m = mb[k * mw + wsel] >> sh;
+        const float a[4] = {(m & 1u) ? av.x : 0.f, (m & 2u) ? av.y : 0.f, (m & 4u) ? av.z : 0.f,
+                            (m & 8u) ? av.w : 0.f};
+        const float b[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+}
+
+// Must be called by all threads of the block.  Xs: n rows, stride sx (zero
+// padding beyond nf), ys: n responses, mb: n * mw mask words.
 // Writes (or adds into) G (nf x (nf+1), row stride nf+1).  scratch: >= blockDim*16 floats.
-__device__ void tile_gram(const float* __restrict__ Xs, int sx, const uint32_t* __restrict__ mb, int mw,
-                          int n, int nf, float* __restrict__ G, float* __restrict__ scratch,
-                          bool accumulate = false) {
+__device__ void tile_gram(const float* __restrict__ Xs, int sx, const float* __restrict__ ys,
+                          const uint32_t* __restrict__ mb, int mw, int n, int nf, float* __restrict__ G,
+                          float* __restrict__ scratch, bool accumulate = false) {
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int RB = (nf + 3) >> 2, CB = sx >> 2, NB = RB * CB;
     const int gs = nf + 1;
+    const int RB = (nf + 3) >> 2, CB = (gs + 3) >> 2, NB = RB * CB;
     if (NB <= nt) {
         const int KG = nt / NB;
         if (tid < NB * KG) {
             const int bid = tid % NB, kg = tid / NB;
-            const int c0 = (bid / CB) * 4, f0 = (bid % CB) * 4;
-            const int wsel = c0 >> 5, sh = c0 & 31;
             float acc[4][4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-#pragma unroll 4
-            for (int k = kg; k < n; k += KG) {
-                const float4 av = *reinterpret_cast<const float4*>(Xs + (size_t)k * sx + c0);
-                const float4 bv = *reinterpret_cast<const float4*>(Xs + (size_t)k * sx + f0);
-                const uint32_t m = mb[k * mw + wsel] >> sh;
-                const float a0 = (m & 1u) ? av.x : 0.f;
-                const float a1 = (m & 2u) ? av.y : 0.f;
-                const float a2 = (m & 4u) ? av.z : 0.f;
-                const float a3 = (m & 8u) ? av.w : 0.f;
-                const float a[4] = {a0, a1, a2, a3};
-                const float b[4] = {bv.x, bv.y, bv.z, bv.w};
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-            }
+            gram_tile(Xs, sx, ys, mb, mw, n, nf, (bid / CB) * 4, (bid % CB) * 4, kg, KG, acc);
             float* out = scratch + (size_t)(kg * NB + bid) * 16;
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -68,24 +81,8 @@ __device__ void tile_gram(const float* __restrict__ Xs, int sx, const uint32_t* 
     } else {
         for (int bid = tid; bid < NB; bid += nt) {
             const int c0 = (bid / CB) * 4, f0 = (bid % CB) * 4;
-            const int wsel = c0 >> 5, sh = c0 & 31;
             float acc[4][4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-            for (int k = 0; k < n; ++k) {
-                const float4 av = *reinterpret_cast<const float4*>(Xs + (size_t)k * sx + c0);
-                const float4 bv = *reinterpret_cast<const float4*>(Xs + (size_t)k * sx + f0);
-                const uint32_t m = mb[k * mw + wsel] >> sh;
-                const float a[4] = {(m & 1u) ? av.x : 0.f, (m & 2u) ? av.y : 0.f, (m & 4u) ? av.z : 0.f,
-                                    (m & 8u) ? av.w : 0.f};
-                const float b[4] = {bv.x, bv.y, bv.z, bv.w};
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-            }
+            gram_tile(Xs, sx, ys, mb, mw, n, nf, c0, f0, 0, 1, acc);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -98,20 +95,123 @@ __device__ void tile_gram(const float* __restrict__ Xs, int sx, const uint32_t* 
     }
 }
 
-// Selection bitmap: bit c of mb[k*mw + c/32] = (key(k, c) >= thr[c]).
-__device__ void build_mask(const float* __restrict__ Xs, int sx, int n, int nf, const uint64_t* thr,
-                           bool full, uint32_t* __restrict__ mb, int mw) {
-    for (int e = threadIdx.x; e < n * mw; e += blockDim.x) {
-        const int k = e / mw, w = e - k * mw;
-        const int cbeg = w * 32, cend = min(nf, cbeg + 32);
-        uint32_t bits = 0;
-        if (full) {
-            bits = (cend - cbeg == 32) ? 0xffffffffu : ((1u << (cend - cbeg)) - 1u);
-        } else {
-            for (int c = cbeg; c < cend; ++c)
-                if (make_key(Xs[(size_t)k * sx + c], (uint32_t)k) >= thr[c]) bits |= 1u << (c - cbeg);
+// Selection bitmap: bit c of mb[k*mw + c/32] = (key(k0 + k, c) >= thr[c]).
+// Lanes run along columns (conflict-free row reads), ballots form the words;
+// for nf <= 16 several rows share a warp.
+__device__ void build_mask(const float* __restrict__ Xs, int sx, int n, int nf, const uint64_t* thr, bool full,
+                           uint32_t* __restrict__ mb, int mw, int k0 = 0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    int P = 32;
+    if (nf <= 16) P = nf <= 1 ? 1 : (nf <= 2 ? 2 : (nf <= 4 ? 4 : (nf <= 8 ? 8 : 16)));
+    const int rpw = 32 / P, sub = lane / P, cl = lane - sub * P;
+    const uint32_t fieldmask = P == 32 ? 0xffffffffu : ((1u << P) - 1u);
+    for (int base = warp * rpw; base < n; base += nwarps * rpw) {
+        const int k = base + sub;
+        for (int w = 0; w < mw; ++w) {
+            const int c = w * 32 + cl;
+            bool bit = false;
+            if (k < n && c < nf)
+                bit = full || make_key(Xs[(size_t)k * sx + c], (uint32_t)(k0 + k)) >= thr[c];
+            const uint32_t bal = __ballot_sync(CALS_FULL_MASK, bit);
+            if (cl == 0 && k < n) mb[k * mw + w] = (bal >> (sub * P)) & fieldmask;
         }
-        mb[e] = bits;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Sparse sketched normal equations (algorithmic flop count): for every column
+// c, G[c][:] = sum_{k in S_c} X[k][c] * [X[k][:] | y[k]] over the kept rows
+// S_c only (_kernels.py:132-145).  A warp task owns CT columns; its lanes are
+// (column slot, q-group, chunk lane): LPC lanes per column each own CPL
+// 16-byte chunks of the row (interleaved, so the lanes of one column read one
+// contiguous row segment), QG q-groups split the kept-row list round-robin and
+// are reduced with shuffles in a fixed order; lane (fl == 0) also owns b[c].
+// Kept-row lists (ascending k) are built from the selection bitmap by the
+// same warp.  Writes rows of G (+lam_n on the diagonal) to Gout (row stride nf+1).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void sparse_gram_warp(const float* __restrict__ Xs, int sx, const float* __restrict__ ys,
+                                                 const uint32_t* __restrict__ mb, int mw, int n, int nf, int s,
+                                                 bool full, uint16_t* __restrict__ lists, int Smax, float lam_n,
+                                                 float* __restrict__ Gout, int warp, int nwarps, int lane) {
+    const int nq = xs_chunks(nf);
+    const int LPC = nq < 4 ? nq : 4;
+    const int CPL = (nq + LPC - 1) / LPC;  // <= 8 for nf <= 128
+    int CT = (nf + nwarps - 1) / nwarps;    // columns per task: power of two, CT * LPC <= 32
+    CT = CT <= 1 ? 1 : (CT <= 2 ? 2 : (CT <= 4 ? 4 : (CT <= 8 ? 8 : (CT <= 16 ? 16 : 32))));
+    while (CT * LPC > 32) CT >>= 1;
+    const int QG = 32 / (CT * LPC);         // power of two
+    const int cs = lane / (QG * LPC);
+    const int qg = (lane / LPC) % QG;
+    const int fl = lane % LPC;
+    const int gs = nf + 1;
+    const int ntask = (nf + CT - 1) / CT;
+    for (int task = warp; task < ntask; task += nwarps) {
+        const int cbase = task * CT;
+        const int c = cbase + cs;
+        const bool cvalid = c < nf;
+        if (!full) {
+            // lists of the task's columns from the bitmap (CT columns share one word)
+            int cnt = 0;  // lane cc keeps column cbase+cc's running count
+            const int wsel = cbase >> 5, sh = cbase & 31;
+            for (int k0 = 0; k0 < n; k0 += 32) {
+                const int k = k0 + lane;
+                const uint32_t word = k < n ? (mb[k * mw + wsel] >> sh) : 0u;
+                for (int cc = 0; cc < CT && cbase + cc < nf; ++cc) {
+                    const bool bit = (word >> cc) & 1u;
+                    const uint32_t bal = __ballot_sync(CALS_FULL_MASK, bit);
+                    const int base = __shfl_sync(CALS_FULL_MASK, cnt, cc);
+                    if (bit) lists[(cbase + cc) * Smax + base + __popc(bal & lanemask_lt())] = (uint16_t)k;
+                    if (lane == cc) cnt += __popc(bal);
+                }
+            }
+            __syncwarp();
+        }
+        const int len = full ? n : s;
+        const uint16_t* L = lists + (size_t)(cvalid ? c : cbase) * Smax;
+        float acc[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+        float accb = 0.f;
+        for (int q = qg; q < len; q += QG) {
+            const int k = full ? q : (int)L[q];
+            const float xc = cvalid ? Xs[(size_t)k * sx + c] : 0.f;
+            const float* xr = Xs + (size_t)k * sx;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int ch = fl + i * LPC;
+                if (i < CPL && ch < nq) {
+                    const float4 v = *reinterpret_cast<const float4*>(xr + 4 * ch);
+                    acc[4 * i + 0] = fmaf(xc, v.x, acc[4 * i + 0]);
+                    acc[4 * i + 1] = fmaf(xc, v.y, acc[4 * i + 1]);
+                    acc[4 * i + 2] = fmaf(xc, v.z, acc[4 * i + 2]);
+                    acc[4 * i + 3] = fmaf(xc, v.w, acc[4 * i + 3]);
+                }
+            }
+            if (fl == 0) accb = fmaf(xc, ys[k], accb);
+        }
+        // fixed-order reduction over the q-groups (lane bits LPC .. LPC*QG)
+        for (int o = LPC; o < LPC * QG; o <<= 1) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (i < 4 * CPL) acc[i] += __shfl_xor_sync(CALS_FULL_MASK, acc[i], o);
+            accb += __shfl_xor_sync(CALS_FULL_MASK, accb, o);
+        }
+        if (cvalid && qg == 0) {
+            float* grow = Gout + (size_t)c * gs;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int ch = fl + i * LPC;
+                if (i < CPL && ch < nq) {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int f = 4 * ch + t;
+                        if (f < nf) grow[f] = acc[4 * i + t] + ((f == c) ? lam_n : 0.f);
+                    }
+                }
+            }
+            if (fl == 0) grow[nf] = accb;
+        }
+        __syncwarp();
     }
 }
 

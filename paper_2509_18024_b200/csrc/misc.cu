@@ -48,6 +48,31 @@ __global__ void __launch_bounds__(256) finish_sum_kernel(const double* __restric
     if (threadIdx.x == 0) out[0] = acc;
 }
 
+// ---- residual only (the fused residual of the last iteration) -------------
+// rss_rows[i] = sum_k (y_k - source[idx_k] . w_i)^2 over row i's ratings,
+// one warp per row, float64 accumulation (_kernels.py:219-230).
+__global__ void __launch_bounds__(256) residual_kernel(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                                                       const float* __restrict__ val, int64_t n_rows,
+                                                       const float* __restrict__ src, int ld_src, int nf,
+                                                       const float* __restrict__ w, int ld_w, double* rss_rows) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = gw; r < n_rows; r += stride) {
+        const int64_t lo = ptr[r], hi = ptr[r + 1];
+        double acc = 0.0;
+        for (int64_t e = lo + lane; e < hi; e += 32) {
+            const float* x = src + (int64_t)idx[e] * ld_src;
+            double pred = 0.0;
+            for (int f = 0; f < nf; ++f) pred = fma((double)x[f], (double)w[r * ld_w + f], pred);
+            const double d = (double)val[e] - pred;
+            acc = fma(d, d, acc);
+        }
+        acc = warp_sum_d(acc);
+        if (lane == 0) rss_rows[r] = acc;
+    }
+}
+
 // ---- public sketch (core.py:95-115) -------------------------------------
 // One warp per column.  ws: p * n keys.
 __global__ void __launch_bounds__(256) ces_sketch_kernel(const float* __restrict__ X, int n, int p, int s,

@@ -13,7 +13,7 @@
 // the candidate range (the bracket ends are candidates), so the loop always
 // terminates; the final <= 32 candidates are sorted and indexed directly.
 #pragma once
-#include "common.cuh"
+#include "sweep_common.cuh"
 
 namespace cals {
 
@@ -99,6 +99,61 @@ __device__ uint64_t warp_select_idx(IdxList<IdxT> L, int m, int need, uint64_t l
         lo = rlo;
         hi = rhi;
     }
+}
+
+// Pre-narrow an index list whose keys all lie in [lo, hi) using the quantile
+// table levels between jhi and jlo as ready-made splitters (no sampling or
+// sorting): one counting pass with kSub-1 ballots per chunk picks the
+// sub-bucket holding the target rank, one pass compacts it.
+template <typename IdxT>
+__device__ void warp_prenarrow(IdxList<IdxT>& L, int& m, int& need, uint64_t& lo, uint64_t& hi,
+                               const uint32_t* qtab_c, int jhi, int jlo, int lane) {
+    const int span = jlo - jhi;
+    if (span < 2 || m <= 32) return;
+    uint32_t lev[kSub - 1];
+    int cnt[kSub - 1];
+#pragma unroll
+    for (int i = 0; i < kSub - 1; ++i) {
+        lev[i] = qtab_c[jhi + (span * (i + 1)) / kSub];
+        cnt[i] = 0;
+    }
+    for (int i0 = 0; i0 < m; i0 += 32) {
+        const int i = i0 + lane;
+        const bool v = i < m;
+        const uint32_t a = v ? (uint32_t)(L.key(i) >> 32) : 0u;
+#pragma unroll
+        for (int t = 0; t < kSub - 1; ++t) cnt[t] += __popc(__ballot_sync(CALS_FULL_MASK, v && a >= lev[t]));
+    }
+    int b = 0;
+#pragma unroll
+    for (int t = 0; t < kSub - 1; ++t) b += (cnt[t] < need) ? 1 : 0;  // counts are non-decreasing in t
+    int above = 0, upto = m;
+    uint64_t nhi = hi, nlo = lo;
+#pragma unroll
+    for (int t = 0; t < kSub - 1; ++t) {
+        if (t == b - 1) { above = cnt[t]; nhi = (uint64_t)lev[t] << 32; }
+        if (t == b) { upto = cnt[t]; nlo = (uint64_t)lev[t] << 32; }
+    }
+    if (nhi > hi) nhi = hi;
+    if (nlo < lo) nlo = lo;
+    int w = 0;
+    for (int i0 = 0; i0 < m; i0 += 32) {
+        const int i = i0 + lane;
+        const bool v = i < m;
+        const uint32_t e = v ? L.elem(i) : 0u;
+        const uint64_t kk = v ? L.key_of_elem(e) : 0ull;
+        const bool in = v && kk >= nlo && kk < nhi;
+        const uint32_t bal = __ballot_sync(CALS_FULL_MASK, in);
+        if (in) L.put(w + __popc(bal & lanemask_lt()), e);
+        w += __popc(bal);
+    }
+    __syncwarp();
+    L.identity = false;
+    m = w;
+    (void)upto;
+    need -= above;
+    lo = nlo;
+    hi = nhi;
 }
 
 // Warp-level select on a key list (in place).

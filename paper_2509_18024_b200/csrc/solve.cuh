@@ -148,44 +148,58 @@ __device__ int block_lu_solve(T* W, int nf, bool spd, T* x_out, int* s_piv) {
     return __syncthreads_or(bad);
 }
 
-// Solve one sketched system with the reference's failure semantics.
-// All threads of the block call it.  G: fp32 augmented matrix in shared
-// memory (left intact).  Fast path: warp-register LU (NFP > 0) or block LU in
-// shared memory on Wf (NFP == 0).  On failure: float64 retry with the
-// diagonal jitter 1e-10*tr(G)/nf (core.py:126-131 / als.py:191-197) on Wd
-// (global scratch, nf*(nf+1) + nf doubles per CTA).  Returns CALS_ROW_*.
-template <int NFP>
-__device__ int solve_row(const float* G, int nf, bool spd, float* wv, float* Wf, double* Wd, int* s_piv,
-                         int* s_flag) {
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-    const int gs = nf + 1, nout = nf * gs;
-    if constexpr (NFP > 0) {
-        if (warp == 0) {
-            const int bad = warp_lu_solve<NFP>(G, gs, nf, spd, wv, lane);
-            if (lane == 0) s_flag[0] = bad;
-        }
-        __syncthreads();
-    } else {
-        for (int e = tid; e < nout; e += nt) Wf[e] = G[e];
-        __syncthreads();
-        const int bad = block_lu_solve<float>(Wf, nf, spd, wv, s_piv);
-        if (tid == 0) s_flag[0] = bad;
-        __syncthreads();
-    }
-    if (!s_flag[0]) return CALS_ROW_OK;
+// Float64 retry of a failed system with the reference's diagonal jitter
+// 1e-10 * tr(G) / nf (core.py:126-131, als.py:191-197).  One warp, lanes over
+// columns, scratch W (nf*(nf+1) doubles, any memory).  Rare path.
+__device__ int warp_retry_f64(const float* G, int nf, bool spd, double* W, double* x, int lane) {
+    const int gs = nf + 1;
     double tr = 0.0;
     for (int c = 0; c < nf; ++c) tr += (double)G[c * gs + c];
     const double jit = 1e-10 * tr / (double)nf;
-    double* xd = Wd + nout;
-    for (int e = tid; e < nout; e += nt) {
+    for (int e = lane; e < nf * gs; e += 32) {
         const int c = e / gs, f = e - c * gs;
-        Wd[e] = (double)G[e] + ((c == f) ? jit : 0.0);
+        W[e] = (double)G[e] + ((c == f) ? jit : 0.0);
     }
-    __syncthreads();
-    const int bad = block_lu_solve<double>(Wd, nf, spd, xd, s_piv);
-    for (int f = tid; f < nf; f += nt) wv[f] = (float)xd[f];
-    __syncthreads();
-    return bad ? CALS_ROW_SINGULAR : CALS_ROW_JITTERED;
+    __syncwarp();
+    for (int k = 0; k < nf; ++k) {
+        int p = k;
+        if (!spd) {
+            double best = -1.0;
+            for (int r = k; r < nf; ++r) {
+                const double v = fabs(W[r * gs + k]);
+                if (v > best) { best = v; p = r; }
+            }
+            if (!(best > 0.0)) return 1;
+        } else if (!(W[k * gs + k] > 0.0)) {
+            return 1;
+        }
+        if (p != k) {
+            for (int jj = lane; jj < gs; jj += 32) {
+                const double t = W[k * gs + jj];
+                W[k * gs + jj] = W[p * gs + jj];
+                W[p * gs + jj] = t;
+            }
+            __syncwarp();
+        }
+        const double d = W[k * gs + k];
+        for (int r = k + 1; r < nf; ++r) {
+            const double f = W[r * gs + k] / d;
+            __syncwarp();
+            for (int jj = k + 1 + lane; jj < gs; jj += 32) W[r * gs + jj] -= f * W[k * gs + jj];
+            __syncwarp();
+        }
+    }
+    int bad = 0;
+    if (lane == 0) {
+        for (int r = nf - 1; r >= 0; --r) {
+            double acc = W[r * gs + nf];
+            for (int jj = r + 1; jj < nf; ++jj) acc -= W[r * gs + jj] * x[jj];
+            x[r] = acc / W[r * gs + r];
+            if (!(x[r] == x[r]) || (x[r] - x[r] != 0.0)) bad = 1;
+        }
+    }
+    __syncwarp();
+    return __shfl_sync(CALS_FULL_MASK, bad, 0);
 }
 
 }  // namespace cals

@@ -9,9 +9,10 @@
 //   big_resolve  one warp per (row, column): exact s-th key from the list
 //                (warp sample-select), or from the whole column if the
 //                bracket missed (fallback, always correct)
-//   big_gram     masked partial Gram per item (fixed-order partials)
-//   big_solve    fixed-order fp64 sum of the partials, + lam*n*I, LU / SPD
-//   big_rss      fused residual of the new row (item side)
+//   big_gram     masked partial Gram per item (fixed-order partials), plus the
+//                item's share of the fused residual of the previous row
+//   big_reduce   fixed-order fp64 sum of the partials, + lam*n*I -> normal
+//                equations for the batched solve (sweep_solve.cu)
 #include "gram.cuh"
 #include "select.cuh"
 #include "solve.cuh"
@@ -29,25 +30,6 @@ __device__ __forceinline__ int find_row(const int64_t* tile_ptr, int64_t n_big, 
     return (int)lo;
 }
 
-// Stage slice rows [k0, k0+kn) of the row starting at rating `lo` into Xs.
-__device__ __forceinline__ void stage_chunk(const SweepArgs& A, int64_t lo, int k0, int kn, float* Xs, int sx,
-                                            const FastDiv& fdiv, bool with_y) {
-    const int nf = A.nf, nt = blockDim.x;
-    const int nel = kn * nf;
-#pragma unroll 4
-    for (int e = threadIdx.x; e < nel; e += nt) {
-        const int k = (int)fdiv.div((uint32_t)e);
-        const int c = e - k * nf;
-        Xs[k * sx + c] = __ldg(A.src + (int64_t)__ldg(A.idx + lo + k0 + k) * A.ld_src + c);
-    }
-    if (with_y) {
-        for (int k = threadIdx.x; k < kn; k += nt) {
-            Xs[k * sx + nf] = __ldg(A.val + lo + k0 + k);
-            for (int c = nf + 1; c < sx; ++c) Xs[k * sx + c] = 0.f;
-        }
-    }
-}
-
 __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs B) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_above[CALS_MAX_NF_DEV], s_in[CALS_MAX_NF_DEV], s_base[CALS_MAX_NF_DEV],
@@ -56,7 +38,7 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
     const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x;
     const int sx = xs_stride(nf);
     float* Xs = reinterpret_cast<float*>(smem);
-    const FastDiv fdiv((uint32_t)nf);
+    const FastDiv fq((uint32_t)xs_chunks(nf));
     for (int64_t t = blockIdx.x; t < B.n_tiles; t += gridDim.x) {
         const int r = find_row(B.tile_ptr, B.n_big, t);
         const int row = B.rows[r];
@@ -79,7 +61,7 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
         for (int k0 = kbeg; k0 < kend; k0 += B.chunk) {
             const int kn = min(B.chunk, kend - k0);
             __syncthreads();
-            stage_chunk(A, lo, k0, kn, Xs, sx, fdiv, false);
+            stage_slice(A, lo, k0, kn, Xs, nullptr, fq);
             if (tid < nf) s_slot[tid] = 0;
             __syncthreads();
             const int per = nt / nf;
@@ -184,13 +166,16 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
 __global__ void __launch_bounds__(kThreads) big_gram_kernel(SweepArgs A, BigArgs B) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t s_thr[CALS_MAX_NF_DEV];
+    __shared__ float wold[CALS_MAX_NF_DEV];
+    __shared__ double red[32];
     const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x;
     const int sx = xs_stride(nf), mw = (nf + 31) / 32, gs = nf + 1;
     float* Xs = reinterpret_cast<float*>(smem);
-    uint32_t* mb = reinterpret_cast<uint32_t*>(smem + align16((size_t)B.chunk * sx * 4));
+    float* ys = reinterpret_cast<float*>(smem + align16((size_t)B.chunk * sx * 4));
+    uint32_t* mb = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(ys) + align16((size_t)B.chunk * 4));
     float* G = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(mb) + align16((size_t)B.chunk * mw * 4));
     float* scratch = G + align16((size_t)nf * gs * 4) / 4;
-    const FastDiv fdiv((uint32_t)nf);
+    const FastDiv fq((uint32_t)xs_chunks(nf));
     for (int64_t t = blockIdx.x; t < B.n_tiles; t += gridDim.x) {
         const int r = find_row(B.tile_ptr, B.n_big, t);
         const int row = B.rows[r];
@@ -200,106 +185,63 @@ __global__ void __launch_bounds__(kThreads) big_gram_kernel(SweepArgs A, BigArgs
         const int kbeg = (int)(t - B.tile_ptr[r]) * B.item_rows;
         const int kend = min(n, kbeg + B.item_rows);
         __syncthreads();
-        if (tid < nf) s_thr[tid] = B.thr[(size_t)r * nf + tid];
+        if (tid < nf) {
+            s_thr[tid] = B.thr[(size_t)r * nf + tid];
+            if (A.tgt_old != nullptr) wold[tid] = A.tgt_old[(int64_t)row * A.ld_old + tid];
+        }
         const int nout = nf * gs;
         bool first = true;
+        double racc = 0.0;
         for (int k0 = kbeg; k0 < kend; k0 += B.chunk) {
             const int kn = min(B.chunk, kend - k0);
             __syncthreads();
-            stage_chunk(A, lo, k0, kn, Xs, sx, fdiv, true);
+            stage_slice(A, lo, k0, kn, Xs, ys, fq);
             __syncthreads();
-            // mask with slice-row ids relative to the whole row (keys carry them)
-            for (int e = tid; e < kn * mw; e += nt) {
-                const int k = e / mw, w = e - k * mw;
-                const int cb = w * 32, ce = min(nf, cb + 32);
-                uint32_t bits = 0;
-                if (full) bits = (ce - cb == 32) ? 0xffffffffu : ((1u << (ce - cb)) - 1u);
-                else
-                    for (int c = cb; c < ce; ++c)
-                        if (make_key(Xs[k * sx + c], (uint32_t)(k0 + k)) >= s_thr[c]) bits |= 1u << (c - cb);
-                mb[e] = bits;
+            if (A.rss_rows != nullptr) {
+                for (int k = tid; k < kn; k += nt) {
+                    double pred = 0.0;
+                    for (int f = 0; f < nf; ++f) pred = fma((double)Xs[k * sx + f], (double)wold[f], pred);
+                    const double d = (double)ys[k] - pred;
+                    racc = fma(d, d, racc);
+                }
             }
+            build_mask(Xs, sx, kn, nf, s_thr, full, mb, mw, k0);
             __syncthreads();
-            tile_gram(Xs, sx, mb, mw, kn, nf, G, scratch, !first);
+            tile_gram(Xs, sx, ys, mb, mw, kn, nf, G, scratch, !first);
             first = false;
         }
         float* out = B.part + (size_t)t * nout;
         for (int e = tid; e < nout; e += nt) out[e] = G[e];
+        if (A.rss_rows != nullptr) {
+            racc = block_sum_d(racc, red);
+            if (tid == 0) B.rss_part[t] = racc;
+        }
     }
 }
 
-template <int NFP>
-__global__ void __launch_bounds__(kThreads) big_solve_kernel(SweepArgs A, BigArgs B) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ float wv[CALS_MAX_NF_DEV];
-    __shared__ int s_piv[1], s_stat[1];
-    const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-    const int gs = nf + 1, nout = nf * gs;
-    float* G = reinterpret_cast<float*>(smem);
-    float* W = G + align16((size_t)nout * 4) / 4;
-    for (int64_t r = blockIdx.x; r < B.n_big; r += gridDim.x) {
+// Big rows [r0, r0 + count): fixed-order float64 sum of the item partials,
+// + lam*n*I on the diagonal -> A.gbuf slot (r - r0); residual partial sums.
+__global__ void __launch_bounds__(kThreads) big_reduce_kernel(SweepArgs A, BigArgs B, int64_t r0, int64_t count) {
+    const int nf = A.nf, gs = nf + 1, nout = nf * gs;
+    for (int64_t q = blockIdx.x; q < count; q += gridDim.x) {
+        const int64_t r = r0 + q;
         const int row = B.rows[r];
         const int n = (int)(A.ptr[row + 1] - A.ptr[row]);
-        const bool full = A.budget[row] >= n;
         const int64_t t0 = B.tile_ptr[r], t1 = B.tile_ptr[r + 1];
         const float lam_n = (float)(A.lam * (double)n);
-        __syncthreads();
-        for (int e = tid; e < nout; e += nt) {
+        float* G = A.gbuf + (size_t)q * nout;
+        for (int e = threadIdx.x; e < nout; e += blockDim.x) {
             double v = 0.0;
             for (int64_t t = t0; t < t1; ++t) v += (double)B.part[(size_t)t * nout + e];
             const int c = e / gs, f = e - c * gs;
             G[e] = (float)v + ((c == f) ? lam_n : 0.f);
         }
-        __syncthreads();
-        const int st = solve_row<NFP>(G, nf, full, wv, W, A.retry_ws + (size_t)blockIdx.x * A.retry_stride, s_piv,
-                                      s_stat);
-        for (int f = tid; f < nf; f += nt) {
-            if (st != CALS_ROW_SINGULAR) A.tgt[(int64_t)row * A.ld_tgt + f] = wv[f];
-            B.wbig[(size_t)r * nf + f] = wv[f];
+        if (A.rss_rows != nullptr && threadIdx.x == 0) {
+            double v = 0.0;
+            for (int64_t t = t0; t < t1; ++t) v += B.rss_part[t];
+            A.rss_rows[row] = v;
         }
-        if (tid == 0) { A.status[row] = st; report_status(A, row, st); }
     }
 }
-
-__global__ void __launch_bounds__(kThreads) big_rss_kernel(SweepArgs A, BigArgs B) {
-    __shared__ double red[32];
-    __shared__ float w[CALS_MAX_NF_DEV];
-    const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x;
-    for (int64_t t = blockIdx.x; t < B.n_tiles; t += gridDim.x) {
-        const int r = find_row(B.tile_ptr, B.n_big, t);
-        const int row = B.rows[r];
-        const int64_t lo = A.ptr[row];
-        const int n = (int)(A.ptr[row + 1] - lo);
-        const int kbeg = (int)(t - B.tile_ptr[r]) * B.item_rows;
-        const int kend = min(n, kbeg + B.item_rows);
-        __syncthreads();
-        for (int f = tid; f < nf; f += nt) w[f] = B.wbig[(size_t)r * nf + f];
-        __syncthreads();
-        double acc = 0.0;
-        for (int k = kbeg + tid; k < kend; k += nt) {
-            const float* xr = A.src + (int64_t)__ldg(A.idx + lo + k) * A.ld_src;
-            double pred = 0.0;
-            for (int f = 0; f < nf; ++f) pred = fma((double)__ldg(xr + f), (double)w[f], pred);
-            const double d = (double)__ldg(A.val + lo + k) - pred;
-            acc = fma(d, d, acc);
-        }
-        acc = block_sum_d(acc, red);
-        if (tid == 0) B.rss_part[t] = acc;
-    }
-}
-
-__global__ void big_rss_reduce_kernel(SweepArgs A, BigArgs B) {
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < B.n_big; r += (int64_t)gridDim.x * blockDim.x) {
-        const int row = B.rows[r];
-        double v = 0.0;
-        for (int64_t t = B.tile_ptr[r]; t < B.tile_ptr[r + 1]; ++t) v += B.rss_part[t];
-        A.rss_rows[row] = (A.status[row] == CALS_ROW_SINGULAR) ? 0.0 : v;
-    }
-}
-
-template __global__ void big_solve_kernel<8>(SweepArgs, BigArgs);
-template __global__ void big_solve_kernel<16>(SweepArgs, BigArgs);
-template __global__ void big_solve_kernel<32>(SweepArgs, BigArgs);
-template __global__ void big_solve_kernel<0>(SweepArgs, BigArgs);
 
 }  // namespace cals

@@ -5,9 +5,10 @@
 namespace cals {
 
 #define CALS_MAX_NF_DEV 128
-constexpr int kThreads = 256;       // threads per sweep CTA
+constexpr int kThreads = 256;       // max threads per sweep CTA (launch bound)
 constexpr int kCap = 256;           // per-column candidate capacity (shared-memory tier)
 constexpr int kQ = 256;             // quantile-table resolution (levels per column)
+constexpr int kSub = 8;             // sub-buckets used to pre-narrow a bracket
 constexpr uint32_t kAbsInf = 0x80000000u;  // sentinel above every abs_bits value
 
 struct SweepArgs {
@@ -17,19 +18,23 @@ struct SweepArgs {
     const int32_t* budget;
     const float* src;
     int64_t n_src;
-    int ld_src;
+    int ld_src;   // multiple of 4 (16-byte rows for cp.async gathers)
     int nf;
-    float* tgt;
+    float* tgt;            // solved rows (the new target matrix)
     int ld_tgt;
+    const float* tgt_old;  // previous-iteration rows for the fused residual (nullable)
+    int ld_old;
     double lam;
-    double* rss_rows;      // nullable
+    double* rss_rows;      // residual of tgt_old rows per regression (nullable)
+    double* pen_rows;      // n_i * |w_i|^2 of the new rows (nullable)
     uint64_t* thr_keys;    // nullable
     int32_t* status;
     const uint32_t* qtab;  // [nf][kQ+1] abs-bit quantiles of the source, or null
     float delta_tab;       // quantile-table sampling margin (rank units)
     unsigned long long* summary;  // nullable: max over rows of (status << 32 | ~row)
-    double* retry_ws;             // per-CTA float64 jitter-retry scratch (retry_stride doubles each)
+    double* retry_ws;             // per-warp float64 jitter-retry scratch (retry_stride doubles each)
     int retry_stride;
+    float* gbuf;                  // normal equations of the current batch: [slot][nf][nf+1]
 };
 
 __device__ __forceinline__ void report_status(const SweepArgs& A, int row, int st) {
@@ -55,19 +60,31 @@ struct BigArgs {
 };
 
 __host__ __device__ inline int round_up4(int x) { return (x + 3) & ~3; }
-__host__ __device__ inline int xs_stride(int nf) { return round_up4(nf + 1); }  // X | y | pad
+// Staged row stride (floats): 16-byte aligned rows for cp.async / LDS.128,
+// padded so that consecutive rows start in different bank groups.
+__host__ __device__ inline int xs_stride(int nf) {
+    const int r = round_up4(nf);
+    return (r % 8 == 0) ? r + 4 : r;
+}
+__host__ __device__ inline int xs_chunks(int nf) { return (nf + 3) >> 2; }  // 16-byte chunks holding data
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-// Bracket [lob, hib) in abs-bit space around the target rank of a row,
-// read from the column's quantile table.  Keys >= (hib << 32) are "above".
-__device__ __forceinline__ void table_bracket(const uint32_t* qtab_c, int n, int s, float delta_tab,
-                                              uint32_t& hib, uint32_t& lob) {
-    float p = (float)s / (float)n;
-    float d = 3.0f * sqrtf(p * (1.0f - p) / (float)n) + delta_tab + 0.5f / (float)kQ;
-    int jhi = (int)floorf((p - d) * (float)kQ);
-    int jlo = (int)ceilf((p + d) * (float)kQ);
+// Table levels [jhi, jlo] around the target rank of a row:
+// keys with abs_bits >= qtab[jhi] are "above", the bracket is
+// [qtab[jlo], qtab[jhi]).  Margin: 3 binomial sigmas + table sampling error.
+__device__ __forceinline__ void table_levels(int n, int s, float delta_tab, int& jhi, int& jlo) {
+    const float p = (float)s / (float)n;
+    const float d = 3.0f * sqrtf(p * (1.0f - p) / (float)n) + delta_tab + 0.5f / (float)kQ;
+    jhi = (int)floorf((p - d) * (float)kQ);
+    jlo = (int)ceilf((p + d) * (float)kQ);
     jhi = jhi < 0 ? 0 : (jhi > kQ ? kQ : jhi);
     jlo = jlo < 0 ? 0 : (jlo > kQ ? kQ : jlo);
+}
+
+__device__ __forceinline__ void table_bracket(const uint32_t* qtab_c, int n, int s, float delta_tab,
+                                              uint32_t& hib, uint32_t& lob) {
+    int jhi, jlo;
+    table_levels(n, s, delta_tab, jhi, jlo);
     hib = qtab_c[jhi];
     lob = qtab_c[jlo];
 }
@@ -76,24 +93,54 @@ __device__ __forceinline__ uint64_t hi_key_of(uint32_t hib) {
     return hib >= kAbsInf ? ~0ull : ((uint64_t)hib << 32);
 }
 
-// Shared-memory footprint of the staged-slice kernel for rows of length <= N.
+// cp.async 16-byte global -> shared copy (L2-only caching: gathers are streamed)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
+// Stage slice rows [k0, k0 + kn) of the regression whose ratings start at
+// `lo`: X rows (16-byte chunks, cp.async) into Xs (stride sx) and y into ys.
+// The caller synchronises the block afterwards.
+__device__ __forceinline__ void stage_slice(const SweepArgs& A, int64_t lo, int k0, int kn, float* Xs, float* ys,
+                                            const FastDiv& fq) {
+    const int sx = xs_stride(A.nf), nq = xs_chunks(A.nf);
+    const int nt = blockDim.x;
+    const int nel = kn * nq;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < nel; e += nt) {
+        const int k = (int)fq.div((uint32_t)e);
+        const int q = e - k * nq;
+        const int64_t r = __ldg(A.idx + lo + k0 + k);
+        cp_async16(Xs + k * sx + 4 * q, A.src + r * A.ld_src + 4 * q);
+    }
+    if (ys != nullptr)
+        for (int k = threadIdx.x; k < kn; k += nt) ys[k] = __ldg(A.val + lo + k0 + k);
+    cp_async_wait_all();
+}
+
+// Shared-memory footprint of the staged-slice kernel for rows of length <= N
+// whose sketch budget is <= S (lists) -- regions reused across phases:
+//   Xs [N][sx] | ys [N] | mb [N][mw] bitmap | R = max(candidates, lists) | scratch
 struct T1Layout {
-    size_t xs, cand, mb, g, w, scratch, region, total;
+    size_t xs, ys, mb, cand, lists, region, scratch, total;
     int sx, mw;
-    __host__ __device__ T1Layout(int N, int nf, int threads) {
+    __host__ __device__ T1Layout(int N, int S, int nf, int threads) {
         sx = xs_stride(nf);
         mw = (nf + 31) / 32;
         xs = align16((size_t)N * sx * sizeof(float));
-        cand = align16((size_t)nf * kCap * sizeof(uint16_t));
+        ys = align16((size_t)N * sizeof(float));
         mb = align16((size_t)N * mw * sizeof(uint32_t));
-        g = align16((size_t)nf * (nf + 1) * sizeof(float));
-        w = nf > 32 ? g : 0;
-        scratch = align16((size_t)threads * 16 * sizeof(float));
-        size_t after = mb + g + w + scratch;
-        region = cand > after ? cand : after;
-        total = xs + region;
+        cand = align16((size_t)nf * kCap * sizeof(uint16_t));
+        lists = align16((size_t)nf * (S > 0 ? S : 1) * sizeof(uint16_t));
+        region = cand > lists ? cand : lists;
+        scratch = align16((size_t)(threads / 32) * kCap * sizeof(uint16_t));
+        total = xs + ys + mb + region + scratch;
     }
 };
 
 }  // namespace cals
-

@@ -1,22 +1,24 @@
 // sweep_small.cu -- the staged-slice (shared-memory) tier of the half-sweep,
 // plus the per-sweep quantile table that seeds its selection brackets.
 //
-// One CTA per regression (persistent over a length-sorted row list):
-//   gather  X = source[idx] and y into shared memory          (core.py:215,220)
-//   select  per column the s_i largest keys                    (_kernels.py:26-120)
-//   gram    G = (P.X)^T X + lam*n*I, b = (P.X)^T y              (_kernels.py:123-146)
-//   solve   LU with partial pivoting / SPD when s_i == n_i      (core.py:120-131, als.py:184-205)
-//   write   target[i] = w; fused residual on the item side      (als.py:286-288, _kernels.py:219-230)
+// Phase A (this file), one CTA per regression, persistent over a
+// length-sorted row list:
+//   stage   X = source[idx] (cp.async, 16-byte rows) and y into shared memory
+//                                                              (core.py:215,220)
+//   resid   optional fused residual of the PREVIOUS iteration's row of this
+//           regression: sum_k (y_k - X_k . w_old)^2            (_kernels.py:219-230)
+//   select  per column the s_i largest keys -> selection bitmap (_kernels.py:26-120)
+//   gram    sparse G = X*^T X + lam*n*I, b = X*^T y -> global  (_kernels.py:123-146)
+// Phase B (sweep_solve.cu) solves the batch of normal equations.
 #include "gram.cuh"
 #include "select.cuh"
-#include "solve.cuh"
 #include "sweep_common.cuh"
 
 namespace cals {
 
 // ---------------------------------------------------------------------------
 // Quantile table: per column, abs-bit quantiles of the source values seen by
-// this side's ratings (a rating-weighted sample, QS deterministic positions).
+// this side's ratings (a rating-weighted sample at QS deterministic positions).
 // qtab[c][0] = kAbsInf (nothing above), qtab[c][kQ] = 0 (everything >= 0).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(1024) quantile_table_kernel(const int32_t* __restrict__ idx, int64_t nnz,
@@ -30,14 +32,13 @@ __global__ void __launch_bounds__(1024) quantile_table_kernel(const int32_t* __r
         sbuf[i] = abs_bits(src[(int64_t)idx[pos] * ld + c]);
     }
     __syncthreads();
-    // bitonic sort, descending
-    for (int size = 2; size <= QS; size <<= 1) {
+    for (int size = 2; size <= QS; size <<= 1) {  // bitonic sort, descending
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int i = threadIdx.x; i < QS / 2; i += blockDim.x) {
-                int lo = 2 * i - (i & (stride - 1));
-                int hi = lo + stride;
-                bool desc = (lo & size) == 0;
-                uint32_t a = sbuf[lo], b = sbuf[hi];
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool desc = (lo & size) == 0;
+                const uint32_t a = sbuf[lo], b = sbuf[hi];
                 if ((a < b) == desc) { sbuf[lo] = b; sbuf[hi] = a; }
             }
             __syncthreads();
@@ -53,33 +54,66 @@ __global__ void __launch_bounds__(1024) quantile_table_kernel(const int32_t* __r
     }
 }
 
+// Threshold key of column c (warp-level, see select.cuh).  `cl` holds the
+// column's bracket candidates (left intact), `scr` is this warp's scratch.
+__device__ __forceinline__ uint64_t resolve_column(const SweepArgs& A, const float* Xs, int sx, int c, int n, int s,
+                                                   bool use_tab, int above, int in, const uint16_t* cl,
+                                                   uint16_t* scr, bool& fallback, int lane) {
+    fallback = false;
+    if (!use_tab) {
+        IdxList<uint16_t> Lst{Xs, sx, c, scr, true};
+        return warp_select_idx(Lst, n, s, 0ull, ~0ull, lane);
+    }
+    const uint32_t* qc = A.qtab + (size_t)c * (kQ + 1);
+    int jhi, jlo;
+    table_levels(n, s, A.delta_tab, jhi, jlo);
+    const uint32_t hib = qc[jhi], lob = qc[jlo];
+    uint64_t hik = hi_key_of(hib), lok = (uint64_t)lob << 32;
+    if (above < s && s <= above + in && in <= kCap && lok < hik) {
+        for (int i = lane; i < in; i += 32) scr[i] = cl[i];
+        __syncwarp();
+        IdxList<uint16_t> Lst{Xs, sx, c, scr, false};
+        int m = in, need = s - above;
+        warp_prenarrow(Lst, m, need, lok, hik, qc, jhi, jlo, lane);
+        return warp_select_idx(Lst, m, need, lok, hik, lane);
+    }
+    // the table bracket missed (or overflowed): exact column-mode search
+    fallback = true;
+    uint64_t rlo, rhi;
+    int m, need;
+    if (above >= s) { rlo = hik; rhi = ~0ull; m = above; need = s; }
+    else if (above + in < s) { rlo = 0ull; rhi = lok; m = n - above - in; need = s - above - in; }
+    else { rlo = lok; rhi = hik; m = in; need = s - above; }
+    auto keyat = [Xs, sx, c](int k) { return make_key(Xs[k * sx + c], (uint32_t)k); };
+    return warp_select_column(keyat, n, m, need, rlo, rhi, reinterpret_cast<uint64_t*>(scr),
+                              (kCap * (int)sizeof(uint16_t)) / 8, lane);
+}
+
 // ---------------------------------------------------------------------------
-// Staged-slice half-sweep kernel.
-// NFP: 8/16/32 -> warp-register LU; 0 -> block LU in shared memory (nf > 32).
+// Phase A kernel (blockDim 128 or 256).  rows / n_list: this batch; the
+// normal equations of rows[li] go to A.gbuf + li * nf * (nf+1).
+// N: longest row of the batch; S: largest budget among its incomplete rows.
 // ---------------------------------------------------------------------------
-template <int NFP>
-__global__ void __launch_bounds__(kThreads, 2) small_sweep_kernel(SweepArgs A, const int32_t* __restrict__ rows,
-                                                               int64_t n_list, int N) {
+__global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, const int32_t* __restrict__ rows,
+                                                                 int64_t n_list, int N, int S) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int cnt_above[CALS_MAX_NF_DEV], cnt_in[CALS_MAX_NF_DEV];
     __shared__ uint64_t thr[CALS_MAX_NF_DEV];
-    __shared__ float wv[CALS_MAX_NF_DEV];
+    __shared__ float wold[CALS_MAX_NF_DEV];
     __shared__ double red[32];
-    __shared__ int s_piv[1];
-    __shared__ int s_stat[1];
 
     const int nf = A.nf;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
-    const T1Layout L(N, nf, nt);
+    const T1Layout L(N, S, nf, nt);
     const int sx = L.sx, mw = L.mw, gs = nf + 1;
     float* Xs = reinterpret_cast<float*>(smem);
-    unsigned char* R = smem + L.xs;
-    uint16_t* cand = reinterpret_cast<uint16_t*>(R);
-    uint32_t* mb = reinterpret_cast<uint32_t*>(R);
-    float* G = reinterpret_cast<float*>(R + L.mb);
-    float* W = reinterpret_cast<float*>(R + L.mb + L.g);
-    float* scratch = reinterpret_cast<float*>(R + L.mb + L.g + L.w);
-    const FastDiv fdiv((uint32_t)nf);
+    float* ys = reinterpret_cast<float*>(smem + L.xs);
+    uint32_t* mb = reinterpret_cast<uint32_t*>(smem + L.xs + L.ys);
+    uint16_t* cand = reinterpret_cast<uint16_t*>(smem + L.xs + L.ys + L.mb);
+    uint16_t* lists = cand;  // reused once the thresholds are known
+    uint16_t* wscr = reinterpret_cast<uint16_t*>(smem + L.xs + L.ys + L.mb + L.region) + warp * kCap;
+    const FastDiv fq((uint32_t)xs_chunks(nf));
+    const bool ballot_bits = (32 % nf == 0) || (nf % 32 == 0);
 
     for (int64_t li = blockIdx.x; li < n_list; li += gridDim.x) {
         const int row = rows[li];
@@ -88,83 +122,100 @@ __global__ void __launch_bounds__(kThreads, 2) small_sweep_kernel(SweepArgs A, c
         const int s = A.budget[row];
         const bool full = (s >= n);
 
-        // ---- gather the slice [X | y] (coalesced within each source row) ----
-        const int nel = n * nf;
-#pragma unroll 4
-        for (int e = tid; e < nel; e += nt) {
-            const int k = (int)fdiv.div((uint32_t)e);
-            const int c = e - k * nf;
-            Xs[k * sx + c] = __ldg(A.src + (int64_t)__ldg(A.idx + lo + k) * A.ld_src + c);
+        // ---- stage the slice [X | y]; clear the bitmap ----
+        stage_slice(A, lo, 0, n, Xs, ys, fq);
+        for (int e = tid; e < n * mw; e += nt) mb[e] = 0u;
+        if (tid < nf) {
+            cnt_above[tid] = 0;
+            cnt_in[tid] = 0;
+            if (A.tgt_old != nullptr) wold[tid] = A.tgt_old[(int64_t)row * A.ld_old + tid];
         }
-        for (int k = tid; k < n; k += nt) {
-            Xs[k * sx + nf] = __ldg(A.val + lo + k);
-            for (int c = nf + 1; c < sx; ++c) Xs[k * sx + c] = 0.f;
-        }
-        if (tid < nf) { cnt_above[tid] = 0; cnt_in[tid] = 0; }
         __syncthreads();
 
-        // ---- selection: threshold key per column ----
+        // ---- fused residual of the previous iteration's row (als.py:287-288) ----
+        if (A.rss_rows != nullptr) {
+            double acc = 0.0;
+            for (int k = tid; k < n; k += nt) {
+                double pred = 0.0;
+                for (int f = 0; f < nf; ++f) pred = fma((double)Xs[k * sx + f], (double)wold[f], pred);
+                const double d = (double)ys[k] - pred;
+                acc = fma(d, d, acc);
+            }
+            acc = block_sum_d(acc, red);
+            if (tid == 0) A.rss_rows[row] = acc;
+        }
+
+        // ---- selection: threshold key per column, kept-set bitmap ----
         if (!full) {
             const bool use_tab = (n > kCap) && (A.qtab != nullptr);
             if (use_tab) {
-                const int per = nt / nf;  // threads per column
-                if (tid < per * nf) {
-                    const int c = tid % nf, j = tid / nf;
-                    uint32_t hib, lob;
-                    table_bracket(A.qtab + (size_t)c * (kQ + 1), n, s, A.delta_tab, hib, lob);
-                    int above = 0;
-                    uint16_t* cl = cand + c * kCap;
-                    for (int k = j; k < n; k += per) {
-                        const uint32_t a = abs_bits(Xs[k * sx + c]);
-                        above += (a >= hib);
-                        if (a >= lob && a < hib) {
-                            int slot = atomicAdd(&cnt_in[c], 1);
-                            if (slot < kCap) cl[slot] = (uint16_t)k;
-                        }
+                // one pass: keys above the table bracket go straight into the
+                // bitmap (ballots), keys inside it are listed per column
+                const int per = nt / nf;
+                const int c = tid % nf, j = tid / nf;
+                uint32_t hib = kAbsInf, lob = kAbsInf;
+                if (tid < per * nf) table_bracket(A.qtab + (size_t)c * (kQ + 1), n, s, A.delta_tab, hib, lob);
+                uint16_t* cl = cand + c * kCap;
+                int above = 0;
+                const int iters = (n + per - 1) / per;
+                const int rsh = (lane / (nf <= 32 ? nf : 32)) * nf;
+                const uint32_t rmask = nf >= 32 ? 0xffffffffu : ((1u << nf) - 1u);
+                const bool writer = nf <= 32 ? (c == 0) : (lane == 0);
+                for (int it = 0; it < iters; ++it) {
+                    const int k = j + it * per;
+                    const bool ok = (tid < per * nf) && k < n;
+                    const uint32_t a = ok ? abs_bits(Xs[k * sx + c]) : 0u;
+                    const bool ab = ok && a >= hib;
+                    above += ab;
+                    if (ok && a >= lob && a < hib) {
+                        const int slot = atomicAdd(&cnt_in[c], 1);
+                        if (slot < kCap) cl[slot] = (uint16_t)k;
                     }
-                    atomicAdd(&cnt_above[c], above);
+                    if (ballot_bits) {
+                        const uint32_t bal = __ballot_sync(CALS_FULL_MASK, ab);
+                        if (writer && ok) mb[k * mw + (c >> 5)] = (bal >> rsh) & rmask;
+                    } else if (ab) {
+                        atomicOr(&mb[k * mw + (c >> 5)], 1u << (c & 31));
+                    }
                 }
+                if (tid < per * nf) atomicAdd(&cnt_above[c], above);
                 __syncthreads();
             }
             for (int c = warp; c < nf; c += nwarps) {
-                uint64_t T;
-                uint16_t* cl = cand + c * kCap;
-                if (!use_tab) {
-                    IdxList<uint16_t> Lst{Xs, sx, c, cl, true};
-                    T = warp_select_idx(Lst, n, s, 0ull, ~0ull, lane);
+                bool fallback;
+                const uint64_t T = resolve_column(A, Xs, sx, c, n, s, use_tab, cnt_above[c], cnt_in[c],
+                                                  cand + c * kCap, wscr, fallback, lane);
+                if (lane == 0) thr[c] = T;
+                const uint32_t bit = 1u << (c & 31);
+                uint32_t* mcol = mb + (c >> 5);
+                if (!use_tab || fallback) {
+                    // (re)derive column c entirely: kept iff key >= T
+                    for (int k = lane; k < n; k += 32) {
+                        const bool keep = make_key(Xs[k * sx + c], (uint32_t)k) >= T;
+                        if (keep) atomicOr(mcol + k * mw, bit);
+                        else if (fallback) atomicAnd(mcol + k * mw, ~bit);
+                    }
                 } else {
-                    uint32_t hib, lob;
-                    table_bracket(A.qtab + (size_t)c * (kQ + 1), n, s, A.delta_tab, hib, lob);
-                    const uint64_t hik = hi_key_of(hib), lok = (uint64_t)lob << 32;
-                    const int above = cnt_above[c], in = cnt_in[c];
-                    if (above < s && s <= above + in && in <= kCap && lok < hik) {
-                        IdxList<uint16_t> Lst{Xs, sx, c, cl, false};
-                        T = warp_select_idx(Lst, in, s - above, lok, hik, lane);
-                    } else {
-                        uint64_t rlo, rhi;
-                        int m, need;
-                        if (above >= s) { rlo = hik; rhi = ~0ull; m = above; need = s; }
-                        else if (above + in < s) { rlo = 0ull; rhi = lok; m = n - above - in; need = s - above - in; }
-                        else { rlo = lok; rhi = hik; m = in; need = s - above; }
-                        const float* Xc = Xs;
-                        auto keyat = [Xc, sx, c](int k) { return make_key(Xc[k * sx + c], (uint32_t)k); };
-                        T = warp_select_column(keyat, n, m, need, rlo, rhi, reinterpret_cast<uint64_t*>(cl),
-                                               (kCap * (int)sizeof(uint16_t)) / 8, lane);
+                    // bracket candidates at or above the threshold join the kept set
+                    const int in = cnt_in[c];
+                    const uint16_t* cl = cand + c * kCap;
+                    for (int i = lane; i < in; i += 32) {
+                        const int k = cl[i];
+                        if (make_key(Xs[k * sx + c], (uint32_t)k) >= T) atomicOr(mcol + k * mw, bit);
                     }
                 }
-                if (lane == 0) thr[c] = T;
             }
         } else if (A.thr_keys != nullptr) {
             // complete sketch: every row kept; report the smallest key per column
             for (int c = warp; c < nf; c += nwarps) {
                 uint64_t mn = ~0ull;
                 for (int k = lane; k < n; k += 32) {
-                    uint64_t kk = make_key(Xs[k * sx + c], (uint32_t)k);
+                    const uint64_t kk = make_key(Xs[k * sx + c], (uint32_t)k);
                     mn = kk < mn ? kk : mn;
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
-                    uint64_t t = __shfl_xor_sync(CALS_FULL_MASK, mn, o);
+                    const uint64_t t = __shfl_xor_sync(CALS_FULL_MASK, mn, o);
                     mn = t < mn ? t : mn;
                 }
                 if (lane == 0) thr[c] = mn;
@@ -172,43 +223,14 @@ __global__ void __launch_bounds__(kThreads, 2) small_sweep_kernel(SweepArgs A, c
         }
         __syncthreads();
 
-        // ---- mask + Gram ----
-        build_mask(Xs, sx, n, nf, thr, full, mb, mw);
-        __syncthreads();
-        tile_gram(Xs, sx, mb, mw, n, nf, G, scratch);
+        // ---- sparse Gram -> global normal equations ----
         const float lam_n = (float)(A.lam * (double)n);
-        for (int c = tid; c < nf; c += nt) G[c * gs + c] += lam_n;
-        __syncthreads();
-
-        // ---- solve ----
-        const int st = solve_row<NFP>(G, nf, full, wv, W, A.retry_ws + (size_t)blockIdx.x * A.retry_stride, s_piv,
-                                      s_stat);
-
-        // ---- write back, residual, diagnostics ----
-        if (st != CALS_ROW_SINGULAR)
-            for (int f = tid; f < nf; f += nt) A.tgt[(int64_t)row * A.ld_tgt + f] = wv[f];
-        if (tid == 0) { A.status[row] = st; report_status(A, row, st); }
+        sparse_gram_warp(Xs, sx, ys, mb, mw, n, nf, s, full, lists, S > 0 ? S : 1, lam_n,
+                         A.gbuf + (size_t)li * nf * gs, warp, nwarps, lane);
         if (A.thr_keys != nullptr)
             for (int c = tid; c < nf; c += nt) A.thr_keys[(int64_t)row * nf + c] = thr[c];
-        if (A.rss_rows != nullptr) {
-            double acc = 0.0;
-            for (int k = tid; k < n; k += nt) {
-                double pred = 0.0;
-                for (int f = 0; f < nf; ++f) pred = fma((double)Xs[k * sx + f], (double)wv[f], pred);
-                const double d = (double)Xs[k * sx + nf] - pred;
-                acc = fma(d, d, acc);
-            }
-            acc = block_sum_d(acc, red);
-            if (tid == 0) A.rss_rows[row] = (st == CALS_ROW_SINGULAR) ? 0.0 : acc;
-        }
         __syncthreads();
     }
 }
-
-// explicit instantiations used by the launcher
-template __global__ void small_sweep_kernel<8>(SweepArgs, const int32_t*, int64_t, int);
-template __global__ void small_sweep_kernel<16>(SweepArgs, const int32_t*, int64_t, int);
-template __global__ void small_sweep_kernel<32>(SweepArgs, const int32_t*, int64_t, int);
-template __global__ void small_sweep_kernel<0>(SweepArgs, const int32_t*, int64_t, int);
 
 }  // namespace cals

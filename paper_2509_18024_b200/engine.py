@@ -3,29 +3,32 @@ alternating loop (/root/reference/pkg/src/coreals/als.py:243-323) driving the
 core sweeper (core.py:173-223).
 
 Ratings live on the device as CSR (users) + CSC (items) with int64 pointers,
-int32 indices and fp32 values; factors are fp32 row-major.  One half-sweep is
-one call into libcoreals_b200.so (``cals_core_half_sweep``), enqueued on the
-current torch stream.  The host only reads back, once per iteration, the
-objective terms and a status word.
+int32 indices and fp32 values; factors are fp32 row-major with rows padded to
+16 bytes, double-buffered (a half-sweep reads the current buffer and writes
+the other one).  One half-sweep is one call into libcoreals_b200.so
+(``cals_core_half_sweep``) on the current torch stream.
+
+Objective bookkeeping.  The reference fuses the residual of iteration t into
+its second half-sweep (als.py:287-288).  Here it rides on the FIRST
+half-sweep of iteration t+1, whose staged slices hold exactly the rows the
+residual needs (each rating against the previous iteration's rows), so it
+costs no extra memory traffic; the last iteration's residual is one extra
+gather pass (``cals_residual``).  obj(t) therefore becomes available one
+half-sweep later; thanks to the double buffers the factors of iteration t are
+still intact when the host decides to stop there.
 """
 
 from __future__ import annotations
 
 import ctypes
-import time
-import warnings
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _lib
-from .errors import ConfigError, NumericalError
+from .errors import ConfigError
 
-__all__ = ["DeviceSide", "CoreEngine"]
-
-
-def _ptr(t):
-    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+__all__ = ["DeviceSide", "CoreEngine", "IterationTerms"]
 
 
 class DeviceSide:
@@ -45,6 +48,7 @@ class DeviceSide:
         counts = np.diff(ptr).astype(np.int64)
         if row_end is None:
             row_end = n_rows
+        self.row_range = (int(row_begin), int(row_end))
         # rows outside [row_begin, row_end) are another rank's shard: no work here
         sched = counts.copy()
         sched[:row_begin] = 0
@@ -64,6 +68,7 @@ class DeviceSide:
         self.small_host = small[:meta.n_small].copy()
         self.big_host = big[:meta.n_big].copy()
         nnz = int(ptr[-1])
+
         def t(a, dt):
             if torch.is_tensor(a):
                 return a.to(device=device, dtype=dt).contiguous()
@@ -88,10 +93,11 @@ class DeviceSide:
         self.ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=device)
         self.status = torch.zeros(n_rows, dtype=torch.int32, device=device)
         self.rss_rows = torch.zeros(n_rows, dtype=torch.float64, device=device)
+        self.pen_rows = torch.zeros(n_rows, dtype=torch.float64, device=device)
         self.summary = torch.zeros(1, dtype=torch.int64, device=device)
         self.nnz = nnz
 
-    def half_sweep(self, source, target, lam, want_rss, thr_keys=None, stream=None):
+    def half_sweep(self, source, target, target_old=None, want_rss=False, thr_keys=None, lam=0.0, stream=None):
         torch = _lib.require_cuda()
         if stream is None:
             stream = torch.cuda.current_stream(self.device).cuda_stream
@@ -99,10 +105,20 @@ class DeviceSide:
         rc = L.cals_core_half_sweep(
             ctypes.byref(self.side), ctypes.byref(self.plan), source.data_ptr(), source.shape[0],
             source.stride(0), self.n_f, float(lam), target.data_ptr(), target.stride(0),
-            self.rss_rows.data_ptr() if want_rss else None,
+            target_old.data_ptr() if target_old is not None else None,
+            target_old.stride(0) if target_old is not None else 0,
+            self.rss_rows.data_ptr() if want_rss else None, self.pen_rows.data_ptr(),
             thr_keys.data_ptr() if thr_keys is not None else None,
             self.status.data_ptr(), self.summary.data_ptr(), self.ws.data_ptr(), self.ws.numel(), stream)
         _lib.check(rc, "cals_core_half_sweep")
+
+    def residual(self, source, rows_w, stream=None):
+        torch = _lib.require_cuda()
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(_lib.load().cals_residual(ctypes.byref(self.side), source.data_ptr(), source.stride(0), self.n_f,
+                                             rows_w.data_ptr(), rows_w.stride(0), self.rss_rows.data_ptr(), stream),
+                   "cals_residual")
 
 
 def decode_summary(word: int):
@@ -115,15 +131,24 @@ def decode_summary(word: int):
 
 @dataclass
 class IterationTerms:
+    """Objective terms of one completed iteration."""
+
     rss: float
-    pen_u: float
-    pen_m: float
+    pen: float  # sum_i n_i |u_i|^2 + sum_j n_j |m_j|^2 (multiply by lam)
     status_first: tuple
     status_second: tuple
 
 
 class CoreEngine:
-    """Device state for one fit: both sides, both factor matrices, scratch."""
+    """Device state for one fit: both sides, double-buffered factors, scratch.
+
+    The loop fit_core runs (pipelined, one host read per iteration):
+        eng.set_factors(U0, M0)
+        for t in range(max_iters):
+            eng.step(first)                 # iteration t (+ residual of t-1)
+            if t: terms = eng.terms(t - 1)  # host read overlaps iteration t's second half
+        eng.finish(first); terms = eng.terms(max_iters - 1)
+    """
 
     def __init__(self, R, n_f, rate, lam, device=None, user_range=None, item_range=None):
         torch = _lib.require_cuda()
@@ -138,59 +163,131 @@ class CoreEngine:
         ir = item_range or (0, self.n_items)
         self.user = DeviceSide(R.row_ptr, R.row_items, R.row_vals, self.n_items, n_f, rate, device, *ur)
         self.item = DeviceSide(R.col_ptr, R.col_users, R.col_vals, self.n_users, n_f, rate, device, *ir)
-        self.U = torch.zeros((self.n_users, self.n_f), dtype=torch.float32, device=device)
-        self.M = torch.zeros((self.n_items, self.n_f), dtype=torch.float32, device=device)
+        # factor rows padded to a multiple of 4 floats (16-byte gathers); padding stays zero
+        self.ld = (self.n_f + 3) // 4 * 4
+        self.Ub = [torch.zeros((self.n_users, self.ld), dtype=torch.float32, device=device) for _ in range(2)]
+        self.Mb = [torch.zeros((self.n_items, self.ld), dtype=torch.float32, device=device) for _ in range(2)]
+        self.cu = self.cm = 0
         self.red_ws = torch.empty(4096, dtype=torch.uint8, device=device)
-        self.scalars = torch.zeros(3, dtype=torch.float64, device=device)
+        # per iteration parity: [rss, pen_user, pen_item, status_first, status_second]
+        self.slots = torch.zeros((2, 5), dtype=torch.float64, device=device)
+        self.host_slots = torch.zeros((2, 5), dtype=torch.float64).pin_memory()
+        self.events = [torch.cuda.Event(), torch.cuda.Event()]
         vals = R.row_vals if torch.is_tensor(R.row_vals) else torch.from_numpy(np.asarray(R.row_vals))
         vals = vals.to(device=device, dtype=torch.float64)
         self.ssq = float(torch.dot(vals, vals).item()) if vals.numel() else 0.0
+        self.iters_done = 0
+
+    # -- factor buffers ------------------------------------------------------
+    @property
+    def U(self):
+        return self.Ub[self.cu]
+
+    @property
+    def M(self):
+        return self.Mb[self.cm]
+
+    @property
+    def U_view(self):
+        return self.U[:, :self.n_f]
+
+    @property
+    def M_view(self):
+        return self.M[:, :self.n_f]
 
     def set_factors(self, U=None, M=None):
+        """Initial factors into BOTH buffers (rows without ratings never change)."""
         torch = _lib.require_cuda()
         if U is not None:
-            self.U.copy_(torch.as_tensor(np.asarray(U, dtype=np.float32)).to(self.device))
+            u = torch.as_tensor(np.asarray(U, dtype=np.float32)).to(self.device)
+            for b in self.Ub:
+                b[:, :self.n_f].copy_(u)
         if M is not None:
-            self.M.copy_(torch.as_tensor(np.asarray(M, dtype=np.float32)).to(self.device))
+            m = torch.as_tensor(np.asarray(M, dtype=np.float32)).to(self.device)
+            for b in self.Mb:
+                b[:, :self.n_f].copy_(m)
+        self.iters_done = 0
 
-    def half(self, side, want_rss=False, thr_keys=None):
+    def _exchange(self, side):  # all-gather of the new rows (sharded engine)
+        pass
+
+    def _reduce_scalars(self, parity, cols):  # all-reduce of objective terms (sharded engine)
+        pass
+
+    def half(self, side, rss=False, thr_keys=None):
+        """One half-sweep into the other buffer; rss: fused residual of the old rows."""
         if side == "user":
-            self.user.half_sweep(self.M, self.U, self.lam, want_rss, thr_keys)
+            new = self.Ub[1 - self.cu]
+            self.user.half_sweep(self.M, new, self.U, rss, thr_keys, self.lam)
+            self.cu = 1 - self.cu
         else:
-            self.item.half_sweep(self.U, self.M, self.lam, want_rss, thr_keys)
+            new = self.Mb[1 - self.cm]
+            self.item.half_sweep(self.U, new, self.M, rss, thr_keys, self.lam)
+            self.cm = 1 - self.cm
+        self._exchange(side)
 
-    def objective_terms(self, rss_side, stream=None):
-        """Enqueue rss (sum of the fused residual rows) and both penalty sums."""
+    def _sum(self, src, dst_ptr):
         torch = _lib.require_cuda()
-        if stream is None:
-            stream = torch.cuda.current_stream(self.device).cuda_stream
-        L = _lib.load()
-        ws, nb = self.red_ws.data_ptr(), self.red_ws.numel()
-        s = self.user if rss_side == "user" else self.item
-        _lib.check(L.cals_sum_f64(s.rss_rows.data_ptr(), s.n_rows, self.scalars.data_ptr(), ws, nb, stream),
-                   "cals_sum_f64")
-        _lib.check(L.cals_weighted_sqnorm(self.U.data_ptr(), self.n_users, self.n_f, self.U.stride(0),
-                                          self.user.ptr.data_ptr(), self.scalars.data_ptr() + 8, ws, nb, stream),
-                   "cals_weighted_sqnorm")
-        _lib.check(L.cals_weighted_sqnorm(self.M.data_ptr(), self.n_items, self.n_f, self.M.stride(0),
-                                          self.item.ptr.data_ptr(), self.scalars.data_ptr() + 16, ws, nb, stream),
-                   "cals_weighted_sqnorm")
+        st = torch.cuda.current_stream(self.device).cuda_stream
+        _lib.check(_lib.load().cals_sum_f64(src.data_ptr(), src.numel(), dst_ptr, self.red_ws.data_ptr(),
+                                            self.red_ws.numel(), st), "cals_sum_f64")
+
+    def _publish(self, t):
+        self.host_slots[t % 2].copy_(self.slots[t % 2], non_blocking=True)
+        self.events[t % 2].record()
+
+    def step(self, first="user"):
+        """Enqueue iteration t = iters_done; its first half also yields the
+        residual of iteration t-1, which is then published to the host."""
+        torch = _lib.require_cuda()
+        t = self.iters_done
+        second = "item" if first == "user" else "user"
+        sf, ss = (self.user, self.item) if first == "user" else (self.item, self.user)
+        self.half(first, rss=t > 0)
+        if t > 0:
+            self._sum(sf.rss_rows, self.slots[(t - 1) % 2, 0:1].data_ptr())
+            self._reduce_scalars((t - 1) % 2, (0,))
+            self._publish(t - 1)
+        s1 = sf.summary.clone()
+        self.half(second, rss=False)
+        cur = self.slots[t % 2]
+        self._sum(self.user.pen_rows, cur[1:2].data_ptr())
+        self._sum(self.item.pen_rows, cur[2:3].data_ptr())
+        cur[3:4].copy_(s1.view(torch.float64))
+        cur[4:5].copy_(ss.summary.view(torch.float64))
+        self._reduce_scalars(t % 2, (1, 2, 3, 4))
+        self.iters_done = t + 1
+
+    def finish(self, first="user"):
+        """Residual of the last iteration: one gather pass over the first side."""
+        t = self.iters_done - 1
+        if t < 0:
+            return
+        sf = self.user if first == "user" else self.item
+        src, rows = (self.M, self.U) if first == "user" else (self.U, self.M)
+        sf.residual(src, rows)
+        self._sum(sf.rss_rows, self.slots[t % 2, 0:1].data_ptr())
+        self._reduce_scalars(t % 2, (0,))
+        self._publish(t)
+
+    def terms(self, t):
+        """Host copy of iteration t's objective terms (waits until published)."""
+        self.events[t % 2].synchronize()
+        h = self.host_slots[t % 2].numpy().copy()
+        w = h[3:5].view(np.int64)
+        return IterationTerms(float(h[0]), float(h[1] + h[2]), decode_summary(int(w[0])), decode_summary(int(w[1])))
 
     def iterate(self, first="user"):
-        """One ALS iteration (both half-sweeps + fused RSS) -> IterationTerms.
-        The only device->host traffic: 3 doubles and 2 status words."""
-        torch = _lib.require_cuda()
-        second = "item" if first == "user" else "user"
-        self.half(first, want_rss=False)
-        s1 = (self.user if first == "user" else self.item).summary.clone()
-        self.half(second, want_rss=True)
-        s2 = (self.user if second == "user" else self.item).summary
-        self.objective_terms(second)
-        host = torch.cat([self.scalars, s1.view(torch.float64), s2.view(torch.float64)]).cpu()
-        rss, pu, pm = (float(x) for x in host[:3])
-        w1 = int(host[3:4].view(torch.int64).item())
-        w2 = int(host[4:5].view(torch.int64).item())
-        return IterationTerms(rss, pu, pm, decode_summary(w1), decode_summary(w2))
+        """One iteration together with its own residual (synchronous form used
+        by tests and the benchmark's per-step timing)."""
+        self.step(first)
+        self.finish(first)
+        return self.terms(self.iters_done - 1)
+
+    def rewind(self):
+        """Make the previous buffers current again (drop the last step's rows)."""
+        self.cu, self.cm = 1 - self.cu, 1 - self.cm
+        self.iters_done -= 1
 
     def factors_host(self):
-        return self.U.double().cpu().numpy(), self.M.double().cpu().numpy()
+        return self.U_view.double().cpu().numpy(), self.M_view.double().cpu().numpy()

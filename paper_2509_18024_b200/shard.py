@@ -59,45 +59,37 @@ def allgather_rows(F, ranges, rank, group=None, scratch=None):
 
 
 class ShardedEngine:
-    """CoreEngine restricted to this rank's row blocks + the per-half-sweep
-    exchange.  Same iterate() contract as CoreEngine."""
+    """Factory returning a CoreEngine restricted to this rank's row blocks,
+    with the per-half-sweep exchange and the objective all-reduce hooked in."""
 
-    def __init__(self, R, n_f, rate, lam, rank, world, group=None, device=None):
+    def __new__(cls, R, n_f, rate, lam, rank, world, group=None, device=None):
         from .engine import CoreEngine
 
-        self.rank, self.world, self.group = rank, world, group
-        self.user_ranges = nnz_balanced_ranges(R.row_ptr, world)
-        self.item_ranges = nnz_balanced_ranges(R.col_ptr, world)
-        self.eng = CoreEngine(R, n_f, rate, lam, device=device, user_range=self.user_ranges[rank],
-                              item_range=self.item_ranges[rank])
-        self._scratch = None
+        user_ranges = nnz_balanced_ranges(R.row_ptr, world)
+        item_ranges = nnz_balanced_ranges(R.col_ptr, world)
 
-    def __getattr__(self, name):
-        return getattr(self.eng, name)
+        class _Sharded(CoreEngine):
+            def _exchange(self, side):
+                if side == "user":
+                    self._scratch = allgather_rows(self.U, user_ranges, rank, group, self._scratch)
+                else:
+                    self._scratch = allgather_rows(self.M, item_ranges, rank, group, self._scratch)
 
-    def _exchange(self, side):
-        if side == "user":
-            self._scratch = allgather_rows(self.eng.U, self.user_ranges, self.rank, self.group, self._scratch)
-        else:
-            self._scratch = allgather_rows(self.eng.M, self.item_ranges, self.rank, self.group, self._scratch)
+            def _reduce_scalars(self, parity, cols):
+                row = self.slots[parity]
+                sums = [c for c in cols if c <= 2]
+                maxes = [c for c in cols if c >= 3]
+                if sums:
+                    t = row[sums[0]:sums[-1] + 1].clone()
+                    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+                    row[sums[0]:sums[-1] + 1].copy_(t)
+                if maxes:
+                    t = row[maxes[0]:maxes[-1] + 1].view(torch.int64).clone()
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+                    row[maxes[0]:maxes[-1] + 1].copy_(t.view(torch.float64))
 
-    def iterate(self, first="user"):
-        from .engine import IterationTerms, decode_summary
-
-        e = self.eng
-        second = "item" if first == "user" else "user"
-        e.half(first, want_rss=False)
-        self._exchange(first)
-        s1 = (e.user if first == "user" else e.item).summary.clone()
-        e.half(second, want_rss=True)
-        self._exchange(second)
-        s2 = (e.user if second == "user" else e.item).summary
-        e.objective_terms(second)
-        rss = e.scalars[:1].clone()
-        dist.all_reduce(rss, op=dist.ReduceOp.SUM, group=self.group)
-        words = torch.stack([s1[0], s2[0]])
-        dist.all_reduce(words, op=dist.ReduceOp.MAX, group=self.group)
-        host = torch.cat([rss, e.scalars[1:3], words.view(torch.float64)]).cpu()
-        w = host[3:5].view(torch.int64)
-        return IterationTerms(float(host[0]), float(host[1]), float(host[2]),
-                              decode_summary(int(w[0])), decode_summary(int(w[1])))
+        eng = _Sharded(R, n_f, rate, lam, device=device, user_range=user_ranges[rank], item_range=item_ranges[rank])
+        eng._scratch = None
+        eng.rank, eng.world, eng.group = rank, world, group
+        eng.user_ranges, eng.item_ranges = user_ranges, item_ranges
+        return eng

@@ -45,9 +45,9 @@ def gpu_half(eng, side, source, init_target=None):
         eng.set_factors(M=source, U=init_target if init_target is not None else np.zeros((eng.n_users, eng.n_f)))
     else:
         eng.set_factors(U=source, M=init_target if init_target is not None else np.zeros((eng.n_items, eng.n_f)))
-    eng.half(side, want_rss=(side == "item"), thr_keys=keys)
+    eng.half(side, rss=False, thr_keys=keys)
     torch.cuda.synchronize()
-    tgt = (eng.U if side == "user" else eng.M).double().cpu().numpy()
+    tgt = (eng.U_view if side == "user" else eng.M_view).double().cpu().numpy()
     return tgt, keys.cpu().numpy().view(np.uint64)
 
 
@@ -132,8 +132,13 @@ def check_against_oracle(R, n_f, lam, rate, source_item, seed=0, ties=False):
     act = np.diff(R.col_ptr) > 0
     np.testing.assert_array_equal(keys[act], ko[act])
     assert row_rel_err(M, Mo, act) <= FACTOR_TOL
+    eng.item.residual(eng.U, eng.M)  # residual of the NEW rows, as the reference fuses it
     rss_g = eng.item.rss_rows.cpu().numpy()
     np.testing.assert_allclose(rss_g[act].sum(), rss_o[act].sum(), rtol=1e-4)
+    # the fused form: the next user half-sweep's residual of the previous rows
+    eng.half("user", rss=True)
+    rss_fused = eng.user.rss_rows.cpu().numpy().sum()
+    np.testing.assert_allclose(rss_fused, rss_o[act].sum(), rtol=1e-4)
     return eng
 
 
@@ -145,15 +150,15 @@ def test_oracle_parity_mixed_tiers(n_f):
     M0 = np.random.default_rng(1).normal(0, 0.1, (400, n_f)).astype(np.float32)
     eng = check_against_oracle(R, n_f, 0.05, 0.2, M0)
     assert eng.user.plan.n_small > 0
-    if n_f >= 16:
+    if n_f >= 32:
         assert eng.item.plan.n_big > 0  # the heavy items exercise the tiled tier
 
 
-@pytest.mark.parametrize("n_f", [1, 5, 8])
+@pytest.mark.parametrize("n_f", [1, 5, 8, 16])
 def test_oracle_parity_tiled_tier_small_rank(n_f):
     """Rows long enough to leave shared memory even at tiny n_f."""
-    u, i, v = random_matrix(100 + n_f, 20000, 60, 0.01, heavy_items=2, heavy_density=0.97)
-    R = cb.RatingMatrix(u, i, v, n_users=20000, n_items=60)
+    u, i, v = random_matrix(100 + n_f, 40000, 60, 0.01, heavy_items=2, heavy_density=0.97)
+    R = cb.RatingMatrix(u, i, v, n_users=40000, n_items=60)
     M0 = np.random.default_rng(5).normal(0, 0.1, (60, n_f)).astype(np.float32)
     eng = check_against_oracle(R, n_f, 0.1, 0.3, M0)
     assert eng.item.plan.n_big > 0
@@ -186,9 +191,11 @@ def test_half_sweep_is_deterministic():
     b, kb = gpu_half(eng, "user", M0)
     assert np.array_equal(a, b) and np.array_equal(ka, kb)
     c, _ = gpu_half(eng, "item", a.astype(np.float32))
-    r1 = eng.item.rss_rows.clone()
+    eng.half("user", rss=True)
+    r1 = eng.user.rss_rows.clone()
     d, _ = gpu_half(eng, "item", a.astype(np.float32))
-    assert np.array_equal(c, d) and torch.equal(r1, eng.item.rss_rows)
+    eng.half("user", rss=True)
+    assert np.array_equal(c, d) and torch.equal(r1, eng.user.rss_rows)
 
 
 def test_ces_sketch_matches_reference_rows_exactly():
