@@ -129,13 +129,12 @@ __device__ void build_mask(const float* __restrict__ Xs, int sx, int n, int nf, 
 // Kept-row lists (ascending k) are built from the selection bitmap by the
 // same warp.  Writes rows of G (+lam_n on the diagonal) to Gout (row stride nf+1).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void sparse_gram_warp(const float* __restrict__ Xs, int sx, const float* __restrict__ ys,
-                                                 const uint32_t* __restrict__ mb, int mw, int n, int nf, int s,
-                                                 bool full, uint16_t* __restrict__ lists, int Smax, float lam_n,
+template <int CPL>
+__device__ __forceinline__ void sparse_gram_warp(uint32_t xs, int sx, uint32_t ys, uint32_t mb, int mw, int n, int nf,
+                                                 int s, bool full, uint32_t lists, int Smax, float lam_n,
                                                  float* __restrict__ Gout, int warp, int nwarps, int lane) {
     const int nq = xs_chunks(nf);
     const int LPC = nq < 4 ? nq : 4;
-    const int CPL = (nq + LPC - 1) / LPC;  // <= 8 for nf <= 128
     int CT = (nf + nwarps - 1) / nwarps;    // columns per task: power of two, CT * LPC <= 32
     CT = CT <= 1 ? 1 : (CT <= 2 ? 2 : (CT <= 4 ? 4 : (CT <= 8 ? 8 : (CT <= 16 ? 16 : 32))));
     while (CT * LPC > 32) CT >>= 1;
@@ -145,6 +144,7 @@ __device__ __forceinline__ void sparse_gram_warp(const float* __restrict__ Xs, i
     const int fl = lane % LPC;
     const int gs = nf + 1;
     const int ntask = (nf + CT - 1) / CT;
+    const uint32_t rowb = 4u * (uint32_t)sx;
     for (int task = warp; task < ntask; task += nwarps) {
         const int cbase = task * CT;
         const int c = cbase + cs;
@@ -155,53 +155,55 @@ __device__ __forceinline__ void sparse_gram_warp(const float* __restrict__ Xs, i
             const int wsel = cbase >> 5, sh = cbase & 31;
             for (int k0 = 0; k0 < n; k0 += 32) {
                 const int k = k0 + lane;
-                const uint32_t word = k < n ? (mb[k * mw + wsel] >> sh) : 0u;
+                const uint32_t word = k < n ? (lds_u32(mb + 4u * (uint32_t)(k * mw + wsel)) >> sh) : 0u;
                 for (int cc = 0; cc < CT && cbase + cc < nf; ++cc) {
                     const bool bit = (word >> cc) & 1u;
                     const uint32_t bal = __ballot_sync(CALS_FULL_MASK, bit);
                     const int base = __shfl_sync(CALS_FULL_MASK, cnt, cc);
-                    if (bit) lists[(cbase + cc) * Smax + base + __popc(bal & lanemask_lt())] = (uint16_t)k;
+                    if (bit)
+                        sts_u16(lists + 2u * (uint32_t)((cbase + cc) * Smax + base + __popc(bal & lanemask_lt())), k);
                     if (lane == cc) cnt += __popc(bal);
                 }
             }
             __syncwarp();
         }
         const int len = full ? n : s;
-        const uint16_t* L = lists + (size_t)(cvalid ? c : cbase) * Smax;
-        float acc[32];
+        const uint32_t L = lists + 2u * (uint32_t)((cvalid ? c : cbase) * Smax);
+        const uint32_t xcol = xs + 4u * (uint32_t)(cvalid ? c : 0);
+        float acc[4 * CPL];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+        for (int i = 0; i < 4 * CPL; ++i) acc[i] = 0.f;
         float accb = 0.f;
+        const bool chunk_ok_last = (fl + (CPL - 1) * LPC) < nq;
         for (int q = qg; q < len; q += QG) {
-            const int k = full ? q : (int)L[q];
-            const float xc = cvalid ? Xs[(size_t)k * sx + c] : 0.f;
-            const float* xr = Xs + (size_t)k * sx;
+            const uint32_t k = full ? (uint32_t)q : lds_u16(L + 2u * (uint32_t)q);
+            const uint32_t rb = k * rowb;
+            const float xc = lds_f32(xcol + rb);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < CPL; ++i) {
                 const int ch = fl + i * LPC;
-                if (i < CPL && ch < nq) {
-                    const float4 v = *reinterpret_cast<const float4*>(xr + 4 * ch);
+                if (i < CPL - 1 || chunk_ok_last) {
+                    const float4 v = lds_f128(xs + rb + 16u * (uint32_t)ch);
                     acc[4 * i + 0] = fmaf(xc, v.x, acc[4 * i + 0]);
                     acc[4 * i + 1] = fmaf(xc, v.y, acc[4 * i + 1]);
                     acc[4 * i + 2] = fmaf(xc, v.z, acc[4 * i + 2]);
                     acc[4 * i + 3] = fmaf(xc, v.w, acc[4 * i + 3]);
                 }
             }
-            if (fl == 0) accb = fmaf(xc, ys[k], accb);
+            if (fl == 0) accb = fmaf(xc, lds_f32(ys + 4u * k), accb);
         }
         // fixed-order reduction over the q-groups (lane bits LPC .. LPC*QG)
         for (int o = LPC; o < LPC * QG; o <<= 1) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-                if (i < 4 * CPL) acc[i] += __shfl_xor_sync(CALS_FULL_MASK, acc[i], o);
+            for (int i = 0; i < 4 * CPL; ++i) acc[i] += __shfl_xor_sync(CALS_FULL_MASK, acc[i], o);
             accb += __shfl_xor_sync(CALS_FULL_MASK, accb, o);
         }
         if (cvalid && qg == 0) {
             float* grow = Gout + (size_t)c * gs;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < CPL; ++i) {
                 const int ch = fl + i * LPC;
-                if (i < CPL && ch < nq) {
+                if (ch < nq) {
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
                         const int f = 4 * ch + t;
@@ -213,6 +215,17 @@ __device__ __forceinline__ void sparse_gram_warp(const float* __restrict__ Xs, i
         }
         __syncwarp();
     }
+}
+
+// CPL (16-byte chunks per lane) dispatch: nq <= 4 -> 1, <= 8 -> 2, <= 16 -> 4, else 8.
+__device__ __forceinline__ void sparse_gram(uint32_t xs, int sx, uint32_t ys, uint32_t mb, int mw, int n, int nf, int s,
+                                            bool full, uint32_t lists, int Smax, float lam_n, float* Gout, int warp,
+                                            int nwarps, int lane) {
+    const int nq = xs_chunks(nf);
+    if (nq <= 4) sparse_gram_warp<1>(xs, sx, ys, mb, mw, n, nf, s, full, lists, Smax, lam_n, Gout, warp, nwarps, lane);
+    else if (nq <= 8) sparse_gram_warp<2>(xs, sx, ys, mb, mw, n, nf, s, full, lists, Smax, lam_n, Gout, warp, nwarps, lane);
+    else if (nq <= 16) sparse_gram_warp<4>(xs, sx, ys, mb, mw, n, nf, s, full, lists, Smax, lam_n, Gout, warp, nwarps, lane);
+    else sparse_gram_warp<8>(xs, sx, ys, mb, mw, n, nf, s, full, lists, Smax, lam_n, Gout, warp, nwarps, lane);
 }
 
 }  // namespace cals

@@ -17,22 +17,21 @@
 
 namespace cals {
 
-// Candidate list of slice-row indices into a staged slice column.
-template <typename IdxT>
+// Candidate list of slice-row indices (uint16, shared memory) into a staged
+// slice column; addresses are 32-bit shared-window addresses.
 struct IdxList {
-    const float* X;  // staged slice, row stride `stride`
+    uint32_t xs;     // staged slice base, row stride `stride` floats
     int stride, c;
-    IdxT* buf;       // compaction buffer (capacity >= current m)
+    uint32_t buf;    // compaction buffer (uint16 entries, capacity >= current m)
     bool identity;   // buf not yet materialised: element i is slice row i
-    __device__ __forceinline__ uint64_t key(int i) const {
-        int k = identity ? i : (int)buf[i];
-        return make_key(X[k * stride + c], (uint32_t)k);
+    __device__ __forceinline__ uint32_t elem(int i) const {
+        return identity ? (uint32_t)i : lds_u16(buf + 2u * (uint32_t)i);
     }
-    __device__ __forceinline__ uint32_t elem(int i) const { return identity ? (uint32_t)i : (uint32_t)buf[i]; }
-    __device__ __forceinline__ void put(int i, uint32_t e) { buf[i] = (IdxT)e; }
     __device__ __forceinline__ uint64_t key_of_elem(uint32_t e) const {
-        return make_key(X[(int)e * stride + c], e);
+        return make_key(lds_f32(xs + 4u * (e * (uint32_t)stride + (uint32_t)c)), e);
     }
+    __device__ __forceinline__ uint64_t key(int i) const { return key_of_elem(elem(i)); }
+    __device__ __forceinline__ void put(int i, uint32_t e) { sts_u16(buf + 2u * (uint32_t)i, e); }
 };
 
 // Candidate list of explicit keys (big rows; may live in global memory).
@@ -54,8 +53,7 @@ __device__ __forceinline__ void choose_bracket(int m, int need, int& a, int& b) 
 
 // Warp-level select on an index list: returns the need-th largest key
 // (1 <= need <= m) among the m listed candidates, all inside [lo, hi).
-template <typename IdxT>
-__device__ uint64_t warp_select_idx(IdxList<IdxT> L, int m, int need, uint64_t lo, uint64_t hi, int lane) {
+__device__ uint64_t warp_select_idx(IdxList L, int m, int need, uint64_t lo, uint64_t hi, int lane) {
     while (true) {
         if (m <= 32) {
             uint64_t v = lane < m ? L.key(lane) : 0ull;
@@ -105,8 +103,7 @@ __device__ uint64_t warp_select_idx(IdxList<IdxT> L, int m, int need, uint64_t l
 // table levels between jhi and jlo as ready-made splitters (no sampling or
 // sorting): one counting pass with kSub-1 ballots per chunk picks the
 // sub-bucket holding the target rank, one pass compacts it.
-template <typename IdxT>
-__device__ void warp_prenarrow(IdxList<IdxT>& L, int& m, int& need, uint64_t& lo, uint64_t& hi,
+__device__ void warp_prenarrow(IdxList& L, int& m, int& need, uint64_t& lo, uint64_t& hi,
                                const uint32_t* qtab_c, int jhi, int jlo, int lane) {
     const int span = jlo - jhi;
     if (span < 2 || m <= 32) return;

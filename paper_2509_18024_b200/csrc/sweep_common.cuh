@@ -94,9 +94,8 @@ __device__ __forceinline__ uint64_t hi_key_of(uint32_t hib) {
 }
 
 // cp.async 16-byte global -> shared copy (L2-only caching: gathers are streamed)
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n" ::);
@@ -111,12 +110,16 @@ __device__ __forceinline__ void stage_slice(const SweepArgs& A, int64_t lo, int 
     const int sx = xs_stride(A.nf), nq = xs_chunks(A.nf);
     const int nt = blockDim.x;
     const int nel = kn * nq;
+    const uint32_t xs_base = smem_u32(Xs);
+    const int32_t* idx = A.idx + lo + k0;
+    const float* src = A.src;
+    const int64_t ld = A.ld_src;
 #pragma unroll 4
     for (int e = threadIdx.x; e < nel; e += nt) {
         const int k = (int)fq.div((uint32_t)e);
         const int q = e - k * nq;
-        const int64_t r = __ldg(A.idx + lo + k0 + k);
-        cp_async16(Xs + k * sx + 4 * q, A.src + r * A.ld_src + 4 * q);
+        const int64_t r = __ldg(idx + k);
+        cp_async16(xs_base + (uint32_t)((k * sx + 4 * q) * 4), src + r * ld + 4 * q);
     }
     if (ys != nullptr)
         for (int k = threadIdx.x; k < kn; k += nt) ys[k] = __ldg(A.val + lo + k0 + k);

@@ -54,14 +54,15 @@ __global__ void __launch_bounds__(1024) quantile_table_kernel(const int32_t* __r
     }
 }
 
-// Threshold key of column c (warp-level, see select.cuh).  `cl` holds the
-// column's bracket candidates (left intact), `scr` is this warp's scratch.
-__device__ __forceinline__ uint64_t resolve_column(const SweepArgs& A, const float* Xs, int sx, int c, int n, int s,
-                                                   bool use_tab, int above, int in, const uint16_t* cl,
-                                                   uint16_t* scr, bool& fallback, int lane) {
+// Threshold key of column c (warp-level, see select.cuh).  `cl` (shared
+// address) holds the column's bracket candidates and is left intact, `scr`
+// is this warp's scratch list.
+__device__ __forceinline__ uint64_t resolve_column(const SweepArgs& A, uint32_t xs, int sx, int c, int n, int s,
+                                                   bool use_tab, int above, int in, uint32_t cl, uint32_t scr,
+                                                   bool& fallback, int lane) {
     fallback = false;
     if (!use_tab) {
-        IdxList<uint16_t> Lst{Xs, sx, c, scr, true};
+        IdxList Lst{xs, sx, c, scr, true};
         return warp_select_idx(Lst, n, s, 0ull, ~0ull, lane);
     }
     const uint32_t* qc = A.qtab + (size_t)c * (kQ + 1);
@@ -70,9 +71,9 @@ __device__ __forceinline__ uint64_t resolve_column(const SweepArgs& A, const flo
     const uint32_t hib = qc[jhi], lob = qc[jlo];
     uint64_t hik = hi_key_of(hib), lok = (uint64_t)lob << 32;
     if (above < s && s <= above + in && in <= kCap && lok < hik) {
-        for (int i = lane; i < in; i += 32) scr[i] = cl[i];
+        for (int i = lane; i < in; i += 32) sts_u16(scr + 2u * i, lds_u16(cl + 2u * i));
         __syncwarp();
-        IdxList<uint16_t> Lst{Xs, sx, c, scr, false};
+        IdxList Lst{xs, sx, c, scr, false};
         int m = in, need = s - above;
         warp_prenarrow(Lst, m, need, lok, hik, qc, jhi, jlo, lane);
         return warp_select_idx(Lst, m, need, lok, hik, lane);
@@ -84,9 +85,9 @@ __device__ __forceinline__ uint64_t resolve_column(const SweepArgs& A, const flo
     if (above >= s) { rlo = hik; rhi = ~0ull; m = above; need = s; }
     else if (above + in < s) { rlo = 0ull; rhi = lok; m = n - above - in; need = s - above - in; }
     else { rlo = lok; rhi = hik; m = in; need = s - above; }
-    auto keyat = [Xs, sx, c](int k) { return make_key(Xs[k * sx + c], (uint32_t)k); };
-    return warp_select_column(keyat, n, m, need, rlo, rhi, reinterpret_cast<uint64_t*>(scr),
-                              (kCap * (int)sizeof(uint16_t)) / 8, lane);
+    auto keyat = [xs, sx, c](int k) { return make_key(lds_f32(xs + 4u * (uint32_t)(k * sx + c)), (uint32_t)k); };
+    uint64_t* keybuf = reinterpret_cast<uint64_t*>(__cvta_shared_to_generic(scr));
+    return warp_select_column(keyat, n, m, need, rlo, rhi, keybuf, (kCap * (int)sizeof(uint16_t)) / 8, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -109,9 +110,13 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
     float* Xs = reinterpret_cast<float*>(smem);
     float* ys = reinterpret_cast<float*>(smem + L.xs);
     uint32_t* mb = reinterpret_cast<uint32_t*>(smem + L.xs + L.ys);
-    uint16_t* cand = reinterpret_cast<uint16_t*>(smem + L.xs + L.ys + L.mb);
-    uint16_t* lists = cand;  // reused once the thresholds are known
-    uint16_t* wscr = reinterpret_cast<uint16_t*>(smem + L.xs + L.ys + L.mb + L.region) + warp * kCap;
+    const uint32_t s_xs = smem_u32(smem);
+    const uint32_t s_ys = s_xs + (uint32_t)L.xs;
+    const uint32_t s_mb = s_ys + (uint32_t)L.ys;
+    const uint32_t s_cand = s_mb + (uint32_t)L.mb;
+    const uint32_t s_lists = s_cand;  // reused once the thresholds are known
+    const uint32_t s_scr = s_cand + (uint32_t)L.region + 2u * (uint32_t)(warp * kCap);
+    const uint32_t rowb = 4u * (uint32_t)sx;
     const FastDiv fq((uint32_t)xs_chunks(nf));
     const bool ballot_bits = (32 % nf == 0) || (nf % 32 == 0);
 
@@ -136,9 +141,10 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
         if (A.rss_rows != nullptr) {
             double acc = 0.0;
             for (int k = tid; k < n; k += nt) {
+                const uint32_t rb = s_xs + (uint32_t)k * rowb;
                 double pred = 0.0;
-                for (int f = 0; f < nf; ++f) pred = fma((double)Xs[k * sx + f], (double)wold[f], pred);
-                const double d = (double)ys[k] - pred;
+                for (int f = 0; f < nf; ++f) pred = fma((double)lds_f32(rb + 4u * f), (double)wold[f], pred);
+                const double d = (double)lds_f32(s_ys + 4u * k) - pred;
                 acc = fma(d, d, acc);
             }
             acc = block_sum_d(acc, red);
@@ -153,55 +159,59 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
                 // bitmap (ballots), keys inside it are listed per column
                 const int per = nt / nf;
                 const int c = tid % nf, j = tid / nf;
+                const bool active = tid < per * nf;
                 uint32_t hib = kAbsInf, lob = kAbsInf;
-                if (tid < per * nf) table_bracket(A.qtab + (size_t)c * (kQ + 1), n, s, A.delta_tab, hib, lob);
-                uint16_t* cl = cand + c * kCap;
+                if (active) table_bracket(A.qtab + (size_t)c * (kQ + 1), n, s, A.delta_tab, hib, lob);
+                const uint32_t cl = s_cand + 2u * (uint32_t)(c * kCap);
                 int above = 0;
                 const int iters = (n + per - 1) / per;
                 const int rsh = (lane / (nf <= 32 ? nf : 32)) * nf;
                 const uint32_t rmask = nf >= 32 ? 0xffffffffu : ((1u << nf) - 1u);
                 const bool writer = nf <= 32 ? (c == 0) : (lane == 0);
-                for (int it = 0; it < iters; ++it) {
-                    const int k = j + it * per;
-                    const bool ok = (tid < per * nf) && k < n;
-                    const uint32_t a = ok ? abs_bits(Xs[k * sx + c]) : 0u;
+                uint32_t addr = s_xs + (uint32_t)j * rowb + 4u * (uint32_t)c;
+                const uint32_t astep = (uint32_t)per * rowb;
+                int k = j;
+                for (int it = 0; it < iters; ++it, k += per, addr += astep) {
+                    const bool ok = active && k < n;
+                    const uint32_t a = ok ? (__float_as_uint(lds_f32(addr)) & 0x7FFFFFFFu) : 0u;
                     const bool ab = ok && a >= hib;
                     above += ab;
                     if (ok && a >= lob && a < hib) {
                         const int slot = atomicAdd(&cnt_in[c], 1);
-                        if (slot < kCap) cl[slot] = (uint16_t)k;
+                        if (slot < kCap) sts_u16(cl + 2u * slot, k);
                     }
                     if (ballot_bits) {
                         const uint32_t bal = __ballot_sync(CALS_FULL_MASK, ab);
-                        if (writer && ok) mb[k * mw + (c >> 5)] = (bal >> rsh) & rmask;
+                        if (writer && ok) sts_u32(s_mb + 4u * (uint32_t)(k * mw + (c >> 5)), (bal >> rsh) & rmask);
                     } else if (ab) {
                         atomicOr(&mb[k * mw + (c >> 5)], 1u << (c & 31));
                     }
                 }
-                if (tid < per * nf) atomicAdd(&cnt_above[c], above);
+                if (active) atomicAdd(&cnt_above[c], above);
                 __syncthreads();
             }
             for (int c = warp; c < nf; c += nwarps) {
                 bool fallback;
-                const uint64_t T = resolve_column(A, Xs, sx, c, n, s, use_tab, cnt_above[c], cnt_in[c],
-                                                  cand + c * kCap, wscr, fallback, lane);
+                const uint32_t cl = s_cand + 2u * (uint32_t)(c * kCap);
+                const uint64_t T = resolve_column(A, s_xs, sx, c, n, s, use_tab, cnt_above[c], cnt_in[c], cl, s_scr,
+                                                  fallback, lane);
                 if (lane == 0) thr[c] = T;
                 const uint32_t bit = 1u << (c & 31);
                 uint32_t* mcol = mb + (c >> 5);
+                const uint32_t xcol = s_xs + 4u * (uint32_t)c;
                 if (!use_tab || fallback) {
                     // (re)derive column c entirely: kept iff key >= T
                     for (int k = lane; k < n; k += 32) {
-                        const bool keep = make_key(Xs[k * sx + c], (uint32_t)k) >= T;
+                        const bool keep = make_key(lds_f32(xcol + (uint32_t)k * rowb), (uint32_t)k) >= T;
                         if (keep) atomicOr(mcol + k * mw, bit);
                         else if (fallback) atomicAnd(mcol + k * mw, ~bit);
                     }
                 } else {
                     // bracket candidates at or above the threshold join the kept set
                     const int in = cnt_in[c];
-                    const uint16_t* cl = cand + c * kCap;
                     for (int i = lane; i < in; i += 32) {
-                        const int k = cl[i];
-                        if (make_key(Xs[k * sx + c], (uint32_t)k) >= T) atomicOr(mcol + k * mw, bit);
+                        const uint32_t k = lds_u16(cl + 2u * i);
+                        if (make_key(lds_f32(xcol + k * rowb), k) >= T) atomicOr(mcol + k * mw, bit);
                     }
                 }
             }
@@ -210,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
             for (int c = warp; c < nf; c += nwarps) {
                 uint64_t mn = ~0ull;
                 for (int k = lane; k < n; k += 32) {
-                    const uint64_t kk = make_key(Xs[k * sx + c], (uint32_t)k);
+                    const uint64_t kk = make_key(lds_f32(s_xs + (uint32_t)k * rowb + 4u * c), (uint32_t)k);
                     mn = kk < mn ? kk : mn;
                 }
 #pragma unroll
@@ -225,8 +235,8 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
 
         // ---- sparse Gram -> global normal equations ----
         const float lam_n = (float)(A.lam * (double)n);
-        sparse_gram_warp(Xs, sx, ys, mb, mw, n, nf, s, full, lists, S > 0 ? S : 1, lam_n,
-                         A.gbuf + (size_t)li * nf * gs, warp, nwarps, lane);
+        sparse_gram(s_xs, sx, s_ys, s_mb, mw, n, nf, s, full, s_lists, S > 0 ? S : 1, lam_n,
+                    A.gbuf + (size_t)li * nf * gs, warp, nwarps, lane);
         if (A.thr_keys != nullptr)
             for (int c = tid; c < nf; c += nt) A.thr_keys[(int64_t)row * nf + c] = thr[c];
         __syncthreads();
