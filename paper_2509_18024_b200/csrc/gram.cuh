@@ -228,4 +228,111 @@ __device__ __forceinline__ void sparse_gram(uint32_t xs, int sx, uint32_t ys, ui
     else sparse_gram_warp<8>(xs, sx, ys, mb, mw, n, nf, s, full, lists, Smax, lam_n, Gout, warp, nwarps, lane);
 }
 
+// ---------------------------------------------------------------------------
+// Warp-owned variant: the calling warp owns columns c = c_first + j * c_step
+// (j < n_cols) and has already built their kept-row lists.  Columns are
+// processed in rounds of CT (power of two, CT * LPC <= 32); q-groups QG split
+// each list round-robin and are reduced with shuffles in a fixed order.
+// ---------------------------------------------------------------------------
+template <int CPL>
+__device__ __forceinline__ void sparse_gram_owned(uint32_t xs, int sx, uint32_t ys, int nf, int len, bool full,
+                                                  uint32_t lists, int Smax, int c_first, int c_step, int n_cols,
+                                                  float lam_n, float* __restrict__ Gout, int lane) {
+    const int nq = xs_chunks(nf);
+    const int LPC = nq < 4 ? nq : 4;
+    const int maxct = 32 / LPC;
+    const int gs = nf + 1;
+    const uint32_t rowb = 4u * (uint32_t)sx;
+    for (int j0 = 0; j0 < n_cols; j0 += maxct) {
+        const int cnt = min(maxct, n_cols - j0);
+        int CT = 1;
+        while (CT < cnt) CT <<= 1;
+        const int QG = 32 / (CT * LPC);
+        const int cs = lane / (QG * LPC);
+        const int qg = (lane / LPC) % QG;
+        const int fl = lane % LPC;
+        const bool cvalid = cs < cnt;
+        const int c = c_first + (j0 + (cvalid ? cs : 0)) * c_step;
+        const uint32_t L = lists + 2u * (uint32_t)(c * Smax);
+        const uint32_t xcol = xs + 4u * (uint32_t)c;
+        float acc[4 * CPL];
+#pragma unroll
+        for (int i = 0; i < 4 * CPL; ++i) acc[i] = 0.f;
+        float accb = 0.f;
+        const bool chunk_ok_last = (fl + (CPL - 1) * LPC) < nq;
+        for (int q = qg; q < len; q += QG) {
+            const uint32_t k = full ? (uint32_t)q : lds_u16(L + 2u * (uint32_t)q);
+            const uint32_t rb = k * rowb;
+            const float xc = cvalid ? lds_f32(xcol + rb) : 0.f;
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) {
+                if (i < CPL - 1 || chunk_ok_last) {
+                    const float4 v = lds_f128(xs + rb + 16u * (uint32_t)(fl + i * LPC));
+                    acc[4 * i + 0] = fmaf(xc, v.x, acc[4 * i + 0]);
+                    acc[4 * i + 1] = fmaf(xc, v.y, acc[4 * i + 1]);
+                    acc[4 * i + 2] = fmaf(xc, v.z, acc[4 * i + 2]);
+                    acc[4 * i + 3] = fmaf(xc, v.w, acc[4 * i + 3]);
+                }
+            }
+            if (fl == 0) accb = fmaf(xc, lds_f32(ys + 4u * k), accb);
+        }
+        for (int o = LPC; o < LPC * QG; o <<= 1) {
+#pragma unroll
+            for (int i = 0; i < 4 * CPL; ++i) acc[i] += __shfl_xor_sync(CALS_FULL_MASK, acc[i], o);
+            accb += __shfl_xor_sync(CALS_FULL_MASK, accb, o);
+        }
+        if (cvalid && qg == 0) {
+            float* grow = Gout + (size_t)c * gs;
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) {
+                const int ch = fl + i * LPC;
+                if (ch < nq) {
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int f = 4 * ch + t;
+                        if (f < nf) grow[f] = acc[4 * i + t] + ((f == c) ? lam_n : 0.f);
+                    }
+                }
+            }
+            if (fl == 0) grow[nf] = accb;
+        }
+        __syncwarp();
+    }
+}
+
+__device__ __forceinline__ void sparse_gram_owned_any(uint32_t xs, int sx, uint32_t ys, int nf, int len, bool full,
+                                                      uint32_t lists, int Smax, int c_first, int c_step, int n_cols,
+                                                      float lam_n, float* Gout, int lane) {
+    const int nq = xs_chunks(nf);
+    if (nq <= 4) sparse_gram_owned<1>(xs, sx, ys, nf, len, full, lists, Smax, c_first, c_step, n_cols, lam_n, Gout, lane);
+    else if (nq <= 8) sparse_gram_owned<2>(xs, sx, ys, nf, len, full, lists, Smax, c_first, c_step, n_cols, lam_n, Gout, lane);
+    else if (nq <= 16) sparse_gram_owned<4>(xs, sx, ys, nf, len, full, lists, Smax, c_first, c_step, n_cols, lam_n, Gout, lane);
+    else sparse_gram_owned<8>(xs, sx, ys, nf, len, full, lists, Smax, c_first, c_step, n_cols, lam_n, Gout, lane);
+}
+
+// Kept-row list of one column from its column-major bitmap words (ascending k).
+__device__ __forceinline__ void bitmap_to_list(uint32_t words, int nwords, uint32_t list, int lane) {
+    int base = 0;
+    for (int w0 = 0; w0 < nwords; w0 += 32) {
+        const int w = w0 + lane;
+        uint32_t word = w < nwords ? lds_u32(words + 4u * (uint32_t)w) : 0u;
+        const int cnt = __popc(word);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(CALS_FULL_MASK, incl, o);
+            if (lane >= o) incl += t;
+        }
+        int pos = base + incl - cnt;
+        while (word) {
+            const int b = __ffs(word) - 1;
+            word &= word - 1;
+            sts_u16(list + 2u * (uint32_t)pos, (uint32_t)(32 * w + b));
+            ++pos;
+        }
+        base += __shfl_sync(CALS_FULL_MASK, incl, 31);
+    }
+    __syncwarp();
+}
+
 }  // namespace cals

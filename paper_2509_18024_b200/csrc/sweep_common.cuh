@@ -127,22 +127,23 @@ __device__ __forceinline__ void stage_slice(const SweepArgs& A, int64_t lo, int 
 }
 
 // Shared-memory footprint of the staged-slice kernel for rows of length <= N
-// whose sketch budget is <= S (lists) -- regions reused across phases:
-//   Xs [N][sx] | ys [N] | mb [N][mw] bitmap | R = max(candidates, lists) | scratch
+// whose sketch budget is <= S:
+//   Xs [N][sx] | ys [N] | bitmap [nf][ceil(N/32)] (column-major) |
+//   lists [nf][S] | per-warp candidates [kCap] | per-warp scratch [kCap]
 struct T1Layout {
-    size_t xs, ys, mb, cand, lists, region, scratch, total;
-    int sx, mw;
+    size_t xs, ys, mb, lists, cand, scr, total;
+    int sx, nw;
     __host__ __device__ T1Layout(int N, int S, int nf, int threads) {
         sx = xs_stride(nf);
-        mw = (nf + 31) / 32;
+        nw = (N + 31) / 32;
+        const int warps = threads / 32;
         xs = align16((size_t)N * sx * sizeof(float));
         ys = align16((size_t)N * sizeof(float));
-        mb = align16((size_t)N * mw * sizeof(uint32_t));
-        cand = align16((size_t)nf * kCap * sizeof(uint16_t));
+        mb = align16((size_t)nf * nw * sizeof(uint32_t));
         lists = align16((size_t)nf * (S > 0 ? S : 1) * sizeof(uint16_t));
-        region = cand > lists ? cand : lists;
-        scratch = align16((size_t)(threads / 32) * kCap * sizeof(uint16_t));
-        total = xs + ys + mb + region + scratch;
+        cand = align16((size_t)warps * kCap * sizeof(uint16_t));
+        scr = cand;
+        total = xs + ys + mb + lists + cand + scr;
     }
 };
 

@@ -54,51 +54,98 @@ __global__ void __launch_bounds__(1024) quantile_table_kernel(const int32_t* __r
     }
 }
 
-// Threshold key of column c (warp-level, see select.cuh).  `cl` (shared
-// address) holds the column's bracket candidates and is left intact, `scr`
-// is this warp's scratch list.
-__device__ __forceinline__ uint64_t resolve_column(const SweepArgs& A, uint32_t xs, int sx, int c, int n, int s,
-                                                   bool use_tab, int above, int in, uint32_t cl, uint32_t scr,
-                                                   bool& fallback, int lane) {
-    fallback = false;
-    if (!use_tab) {
+// One warp selects column c end to end: threshold key T (the s-th largest
+// key, select.cuh), the column's kept-set bitmap words (bit k of word k/32 =
+// key(k) >= T) and its ascending kept-row list.  `cand` / `scr` are this
+// warp's candidate and scratch lists (shared addresses, kCap entries each).
+__device__ __forceinline__ uint64_t select_column(const SweepArgs& A, uint32_t xs, int sx, int c, int n, int s,
+                                                  uint32_t words, uint32_t list, uint32_t cand, uint32_t scr,
+                                                  int lane) {
+    const uint32_t rowb = 4u * (uint32_t)sx;
+    const uint32_t xcol = xs + 4u * (uint32_t)c;
+    auto keyat = [xcol, rowb](int k) { return make_key(lds_f32(xcol + (uint32_t)k * rowb), (uint32_t)k); };
+    const int nwords = (n + 31) >> 5;
+    uint64_t T;
+    bool rebuild = true;  // derive all bitmap words from T
+    if (n <= kCap || A.qtab == nullptr) {
         IdxList Lst{xs, sx, c, scr, true};
-        return warp_select_idx(Lst, n, s, 0ull, ~0ull, lane);
-    }
-    const uint32_t* qc = A.qtab + (size_t)c * (kQ + 1);
-    int jhi, jlo;
-    table_levels(n, s, A.delta_tab, jhi, jlo);
-    const uint32_t hib = qc[jhi], lob = qc[jlo];
-    uint64_t hik = hi_key_of(hib), lok = (uint64_t)lob << 32;
-    if (above < s && s <= above + in && in <= kCap && lok < hik) {
-        for (int i = lane; i < in; i += 32) sts_u16(scr + 2u * i, lds_u16(cl + 2u * i));
+        T = warp_select_idx(Lst, n, s, 0ull, ~0ull, lane);
+    } else {
+        // one pass over the column: keys above the table bracket go straight
+        // into the bitmap, keys inside it are listed (ascending k)
+        const uint32_t* qc = A.qtab + (size_t)c * (kQ + 1);
+        int jhi, jlo;
+        table_levels(n, s, A.delta_tab, jhi, jlo);
+        const uint32_t hib = qc[jhi], lob = qc[jlo];
+        const uint64_t hik = hi_key_of(hib), lok = (uint64_t)lob << 32;
+        int above = 0, nin = 0;
+        uint32_t addr = xcol + (uint32_t)lane * rowb;
+        const uint32_t astep = 32u * rowb;
+        for (int k0 = 0; k0 < n; k0 += 32, addr += astep) {
+            const int k = k0 + lane;
+            const bool ok = k < n;
+            const uint32_t a = ok ? (__float_as_uint(lds_f32(addr)) & 0x7FFFFFFFu) : 0u;
+            const uint32_t bA = __ballot_sync(CALS_FULL_MASK, ok && a >= hib);
+            const bool in = ok && a >= lob && a < hib;
+            const uint32_t bI = __ballot_sync(CALS_FULL_MASK, in);
+            if (lane == 0) sts_u32(words + 4u * (uint32_t)(k0 >> 5), bA);
+            if (in) {
+                const int p = nin + __popc(bI & lanemask_lt());
+                if (p < kCap) sts_u16(cand + 2u * (uint32_t)p, (uint32_t)k);
+            }
+            above += __popc(bA);
+            nin += __popc(bI);
+        }
         __syncwarp();
-        IdxList Lst{xs, sx, c, scr, false};
-        int m = in, need = s - above;
-        warp_prenarrow(Lst, m, need, lok, hik, qc, jhi, jlo, lane);
-        return warp_select_idx(Lst, m, need, lok, hik, lane);
+        if (above < s && s <= above + nin && nin <= kCap && lok < hik) {
+            for (int i = lane; i < nin; i += 32) sts_u16(scr + 2u * i, lds_u16(cand + 2u * i));
+            __syncwarp();
+            IdxList Lst{xs, sx, c, scr, false};
+            int m = nin, need = s - above;
+            uint64_t lo = lok, hi = hik;
+            warp_prenarrow(Lst, m, need, lo, hi, qc, jhi, jlo, lane);
+            T = warp_select_idx(Lst, m, need, lo, hi, lane);
+            // bracket candidates at or above T join the kept set (above keys already in)
+            for (int i = lane; i < nin; i += 32) {
+                const uint32_t k = lds_u16(cand + 2u * i);
+                if (keyat((int)k) >= T) atoms_or(words + 4u * (k >> 5), 1u << (k & 31));
+            }
+            __syncwarp();
+            rebuild = false;
+        } else {
+            // the table bracket missed (or overflowed): exact column-mode search
+            uint64_t rlo, rhi;
+            int m, need;
+            if (above >= s) { rlo = hik; rhi = ~0ull; m = above; need = s; }
+            else if (above + nin < s) { rlo = 0ull; rhi = lok; m = n - above - nin; need = s - above - nin; }
+            else { rlo = lok; rhi = hik; m = nin; need = s - above; }
+            uint64_t* keybuf = reinterpret_cast<uint64_t*>(__cvta_shared_to_generic(scr));
+            T = warp_select_column(keyat, n, m, need, rlo, rhi, keybuf, (kCap * (int)sizeof(uint16_t)) / 8, lane);
+        }
     }
-    // the table bracket missed (or overflowed): exact column-mode search
-    fallback = true;
-    uint64_t rlo, rhi;
-    int m, need;
-    if (above >= s) { rlo = hik; rhi = ~0ull; m = above; need = s; }
-    else if (above + in < s) { rlo = 0ull; rhi = lok; m = n - above - in; need = s - above - in; }
-    else { rlo = lok; rhi = hik; m = in; need = s - above; }
-    auto keyat = [xs, sx, c](int k) { return make_key(lds_f32(xs + 4u * (uint32_t)(k * sx + c)), (uint32_t)k); };
-    uint64_t* keybuf = reinterpret_cast<uint64_t*>(__cvta_shared_to_generic(scr));
-    return warp_select_column(keyat, n, m, need, rlo, rhi, keybuf, (kCap * (int)sizeof(uint16_t)) / 8, lane);
+    if (rebuild) {
+        for (int k0 = 0; k0 < n; k0 += 32) {
+            const int k = k0 + lane;
+            const uint32_t b = __ballot_sync(CALS_FULL_MASK, k < n && keyat(k) >= T);
+            if (lane == 0) sts_u32(words + 4u * (uint32_t)(k0 >> 5), b);
+        }
+        __syncwarp();
+    }
+    bitmap_to_list(words, nwords, list, lane);
+    return T;
 }
 
 // ---------------------------------------------------------------------------
 // Phase A kernel (blockDim 128 or 256).  rows / n_list: this batch; the
 // normal equations of rows[li] go to A.gbuf + li * nf * (nf+1).
 // N: longest row of the batch; S: largest budget among its incomplete rows.
+// Warp w owns columns w, w + nwarps, ... of every row: selection, bitmap,
+// list and Gram rows of a column never leave its warp, so a row costs two
+// block barriers (after staging, before the next row's staging).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, const int32_t* __restrict__ rows,
                                                                  int64_t n_list, int N, int S) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ int cnt_above[CALS_MAX_NF_DEV], cnt_in[CALS_MAX_NF_DEV];
     __shared__ uint64_t thr[CALS_MAX_NF_DEV];
     __shared__ float wold[CALS_MAX_NF_DEV];
     __shared__ double red[32];
@@ -106,19 +153,19 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
     const int nf = A.nf;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const T1Layout L(N, S, nf, nt);
-    const int sx = L.sx, mw = L.mw, gs = nf + 1;
+    const int sx = L.sx, gs = nf + 1;
+    const int Smax = S > 0 ? S : 1;
     float* Xs = reinterpret_cast<float*>(smem);
     float* ys = reinterpret_cast<float*>(smem + L.xs);
-    uint32_t* mb = reinterpret_cast<uint32_t*>(smem + L.xs + L.ys);
     const uint32_t s_xs = smem_u32(smem);
     const uint32_t s_ys = s_xs + (uint32_t)L.xs;
     const uint32_t s_mb = s_ys + (uint32_t)L.ys;
-    const uint32_t s_cand = s_mb + (uint32_t)L.mb;
-    const uint32_t s_lists = s_cand;  // reused once the thresholds are known
-    const uint32_t s_scr = s_cand + (uint32_t)L.region + 2u * (uint32_t)(warp * kCap);
+    const uint32_t s_lists = s_mb + (uint32_t)L.mb;
+    const uint32_t s_cand = s_lists + (uint32_t)L.lists + 2u * (uint32_t)(warp * kCap);
+    const uint32_t s_scr = s_lists + (uint32_t)L.lists + (uint32_t)L.cand + 2u * (uint32_t)(warp * kCap);
     const uint32_t rowb = 4u * (uint32_t)sx;
     const FastDiv fq((uint32_t)xs_chunks(nf));
-    const bool ballot_bits = (32 % nf == 0) || (nf % 32 == 0);
+    const int my_cols = warp < nf ? (nf - 1 - warp) / nwarps + 1 : 0;
 
     for (int64_t li = blockIdx.x; li < n_list; li += gridDim.x) {
         const int row = rows[li];
@@ -127,119 +174,69 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
         const int s = A.budget[row];
         const bool full = (s >= n);
 
-        // ---- stage the slice [X | y]; clear the bitmap ----
         stage_slice(A, lo, 0, n, Xs, ys, fq);
-        for (int e = tid; e < n * mw; e += nt) mb[e] = 0u;
-        if (tid < nf) {
-            cnt_above[tid] = 0;
-            cnt_in[tid] = 0;
-            if (A.tgt_old != nullptr) wold[tid] = A.tgt_old[(int64_t)row * A.ld_old + tid];
-        }
+        if (tid < nf && A.tgt_old != nullptr) wold[tid] = A.tgt_old[(int64_t)row * A.ld_old + tid];
         __syncthreads();
 
         // ---- fused residual of the previous iteration's row (als.py:287-288) ----
         if (A.rss_rows != nullptr) {
             double acc = 0.0;
+            const int nq = xs_chunks(nf);
             for (int k = tid; k < n; k += nt) {
                 const uint32_t rb = s_xs + (uint32_t)k * rowb;
-                double pred = 0.0;
-                for (int f = 0; f < nf; ++f) pred = fma((double)lds_f32(rb + 4u * f), (double)wold[f], pred);
-                const double d = (double)lds_f32(s_ys + 4u * k) - pred;
+                float pred = 0.f;
+                for (int q = 0; q < nq; ++q) {
+                    const float4 v = lds_f128(rb + 16u * q);
+                    const int f = 4 * q;
+                    pred = fmaf(v.x, wold[f], pred);
+                    if (f + 1 < nf) pred = fmaf(v.y, wold[f + 1], pred);
+                    if (f + 2 < nf) pred = fmaf(v.z, wold[f + 2], pred);
+                    if (f + 3 < nf) pred = fmaf(v.w, wold[f + 3], pred);
+                }
+                const double d = (double)lds_f32(s_ys + 4u * k) - (double)pred;
                 acc = fma(d, d, acc);
             }
-            acc = block_sum_d(acc, red);
-            if (tid == 0) A.rss_rows[row] = acc;
+            acc = warp_sum_d(acc);
+            if (lane == 0) red[warp] = acc;
         }
 
-        // ---- selection: threshold key per column, kept-set bitmap ----
-        if (!full) {
-            const bool use_tab = (n > kCap) && (A.qtab != nullptr);
-            if (use_tab) {
-                // one pass: keys above the table bracket go straight into the
-                // bitmap (ballots), keys inside it are listed per column
-                const int per = nt / nf;
-                const int c = tid % nf, j = tid / nf;
-                const bool active = tid < per * nf;
-                uint32_t hib = kAbsInf, lob = kAbsInf;
-                if (active) table_bracket(A.qtab + (size_t)c * (kQ + 1), n, s, A.delta_tab, hib, lob);
-                const uint32_t cl = s_cand + 2u * (uint32_t)(c * kCap);
-                int above = 0;
-                const int iters = (n + per - 1) / per;
-                const int rsh = (lane / (nf <= 32 ? nf : 32)) * nf;
-                const uint32_t rmask = nf >= 32 ? 0xffffffffu : ((1u << nf) - 1u);
-                const bool writer = nf <= 32 ? (c == 0) : (lane == 0);
-                uint32_t addr = s_xs + (uint32_t)j * rowb + 4u * (uint32_t)c;
-                const uint32_t astep = (uint32_t)per * rowb;
-                int k = j;
-                for (int it = 0; it < iters; ++it, k += per, addr += astep) {
-                    const bool ok = active && k < n;
-                    const uint32_t a = ok ? (__float_as_uint(lds_f32(addr)) & 0x7FFFFFFFu) : 0u;
-                    const bool ab = ok && a >= hib;
-                    above += ab;
-                    if (ok && a >= lob && a < hib) {
-                        const int slot = atomicAdd(&cnt_in[c], 1);
-                        if (slot < kCap) sts_u16(cl + 2u * slot, k);
-                    }
-                    if (ballot_bits) {
-                        const uint32_t bal = __ballot_sync(CALS_FULL_MASK, ab);
-                        if (writer && ok) sts_u32(s_mb + 4u * (uint32_t)(k * mw + (c >> 5)), (bal >> rsh) & rmask);
-                    } else if (ab) {
-                        atomicOr(&mb[k * mw + (c >> 5)], 1u << (c & 31));
-                    }
-                }
-                if (active) atomicAdd(&cnt_above[c], above);
-                __syncthreads();
-            }
-            for (int c = warp; c < nf; c += nwarps) {
-                bool fallback;
-                const uint32_t cl = s_cand + 2u * (uint32_t)(c * kCap);
-                const uint64_t T = resolve_column(A, s_xs, sx, c, n, s, use_tab, cnt_above[c], cnt_in[c], cl, s_scr,
-                                                  fallback, lane);
-                if (lane == 0) thr[c] = T;
-                const uint32_t bit = 1u << (c & 31);
-                uint32_t* mcol = mb + (c >> 5);
-                const uint32_t xcol = s_xs + 4u * (uint32_t)c;
-                if (!use_tab || fallback) {
-                    // (re)derive column c entirely: kept iff key >= T
+        // ---- per owned column: selection -> bitmap -> kept-row list ----
+        for (int j = 0; j < my_cols; ++j) {
+            const int c = warp + j * nwarps;
+            uint64_t T;
+            if (!full) {
+                T = select_column(A, s_xs, sx, c, n, s, s_mb + 4u * (uint32_t)(c * L.nw),
+                                  s_lists + 2u * (uint32_t)(c * Smax), s_cand, s_scr, lane);
+            } else {
+                T = ~0ull;
+                if (A.thr_keys != nullptr) {  // complete sketch: report the smallest key
                     for (int k = lane; k < n; k += 32) {
-                        const bool keep = make_key(lds_f32(xcol + (uint32_t)k * rowb), (uint32_t)k) >= T;
-                        if (keep) atomicOr(mcol + k * mw, bit);
-                        else if (fallback) atomicAnd(mcol + k * mw, ~bit);
+                        const uint64_t kk = make_key(lds_f32(s_xs + (uint32_t)k * rowb + 4u * c), (uint32_t)k);
+                        T = kk < T ? kk : T;
                     }
-                } else {
-                    // bracket candidates at or above the threshold join the kept set
-                    const int in = cnt_in[c];
-                    for (int i = lane; i < in; i += 32) {
-                        const uint32_t k = lds_u16(cl + 2u * i);
-                        if (make_key(lds_f32(xcol + k * rowb), k) >= T) atomicOr(mcol + k * mw, bit);
-                    }
-                }
-            }
-        } else if (A.thr_keys != nullptr) {
-            // complete sketch: every row kept; report the smallest key per column
-            for (int c = warp; c < nf; c += nwarps) {
-                uint64_t mn = ~0ull;
-                for (int k = lane; k < n; k += 32) {
-                    const uint64_t kk = make_key(lds_f32(s_xs + (uint32_t)k * rowb + 4u * c), (uint32_t)k);
-                    mn = kk < mn ? kk : mn;
-                }
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const uint64_t t = __shfl_xor_sync(CALS_FULL_MASK, mn, o);
-                    mn = t < mn ? t : mn;
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const uint64_t t = __shfl_xor_sync(CALS_FULL_MASK, T, o);
+                        T = t < T ? t : T;
+                    }
                 }
-                if (lane == 0) thr[c] = mn;
             }
+            if (lane == 0) thr[c] = T;
         }
-        __syncthreads();
 
-        // ---- sparse Gram -> global normal equations ----
+        // ---- sparse Gram of the owned columns -> global normal equations ----
         const float lam_n = (float)(A.lam * (double)n);
-        sparse_gram(s_xs, sx, s_ys, s_mb, mw, n, nf, s, full, s_lists, S > 0 ? S : 1, lam_n,
-                    A.gbuf + (size_t)li * nf * gs, warp, nwarps, lane);
+        if (my_cols > 0)
+            sparse_gram_owned_any(s_xs, sx, s_ys, nf, full ? n : s, full, s_lists, Smax, warp, nwarps, my_cols, lam_n,
+                                  A.gbuf + (size_t)li * nf * gs, lane);
+        __syncthreads();
+        if (A.rss_rows != nullptr && tid == 0) {
+            double r = 0.0;
+            for (int w = 0; w < nwarps; ++w) r += red[w];
+            A.rss_rows[row] = r;
+        }
         if (A.thr_keys != nullptr)
             for (int c = tid; c < nf; c += nt) A.thr_keys[(int64_t)row * nf + c] = thr[c];
-        __syncthreads();
     }
 }
 
