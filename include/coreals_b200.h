@@ -167,6 +167,10 @@ int cals_predict_entries(const float* U, const float* M, int n_f, int ld_u, int 
  * (for bench.py's roofline numbers).  collect() synchronises on the recorded
  * events, writes "name launches total_ms" lines into buf, and resets. */
 void cals_profile_enable(int on);
+/* Debug: point the sweep kernels at 16 device uint64 counters (NULL = off):
+ * [0] table-resolved columns, [1] bracket fallbacks, [2] bracket candidates,
+ * [3] candidates after pre-narrowing, [4] extra select rounds, [5] rows. */
+void cals_debug_stats(void* device_counters);
 int cals_profile_collect(char* buf, size_t len);
 
 const char* cals_strerror(int status);

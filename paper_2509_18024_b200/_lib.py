@@ -50,6 +50,7 @@ SIGNATURES = {
     "cals_update_core": (i32, [P, i64, i32, P, P, P, f64, i32, P, P, P]),
     "cals_predict_entries": (i32, [P, P, i32, i32, i32, P, P, i64, P, P]),
     "cals_profile_enable": (None, [i32]),
+    "cals_debug_stats": (None, [P]),
     "cals_profile_collect": (i32, [ctypes.c_char_p, sz]),
     "cals_strerror": (ctypes.c_char_p, [i32]),
     "cals_build_info": (ctypes.c_char_p, []),

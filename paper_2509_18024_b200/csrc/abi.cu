@@ -21,6 +21,7 @@ constexpr int kQSsmall = 4096, kQSbig = 8192;
 constexpr int kItemRowsMin = 4096;
 
 thread_local char g_err[256] = "";
+unsigned long long* g_stats = nullptr;  // debug counters (device), see cals_debug_stats
 
 // ---- optional per-kernel timing (CUDA events on the launch stream) --------
 struct ProfRec {
@@ -70,7 +71,7 @@ struct ProfScope {
 
 inline float delta_tab_for(int QS) { return 3.0f * 0.5f / std::sqrt((float)QS); }
 
-constexpr size_t kSmallSmem = 110 * 1024;  // staged-tier CTA budget: two CTAs per SM
+constexpr size_t kSmallSmem = 150 * 1024;  // staged-tier CTA budget
 
 inline int budget_of(int64_t n, double rate) {
     volatile double prod = (double)n * rate;
@@ -229,9 +230,23 @@ void launch_solve(const SweepArgs& A, const int32_t* rows, int64_t count, cudaSt
     }
 }
 
+template <int CPL>
+void launch_gram(const SweepArgs& A, int grid, int threads, size_t smem, cudaStream_t st, const int32_t* rows,
+                 int64_t cnt, int N, int S) {
+    allow_smem(small_gram_kernel<CPL>);
+    small_gram_kernel<CPL><<<grid, threads, smem, st>>>(A, rows, cnt, N, S);
+}
+
+template <int CPL>
+int gram_grid(size_t smem, int64_t cnt, int threads) {
+    allow_smem(small_gram_kernel<CPL>);
+    return grid_for(small_gram_kernel<CPL>, smem, cnt, 16, threads);
+}
+
 template <int NFP>
 int launch_small(SweepArgs A, const cals_plan* P, const Work& w, cudaStream_t st) {
-    allow_smem(small_gram_kernel);
+    const int nq = xs_chunks(A.nf);
+    const int CPL = nq <= 4 ? 1 : (nq <= 8 ? 2 : (nq <= 16 ? 4 : 8));
     for (int g = 0; g < 3; ++g) {
         const int64_t b = P->small_seg[g], e = P->small_seg[g + 1];
         if (e <= b) continue;
@@ -241,10 +256,13 @@ int launch_small(SweepArgs A, const cals_plan* P, const Work& w, cudaStream_t st
         const size_t smem = T1Layout(N, S, A.nf, threads).total;
         for (int64_t b0 = b; b0 < e; b0 += w.gbuf_rows) {
             const int64_t cnt = std::min<int64_t>(w.gbuf_rows, e - b0);
-            const int grid = grid_for(small_gram_kernel, smem, cnt, 16, threads);
             {
                 ProfScope ps("small_gram_kernel", st);
-                small_gram_kernel<<<grid, threads, smem, st>>>(A, P->small_rows + b0, cnt, N, S);
+                const int32_t* rr = P->small_rows + b0;
+                if (CPL == 1) launch_gram<1>(A, gram_grid<1>(smem, cnt, threads), threads, smem, st, rr, cnt, N, S);
+                else if (CPL == 2) launch_gram<2>(A, gram_grid<2>(smem, cnt, threads), threads, smem, st, rr, cnt, N, S);
+                else if (CPL == 4) launch_gram<4>(A, gram_grid<4>(smem, cnt, threads), threads, smem, st, rr, cnt, N, S);
+                else launch_gram<8>(A, gram_grid<8>(smem, cnt, threads), threads, smem, st, rr, cnt, N, S);
             }
             launch_solve<NFP>(A, P->small_rows + b0, cnt, st);
         }
@@ -414,13 +432,14 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.pen_rows = pen_rows;
     A.thr_keys = thr_keys;
     A.gbuf = w.gbuf;
+    A.stats = g_stats;
     A.status = row_status;
     A.summary = reinterpret_cast<unsigned long long*>(status_summary);
     A.qtab = nullptr;
     A.retry_ws = w.retry;
     A.retry_stride = retry_stride(n_f);
 
-    const bool long_small = P->n_small > 0 && P->small_seg_maxn[0] > kCap;
+    const bool long_small = P->n_small > 0 && P->small_seg_maxn[0] > 16;
     if ((long_small || P->n_big > 0) && side->nnz > 0) {
         const int QS = P->n_big > 0 ? kQSbig : kQSsmall;
         allow_smem(quantile_table_kernel);
@@ -527,6 +546,8 @@ int cals_predict_entries(const float* U, const float* M, int n_f, int ld_u, int 
     predict_entries_kernel<<<(int)blocks, 256, 0, st>>>(U, M, n_f, ld_u, ld_m, users, items, n, out);
     return cuda_status("cals_predict_entries");
 }
+
+void cals_debug_stats(void* device_counters) { g_stats = (unsigned long long*)device_counters; }
 
 void cals_profile_enable(int on) {
     Prof& P = prof();

@@ -35,7 +35,14 @@ struct SweepArgs {
     double* retry_ws;             // per-warp float64 jitter-retry scratch (retry_stride doubles each)
     int retry_stride;
     float* gbuf;                  // normal equations of the current batch: [slot][nf][nf+1]
+    unsigned long long* stats;    // nullable debug counters (cals_debug_stats)
 };
+
+// Debug counters (only when A.stats != nullptr): see cals_debug_stats.
+enum StatId { kStColumns = 0, kStFallback, kStCandidates, kStAfterPrenarrow, kStSelectRounds, kStRows, kStCount = 16 };
+__device__ __forceinline__ void stat_add(const SweepArgs& A, int id, unsigned long long v) {
+    if (A.stats != nullptr) atomicAdd(A.stats + id, v);
+}
 
 __device__ __forceinline__ void report_status(const SweepArgs& A, int row, int st) {
     if (st != 0 && A.summary != nullptr)
@@ -126,24 +133,55 @@ __device__ __forceinline__ void stage_slice(const SweepArgs& A, int64_t lo, int 
     cp_async_wait_all();
 }
 
+// Column lanes / slots of the staged-slice kernel: thread t handles column
+// t % NFP over the k-range of slot t / NFP (ranges are multiples of 32 rows,
+// so every bitmap word has a single owner).
+struct SlotMap {
+    int NFP, P;
+    __host__ __device__ SlotMap(int nf, int threads) {
+        if (nf <= 32) {
+            NFP = 1;
+            while (NFP < nf) NFP <<= 1;
+        } else {
+            NFP = (nf + 31) / 32 * 32;
+        }
+        P = threads / NFP;
+        if (P < 1) P = 1;
+    }
+    __host__ __device__ int chunk(int n) const { return ((n + P - 1) / P + 31) / 32 * 32; }
+    __host__ __device__ int caps(int chunk_rows) const {
+        const int c = 16 + chunk_rows / 4;
+        return c < chunk_rows ? c : chunk_rows;
+    }
+};
+
+constexpr int kFinalCap = 64;  // per-column candidates of the chosen sub-bucket
+
 // Shared-memory footprint of the staged-slice kernel for rows of length <= N
 // whose sketch budget is <= S:
-//   Xs [N][sx] | ys [N] | bitmap [nf][ceil(N/32)] (column-major) |
-//   lists [nf][S] | per-warp candidates [kCap] | per-warp scratch [kCap]
+//   Xs [N][sx] | ys [N] | bitmap [nf][ceil(N/32)] (column-major) | lists [nf][S] |
+//   slot candidates [P][CAPS][NFP] u16 | slot level counts [P][8][NFP] u8 |
+//   slot above/in counts [P][NFP] 2 x u16 | final buffers [nf][kFinalCap] u16 |
+//   per-warp key scratch [kFinalCap] u64
 struct T1Layout {
-    size_t xs, ys, mb, lists, cand, scr, total;
-    int sx, nw;
+    size_t xs, ys, mb, lists, cand, lvl, cnts, fb, scr, total;
+    int sx, nw, caps;
     __host__ __device__ T1Layout(int N, int S, int nf, int threads) {
+        const SlotMap M(nf, threads);
         sx = xs_stride(nf);
         nw = (N + 31) / 32;
+        caps = M.caps(M.chunk(N));
         const int warps = threads / 32;
         xs = align16((size_t)N * sx * sizeof(float));
         ys = align16((size_t)N * sizeof(float));
         mb = align16((size_t)nf * nw * sizeof(uint32_t));
         lists = align16((size_t)nf * (S > 0 ? S : 1) * sizeof(uint16_t));
-        cand = align16((size_t)warps * kCap * sizeof(uint16_t));
-        scr = cand;
-        total = xs + ys + mb + lists + cand + scr;
+        cand = align16((size_t)M.P * caps * M.NFP * sizeof(uint16_t));
+        lvl = align16((size_t)M.P * 8 * M.NFP);
+        cnts = align16((size_t)M.P * M.NFP * 2 * sizeof(uint16_t));
+        fb = align16((size_t)nf * kFinalCap * sizeof(uint16_t));
+        scr = align16((size_t)warps * kFinalCap * sizeof(uint64_t));
+        total = xs + ys + mb + lists + cand + lvl + cnts + fb + scr;
     }
 };
 

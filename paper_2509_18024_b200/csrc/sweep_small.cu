@@ -54,106 +54,35 @@ __global__ void __launch_bounds__(1024) quantile_table_kernel(const int32_t* __r
     }
 }
 
-// One warp selects column c end to end: threshold key T (the s-th largest
-// key, select.cuh), the column's kept-set bitmap words (bit k of word k/32 =
-// key(k) >= T) and its ascending kept-row list.  `cand` / `scr` are this
-// warp's candidate and scratch lists (shared addresses, kCap entries each).
-__device__ __forceinline__ uint64_t select_column(const SweepArgs& A, uint32_t xs, int sx, int c, int n, int s,
-                                                  uint32_t words, uint32_t list, uint32_t cand, uint32_t scr,
-                                                  int lane) {
-    const uint32_t rowb = 4u * (uint32_t)sx;
-    const uint32_t xcol = xs + 4u * (uint32_t)c;
-    auto keyat = [xcol, rowb](int k) { return make_key(lds_f32(xcol + (uint32_t)k * rowb), (uint32_t)k); };
-    const int nwords = (n + 31) >> 5;
-    uint64_t T;
-    bool rebuild = true;  // derive all bitmap words from T
-    if (n <= kCap || A.qtab == nullptr) {
-        IdxList Lst{xs, sx, c, scr, true};
-        T = warp_select_idx(Lst, n, s, 0ull, ~0ull, lane);
-    } else {
-        // one pass over the column: keys above the table bracket go straight
-        // into the bitmap, keys inside it are listed (ascending k)
-        const uint32_t* qc = A.qtab + (size_t)c * (kQ + 1);
-        int jhi, jlo;
-        table_levels(n, s, A.delta_tab, jhi, jlo);
-        const uint32_t hib = qc[jhi], lob = qc[jlo];
-        const uint64_t hik = hi_key_of(hib), lok = (uint64_t)lob << 32;
-        int above = 0, nin = 0;
-        uint32_t addr = xcol + (uint32_t)lane * rowb;
-        const uint32_t astep = 32u * rowb;
-        for (int k0 = 0; k0 < n; k0 += 32, addr += astep) {
-            const int k = k0 + lane;
-            const bool ok = k < n;
-            const uint32_t a = ok ? (__float_as_uint(lds_f32(addr)) & 0x7FFFFFFFu) : 0u;
-            const uint32_t bA = __ballot_sync(CALS_FULL_MASK, ok && a >= hib);
-            const bool in = ok && a >= lob && a < hib;
-            const uint32_t bI = __ballot_sync(CALS_FULL_MASK, in);
-            if (lane == 0) sts_u32(words + 4u * (uint32_t)(k0 >> 5), bA);
-            if (in) {
-                const int p = nin + __popc(bI & lanemask_lt());
-                if (p < kCap) sts_u16(cand + 2u * (uint32_t)p, (uint32_t)k);
-            }
-            above += __popc(bA);
-            nin += __popc(bI);
-        }
-        __syncwarp();
-        if (above < s && s <= above + nin && nin <= kCap && lok < hik) {
-            for (int i = lane; i < nin; i += 32) sts_u16(scr + 2u * i, lds_u16(cand + 2u * i));
-            __syncwarp();
-            IdxList Lst{xs, sx, c, scr, false};
-            int m = nin, need = s - above;
-            uint64_t lo = lok, hi = hik;
-            warp_prenarrow(Lst, m, need, lo, hi, qc, jhi, jlo, lane);
-            T = warp_select_idx(Lst, m, need, lo, hi, lane);
-            // bracket candidates at or above T join the kept set (above keys already in)
-            for (int i = lane; i < nin; i += 32) {
-                const uint32_t k = lds_u16(cand + 2u * i);
-                if (keyat((int)k) >= T) atoms_or(words + 4u * (k >> 5), 1u << (k & 31));
-            }
-            __syncwarp();
-            rebuild = false;
-        } else {
-            // the table bracket missed (or overflowed): exact column-mode search
-            uint64_t rlo, rhi;
-            int m, need;
-            if (above >= s) { rlo = hik; rhi = ~0ull; m = above; need = s; }
-            else if (above + nin < s) { rlo = 0ull; rhi = lok; m = n - above - nin; need = s - above - nin; }
-            else { rlo = lok; rhi = hik; m = nin; need = s - above; }
-            uint64_t* keybuf = reinterpret_cast<uint64_t*>(__cvta_shared_to_generic(scr));
-            T = warp_select_column(keyat, n, m, need, rlo, rhi, keybuf, (kCap * (int)sizeof(uint16_t)) / 8, lane);
-        }
-    }
-    if (rebuild) {
-        for (int k0 = 0; k0 < n; k0 += 32) {
-            const int k = k0 + lane;
-            const uint32_t b = __ballot_sync(CALS_FULL_MASK, k < n && keyat(k) >= T);
-            if (lane == 0) sts_u32(words + 4u * (uint32_t)(k0 >> 5), b);
-        }
-        __syncwarp();
-    }
-    bitmap_to_list(words, nwords, list, lane);
-    return T;
-}
-
 // ---------------------------------------------------------------------------
 // Phase A kernel (blockDim 128 or 256).  rows / n_list: this batch; the
 // normal equations of rows[li] go to A.gbuf + li * nf * (nf+1).
 // N: longest row of the batch; S: largest budget among its incomplete rows.
-// Warp w owns columns w, w + nwarps, ... of every row: selection, bitmap,
-// list and Gram rows of a column never leave its warp, so a row costs two
-// block barriers (after staging, before the next row's staging).
+//
+// Selection runs SIMT across columns: thread (c, slot) scans column c over
+// its slot's k-range (sequential, conflict-free shared loads), writes the
+// "above the table bracket" bits of its own bitmap words, lists the keys in
+// the bracket and counts them against the table levels inside the bracket.
+// One thread per column then picks the sub-bucket holding the target rank,
+// the slot threads forward that sub-bucket's keys (typically ~10), and one
+// warp per column sorts them to read off the threshold key T.  Keys of the
+// bracket at or above T join the bitmap; lists are built from the bitmap.
+// Any miss (bracket, capacity) falls back to an exact warp search.
 // ---------------------------------------------------------------------------
+template <int CPL>
 __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, const int32_t* __restrict__ rows,
                                                                  int64_t n_list, int N, int S) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ uint64_t thr[CALS_MAX_NF_DEV];
+    __shared__ uint64_t thr[CALS_MAX_NF_DEV], c_lo[CALS_MAX_NF_DEV], c_hi[CALS_MAX_NF_DEV];
+    __shared__ int c_need[CALS_MAX_NF_DEV], c_flag[CALS_MAX_NF_DEV], c_fc[CALS_MAX_NF_DEV];
     __shared__ float wold[CALS_MAX_NF_DEV];
     __shared__ double red[32];
 
     const int nf = A.nf;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const T1Layout L(N, S, nf, nt);
-    const int sx = L.sx, gs = nf + 1;
+    const SlotMap SM(nf, nt);
+    const int sx = L.sx, gs = nf + 1, NW = L.nw, CAPS = L.caps, NFP = SM.NFP, P = SM.P;
     const int Smax = S > 0 ? S : 1;
     float* Xs = reinterpret_cast<float*>(smem);
     float* ys = reinterpret_cast<float*>(smem + L.xs);
@@ -161,11 +90,17 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
     const uint32_t s_ys = s_xs + (uint32_t)L.xs;
     const uint32_t s_mb = s_ys + (uint32_t)L.ys;
     const uint32_t s_lists = s_mb + (uint32_t)L.mb;
-    const uint32_t s_cand = s_lists + (uint32_t)L.lists + 2u * (uint32_t)(warp * kCap);
-    const uint32_t s_scr = s_lists + (uint32_t)L.lists + (uint32_t)L.cand + 2u * (uint32_t)(warp * kCap);
+    const uint32_t s_cand = s_lists + (uint32_t)L.lists;
+    const uint32_t s_lvl = s_cand + (uint32_t)L.cand;
+    const uint32_t s_cnt = s_lvl + (uint32_t)L.lvl;
+    const uint32_t s_fb = s_cnt + (uint32_t)L.cnts;
+    uint64_t* wscr = reinterpret_cast<uint64_t*>(smem + L.xs + L.ys + L.mb + L.lists + L.cand + L.lvl + L.cnts + L.fb) +
+                     warp * kFinalCap;
     const uint32_t rowb = 4u * (uint32_t)sx;
     const FastDiv fq((uint32_t)xs_chunks(nf));
     const int my_cols = warp < nf ? (nf - 1 - warp) / nwarps + 1 : 0;
+    const int cl = tid % NFP, slot = tid / NFP;
+    const bool col_thread = cl < nf && slot < P;
 
     for (int64_t li = blockIdx.x; li < n_list; li += gridDim.x) {
         const int row = rows[li];
@@ -173,6 +108,10 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
         const int n = (int)(A.ptr[row + 1] - lo);
         const int s = A.budget[row];
         const bool full = (s >= n);
+        const bool use_tab = !full && A.qtab != nullptr && n > 16;
+        int jhi = 0, jlo = 0;
+        if (use_tab) table_levels(n, s, A.delta_tab, jhi, jlo);
+        const int chunk = SM.chunk(n);
 
         stage_slice(A, lo, 0, n, Xs, ys, fq);
         if (tid < nf && A.tgt_old != nullptr) wold[tid] = A.tgt_old[(int64_t)row * A.ld_old + tid];
@@ -200,18 +139,130 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
             if (lane == 0) red[warp] = acc;
         }
 
-        // ---- per owned column: selection -> bitmap -> kept-row list ----
+        if (use_tab) {
+            // ---- S2: per (column, slot) scan of the k-range ----
+            if (col_thread) {
+                const uint32_t* qc = A.qtab + (size_t)cl * (kQ + 1);
+                const uint32_t hib = qc[jhi], lob = qc[jlo];
+                const int span = jlo - jhi;
+                const int k0 = slot * chunk, k1 = min(n, k0 + chunk);
+                int above = 0, nin = 0;
+                uint32_t word = 0;
+                uint32_t addr = s_xs + (uint32_t)k0 * rowb + 4u * (uint32_t)cl;
+                const uint32_t cbase = s_cand + 2u * (uint32_t)(slot * CAPS * NFP + cl);
+                for (int k = k0; k < k1; ++k, addr += rowb) {
+                    const uint32_t a = __float_as_uint(lds_f32(addr)) & 0x7FFFFFFFu;
+                    const uint32_t ab = a >= hib ? 1u : 0u;
+                    word |= ab << (k & 31);
+                    above += (int)ab;
+                    if (a >= lob && a < hib) {
+                        if (nin < CAPS) sts_u16(cbase + 2u * (uint32_t)(nin * NFP), (uint32_t)k);
+                        ++nin;
+                    }
+                    if ((k & 31) == 31 || k == k1 - 1) {
+                        sts_u32(s_mb + 4u * (uint32_t)(cl * NW + (k >> 5)), word);
+                        word = 0u;
+                    }
+                }
+                const uint32_t ci = s_cnt + 4u * (uint32_t)(slot * NFP + cl);
+                sts_u16(ci, (uint32_t)above);
+                sts_u16(ci + 2u, nin > CAPS ? 0xFFFFu : (uint32_t)nin);
+                // counts of the listed keys against the table levels inside the bracket
+                uint32_t lev[kSub - 1];
+                int lc[kSub - 1];
+#pragma unroll
+                for (int t = 0; t < kSub - 1; ++t) {
+                    lev[t] = qc[jhi + (span * (t + 1)) / kSub];
+                    lc[t] = 0;
+                }
+                const int nl = min(nin, CAPS);
+                const uint32_t xcol = s_xs + 4u * (uint32_t)cl;
+                for (int i = 0; i < nl; ++i) {
+                    const uint32_t k = lds_u16(cbase + 2u * (uint32_t)(i * NFP));
+                    const uint32_t a = __float_as_uint(lds_f32(xcol + k * rowb)) & 0x7FFFFFFFu;
+#pragma unroll
+                    for (int t = 0; t < kSub - 1; ++t) lc[t] += (a >= lev[t]) ? 1 : 0;
+                }
+#pragma unroll
+                for (int t = 0; t < kSub - 1; ++t)
+                    sts_u8(s_lvl + (uint32_t)((slot * 8 + t) * NFP + cl), (uint32_t)min(lc[t], 255));
+            }
+            __syncthreads();
+            // ---- S3: per column, the sub-bucket that holds the target rank ----
+            if (tid < nf) {
+                const int c = tid;
+                int above = 0, nin = 0;
+                bool over = false;
+                int cge[kSub - 1];
+#pragma unroll
+                for (int t = 0; t < kSub - 1; ++t) cge[t] = 0;
+                for (int q = 0; q < P; ++q) {
+                    const uint32_t ci = s_cnt + 4u * (uint32_t)(q * NFP + c);
+                    above += (int)lds_u16(ci);
+                    const uint32_t ni = lds_u16(ci + 2u);
+                    over |= (ni == 0xFFFFu);
+                    nin += (int)(ni & 0xFFFFu);
+#pragma unroll
+                    for (int t = 0; t < kSub - 1; ++t) cge[t] += (int)lds_u8(s_lvl + (uint32_t)((q * 8 + t) * NFP + c));
+                }
+                const uint32_t* qc = A.qtab + (size_t)c * (kQ + 1);
+                const uint32_t hib = qc[jhi], lob = qc[jlo];
+                const uint64_t hik = hi_key_of(hib), lok = (uint64_t)lob << 32;
+                const bool ok = !over && above < s && s <= above + nin && lok < hik;
+                c_flag[c] = ok ? 0 : 1;
+                c_fc[c] = 0;
+                if (ok) {
+                    const int need = s - above;
+                    const int span = jlo - jhi;
+                    int b = 0;
+#pragma unroll
+                    for (int t = 0; t < kSub - 1; ++t) b += (cge[t] < need) ? 1 : 0;
+                    uint64_t bhi = hik, blo = lok;
+                    int before = 0;
+#pragma unroll
+                    for (int t = 0; t < kSub - 1; ++t) {
+                        const uint64_t lv = (uint64_t)qc[jhi + (span * (t + 1)) / kSub] << 32;
+                        if (t == b - 1) { bhi = lv < hik ? lv : hik; before = cge[t]; }
+                        if (t == b) blo = lv > lok ? lv : lok;
+                    }
+                    c_lo[c] = blo;
+                    c_hi[c] = bhi;
+                    c_need[c] = need - before;
+                }
+                if (lane == 0 && A.stats != nullptr) {
+                    stat_add(A, kStColumns, 1);
+                    stat_add(A, kStCandidates, (unsigned long long)nin);
+                }
+            }
+            __syncthreads();
+            // ---- S4: forward the chosen sub-bucket's keys ----
+            if (col_thread && c_flag[cl] == 0) {
+                const int nin = min((int)lds_u16(s_cnt + 4u * (uint32_t)(slot * NFP + cl) + 2u), CAPS);
+                const uint32_t cbase = s_cand + 2u * (uint32_t)(slot * CAPS * NFP + cl);
+                const uint64_t blo = c_lo[cl], bhi = c_hi[cl];
+                const uint32_t xcol = s_xs + 4u * (uint32_t)cl;
+                for (int i = 0; i < nin; ++i) {
+                    const uint32_t k = lds_u16(cbase + 2u * (uint32_t)(i * NFP));
+                    const uint64_t key = make_key(lds_f32(xcol + k * rowb), k);
+                    if (key >= blo && key < bhi) {
+                        const int p = atomicAdd(&c_fc[cl], 1);
+                        if (p < kFinalCap) sts_u16(s_fb + 2u * (uint32_t)(cl * kFinalCap + p), k);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+
+        // ---- S5: threshold key per column (warp per column) ----
         for (int j = 0; j < my_cols; ++j) {
             const int c = warp + j * nwarps;
-            uint64_t T;
-            if (!full) {
-                T = select_column(A, s_xs, sx, c, n, s, s_mb + 4u * (uint32_t)(c * L.nw),
-                                  s_lists + 2u * (uint32_t)(c * Smax), s_cand, s_scr, lane);
-            } else {
-                T = ~0ull;
+            const uint32_t xcol = s_xs + 4u * (uint32_t)c;
+            auto keyat = [xcol, rowb](int k) { return make_key(lds_f32(xcol + (uint32_t)k * rowb), (uint32_t)k); };
+            uint64_t T = ~0ull;
+            if (full) {
                 if (A.thr_keys != nullptr) {  // complete sketch: report the smallest key
                     for (int k = lane; k < n; k += 32) {
-                        const uint64_t kk = make_key(lds_f32(s_xs + (uint32_t)k * rowb + 4u * c), (uint32_t)k);
+                        const uint64_t kk = keyat(k);
                         T = kk < T ? kk : T;
                     }
 #pragma unroll
@@ -220,15 +271,64 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
                         T = t < T ? t : T;
                     }
                 }
+            } else {
+                const int m = use_tab ? c_fc[c] : 0;
+                const bool exact = !use_tab || c_flag[c] != 0 || m > kFinalCap;
+                if (!exact) {
+                    const int need = c_need[c];
+                    if (m <= 32) {
+                        uint64_t v = lane < m ? keyat((int)lds_u16(s_fb + 2u * (uint32_t)(c * kFinalCap + lane))) : 0ull;
+                        v = warp_sort_desc(v, lane);
+                        T = __shfl_sync(CALS_FULL_MASK, v, need - 1);
+                    } else {
+                        for (int i = lane; i < m; i += 32)
+                            wscr[i] = keyat((int)lds_u16(s_fb + 2u * (uint32_t)(c * kFinalCap + i)));
+                        __syncwarp();
+                        T = warp_select_keys(KeyList{wscr}, m, need, c_lo[c], c_hi[c], lane);
+                    }
+                } else {
+                    if (use_tab && lane == 0) stat_add(A, kStFallback, 1);
+                    T = warp_select_column(keyat, n, n, s, 0ull, ~0ull, wscr, kFinalCap, lane);
+                    // the whole column's bitmap words from T
+                    for (int k0 = 0; k0 < n; k0 += 32) {
+                        const int k = k0 + lane;
+                        const uint32_t b = __ballot_sync(CALS_FULL_MASK, k < n && keyat(k) >= T);
+                        if (lane == 0) sts_u32(s_mb + 4u * (uint32_t)(c * NW + (k0 >> 5)), b);
+                    }
+                    if (lane == 0) c_flag[c] = 1;
+                }
             }
             if (lane == 0) thr[c] = T;
         }
+        __syncthreads();
 
-        // ---- sparse Gram of the owned columns -> global normal equations ----
+        // ---- S6: bracket keys at or above T join the kept set (own bitmap words) ----
+        if (use_tab && col_thread && c_flag[cl] == 0) {
+            const int nin = min((int)lds_u16(s_cnt + 4u * (uint32_t)(slot * NFP + cl) + 2u), CAPS);
+            const uint32_t cbase = s_cand + 2u * (uint32_t)(slot * CAPS * NFP + cl);
+            const uint32_t xcol = s_xs + 4u * (uint32_t)cl;
+            const uint64_t T = thr[cl];
+            for (int i = 0; i < nin; ++i) {
+                const uint32_t k = lds_u16(cbase + 2u * (uint32_t)(i * NFP));
+                if (make_key(lds_f32(xcol + k * rowb), k) >= T) {
+                    const uint32_t wa = s_mb + 4u * (uint32_t)(cl * NW + (k >> 5));
+                    sts_u32(wa, lds_u32(wa) | (1u << (k & 31)));
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---- S7: kept-row lists + sparse Gram of the owned columns -> global ----
+        if (!full)
+            for (int j = 0; j < my_cols; ++j) {
+                const int c = warp + j * nwarps;
+                bitmap_to_list(s_mb + 4u * (uint32_t)(c * NW), (n + 31) >> 5, s_lists + 2u * (uint32_t)(c * Smax),
+                               lane);
+            }
         const float lam_n = (float)(A.lam * (double)n);
         if (my_cols > 0)
-            sparse_gram_owned_any(s_xs, sx, s_ys, nf, full ? n : s, full, s_lists, Smax, warp, nwarps, my_cols, lam_n,
-                                  A.gbuf + (size_t)li * nf * gs, lane);
+            sparse_gram_owned<CPL>(s_xs, sx, s_ys, nf, full ? n : s, full, s_lists, Smax, warp, nwarps, my_cols, lam_n,
+                                   A.gbuf + (size_t)li * nf * gs, lane);
         __syncthreads();
         if (A.rss_rows != nullptr && tid == 0) {
             double r = 0.0;
@@ -239,5 +339,10 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
             for (int c = tid; c < nf; c += nt) A.thr_keys[(int64_t)row * nf + c] = thr[c];
     }
 }
+
+template __global__ void small_gram_kernel<1>(SweepArgs, const int32_t*, int64_t, int, int);
+template __global__ void small_gram_kernel<2>(SweepArgs, const int32_t*, int64_t, int, int);
+template __global__ void small_gram_kernel<4>(SweepArgs, const int32_t*, int64_t, int, int);
+template __global__ void small_gram_kernel<8>(SweepArgs, const int32_t*, int64_t, int, int);
 
 }  // namespace cals
