@@ -89,17 +89,21 @@ int small_nmax(int nf, double rate) {
 }
 
 int big_chunk(int nf) {
-    // largest power of two whose staged chunk fits ~96 KB alongside mask/G/scratch
-    const size_t per = (size_t)xs_stride(nf) * 4 + 4 + (size_t)((nf + 31) / 32) * 4;
+    // largest power of two whose staged chunk (+ y + kept-row lists) fits ~96 KB
+    const size_t per = (size_t)xs_stride(nf) * 4 + 4 + (size_t)nf * 2;
     int ch = 1024;
     while (ch > 64 && (size_t)ch * per > 96 * 1024) ch >>= 1;
     return ch;
 }
 
 size_t big_gram_smem(int nf, int chunk) {
-    const int sx = xs_stride(nf), mw = (nf + 31) / 32;
-    return align16((size_t)chunk * sx * 4) + align16((size_t)chunk * 4) + align16((size_t)chunk * mw * 4) +
-           align16((size_t)nf * (nf + 1) * 4) + (size_t)kThreads * 16 * 4;
+    const int sx = xs_stride(nf);
+    return align16((size_t)chunk * sx * 4) + align16((size_t)chunk * 4) + align16((size_t)nf * (nf + 1) * 4) +
+           align16((size_t)nf * chunk * 2 + (size_t)nf * 4);
+}
+
+size_t big_scan_smem(int nf, int chunk) {
+    return align16((size_t)chunk * xs_stride(nf) * 4) + align16((size_t)nf * kHB * 4);
 }
 
 int64_t cand_cap(int64_t n, float delta_tab) {
@@ -182,6 +186,7 @@ struct Work {
     uint64_t* thr;
     float* part;
     double* rss_part;
+    int* hist;
     double* retry;
     float* gbuf;
     int64_t gbuf_rows;
@@ -208,6 +213,7 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
     w.thr = c.take<uint64_t>((size_t)P->n_big * nf);
     w.part = c.take<float>((size_t)P->n_big_tiles * nf * (nf + 1));
     w.rss_part = c.take<double>((size_t)P->n_big_tiles);
+    w.hist = c.take<int>((size_t)P->n_big * nf * kHB);
     w.retry = c.take<double>((size_t)std::max<int64_t>(kMaxGrid, kMaxSolveWarps) * retry_stride(nf));
     w.gbuf_rows = gbuf_rows_for(nf, P->n_small + P->n_big);
     w.gbuf = c.take<float>((size_t)w.gbuf_rows * nf * (nf + 1));
@@ -270,6 +276,12 @@ int launch_small(SweepArgs A, const cals_plan* P, const Work& w, cudaStream_t st
     return cuda_status("small tier");
 }
 
+template <int CPL>
+void launch_big_gram(const SweepArgs& A, const BigArgs& B, size_t smem, cudaStream_t st) {
+    allow_smem(big_gram_kernel<CPL>);
+    big_gram_kernel<CPL><<<grid_for(big_gram_kernel<CPL>, smem, B.n_tiles), kThreads, smem, st>>>(A, B);
+}
+
 template <int NFP>
 int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream_t st) {
     const int nf = A.nf;
@@ -286,8 +298,10 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
     B.thr = w.thr;
     B.part = w.part;
     B.rss_part = w.rss_part;
+    B.hist = w.hist;
     cudaMemsetAsync(w.cnt, 0, sizeof(int) * (size_t)P->n_big * nf * 2, st);
-    const size_t scan_smem = align16((size_t)B.chunk * xs_stride(nf) * 4);
+    cudaMemsetAsync(w.hist, 0, sizeof(int) * (size_t)P->n_big * nf * kHB, st);
+    const size_t scan_smem = big_scan_smem(nf, B.chunk);
     allow_smem(big_scan_kernel);
     {
         ProfScope ps("big_scan_kernel", st);
@@ -300,10 +314,13 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
         big_resolve_kernel<<<(int)std::max<int64_t>(1, blocks), kThreads, 0, st>>>(A, B);
     }
     const size_t gram_smem = big_gram_smem(nf, B.chunk);
-    allow_smem(big_gram_kernel);
     {
         ProfScope ps("big_gram_kernel", st);
-        big_gram_kernel<<<grid_for(big_gram_kernel, gram_smem, B.n_tiles), kThreads, gram_smem, st>>>(A, B);
+        const int nq = xs_chunks(nf);
+        if (nq <= 4) launch_big_gram<1>(A, B, gram_smem, st);
+        else if (nq <= 8) launch_big_gram<2>(A, B, gram_smem, st);
+        else if (nq <= 16) launch_big_gram<4>(A, B, gram_smem, st);
+        else launch_big_gram<8>(A, B, gram_smem, st);
     }
     for (int64_t r0 = 0; r0 < B.n_big; r0 += w.gbuf_rows) {
         const int64_t cnt = std::min<int64_t>(w.gbuf_rows, B.n_big - r0);

@@ -237,7 +237,8 @@ __device__ __forceinline__ void sparse_gram(uint32_t xs, int sx, uint32_t ys, ui
 template <int CPL>
 __device__ __forceinline__ void sparse_gram_owned(uint32_t xs, int sx, uint32_t ys, int nf, int len, bool full,
                                                   uint32_t lists, int Smax, int c_first, int c_step, int n_cols,
-                                                  float lam_n, float* __restrict__ Gout, int lane) {
+                                                  float lam_n, float* __restrict__ Gout, int lane,
+                                                  bool accumulate = false) {
     const int nq = xs_chunks(nf);
     const int LPC = nq < 4 ? nq : 4;
     const int maxct = 32 / LPC;
@@ -290,11 +291,11 @@ __device__ __forceinline__ void sparse_gram_owned(uint32_t xs, int sx, uint32_t 
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
                         const int f = 4 * ch + t;
-                        if (f < nf) grow[f] = acc[4 * i + t] + ((f == c) ? lam_n : 0.f);
+                        if (f < nf) grow[f] = (accumulate ? grow[f] : 0.f) + acc[4 * i + t] + ((f == c) ? lam_n : 0.f);
                     }
                 }
             }
-            if (fl == 0) grow[nf] = accb;
+            if (fl == 0) grow[nf] = (accumulate ? grow[nf] : 0.f) + accb;
         }
         __syncwarp();
     }

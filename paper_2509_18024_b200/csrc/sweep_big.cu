@@ -4,13 +4,15 @@
 //
 // A big row is cut into work items of `item_rows` slice rows, processed in
 // shared-memory chunks.  Per half-sweep:
-//   big_scan     counts per column above / inside the table bracket and
-//                appends the bracket's keys to a per-(row, column) list
-//   big_resolve  one warp per (row, column): exact s-th key from the list
-//                (warp sample-select), or from the whole column if the
-//                bracket missed (fallback, always correct)
-//   big_gram     masked partial Gram per item (fixed-order partials), plus the
-//                item's share of the fused residual of the previous row
+//   big_scan     counts per column above / inside the table bracket, a
+//                32-bucket histogram of the bracket, and appends the
+//                bracket's keys to a per-(row, column) list
+//   big_resolve  one warp per (row, column): the histogram names the bucket
+//                holding the target rank, one filtering pass keeps its keys,
+//                a warp select finishes (or an exact whole-column search if
+//                the bracket missed: always correct)
+//   big_gram     sparse partial Gram per item from per-chunk kept-row lists
+//                (fixed order), plus the item's share of the fused residual
 //   big_reduce   fixed-order fp64 sum of the partials, + lam*n*I -> normal
 //                equations for the batched solve (sweep_solve.cu)
 #include "gram.cuh"
@@ -32,12 +34,14 @@ __device__ __forceinline__ int find_row(const int64_t* tile_ptr, int64_t n_big, 
 
 __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs B) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ int s_above[CALS_MAX_NF_DEV], s_in[CALS_MAX_NF_DEV], s_base[CALS_MAX_NF_DEV],
-        s_slot[CALS_MAX_NF_DEV];
+    __shared__ int s_above[CALS_MAX_NF_DEV], s_base[CALS_MAX_NF_DEV], s_slot[CALS_MAX_NF_DEV];
     __shared__ uint32_t s_hib[CALS_MAX_NF_DEV], s_lob[CALS_MAX_NF_DEV];
     const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x;
     const int sx = xs_stride(nf);
     float* Xs = reinterpret_cast<float*>(smem);
+    int* s_hist = reinterpret_cast<int*>(smem + align16((size_t)B.chunk * sx * 4));  // [nf][kHB]
+    const uint32_t s_xs = smem_u32(Xs);
+    const uint32_t rowb = 4u * (uint32_t)sx;
     const FastDiv fq((uint32_t)xs_chunks(nf));
     for (int64_t t = blockIdx.x; t < B.n_tiles; t += gridDim.x) {
         const int r = find_row(B.tile_ptr, B.n_big, t);
@@ -48,14 +52,15 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
         if (s >= n) continue;  // complete sketch: nothing to select (uniform per block)
         const int kbeg = (int)(t - B.tile_ptr[r]) * B.item_rows;
         const int kend = min(n, kbeg + B.item_rows);
+        __syncthreads();
         if (tid < nf) {
             uint32_t hib, lob;
             table_bracket(A.qtab + (size_t)tid * (kQ + 1), n, s, A.delta_tab, hib, lob);
             s_hib[tid] = hib;
             s_lob[tid] = lob;
             s_above[tid] = 0;
-            s_in[tid] = 0;
         }
+        for (int e = tid; e < nf * kHB; e += nt) s_hist[e] = 0;
         const int64_t cbase = B.cand_ptr[r];
         const int capB = (int)((B.cand_ptr[r + 1] - cbase) / nf);
         for (int k0 = kbeg; k0 < kend; k0 += B.chunk) {
@@ -68,11 +73,14 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
             int my_in = 0, my_above = 0;
             const int c = tid % nf, j = tid / nf;
             if (tid < per * nf) {
-                const uint32_t hib = s_hib[c], lob = s_lob[c];
+                const uint32_t hib = s_hib[c], lob = s_lob[c], span = hib - lob;
                 for (int k = j; k < kn; k += per) {
-                    const uint32_t a = abs_bits(Xs[k * sx + c]);
+                    const uint32_t a = __float_as_uint(lds_f32(s_xs + (uint32_t)k * rowb + 4u * c)) & 0x7FFFFFFFu;
                     my_above += (a >= hib);
-                    my_in += (a >= lob && a < hib);
+                    if (a >= lob && a < hib) {
+                        ++my_in;
+                        atomicAdd(&s_hist[c * kHB + hb_bucket(a, lob, span)], 1);
+                    }
                 }
                 atomicAdd(&s_above[c], my_above);
                 if (my_in) atomicAdd(&s_slot[c], my_in);
@@ -88,7 +96,7 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
                 const uint32_t hib = s_hib[c], lob = s_lob[c];
                 uint64_t* cl = B.cand + cbase + (int64_t)c * capB;
                 for (int k = j; k < kn; k += per) {
-                    const float x = Xs[k * sx + c];
+                    const float x = lds_f32(s_xs + (uint32_t)k * rowb + 4u * c);
                     const uint32_t a = abs_bits(x);
                     if (a >= lob && a < hib) {
                         const int pos = s_base[c] + atomicAdd(&s_slot[c], 1);
@@ -99,7 +107,8 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
         }
         __syncthreads();
         if (tid < nf && s_above[tid]) atomicAdd(&B.cnt[((size_t)r * nf + tid) * 2], s_above[tid]);
-        __syncthreads();
+        for (int e = tid; e < nf * kHB; e += nt)
+            if (s_hist[e]) atomicAdd(&B.hist[(size_t)r * nf * kHB + e], s_hist[e]);
     }
 }
 
@@ -126,12 +135,12 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
             uint64_t mn = ~0ull;
             if (A.thr_keys != nullptr) {
                 for (int k = lane; k < n; k += 32) {
-                    uint64_t kk = keyat(k);
+                    const uint64_t kk = keyat(k);
                     mn = kk < mn ? kk : mn;
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
-                    uint64_t t2 = __shfl_xor_sync(CALS_FULL_MASK, mn, o);
+                    const uint64_t t2 = __shfl_xor_sync(CALS_FULL_MASK, mn, o);
                     mn = t2 < mn ? t2 : mn;
                 }
             }
@@ -146,8 +155,39 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
             table_bracket(A.qtab + (size_t)c * (kQ + 1), n, s, A.delta_tab, hib, lob);
             const uint64_t hik = hi_key_of(hib), lok = (uint64_t)lob << 32;
             if (above < s && s <= above + in && in <= capB && lok < hik) {
-                T = warp_select_keys(KeyList{cl}, in, s - above, lok, hik, lane);
+                // bucket holding the target rank: inclusive scan of the histogram from the top
+                const int need = s - above;
+                const int bl = kHB - 1 - lane;  // lane 0 = highest bucket
+                const int cnt_b = B.hist[((size_t)r * nf + c) * kHB + bl];
+                int incl = cnt_b;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int t2 = __shfl_up_sync(CALS_FULL_MASK, incl, o);
+                    if (lane >= o) incl += t2;
+                }
+                const uint32_t hit = __ballot_sync(CALS_FULL_MASK, incl >= need);
+                const int L = __ffs(hit) - 1;  // first lane whose prefix reaches need
+                const int before = __shfl_sync(CALS_FULL_MASK, incl - cnt_b, L);
+                const int bT = kHB - 1 - L;
+                const uint32_t span = hib - lob;
+                const uint64_t blo = (uint64_t)hb_lower(bT, lob, span) << 32;
+                const uint64_t bhi = bT == kHB - 1 ? hik : ((uint64_t)hb_lower(bT + 1, lob, span) << 32);
+                // keep that bucket's keys (in place), then select among them
+                int m = 0;
+                for (int i0 = 0; i0 < in; i0 += 32) {
+                    const int i = i0 + lane;
+                    const uint64_t kk = i < in ? cl[i] : 0ull;
+                    const bool keep = i < in && kk >= blo && kk < bhi;
+                    const uint32_t bal = __ballot_sync(CALS_FULL_MASK, keep);
+                    __syncwarp();
+                    if (keep) cl[m + __popc(bal & lanemask_lt())] = kk;
+                    m += __popc(bal);
+                }
+                __syncwarp();
+                if (lane == 0) stat_add(A, kStBigColumns, 1);
+                T = warp_select_keys(KeyList{cl}, m, need - before, blo, bhi, lane);
             } else {
+                if (lane == 0) stat_add(A, kStBigFallback, 1);
                 uint64_t rlo, rhi;
                 int m, need;
                 if (above >= s) { rlo = hik; rhi = ~0ull; m = above; need = s; }
@@ -163,19 +203,28 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
     }
 }
 
+// Partial normal equations of one work item: per staged chunk, warp w builds
+// the kept-row lists of its columns (ballots on key >= T) and accumulates
+// their sparse Gram rows in shared memory; the item's partial goes to global.
+template <int CPL>
 __global__ void __launch_bounds__(kThreads) big_gram_kernel(SweepArgs A, BigArgs B) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t s_thr[CALS_MAX_NF_DEV];
     __shared__ float wold[CALS_MAX_NF_DEV];
     __shared__ double red[32];
-    const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x;
-    const int sx = xs_stride(nf), mw = (nf + 31) / 32, gs = nf + 1;
+    const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+    const int sx = xs_stride(nf), gs = nf + 1;
+    const int CH = B.chunk;
     float* Xs = reinterpret_cast<float*>(smem);
-    float* ys = reinterpret_cast<float*>(smem + align16((size_t)B.chunk * sx * 4));
-    uint32_t* mb = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(ys) + align16((size_t)B.chunk * 4));
-    float* G = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(mb) + align16((size_t)B.chunk * mw * 4));
-    float* scratch = G + align16((size_t)nf * gs * 4) / 4;
+    float* ys = reinterpret_cast<float*>(smem + align16((size_t)CH * sx * 4));
+    unsigned char* after_ys = reinterpret_cast<unsigned char*>(ys) + align16((size_t)CH * 4);
+    float* G = reinterpret_cast<float*>(after_ys);
+    unsigned char* after_g = after_ys + align16((size_t)nf * gs * 4);
+    const uint32_t s_xs = smem_u32(Xs), s_ys = smem_u32(ys);
+    const uint32_t s_lists = smem_u32(after_g);  // [nf][CH] u16
+    const uint32_t rowb = 4u * (uint32_t)sx;
     const FastDiv fq((uint32_t)xs_chunks(nf));
+    const int my_cols = warp < nf ? (nf - 1 - warp) / nwarps + 1 : 0;
     for (int64_t t = blockIdx.x; t < B.n_tiles; t += gridDim.x) {
         const int r = find_row(B.tile_ptr, B.n_big, t);
         const int row = B.rows[r];
@@ -189,35 +238,65 @@ __global__ void __launch_bounds__(kThreads) big_gram_kernel(SweepArgs A, BigArgs
             s_thr[tid] = B.thr[(size_t)r * nf + tid];
             if (A.tgt_old != nullptr) wold[tid] = A.tgt_old[(int64_t)row * A.ld_old + tid];
         }
-        const int nout = nf * gs;
-        bool first = true;
         double racc = 0.0;
-        for (int k0 = kbeg; k0 < kend; k0 += B.chunk) {
-            const int kn = min(B.chunk, kend - k0);
+        for (int k0 = kbeg; k0 < kend; k0 += CH) {
+            const int kn = min(CH, kend - k0);
             __syncthreads();
             stage_slice(A, lo, k0, kn, Xs, ys, fq);
             __syncthreads();
             if (A.rss_rows != nullptr) {
                 for (int k = tid; k < kn; k += nt) {
                     double pred = 0.0;
-                    for (int f = 0; f < nf; ++f) pred = fma((double)Xs[k * sx + f], (double)wold[f], pred);
-                    const double d = (double)ys[k] - pred;
+                    for (int f = 0; f < nf; ++f)
+                        pred = fma((double)lds_f32(s_xs + (uint32_t)k * rowb + 4u * f), (double)wold[f], pred);
+                    const double d = (double)lds_f32(s_ys + 4u * k) - pred;
                     racc = fma(d, d, racc);
                 }
             }
-            build_mask(Xs, sx, kn, nf, s_thr, full, mb, mw, k0);
-            __syncthreads();
-            tile_gram(Xs, sx, ys, mb, mw, kn, nf, G, scratch, !first);
-            first = false;
+            int len = kn;
+            if (!full) {
+                // kept-row lists of the owned columns (ascending k), same length
+                // for all columns only when complete, so each column keeps its own
+                for (int j = 0; j < my_cols; ++j) {
+                    const int c = warp + j * nwarps;
+                    const uint64_t T = s_thr[c];
+                    const uint32_t xcol = s_xs + 4u * (uint32_t)c;
+                    const uint32_t L = s_lists + 2u * (uint32_t)(c * CH);
+                    int w = 0;
+                    for (int kk0 = 0; kk0 < kn; kk0 += 32) {
+                        const int k = kk0 + lane;
+                        const bool keep = k < kn && make_key(lds_f32(xcol + (uint32_t)k * rowb), (uint32_t)(k0 + k)) >= T;
+                        const uint32_t bal = __ballot_sync(CALS_FULL_MASK, keep);
+                        if (keep) sts_u16(L + 2u * (uint32_t)(w + __popc(bal & lanemask_lt())), (uint32_t)k);
+                        w += __popc(bal);
+                    }
+                    if (lane == 0) sts_u32(s_lists + 2u * (uint32_t)(nf * CH) + 4u * c, (uint32_t)w);
+                }
+                __syncwarp();
+            }
+            // sparse accumulate (columns may have different list lengths here)
+            for (int j = 0; j < my_cols; ++j) {
+                const int c = warp + j * nwarps;
+                const int lc = full ? kn : (int)lds_u32(s_lists + 2u * (uint32_t)(nf * CH) + 4u * c);
+                sparse_gram_owned<CPL>(s_xs, sx, s_ys, nf, lc, full, s_lists, CH, c, nwarps, 1, 0.f, G, lane,
+                                       k0 != kbeg);
+            }
+            (void)len;
         }
-        float* out = B.part + (size_t)t * nout;
-        for (int e = tid; e < nout; e += nt) out[e] = G[e];
+        __syncthreads();
+        float* out = B.part + (size_t)t * nf * gs;
+        for (int e = tid; e < nf * gs; e += nt) out[e] = G[e];
         if (A.rss_rows != nullptr) {
             racc = block_sum_d(racc, red);
             if (tid == 0) B.rss_part[t] = racc;
         }
     }
 }
+
+template __global__ void big_gram_kernel<1>(SweepArgs, BigArgs);
+template __global__ void big_gram_kernel<2>(SweepArgs, BigArgs);
+template __global__ void big_gram_kernel<4>(SweepArgs, BigArgs);
+template __global__ void big_gram_kernel<8>(SweepArgs, BigArgs);
 
 // Big rows [r0, r0 + count): fixed-order float64 sum of the item partials,
 // + lam*n*I on the diagonal -> A.gbuf slot (r - r0); residual partial sums.

@@ -39,7 +39,8 @@ struct SweepArgs {
 };
 
 // Debug counters (only when A.stats != nullptr): see cals_debug_stats.
-enum StatId { kStColumns = 0, kStFallback, kStCandidates, kStAfterPrenarrow, kStSelectRounds, kStRows, kStCount = 16 };
+enum StatId { kStColumns = 0, kStFallback, kStCandidates, kStAfterPrenarrow, kStSelectRounds, kStRows,
+              kStBigColumns, kStBigFallback, kStSmallOver, kStSmallMiss, kStFinalOver, kStCount = 16 };
 __device__ __forceinline__ void stat_add(const SweepArgs& A, int id, unsigned long long v) {
     if (A.stats != nullptr) atomicAdd(A.stats + id, v);
 }
@@ -64,7 +65,19 @@ struct BigArgs {
     float* part;              // [n_tiles][nf][nf+1]
     float* wbig;              // [n_big][nf]
     double* rss_part;         // [n_tiles]
+    int* hist;                // [n_big][nf][kHB] in-bracket counts per sub-bucket
 };
+
+constexpr int kHB = 32;  // sub-buckets of a big row's bracket (linear in abs-bit space)
+
+// Sub-bucket of an in-bracket abs value a in [lob, hib): floor((a - lob) * kHB / span).
+__device__ __forceinline__ int hb_bucket(uint32_t a, uint32_t lob, uint32_t span) {
+    return (int)(((uint64_t)(a - lob) * kHB) / span);
+}
+// Smallest abs value of sub-bucket b: lob + ceil(b * span / kHB).
+__device__ __forceinline__ uint32_t hb_lower(int b, uint32_t lob, uint32_t span) {
+    return lob + (uint32_t)(((uint64_t)b * span + kHB - 1) / kHB);
+}
 
 __host__ __device__ inline int round_up4(int x) { return (x + 3) & ~3; }
 // Staged row stride (floats): 16-byte aligned rows for cp.async / LDS.128,

@@ -210,6 +210,10 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
                 const uint64_t hik = hi_key_of(hib), lok = (uint64_t)lob << 32;
                 const bool ok = !over && above < s && s <= above + nin && lok < hik;
                 c_flag[c] = ok ? 0 : 1;
+                if (A.stats != nullptr) {
+                    if (over) stat_add(A, kStSmallOver, 1);
+                    else if (!ok) stat_add(A, kStSmallMiss, 1);
+                }
                 c_fc[c] = 0;
                 if (ok) {
                     const int need = s - above;
@@ -274,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, co
             } else {
                 const int m = use_tab ? c_fc[c] : 0;
                 const bool exact = !use_tab || c_flag[c] != 0 || m > kFinalCap;
+                if (use_tab && c_flag[c] == 0 && m > kFinalCap && lane == 0) stat_add(A, kStFinalOver, 1);
                 if (!exact) {
                     const int need = c_need[c];
                     if (m <= 32) {

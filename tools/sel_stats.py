@@ -22,8 +22,8 @@ eng.step("user")
 torch.cuda.synchronize()
 _lib.load().cals_debug_stats(None)
 v = st.cpu().numpy()
-print(cfg, "columns", v[0], "fallback", v[1], "cand/col", v[2] / max(v[0], 1),
-      "after-prenarrow/col", v[3] / max(v[0], 1), "extra rounds", v[4])
+print(cfg, "rows(small, table)", v[0], "fallback", v[1], "cand/col", v[2] / max(v[0], 1),
+      "small over", v[8], "small miss", v[9], "final over", v[10], "big cols", v[6], "big fallback", v[7])
 for side in (eng.user, eng.item):
     c = side.counts[side.counts > 0]
     print("rows", c.size, "n mean", round(float(c.mean()), 1), "max", c.max(), "small", side.plan.n_small,
