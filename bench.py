@@ -79,7 +79,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except OSError:
@@ -298,6 +298,11 @@ def main():
     b_iter = algorithmic_bytes(np.diff(data.row_ptr.cpu().numpy()), n_f) + algorithmic_bytes(
         np.diff(data.col_ptr.cpu().numpy()), n_f)
     gpu_launches = sum(c for c, _ in prof.values())
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get(args.config, {}).get(dom_name, {}).get("dram_bytes_per_launch")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -307,7 +312,9 @@ def main():
                    "l2": "512 MiB flush before every timed step (outside its events)",
                    "init": "M0 ~ N(0, 0.1^2) numpy seed 0, fp32; U0 = 0"},
         "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": (achieved / hbm) if achieved else None, "traffic": None, "peak_kind": peak_kind,
+                     "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
+                     "alg_bytes_per_launch": (dom_bytes / dom_cnt) if dom_bytes and dom_cnt else None,
+                     "peak_kind": peak_kind,
                      "launches": dom_cnt, "kernel_ms_total": dom_ms,
                      "step_alg_bytes": b_iter,
                      "step_frac": (b_iter / (hbm * 1e9)) / (total_ms / 1e3 / args.steps)},
