@@ -226,7 +226,8 @@ void launch_solve(const SweepArgs& A, const int32_t* rows, int64_t count, cudaSt
     if (count <= 0) return;
     ProfScope ps("solve_kernel", st);
     if constexpr (NFP > 0) {
-        const int64_t blocks = std::min<int64_t>((count + 7) / 8, kMaxSolveWarps / 8);
+        const int64_t warps = (count + (32 / NFP) - 1) / (32 / NFP);
+        const int64_t blocks = std::min<int64_t>((warps + 7) / 8, kMaxSolveWarps / 8);
         solve_warp_kernel<NFP><<<(int)blocks, 256, 0, st>>>(A, rows, count);
     } else {
         const size_t smem = align16((size_t)A.nf * (A.nf + 1) * 4);

@@ -148,6 +148,76 @@ __device__ int block_lu_solve(T* W, int nf, bool spd, T* x_out, int* s_piv) {
     return __syncthreads_or(bad);
 }
 
+// Segmented warp LU: 32/NFP systems per warp, NFP lanes per system (lane r of
+// a segment owns row r).  Partial pivoting without physical row swaps: the
+// pivot row of step k is broadcast once and every unused row is eliminated
+// against it; back substitution walks the pivot order.  Same arithmetic as
+// row-swapping LU (first max |a| wins ties, like LAPACK idamax).
+// Returns, per lane, whether ITS system failed (uniform within a segment);
+// x: the lane's unknown (variable r of its system).
+template <int NFP>
+__device__ __forceinline__ bool seg_lu_solve(const float* __restrict__ Grow, int nf, bool spd, bool seg_valid,
+                                             float& x, int lane) {
+    const int r = lane & (NFP - 1);
+    const bool rv = seg_valid && r < nf;
+    float a[NFP];
+    float rhs = 0.f;
+#pragma unroll
+    for (int j = 0; j < NFP; ++j) a[j] = (rv && j < nf) ? Grow[j] : 0.f;
+    if (rv) rhs = Grow[nf];
+    bool used = !rv;
+    int ord = -1;
+    bool fail = !seg_valid;
+#pragma unroll
+    for (int k = 0; k < NFP; ++k) {
+        if (k < nf) {
+            // argmax over the segment's unused rows (all lanes shuffle: spd differs per segment)
+            float best = used ? -1.f : fabsf(a[k]);
+            int bi = r;
+#pragma unroll
+            for (int o = NFP / 2; o > 0; o >>= 1) {
+                const float ob = __shfl_xor_sync(CALS_FULL_MASK, best, o, NFP);
+                const int oi = __shfl_xor_sync(CALS_FULL_MASK, bi, o, NFP);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            const int p = spd ? k : bi;
+            if (!spd) fail |= !(best > 0.f);
+            const float d = __shfl_sync(CALS_FULL_MASK, a[k], p, NFP);
+            fail |= spd ? !(d > 0.f) : !(d == d);
+            const bool me = (r == p);
+            if (me) { used = true; ord = k; }
+            const float f = (!used && !fail) ? a[k] / d : 0.f;
+#pragma unroll
+            for (int j = 0; j < NFP; ++j) {
+                if (j > k && j < nf) {
+                    const float vp = __shfl_sync(CALS_FULL_MASK, a[j], p, NFP);
+                    a[j] = fmaf(-f, vp, a[j]);
+                }
+            }
+            const float bp = __shfl_sync(CALS_FULL_MASK, rhs, p, NFP);
+            rhs = fmaf(-f, bp, rhs);
+        }
+    }
+    x = 0.f;
+    const int seg_base = lane & ~(NFP - 1);
+#pragma unroll
+    for (int k = NFP - 1; k >= 0; --k) {
+        if (k < nf) {
+            const uint32_t bal = __ballot_sync(CALS_FULL_MASK, ord == k);
+            const uint32_t segbits = (NFP == 32) ? bal : ((bal >> seg_base) & ((1u << NFP) - 1u));
+            const int pk = segbits ? (__ffs(segbits) - 1) : 0;
+            float xk = (ord == k) ? rhs / a[k] : 0.f;
+            xk = __shfl_sync(CALS_FULL_MASK, xk, pk, NFP);
+            if (r == k) x = xk;
+            if (ord >= 0 && ord < k) rhs = fmaf(-a[k], xk, rhs);
+        }
+    }
+    const bool bad = rv && (!(x == x) || (x - x != 0.f));
+    const uint32_t anybad = __ballot_sync(CALS_FULL_MASK, bad);
+    const uint32_t segm = (NFP == 32) ? 0xffffffffu : (((1u << NFP) - 1u) << seg_base);
+    return fail || (anybad & segm) != 0;
+}
+
 // Float64 retry of a failed system with the reference's diagonal jitter
 // 1e-10 * tr(G) / nf (core.py:126-131, als.py:191-197).  One warp, lanes over
 // columns, scratch W (nf*(nf+1) doubles, any memory).  Rare path.

@@ -8,44 +8,62 @@
 
 namespace cals {
 
-// One warp per system (nf <= 32).
+// 32/NFP systems per warp (nf <= 32): segmented register LU.
 template <int NFP>
-__global__ void __launch_bounds__(256) solve_warp_kernel(SweepArgs A, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, 2) solve_warp_kernel(SweepArgs A, const int32_t* __restrict__ rows,
                                                          int64_t n_list) {
-    __shared__ float xs[8][32];
-    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int nf = A.nf, gs = nf + 1;
+    constexpr int SPW = 32 / NFP;  // systems per warp
+    const int seg = lane / NFP, r = lane % NFP;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t li = gw; li < n_list; li += stride) {
-        const int row = rows[li];
-        const int n = (int)(A.ptr[row + 1] - A.ptr[row]);
-        const bool spd = A.budget[row] >= n;
-        const float* G = A.gbuf + (size_t)li * nf * gs;
-        float* x = xs[wl];
+    for (int64_t b0 = gw * SPW; b0 < n_list; b0 += stride * SPW) {
+        const int64_t li = b0 + seg;
+        const bool sv = li < n_list;
+        const int row = sv ? rows[li] : 0;
+        const int n = sv ? (int)(A.ptr[row + 1] - A.ptr[row]) : 1;
+        const bool spd = sv && A.budget[row] >= n;
+        const float* G = A.gbuf + (size_t)(sv ? li : 0) * nf * gs;
+        float x;
+        const bool bad = seg_lu_solve<NFP>(G + (size_t)(r < nf ? r : 0) * gs, nf, spd, sv, x, lane);
         int st = CALS_ROW_OK;
-        if (warp_lu_solve<NFP>(G, gs, nf, spd, x, lane)) {
+        // rare path: float64 retry with the reference's jitter, one system at a time
+        const uint32_t badmask = __ballot_sync(CALS_FULL_MASK, bad && sv && r == 0);
+        if (badmask) {
             double* W = A.retry_ws + (size_t)gw * A.retry_stride;
             double* xd = W + nf * gs;
-            const int bad = warp_retry_f64(G, nf, spd, W, xd, lane);
-            __syncwarp();
-            if (lane < nf) x[lane] = (float)xd[lane];
-            st = bad ? CALS_ROW_SINGULAR : CALS_ROW_JITTERED;
+            uint32_t m = badmask;
+            while (m) {
+                const int sl = __ffs(m) - 1;
+                m &= m - 1;
+                const int q = sl / NFP;
+                const int64_t lq = b0 + q;
+                const int rq = rows[lq];
+                const int nq = (int)(A.ptr[rq + 1] - A.ptr[rq]);
+                const bool spdq = A.budget[rq] >= nq;
+                const int bq = warp_retry_f64(A.gbuf + (size_t)lq * nf * gs, nf, spdq, W, xd, lane);
+                __syncwarp();
+                if (seg == q) {
+                    if (r < nf) x = (float)xd[r];
+                    st = bq ? CALS_ROW_SINGULAR : CALS_ROW_JITTERED;
+                }
+                __syncwarp();
+            }
         }
-        __syncwarp();
-        const float w = lane < nf ? x[lane] : 0.f;
-        if (st != CALS_ROW_SINGULAR && lane < nf) A.tgt[(int64_t)row * A.ld_tgt + lane] = w;
+        if (sv) {
+            if (st != CALS_ROW_SINGULAR && r < nf) A.tgt[(int64_t)row * A.ld_tgt + r] = x;
+        }
         if (A.pen_rows != nullptr) {
-            double p = (double)w * (double)w;
+            double p = (sv && r < nf) ? (double)x * (double)x : 0.0;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(CALS_FULL_MASK, p, o);
-            if (lane == 0) A.pen_rows[row] = (st == CALS_ROW_SINGULAR) ? 0.0 : (double)n * p;
+            for (int o = NFP / 2; o > 0; o >>= 1) p += __shfl_xor_sync(CALS_FULL_MASK, p, o, NFP);
+            if (sv && r == 0) A.pen_rows[row] = (st == CALS_ROW_SINGULAR) ? 0.0 : (double)n * p;
         }
-        if (lane == 0) {
+        if (sv && r == 0) {
             A.status[row] = st;
             report_status(A, row, st);
         }
-        __syncwarp();
     }
 }
 
