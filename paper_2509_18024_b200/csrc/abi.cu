@@ -107,7 +107,9 @@ size_t big_scan_smem(int nf, int chunk) {
 }
 
 int64_t cand_cap(int64_t n, float delta_tab) {
-    const double d = 3.0 * std::sqrt(0.25 / (double)n) + delta_tab + 0.5 / kQ;
+    // must cover the kernel's bracket (table_levels): 2 d n plus level rounding
+    const double ks = n > 2048 ? 4.0 : 3.0, kt = n > 2048 ? 1.5 : 1.0;
+    const double d = ks * std::sqrt(0.25 / (double)n) + kt * delta_tab + 1.5 / kQ;
     int64_t cap = (int64_t)std::ceil(3.0 * d * (double)n) + 64;
     cap = std::max<int64_t>(cap, 64);
     return std::min<int64_t>(cap, std::max<int64_t>(n, 64));
@@ -194,7 +196,7 @@ struct Work {
 
 constexpr int kMaxGrid = 160 * 16;  // grid_for never exceeds min(SMs, 160) * 16 CTAs
 inline int retry_stride(int nf) { return ((nf * (nf + 1) + nf) + 31) & ~31; }
-constexpr int64_t kMaxSolveWarps = 160 * 4 * 8;  // solve_warp_kernel grid cap (4 CTAs of 8 warps per SM)
+constexpr int64_t kMaxSolveWarps = 160 * 64;  // solve_warp_kernel grid cap (64 warps per SM)
 
 // Normal-equation batch: rows solved per phase-A/phase-B launch pair (<= ~1 GiB).
 int64_t gbuf_rows_for(int nf, int64_t rows) {
@@ -250,6 +252,17 @@ int gram_grid(size_t smem, int64_t cnt, int threads) {
     return grid_for(small_gram_kernel<CPL>, smem, cnt, 16, threads);
 }
 
+template <int CPL>
+void launch_tiny(const SweepArgs& A, const int32_t* rows, int64_t cnt, cudaStream_t st) {
+    const size_t smem = tiny_warp_bytes(A.nf) * kTinyWarps;
+    allow_smem(tiny_gram_kernel<CPL>);
+    const int64_t blocks = (cnt + kTinyWarps - 1) / kTinyWarps;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tiny_gram_kernel<CPL>, kTinyWarps * 32, smem);
+    const int64_t cap = (int64_t)std::min(dev().sms, 160) * std::max(occ, 1);
+    tiny_gram_kernel<CPL><<<(int)std::max<int64_t>(1, std::min(blocks, cap)), kTinyWarps * 32, smem, st>>>(A, rows, cnt);
+}
+
 template <int NFP>
 int launch_small(SweepArgs A, const cals_plan* P, const Work& w, cudaStream_t st) {
     const int nq = xs_chunks(A.nf);
@@ -259,6 +272,21 @@ int launch_small(SweepArgs A, const cals_plan* P, const Work& w, cudaStream_t st
         if (e <= b) continue;
         const int N = P->small_seg_maxn[g];
         const int S = P->small_seg_maxs[g];
+        if (N <= kTinyN) {  // warp-per-row kernel
+            for (int64_t b0 = b; b0 < e; b0 += w.gbuf_rows) {
+                const int64_t cnt = std::min<int64_t>(w.gbuf_rows, e - b0);
+                {
+                    ProfScope ps("tiny_gram_kernel", st);
+                    const int32_t* rr = P->small_rows + b0;
+                    if (CPL == 1) launch_tiny<1>(A, rr, cnt, st);
+                    else if (CPL == 2) launch_tiny<2>(A, rr, cnt, st);
+                    else if (CPL == 4) launch_tiny<4>(A, rr, cnt, st);
+                    else launch_tiny<8>(A, rr, cnt, st);
+                }
+                launch_solve<NFP>(A, P->small_rows + b0, cnt, st);
+            }
+            continue;
+        }
         const int threads = N <= 256 ? 128 : 256;
         const size_t smem = T1Layout(N, S, A.nf, threads).total;
         for (int64_t b0 = b; b0 < e; b0 += w.gbuf_rows) {

@@ -84,6 +84,32 @@ __device__ __forceinline__ uint64_t warp_sort_desc(uint64_t v, int lane) {
     return v;
 }
 
+// Bitonic sort of 64 keys held two per lane (element e = lane + 32*h), descending
+// by element index: after the call v0 = rank lane, v1 = rank lane + 32.
+__device__ __forceinline__ void warp_sort64_desc(uint64_t& v0, uint64_t& v1, int lane) {
+#pragma unroll
+    for (int size = 2; size <= 64; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride == 32) {
+                // partner is the other register of the same lane (e and e + 32)
+                const bool desc_block = (lane & size) == 0;  // size == 64: all descending
+                const uint64_t hi = v0 > v1 ? v0 : v1, lo = v0 > v1 ? v1 : v0;
+                v0 = desc_block ? hi : lo;
+                v1 = desc_block ? lo : hi;
+            } else {
+                const uint64_t o0 = __shfl_xor_sync(CALS_FULL_MASK, v0, stride);
+                const uint64_t o1 = __shfl_xor_sync(CALS_FULL_MASK, v1, stride);
+                const bool lower = (lane & stride) == 0;
+                const bool d0 = ((lane & size) == 0), d1 = (((lane + 32) & size) == 0);
+                const bool k0 = (lower == d0), k1 = (lower == d1);
+                v0 = k0 ? (v0 > o0 ? v0 : o0) : (v0 < o0 ? v0 : o0);
+                v1 = k1 ? (v1 > o1 ? v1 : o1) : (v1 < o1 ? v1 : o1);
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ int warp_sum_i(int v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CALS_FULL_MASK, v, o);

@@ -94,7 +94,9 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t
 // [qtab[jlo], qtab[jhi]).  Margin: 3 binomial sigmas + table sampling error.
 __device__ __forceinline__ void table_levels(int n, int s, float delta_tab, int& jhi, int& jlo) {
     const float p = (float)s / (float)n;
-    const float d = 3.0f * sqrtf(p * (1.0f - p) / (float)n) + delta_tab + 0.5f / (float)kQ;
+    // tiled rows get a wider margin: a miss there costs whole-column passes
+    const float ks = n > 2048 ? 4.0f : 3.0f, kt = n > 2048 ? 1.5f : 1.0f;
+    const float d = ks * sqrtf(p * (1.0f - p) / (float)n) + kt * delta_tab + 0.5f / (float)kQ;
     jhi = (int)floorf((p - d) * (float)kQ);
     jlo = (int)ceilf((p + d) * (float)kQ);
     jhi = jhi < 0 ? 0 : (jhi > kQ ? kQ : jhi);

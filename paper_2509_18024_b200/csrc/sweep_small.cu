@@ -350,4 +350,110 @@ template __global__ void small_gram_kernel<2>(SweepArgs, const int32_t*, int64_t
 template __global__ void small_gram_kernel<4>(SweepArgs, const int32_t*, int64_t, int, int);
 template __global__ void small_gram_kernel<8>(SweepArgs, const int32_t*, int64_t, int, int);
 
+// ---------------------------------------------------------------------------
+// Tiny regressions (n <= 64): one warp per row, no block barriers.  Per column
+// the n keys are bitonic-sorted across the warp (one or two per lane) and the
+// s-th is the threshold; kept rows come out of a ballot in ascending k.  The
+// warp then runs the same sparse Gram over all columns and writes the normal
+// equations for the batched solve.  kTinyN rows x sx floats per warp.
+// ---------------------------------------------------------------------------
+constexpr int kTinyN = 64;
+constexpr int kTinyWarps = 4;
+
+__host__ __device__ inline size_t tiny_warp_bytes(int nf) {
+    return align16((size_t)kTinyN * xs_stride(nf) * 4) + align16(kTinyN * 4) + align16((size_t)nf * 4) +
+           align16((size_t)nf * kTinyN * 2);
+}
+
+template <int CPL>
+__global__ void __launch_bounds__(kTinyWarps * 32) tiny_gram_kernel(SweepArgs A, const int32_t* __restrict__ rows,
+                                                                    int64_t n_list) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int nf = A.nf, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sx = xs_stride(nf), gs = nf + 1;
+    unsigned char* base = smem + (size_t)warp * tiny_warp_bytes(nf);
+    float* Xs = reinterpret_cast<float*>(base);
+    float* ys = reinterpret_cast<float*>(base + align16((size_t)kTinyN * sx * 4));
+    float* wold = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(ys) + align16(kTinyN * 4));
+    const uint32_t s_xs = smem_u32(Xs), s_ys = smem_u32(ys);
+    const uint32_t s_lists = smem_u32(reinterpret_cast<unsigned char*>(wold) + align16((size_t)nf * 4));
+    const uint32_t rowb = 4u * (uint32_t)sx;
+    const int nq = xs_chunks(nf);
+    const int64_t gw = (int64_t)blockIdx.x * kTinyWarps + warp;
+    const int64_t stride = (int64_t)gridDim.x * kTinyWarps;
+    for (int64_t li = gw; li < n_list; li += stride) {
+        const int row = rows[li];
+        const int64_t lo = A.ptr[row];
+        const int n = (int)(A.ptr[row + 1] - lo);
+        const int s = A.budget[row];
+        const bool full = s >= n;
+        __syncwarp();
+        // stage (warp-level cp.async)
+        for (int e = lane; e < n * nq; e += 32) {
+            const int kk = e / nq, q = e - kk * nq;
+            const int64_t r = __ldg(A.idx + lo + kk);
+            cp_async16(s_xs + (uint32_t)kk * rowb + 16u * q, A.src + r * A.ld_src + 4 * q);
+        }
+        for (int kk = lane; kk < n; kk += 32) ys[kk] = __ldg(A.val + lo + kk);
+        if (A.tgt_old != nullptr)
+            for (int c = lane; c < nf; c += 32) wold[c] = A.tgt_old[(int64_t)row * A.ld_old + c];
+        cp_async_wait_all();
+        __syncwarp();
+        // fused residual of the previous iteration's row
+        if (A.rss_rows != nullptr) {
+            double acc = 0.0;
+            for (int kk = lane; kk < n; kk += 32) {
+                float pred = 0.f;
+                for (int f = 0; f < nf; ++f) pred = fmaf(lds_f32(s_xs + (uint32_t)kk * rowb + 4u * f), wold[f], pred);
+                const double d = (double)ys[kk] - (double)pred;
+                acc = fma(d, d, acc);
+            }
+            acc = warp_sum_d(acc);
+            if (lane == 0) A.rss_rows[row] = acc;
+        }
+        // per column: threshold key by a warp sort, kept rows by ballot
+        for (int c = 0; c < nf; ++c) {
+            const uint32_t xcol = s_xs + 4u * (uint32_t)c;
+            auto keyat = [xcol, rowb](int kk) { return make_key(lds_f32(xcol + (uint32_t)kk * rowb), (uint32_t)kk); };
+            const uint64_t k0 = lane < n ? keyat(lane) : 0ull;
+            const uint64_t k1 = lane + 32 < n ? keyat(lane + 32) : 0ull;
+            uint64_t T;
+            if (full) {
+                uint64_t mn = lane < n ? k0 : ~0ull;
+                if (lane + 32 < n) mn = k1 < mn ? k1 : mn;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const uint64_t t2 = __shfl_xor_sync(CALS_FULL_MASK, mn, o);
+                    mn = t2 < mn ? t2 : mn;
+                }
+                T = mn;
+            } else if (n <= 32) {
+                const uint64_t v = warp_sort_desc(k0, lane);
+                T = __shfl_sync(CALS_FULL_MASK, v, s - 1);
+            } else {
+                uint64_t v0 = k0, v1 = k1;
+                warp_sort64_desc(v0, v1, lane);
+                T = s - 1 < 32 ? __shfl_sync(CALS_FULL_MASK, v0, s - 1) : __shfl_sync(CALS_FULL_MASK, v1, s - 1 - 32);
+            }
+            if (A.thr_keys != nullptr && lane == 0) A.thr_keys[(int64_t)row * nf + c] = T;
+            if (!full) {
+                const uint32_t L = s_lists + 2u * (uint32_t)(c * kTinyN);
+                const bool a0 = lane < n && k0 >= T, a1 = lane + 32 < n && k1 >= T;
+                const uint32_t b0 = __ballot_sync(CALS_FULL_MASK, a0), b1 = __ballot_sync(CALS_FULL_MASK, a1);
+                if (a0) sts_u16(L + 2u * (uint32_t)__popc(b0 & lanemask_lt()), (uint32_t)lane);
+                if (a1) sts_u16(L + 2u * (uint32_t)(__popc(b0) + __popc(b1 & lanemask_lt())), (uint32_t)(lane + 32));
+            }
+        }
+        __syncwarp();
+        const float lam_n = (float)(A.lam * (double)n);
+        sparse_gram_owned<CPL>(s_xs, sx, s_ys, nf, full ? n : s, full, s_lists, kTinyN, 0, 1, nf, lam_n,
+                               A.gbuf + (size_t)li * nf * gs, lane);
+    }
+}
+
+template __global__ void tiny_gram_kernel<1>(SweepArgs, const int32_t*, int64_t);
+template __global__ void tiny_gram_kernel<2>(SweepArgs, const int32_t*, int64_t);
+template __global__ void tiny_gram_kernel<4>(SweepArgs, const int32_t*, int64_t);
+template __global__ void tiny_gram_kernel<8>(SweepArgs, const int32_t*, int64_t);
+
 }  // namespace cals

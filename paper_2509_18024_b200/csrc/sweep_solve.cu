@@ -10,7 +10,7 @@ namespace cals {
 
 // 32/NFP systems per warp (nf <= 32): segmented register LU.
 template <int NFP>
-__global__ void __launch_bounds__(256, 2) solve_warp_kernel(SweepArgs A, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256, 3) solve_warp_kernel(SweepArgs A, const int32_t* __restrict__ rows,
                                                          int64_t n_list) {
     const int lane = threadIdx.x & 31;
     const int nf = A.nf, gs = nf + 1;
