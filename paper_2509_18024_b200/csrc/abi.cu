@@ -287,7 +287,9 @@ int launch_small(SweepArgs A, const cals_plan* P, const Work& w, cudaStream_t st
             }
             continue;
         }
-        const int threads = N <= 256 ? 128 : 256;
+        // one big CTA per SM when two would not fit in shared memory
+        int threads = N <= 256 ? 128 : 256;
+        if (threads == 256 && T1Layout(N, S, A.nf, 256).total > 112 * 1024) threads = 512;
         const size_t smem = T1Layout(N, S, A.nf, threads).total;
         for (int64_t b0 = b; b0 < e; b0 += w.gbuf_rows) {
             const int64_t cnt = std::min<int64_t>(w.gbuf_rows, e - b0);

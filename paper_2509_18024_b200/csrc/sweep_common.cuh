@@ -5,6 +5,7 @@
 namespace cals {
 
 #define CALS_MAX_NF_DEV 128
+#define CALS_MAX_WARPS 16
 constexpr int kThreads = 256;       // max threads per sweep CTA (launch bound)
 constexpr int kCap = 256;           // per-column candidate capacity (shared-memory tier)
 constexpr int kQ = 256;             // quantile-table resolution (levels per column)

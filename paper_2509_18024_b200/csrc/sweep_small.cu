@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(1024) quantile_table_kernel(const int32_t* __r
 // Any miss (bracket, capacity) falls back to an exact warp search.
 // ---------------------------------------------------------------------------
 template <int CPL>
-__global__ void __launch_bounds__(kThreads, 2) small_gram_kernel(SweepArgs A, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(512, 1) small_gram_kernel(SweepArgs A, const int32_t* __restrict__ rows,
                                                                  int64_t n_list, int N, int S) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t thr[CALS_MAX_NF_DEV], c_lo[CALS_MAX_NF_DEV], c_hi[CALS_MAX_NF_DEV];
