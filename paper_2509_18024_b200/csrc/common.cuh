@@ -84,6 +84,23 @@ __device__ __forceinline__ uint64_t warp_sort_desc(uint64_t v, int lane) {
     return v;
 }
 
+// Bitonic sort within aligned groups of W lanes (W <= 32), descending.
+template <int W>
+__device__ __forceinline__ uint64_t warp_sort_desc_w(uint64_t v, int lane) {
+#pragma unroll
+    for (int size = 2; size <= W; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const uint64_t o = __shfl_xor_sync(CALS_FULL_MASK, v, stride);
+            const bool lower = (lane & stride) == 0;
+            const bool desc_block = (lane & size) == 0 || size == W;
+            const bool keep_max = (lower == desc_block);
+            v = keep_max ? (v > o ? v : o) : (v < o ? v : o);
+        }
+    }
+    return v;
+}
+
 // Bitonic sort of 64 keys held two per lane (element e = lane + 32*h), descending
 // by element index: after the call v0 = rank lane, v1 = rank lane + 32.
 __device__ __forceinline__ void warp_sort64_desc(uint64_t& v0, uint64_t& v1, int lane) {

@@ -147,21 +147,34 @@ __global__ void __launch_bounds__(512, 1) small_gram_kernel(SweepArgs A, const i
                 const int span = jlo - jhi;
                 const int k0 = slot * chunk, k1 = min(n, k0 + chunk);
                 int above = 0, nin = 0;
-                uint32_t word = 0;
+                const uint32_t span_ab = hib > lob ? hib - lob : 0u;
                 uint32_t addr = s_xs + (uint32_t)k0 * rowb + 4u * (uint32_t)cl;
                 const uint32_t cbase = s_cand + 2u * (uint32_t)(slot * CAPS * NFP + cl);
-                for (int k = k0; k < k1; ++k, addr += rowb) {
-                    const uint32_t a = __float_as_uint(lds_f32(addr)) & 0x7FFFFFFFu;
-                    const uint32_t ab = a >= hib ? 1u : 0u;
-                    word |= ab << (k & 31);
-                    above += (int)ab;
-                    if (a >= lob && a < hib) {
-                        if (nin < CAPS) sts_u16(cbase + 2u * (uint32_t)(nin * NFP), (uint32_t)k);
-                        ++nin;
+                // 32 rows per step: two bit words (above the bracket / inside it)
+                for (int kb = k0; kb < k1; kb += 32, addr += 32u * rowb) {
+                    const int cnt = min(32, k1 - kb);
+                    uint32_t wa = 0u, wi = 0u;
+                    if (cnt == 32) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const uint32_t a = __float_as_uint(lds_f32(addr + (uint32_t)i * rowb)) & 0x7FFFFFFFu;
+                            wa |= (a >= hib) ? (1u << i) : 0u;
+                            wi |= (a - lob < span_ab) ? (1u << i) : 0u;
+                        }
+                    } else {
+                        for (int i = 0; i < cnt; ++i) {
+                            const uint32_t a = __float_as_uint(lds_f32(addr + (uint32_t)i * rowb)) & 0x7FFFFFFFu;
+                            wa |= (a >= hib) ? (1u << i) : 0u;
+                            wi |= (a - lob < span_ab) ? (1u << i) : 0u;
+                        }
                     }
-                    if ((k & 31) == 31 || k == k1 - 1) {
-                        sts_u32(s_mb + 4u * (uint32_t)(cl * NW + (k >> 5)), word);
-                        word = 0u;
+                    sts_u32(s_mb + 4u * (uint32_t)(cl * NW + (kb >> 5)), wa);
+                    above += __popc(wa);
+                    while (wi) {
+                        const int i = __ffs(wi) - 1;
+                        wi &= wi - 1;
+                        if (nin < CAPS) sts_u16(cbase + 2u * (uint32_t)(nin * NFP), (uint32_t)(kb + i));
+                        ++nin;
                     }
                 }
                 const uint32_t ci = s_cnt + 4u * (uint32_t)(slot * NFP + cl);
@@ -282,8 +295,8 @@ __global__ void __launch_bounds__(512, 1) small_gram_kernel(SweepArgs A, const i
                 if (!exact) {
                     const int need = c_need[c];
                     if (m <= 32) {
-                        uint64_t v = lane < m ? keyat((int)lds_u16(s_fb + 2u * (uint32_t)(c * kFinalCap + lane))) : 0ull;
-                        v = warp_sort_desc(v, lane);
+                        uint64_t v = lane < m ? keyat((int)lds_u16(s_fb + 2u * (uint32_t)(c * kFinalCap + (lane & 31)))) : 0ull;
+                        v = m <= 16 ? warp_sort_desc_w<16>(v, lane) : warp_sort_desc(v, lane);
                         T = __shfl_sync(CALS_FULL_MASK, v, need - 1);
                     } else {
                         for (int i = lane; i < m; i += 32)
