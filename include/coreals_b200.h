@@ -81,6 +81,8 @@ typedef struct cals_plan {
     int64_t big_cand_total;
     int32_t item_rows;            /* slice rows per work item of a big row */
     int32_t n_f;                  /* rank the plan was built for */
+    const int64_t* big_tile_ptr_host;  /* host copies (caller-owned) used to batch the tiled tier */
+    const int64_t* big_cand_ptr_host;
 } cals_plan;
 
 /* Host: reference budget rule for every row (core.py:48-54), fp64, no FMA. */
@@ -171,6 +173,10 @@ void cals_profile_enable(int on);
  * [0] table-resolved columns, [1] bracket fallbacks, [2] bracket candidates,
  * [3] candidates after pre-narrowing, [4] extra select rounds, [5] rows. */
 void cals_debug_stats(void* device_counters);
+/* Debug: override the tiled-tier batch budgets (candidate keys, work items per
+ * batch; 0 = defaults of 2^27 keys and 1 GiB of partial normal equations).
+ * Must stay in effect from sizing a workspace until its last half-sweep. */
+void cals_debug_big_batch(int64_t cand_keys, int64_t tiles);
 int cals_profile_collect(char* buf, size_t len);
 
 const char* cals_strerror(int status);

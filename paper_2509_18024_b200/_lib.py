@@ -31,6 +31,7 @@ class cals_plan(ctypes.Structure):
         ("big_rows", P), ("n_big", i64), ("big_tile_ptr", P), ("n_big_tiles", i64),
         ("big_cand_ptr", P), ("big_cand_total", i64), ("item_rows", ctypes.c_int32),
         ("n_f", ctypes.c_int32),
+        ("big_tile_ptr_host", P), ("big_cand_ptr_host", P),
     ]
 
 
@@ -51,6 +52,7 @@ SIGNATURES = {
     "cals_predict_entries": (i32, [P, P, i32, i32, i32, P, P, i64, P, P]),
     "cals_profile_enable": (None, [i32]),
     "cals_debug_stats": (None, [P]),
+    "cals_debug_big_batch": (None, [ctypes.c_int64, ctypes.c_int64]),
     "cals_profile_collect": (i32, [ctypes.c_char_p, sz]),
     "cals_strerror": (ctypes.c_char_p, [i32]),
     "cals_build_info": (ctypes.c_char_p, []),

@@ -21,6 +21,7 @@ constexpr int kQSsmall = 4096, kQSbig = 8192;
 constexpr int kItemRowsMin = 4096;
 
 thread_local char g_err[256] = "";
+int64_t g_big_cand_budget = 0, g_big_tile_budget = 0;  // debug overrides, see cals_debug_big_batch
 unsigned long long* g_stats = nullptr;  // debug counters (device), see cals_debug_stats
 
 // ---- optional per-kernel timing (CUDA events on the launch stream) --------
@@ -181,6 +182,46 @@ int cuda_status(const char* where) {
     return CALS_OK;
 }
 
+// Tiled-tier batches: rows [r[i], r[i+1]) share one scan/resolve/gram pass,
+// bounded so candidate keys and partial normal equations fit the workspace.
+struct BigBatches {
+    std::vector<int64_t> r;
+    int64_t max_rows = 0, max_tiles = 0, max_cand = 0;
+};
+BigBatches big_batches(const cals_plan* P) {
+    BigBatches b;
+    b.r.push_back(0);
+    if (P->n_big <= 0 || !P->big_tile_ptr_host || !P->big_cand_ptr_host) {
+        b.max_rows = P->n_big;
+        b.max_tiles = P->n_big_tiles;
+        b.max_cand = P->big_cand_total;
+        if (P->n_big > 0) b.r.push_back(P->n_big);
+        return b;
+    }
+    const int nf = P->n_f;
+    const int64_t cand_budget = g_big_cand_budget > 0 ? g_big_cand_budget : (int64_t)1 << 27;  // 1 GiB of keys
+    const int64_t tile_budget = g_big_tile_budget > 0
+                                    ? g_big_tile_budget
+                                    : std::max<int64_t>(1, ((int64_t)1 << 30) / ((int64_t)nf * (nf + 1) * 4));
+    const int64_t* tp = P->big_tile_ptr_host;
+    const int64_t* cp = P->big_cand_ptr_host;
+    int64_t start = 0;
+    for (int64_t r = 0; r < P->n_big; ++r) {
+        const bool over = (cp[r + 1] - cp[start] > cand_budget) || (tp[r + 1] - tp[start] > tile_budget);
+        if (over && r > start) {
+            b.r.push_back(r);
+            start = r;
+        }
+    }
+    b.r.push_back(P->n_big);
+    for (size_t i = 0; i + 1 < b.r.size(); ++i) {
+        b.max_rows = std::max(b.max_rows, b.r[i + 1] - b.r[i]);
+        b.max_tiles = std::max(b.max_tiles, tp[b.r[i + 1]] - tp[b.r[i]]);
+        b.max_cand = std::max(b.max_cand, cp[b.r[i + 1]] - cp[b.r[i]]);
+    }
+    return b;
+}
+
 struct Work {
     uint32_t* qtab;
     int* cnt;
@@ -210,12 +251,13 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
     Work w{};
     const int nf = P->n_f;
     w.qtab = c.take<uint32_t>((size_t)nf * (kQ + 1));
-    w.cnt = c.take<int>((size_t)P->n_big * nf * 2);
-    w.cand = c.take<uint64_t>((size_t)P->big_cand_total);
-    w.thr = c.take<uint64_t>((size_t)P->n_big * nf);
-    w.part = c.take<float>((size_t)P->n_big_tiles * nf * (nf + 1));
-    w.rss_part = c.take<double>((size_t)P->n_big_tiles);
-    w.hist = c.take<int>((size_t)P->n_big * nf * kHB);
+    const BigBatches bb = big_batches(P);
+    w.cnt = c.take<int>((size_t)bb.max_rows * nf * 2);
+    w.cand = c.take<uint64_t>((size_t)bb.max_cand);
+    w.thr = c.take<uint64_t>((size_t)bb.max_rows * nf);
+    w.part = c.take<float>((size_t)bb.max_tiles * nf * (nf + 1));
+    w.rss_part = c.take<double>((size_t)bb.max_tiles);
+    w.hist = c.take<int>((size_t)bb.max_rows * nf * kHB);
     w.retry = c.take<double>((size_t)std::max<int64_t>(kMaxGrid, kMaxSolveWarps) * retry_stride(nf));
     w.gbuf_rows = gbuf_rows_for(nf, P->n_small + P->n_big);
     w.gbuf = c.take<float>((size_t)w.gbuf_rows * nf * (nf + 1));
@@ -231,6 +273,17 @@ void launch_solve(const SweepArgs& A, const int32_t* rows, int64_t count, cudaSt
         const int64_t warps = (count + (32 / NFP) - 1) / (32 / NFP);
         const int64_t blocks = std::min<int64_t>((warps + 7) / 8, kMaxSolveWarps / 8);
         solve_warp_kernel<NFP><<<(int)blocks, 256, 0, st>>>(A, rows, count);
+    } else if (A.nf <= 64) {
+        const int64_t blocks = std::min<int64_t>((count + 3) / 4, (int64_t)dev().sms * 3 * 4);
+        if (A.nf <= 48) {
+            const size_t smem = (size_t)4 * 48 * 49 * 4;
+            allow_smem(solve_wide_kernel<48>);
+            solve_wide_kernel<48><<<(int)blocks, 128, smem, st>>>(A, rows, count);
+        } else {
+            const size_t smem = (size_t)4 * 64 * 65 * 4;
+            allow_smem(solve_wide_kernel<64>);
+            solve_wide_kernel<64><<<(int)blocks, 128, smem, st>>>(A, rows, count);
+        }
     } else {
         const size_t smem = align16((size_t)A.nf * (A.nf + 1) * 4);
         allow_smem(solve_block_kernel);
@@ -316,52 +369,63 @@ void launch_big_gram(const SweepArgs& A, const BigArgs& B, size_t smem, cudaStre
 template <int NFP>
 int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream_t st) {
     const int nf = A.nf;
-    BigArgs B{};
-    B.rows = P->big_rows;
-    B.tile_ptr = P->big_tile_ptr;
-    B.cand_ptr = P->big_cand_ptr;
-    B.n_big = P->n_big;
-    B.n_tiles = P->n_big_tiles;
-    B.item_rows = P->item_rows;
-    B.chunk = big_chunk(nf);
-    B.cnt = w.cnt;
-    B.cand = w.cand;
-    B.thr = w.thr;
-    B.part = w.part;
-    B.rss_part = w.rss_part;
-    B.hist = w.hist;
-    cudaMemsetAsync(w.cnt, 0, sizeof(int) * (size_t)P->n_big * nf * 2, st);
-    cudaMemsetAsync(w.hist, 0, sizeof(int) * (size_t)P->n_big * nf * kHB, st);
-    const size_t scan_smem = big_scan_smem(nf, B.chunk);
-    allow_smem(big_scan_kernel);
-    {
-        ProfScope ps("big_scan_kernel", st);
-        big_scan_kernel<<<grid_for(big_scan_kernel, scan_smem, B.n_tiles), kThreads, scan_smem, st>>>(A, B);
-    }
-    {
-        const int64_t warps = B.n_big * nf;
-        const int64_t blocks = std::min<int64_t>((warps + 7) / 8, (int64_t)dev().sms * 8);
-        ProfScope ps("big_resolve_kernel", st);
-        big_resolve_kernel<<<(int)std::max<int64_t>(1, blocks), kThreads, 0, st>>>(A, B);
-    }
-    const size_t gram_smem = big_gram_smem(nf, B.chunk);
-    {
-        ProfScope ps("big_gram_kernel", st);
-        const int nq = xs_chunks(nf);
-        if (nq <= 4) launch_big_gram<1>(A, B, gram_smem, st);
-        else if (nq <= 8) launch_big_gram<2>(A, B, gram_smem, st);
-        else if (nq <= 16) launch_big_gram<4>(A, B, gram_smem, st);
-        else launch_big_gram<8>(A, B, gram_smem, st);
-    }
-    for (int64_t r0 = 0; r0 < B.n_big; r0 += w.gbuf_rows) {
-        const int64_t cnt = std::min<int64_t>(w.gbuf_rows, B.n_big - r0);
+    const BigBatches bb = big_batches(P);
+    const int64_t* tp = P->big_tile_ptr_host;
+    const int64_t* cp = P->big_cand_ptr_host;
+    for (size_t bi = 0; bi + 1 < bb.r.size(); ++bi) {
+        const int64_t r0 = bb.r[bi], r1 = bb.r[bi + 1];
+        BigArgs B{};
+        B.rows = P->big_rows + r0;
+        B.tile_ptr = P->big_tile_ptr + r0;
+        B.cand_ptr = P->big_cand_ptr + r0;
+        B.n_big = r1 - r0;
+        B.tile_base = tp ? tp[r0] : 0;
+        B.cand_base = cp ? cp[r0] : 0;
+        B.n_tiles = tp ? tp[r1] - tp[r0] : P->n_big_tiles;
+        B.item_rows = P->item_rows;
+        B.chunk = big_chunk(nf);
+        B.cnt = w.cnt;
+        B.cand = w.cand;
+        B.thr = w.thr;
+        B.part = w.part;
+        B.rss_part = w.rss_part;
+        B.hist = w.hist;
+        cudaMemsetAsync(w.cnt, 0, sizeof(int) * (size_t)B.n_big * nf * 2, st);
+        cudaMemsetAsync(w.hist, 0, sizeof(int) * (size_t)B.n_big * nf * kHB, st);
+        const size_t scan_smem = big_scan_smem(nf, B.chunk);
+        allow_smem(big_scan_kernel);
         {
-            ProfScope ps("big_reduce_kernel", st);
-            big_reduce_kernel<<<(int)std::min<int64_t>(cnt, (int64_t)dev().sms * 8), kThreads, 0, st>>>(A, B, r0, cnt);
+            ProfScope ps("big_scan_kernel", st);
+            big_scan_kernel<<<grid_for(big_scan_kernel, scan_smem, B.n_tiles), kThreads, scan_smem, st>>>(A, B);
         }
-        launch_solve<NFP>(A, P->big_rows + r0, cnt, st);
+        {
+            const int64_t warps = B.n_big * nf;
+            const int64_t blocks = std::min<int64_t>((warps + 7) / 8, (int64_t)dev().sms * 8);
+            ProfScope ps("big_resolve_kernel", st);
+            big_resolve_kernel<<<(int)std::max<int64_t>(1, blocks), kThreads, 0, st>>>(A, B);
+        }
+        const size_t gram_smem = big_gram_smem(nf, B.chunk);
+        {
+            ProfScope ps("big_gram_kernel", st);
+            const int nq = xs_chunks(nf);
+            if (nq <= 4) launch_big_gram<1>(A, B, gram_smem, st);
+            else if (nq <= 8) launch_big_gram<2>(A, B, gram_smem, st);
+            else if (nq <= 16) launch_big_gram<4>(A, B, gram_smem, st);
+            else launch_big_gram<8>(A, B, gram_smem, st);
+        }
+        for (int64_t q0 = 0; q0 < B.n_big; q0 += w.gbuf_rows) {
+            const int64_t cnt = std::min<int64_t>(w.gbuf_rows, B.n_big - q0);
+            {
+                ProfScope ps("big_reduce_kernel", st);
+                big_reduce_kernel<<<(int)std::min<int64_t>(cnt, (int64_t)dev().sms * 8), kThreads, 0, st>>>(A, B, q0,
+                                                                                                         cnt);
+            }
+            launch_solve<NFP>(A, B.rows + q0, cnt, st);
+        }
+        const int rc = cuda_status("big-row kernels");
+        if (rc) return rc;
     }
-    return cuda_status("big-row kernels");
+    return CALS_OK;
 }
 
 }  // namespace
@@ -596,6 +660,10 @@ int cals_predict_entries(const float* U, const float* M, int n_f, int ld_u, int 
 }
 
 void cals_debug_stats(void* device_counters) { g_stats = (unsigned long long*)device_counters; }
+void cals_debug_big_batch(int64_t cand_keys, int64_t tiles) {
+    g_big_cand_budget = cand_keys;
+    g_big_tile_budget = tiles;
+}
 
 void cals_profile_enable(int on) {
     Prof& P = prof();

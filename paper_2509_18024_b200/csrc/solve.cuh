@@ -11,6 +11,8 @@
 //
 // Input: augmented matrix G[r * gs + j], j < nf the Gram, j == nf the RHS.
 #pragma once
+#include <utility>
+
 #include "common.cuh"
 
 namespace cals {
@@ -216,6 +218,125 @@ __device__ __forceinline__ bool seg_lu_solve(const float* __restrict__ Grow, int
     const uint32_t anybad = __ballot_sync(CALS_FULL_MASK, bad);
     const uint32_t segm = (NFP == 32) ? 0xffffffffu : (((1u << NFP) - 1u) << seg_base);
     return fail || (anybad & segm) != 0;
+}
+
+// Wide warp LU (32 < nf <= NF <= 64): lane owns rows `lane` and `lane + 32`
+// of ONE system in registers; same no-swap partial pivoting and pivot-order
+// back substitution as seg_lu_solve.  W: the augmented system (stride nf+1,
+// any memory space).  Returns whether the system failed (warp-uniform); lane
+// l ends with x0 = unknown l and x1 = unknown l + 32.
+// Register select that keeps both operands in registers (a plain ?: between
+// two register arrays can be rewritten as a pointer select into local memory).
+__device__ __forceinline__ float sel_f32(bool hi, float b, float a) {
+    float r;
+    asm("{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n selp.f32 %0, %1, %2, p;\n}\n"
+        : "=f"(r) : "f"(b), "f"(a), "r"((unsigned)hi));
+    return r;
+}
+
+template <int NF>
+struct WideLU {
+    float a[NF], b[NF];
+    float ra, rb;
+    bool ua, ub, fail;
+    int oa, ob;
+};
+
+// Elimination step K (compile-time, so every register index is static).
+template <int NF, int K>
+__device__ __forceinline__ void wide_step(WideLU<NF>& S, bool spd, int lane) {
+    const int r0 = lane, r1 = lane + 32;
+    int p = K;
+    if (!spd) {
+        float best = S.ua ? -1.f : fabsf(S.a[K]);
+        int bi = r0;
+        const float vb = S.ub ? -1.f : fabsf(S.b[K]);
+        if (vb > best) { best = vb; bi = r1; }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float obst = __shfl_xor_sync(CALS_FULL_MASK, best, o);
+            const int oi = __shfl_xor_sync(CALS_FULL_MASK, bi, o);
+            if (obst > best || (obst == best && oi < bi)) { best = obst; bi = oi; }
+        }
+        S.fail |= !(best > 0.f);
+        p = bi;
+    }
+    const bool hi = p >= 32;
+    const int pl = p & 31;
+    const float d = __shfl_sync(CALS_FULL_MASK, sel_f32(hi, S.b[K], S.a[K]), pl);
+    S.fail |= spd ? !(d > 0.f) : !(d == d);
+    if (lane == pl) {
+        if (hi) { S.ub = true; S.ob = K; } else { S.ua = true; S.oa = K; }
+    }
+    const float inv = __frcp_rn(d);
+    const float fa = S.ua ? 0.f : S.a[K] * inv;
+    const float fb = S.ub ? 0.f : S.b[K] * inv;
+#pragma unroll
+    for (int j = K + 1; j < NF; ++j) {
+        const float vp = __shfl_sync(CALS_FULL_MASK, sel_f32(hi, S.b[j], S.a[j]), pl);
+        S.a[j] = fmaf(-fa, vp, S.a[j]);
+        S.b[j] = fmaf(-fb, vp, S.b[j]);
+    }
+    const float bp = __shfl_sync(CALS_FULL_MASK, sel_f32(hi, S.rb, S.ra), pl);
+    S.ra = fmaf(-fa, bp, S.ra);
+    S.rb = fmaf(-fb, bp, S.rb);
+}
+
+// Back-substitution step K (pivot order): unknown K from the row pivoted at step K.
+template <int NF, int K>
+__device__ __forceinline__ void wide_back(WideLU<NF>& S, float& x0, float& x1, int lane) {
+    const uint32_t ba = __ballot_sync(CALS_FULL_MASK, S.oa == K);
+    const uint32_t bb = __ballot_sync(CALS_FULL_MASK, S.ob == K);
+    const int pl = ba ? __ffs(ba) - 1 : (bb ? __ffs(bb) - 1 : 0);
+    float xk = (S.oa == K) ? S.ra / S.a[K] : 0.f;
+    if (S.ob == K) xk = S.rb / S.b[K];
+    xk = __shfl_sync(CALS_FULL_MASK, xk, pl);
+    if (lane == (K & 31)) {
+        if (K < 32) x0 = xk; else x1 = xk;
+    }
+    if (S.oa >= 0 && S.oa < K) S.ra = fmaf(-S.a[K], xk, S.ra);
+    if (S.ob >= 0 && S.ob < K) S.rb = fmaf(-S.b[K], xk, S.rb);
+}
+
+template <int NF, int... K>
+__device__ __forceinline__ void wide_eliminate(WideLU<NF>& S, bool spd, int lane,
+                                               std::integer_sequence<int, K...>) {
+    (wide_step<NF, K>(S, spd, lane), ...);
+}
+template <int NF, int... K>
+__device__ __forceinline__ void wide_substitute(WideLU<NF>& S, float& x0, float& x1, int lane,
+                                                std::integer_sequence<int, K...>) {
+    (wide_back<NF, NF - 1 - K>(S, x0, x1, lane), ...);
+}
+
+template <int NF>
+__device__ __forceinline__ bool wide_lu_solve(const float* __restrict__ W, int nf, bool spd, float& x0, float& x1,
+                                              int lane) {
+    static_assert(NF > 32 && NF <= 64, "two rows per lane");
+    const int gs = nf + 1;
+    const int r0 = lane, r1 = lane + 32;
+    const bool v0 = r0 < nf, v1 = r1 < nf;
+    WideLU<NF> S;
+    // rows >= nf are identity rows with a zero right-hand side: their steps
+    // pivot on themselves and leave x = 0, so no step needs a bound check
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+        S.a[j] = (v0 && j < nf) ? W[r0 * gs + j] : (j == r0 ? 1.f : 0.f);
+        S.b[j] = (v1 && j < nf) ? W[r1 * gs + j] : (j == r1 ? 1.f : 0.f);
+    }
+    S.ra = v0 ? W[r0 * gs + nf] : 0.f;
+    S.rb = v1 ? W[r1 * gs + nf] : 0.f;
+    S.ua = false;
+    S.ub = false;
+    S.oa = -1;
+    S.ob = -1;
+    S.fail = false;
+    wide_eliminate<NF>(S, spd, lane, std::make_integer_sequence<int, NF>{});
+    x0 = 0.f;
+    x1 = 0.f;
+    wide_substitute<NF>(S, x0, x1, lane, std::make_integer_sequence<int, NF>{});
+    const bool bad = (v0 && (!(x0 == x0) || (x0 - x0 != 0.f))) || (v1 && (!(x1 == x1) || (x1 - x1 != 0.f)));
+    return S.fail || __any_sync(CALS_FULL_MASK, bad);
 }
 
 // Float64 retry of a failed system with the reference's diagonal jitter

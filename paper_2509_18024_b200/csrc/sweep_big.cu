@@ -44,13 +44,14 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
     const uint32_t rowb = 4u * (uint32_t)sx;
     const FastDiv fq((uint32_t)xs_chunks(nf));
     for (int64_t t = blockIdx.x; t < B.n_tiles; t += gridDim.x) {
-        const int r = find_row(B.tile_ptr, B.n_big, t);
+        const int64_t T_abs = B.tile_base + t;
+        const int r = find_row(B.tile_ptr, B.n_big, T_abs);
         const int row = B.rows[r];
         const int64_t lo = A.ptr[row];
         const int n = (int)(A.ptr[row + 1] - lo);
         const int s = A.budget[row];
         if (s >= n) continue;  // complete sketch: nothing to select (uniform per block)
-        const int kbeg = (int)(t - B.tile_ptr[r]) * B.item_rows;
+        const int kbeg = (int)(T_abs - B.tile_ptr[r]) * B.item_rows;
         const int kend = min(n, kbeg + B.item_rows);
         __syncthreads();
         if (tid < nf) {
@@ -61,8 +62,8 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
             s_above[tid] = 0;
         }
         for (int e = tid; e < nf * kHB; e += nt) s_hist[e] = 0;
-        const int64_t cbase = B.cand_ptr[r];
-        const int capB = (int)((B.cand_ptr[r + 1] - cbase) / nf);
+        const int64_t cbase = B.cand_ptr[r] - B.cand_base;
+        const int capB = (int)((B.cand_ptr[r + 1] - B.cand_ptr[r]) / nf);
         for (int k0 = kbeg; k0 < kend; k0 += B.chunk) {
             const int kn = min(B.chunk, kend - k0);
             __syncthreads();
@@ -148,8 +149,8 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
         } else {
             const int above = B.cnt[((size_t)r * nf + c) * 2];
             const int in = B.cnt[((size_t)r * nf + c) * 2 + 1];
-            const int64_t cbase = B.cand_ptr[r];
-            const int capB = (int)((B.cand_ptr[r + 1] - cbase) / nf);
+            const int64_t cbase = B.cand_ptr[r] - B.cand_base;
+            const int capB = (int)((B.cand_ptr[r + 1] - B.cand_ptr[r]) / nf);
             uint64_t* cl = B.cand + cbase + (int64_t)c * capB;
             uint32_t hib, lob;
             table_bracket(A.qtab + (size_t)c * (kQ + 1), n, s, A.delta_tab, hib, lob);
@@ -226,12 +227,13 @@ __global__ void __launch_bounds__(kThreads) big_gram_kernel(SweepArgs A, BigArgs
     const FastDiv fq((uint32_t)xs_chunks(nf));
     const int my_cols = warp < nf ? (nf - 1 - warp) / nwarps + 1 : 0;
     for (int64_t t = blockIdx.x; t < B.n_tiles; t += gridDim.x) {
-        const int r = find_row(B.tile_ptr, B.n_big, t);
+        const int64_t T_abs = B.tile_base + t;
+        const int r = find_row(B.tile_ptr, B.n_big, T_abs);
         const int row = B.rows[r];
         const int64_t lo = A.ptr[row];
         const int n = (int)(A.ptr[row + 1] - lo);
         const bool full = A.budget[row] >= n;
-        const int kbeg = (int)(t - B.tile_ptr[r]) * B.item_rows;
+        const int kbeg = (int)(T_abs - B.tile_ptr[r]) * B.item_rows;
         const int kend = min(n, kbeg + B.item_rows);
         __syncthreads();
         if (tid < nf) {
@@ -306,7 +308,7 @@ __global__ void __launch_bounds__(kThreads) big_reduce_kernel(SweepArgs A, BigAr
         const int64_t r = r0 + q;
         const int row = B.rows[r];
         const int n = (int)(A.ptr[row + 1] - A.ptr[row]);
-        const int64_t t0 = B.tile_ptr[r], t1 = B.tile_ptr[r + 1];
+        const int64_t t0 = B.tile_ptr[r] - B.tile_base, t1 = B.tile_ptr[r + 1] - B.tile_base;
         const float lam_n = (float)(A.lam * (double)n);
         float* G = A.gbuf + (size_t)q * nout;
         for (int e = threadIdx.x; e < nout; e += blockDim.x) {

@@ -56,8 +56,10 @@ struct BigArgs {
     const int32_t* rows;      // [n_big] row ids
     const int64_t* tile_ptr;  // [n_big + 1] item prefix per row
     const int64_t* cand_ptr;  // [n_big + 1] candidate key offsets (nf equal column regions)
-    int64_t n_big;
-    int64_t n_tiles;
+    int64_t n_big;            // rows of this batch
+    int64_t n_tiles;          // work items of this batch
+    int64_t tile_base;        // absolute index of the batch's first work item
+    int64_t cand_base;        // absolute offset of the batch's first candidate key
     int item_rows;            // slice rows per work item
     int chunk;                // slice rows staged per shared-memory chunk
     int* cnt;                 // [n_big][nf][2]  (above, in)

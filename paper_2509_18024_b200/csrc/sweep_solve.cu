@@ -113,6 +113,57 @@ __global__ void __launch_bounds__(128) solve_block_kernel(SweepArgs A, const int
     }
 }
 
+// One warp per system (32 < nf <= NF <= 64): wide register LU on a copy of
+// the system staged (coalesced) into the warp's shared-memory slot.
+template <int NF>
+__global__ void __launch_bounds__(128, 3) solve_wide_kernel(SweepArgs A, const int32_t* __restrict__ rows,
+                                                          int64_t n_list) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nf = A.nf, gs = nf + 1, nout = nf * gs;
+    float* W = reinterpret_cast<float*>(smem) + (size_t)warp * NF * (NF + 1);
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t li = gw; li < n_list; li += stride) {
+        const int row = rows[li];
+        const int n = (int)(A.ptr[row + 1] - A.ptr[row]);
+        const bool spd = A.budget[row] >= n;
+        const float* G = A.gbuf + (size_t)li * nout;
+        __syncwarp();
+        for (int e = lane; e < nout; e += 32) W[e] = __ldcs(G + e);
+        __syncwarp();
+        float x0, x1;
+        int st = CALS_ROW_OK;
+        if (wide_lu_solve<NF>(W, nf, spd, x0, x1, lane)) {
+            double* Wd = A.retry_ws + (size_t)gw * A.retry_stride;
+            double* xd = Wd + nout;
+            const int bad = warp_retry_f64(G, nf, spd, Wd, xd, lane);
+            __syncwarp();
+            x0 = lane < nf ? (float)xd[lane] : 0.f;
+            x1 = lane + 32 < nf ? (float)xd[lane + 32] : 0.f;
+            st = bad ? CALS_ROW_SINGULAR : CALS_ROW_JITTERED;
+        }
+        float* out = A.tgt + (int64_t)row * A.ld_tgt;
+        if (st != CALS_ROW_SINGULAR) {
+            if (lane < nf) out[lane] = x0;
+            if (lane + 32 < nf) out[lane + 32] = x1;
+        }
+        if (A.pen_rows != nullptr) {
+            double p = (lane < nf ? (double)x0 * (double)x0 : 0.0) + (lane + 32 < nf ? (double)x1 * (double)x1 : 0.0);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(CALS_FULL_MASK, p, o);
+            if (lane == 0) A.pen_rows[row] = (st == CALS_ROW_SINGULAR) ? 0.0 : (double)n * p;
+        }
+        if (lane == 0) {
+            A.status[row] = st;
+            report_status(A, row, st);
+        }
+    }
+}
+
+template __global__ void solve_wide_kernel<48>(SweepArgs, const int32_t*, int64_t);
+template __global__ void solve_wide_kernel<64>(SweepArgs, const int32_t*, int64_t);
+
 template __global__ void solve_warp_kernel<8>(SweepArgs, const int32_t*, int64_t);
 template __global__ void solve_warp_kernel<16>(SweepArgs, const int32_t*, int64_t);
 template __global__ void solve_warp_kernel<32>(SweepArgs, const int32_t*, int64_t);

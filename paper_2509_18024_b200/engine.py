@@ -87,6 +87,10 @@ class DeviceSide:
         meta.big_rows = self.big.data_ptr()
         meta.big_tile_ptr = self.tile_ptr.data_ptr()
         meta.big_cand_ptr = self.cand_ptr.data_ptr()
+        self.tile_ptr_host = np.ascontiguousarray(tile_ptr[:meta.n_big + 1])
+        self.cand_ptr_host = np.ascontiguousarray(cand_ptr[:meta.n_big + 1])
+        meta.big_tile_ptr_host = self.tile_ptr_host.ctypes.data
+        meta.big_cand_ptr_host = self.cand_ptr_host.ctypes.data
         self.plan = meta
         self.side = _lib.cals_side(self.ptr.data_ptr(), self.idx.data_ptr(), self.val.data_ptr(), n_rows, nnz)
         self.ws_bytes = int(L.cals_workspace_bytes(ctypes.byref(meta)))

@@ -164,6 +164,32 @@ def test_oracle_parity_tiled_tier_small_rank(n_f):
     assert eng.item.plan.n_big > 0
 
 
+@pytest.mark.parametrize("budget", [(1, 1), (20000, 7), (60000, 1 << 20)])
+def test_tiled_tier_batches_match_single_pass(budget):
+    """Forcing the tiled tier into several batches (down to one row per batch)
+    gives bit-identical rows and keys to the single-pass schedule."""
+    from paper_2509_18024_b200 import _lib
+    u, i, v = random_matrix(21, 30000, 400, 0.01, heavy_items=12, heavy_density=0.6)
+    R = cb.RatingMatrix(u, i, v, n_users=30000, n_items=400)
+    M0 = np.random.default_rng(6).normal(0, 0.1, (400, 32)).astype(np.float32)
+    ref = CoreEngine(R, 32, 0.2, 0.05)
+    assert ref.item.plan.n_big >= 12
+    U, _ = gpu_half(ref, "user", M0)
+    Mr, kr = gpu_half(ref, "item", U.astype(np.float32))
+    ref.half("user", rss=True)
+    rss_ref = ref.user.rss_rows.clone()
+    _lib.load().cals_debug_big_batch(*budget)
+    try:
+        eng = CoreEngine(R, 32, 0.2, 0.05)
+        gpu_half(eng, "user", M0)
+        Mb, kb = gpu_half(eng, "item", U.astype(np.float32))
+        eng.half("user", rss=True)
+    finally:
+        _lib.load().cals_debug_big_batch(0, 0)
+    assert np.array_equal(kr, kb) and np.array_equal(Mr, Mb)
+    assert torch.equal(rss_ref, eng.user.rss_rows)
+
+
 @pytest.mark.parametrize("rate", [0.02, 0.1, 0.3, 0.5, 0.999, 1.0])
 def test_oracle_parity_rates(rate):
     u, i, v = random_matrix(7, 2000, 300, 0.1, heavy_items=3, heavy_density=1.0)

@@ -28,3 +28,21 @@ for side in (eng.user, eng.item):
     c = side.counts[side.counts > 0]
     print("rows", c.size, "n mean", round(float(c.mean()), 1), "max", c.max(), "small", side.plan.n_small,
           "big", side.plan.n_big, "segs", list(side.plan.small_seg), list(side.plan.small_seg_maxn))
+for side in (eng.user, eng.item):
+    if side.plan.n_big:
+        c = side.counts[side.counts > 0]
+        big = np.sort(c)[-side.plan.n_big:]
+        print("big rows n quantiles (0,.5,.9,.99,1):", np.quantile(big, [0, .5, .9, .99, 1]).astype(int),
+              "big nnz share", round(float(big.sum() / c.sum()), 3), "tiles", side.plan.n_big_tiles,
+              "cand", side.plan.big_cand_total)
+_lib.profile_enable(True)
+for s in ("user", "item"):
+    for _ in range(2):
+        eng.half(s)
+    torch.cuda.synchronize()
+    _lib.profile_collect()
+    eng.half(s)
+    torch.cuda.synchronize()
+    prof = _lib.profile_collect()
+    print(s, "half-sweep kernels (ms):", {k: round(v[1], 3) if isinstance(v, tuple) else v for k, v in prof.items()})
+_lib.profile_enable(False)
