@@ -230,6 +230,7 @@ struct Work {
     float* part;
     double* rss_part;
     int* hist;
+    uint32_t* brk;
     double* retry;
     float* gbuf;
     int64_t gbuf_rows;
@@ -258,6 +259,7 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
     w.part = c.take<float>((size_t)bb.max_tiles * nf * (nf + 1));
     w.rss_part = c.take<double>((size_t)bb.max_tiles);
     w.hist = c.take<int>((size_t)bb.max_rows * nf * kHB);
+    w.brk = c.take<uint32_t>((size_t)bb.max_rows * nf);
     w.retry = c.take<double>((size_t)std::max<int64_t>(kMaxGrid, kMaxSolveWarps) * retry_stride(nf));
     w.gbuf_rows = gbuf_rows_for(nf, P->n_small + P->n_big);
     w.gbuf = c.take<float>((size_t)w.gbuf_rows * nf * (nf + 1));
@@ -390,7 +392,20 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
         B.part = w.part;
         B.rss_part = w.rss_part;
         B.hist = w.hist;
+        B.brk = w.brk;
         cudaMemsetAsync(w.cnt, 0, sizeof(int) * (size_t)B.n_big * nf * 2, st);
+        cudaMemsetAsync(w.brk, 0xFF, sizeof(uint32_t) * (size_t)B.n_big * nf, st);
+        // rows spanning >= 2 work items get row-local bracket levels (rows are sorted by length)
+        int64_t n_calib = 0;
+        if (tp)
+            while (n_calib < B.n_big && tp[r0 + n_calib + 1] - tp[r0 + n_calib] >= 2) ++n_calib;
+        if (n_calib > 0) {
+            const size_t smem = (size_t)2 * kCalibCols * (kQ + 1) * sizeof(uint32_t);
+            allow_smem(big_calib_kernel);
+            ProfScope ps("big_calib_kernel", st);
+            big_calib_kernel<<<(int)std::min<int64_t>(n_calib, (int64_t)dev().sms * 3), kThreads, smem, st>>>(A, B,
+                                                                                                      n_calib);
+        }
         cudaMemsetAsync(w.hist, 0, sizeof(int) * (size_t)B.n_big * nf * kHB, st);
         const size_t scan_smem = big_scan_smem(nf, B.chunk);
         allow_smem(big_scan_kernel);

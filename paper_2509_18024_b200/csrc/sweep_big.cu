@@ -32,6 +32,83 @@ __device__ __forceinline__ int find_row(const int64_t* tile_ptr, int64_t n_big, 
     return (int)lo;
 }
 
+// Row-local bracket calibration for long rows: the table describes the
+// rating-weighted population of source values, and a long row's own values
+// can sit systematically above or below it (a popular item is rated by
+// nearly every user, not by an activity-weighted draw).  A deterministic
+// strided sample of kCalibSamples slice rows is counted against the table
+// levels of each column; the bracket levels are the sample's rank estimates
+// of the target fraction s/n, +- kCalibZ sampling sigmas.  A miss is still
+// caught (and resolved exactly) by big_resolve.
+constexpr int kCalibSamples = 4096;
+constexpr float kCalibZ = 5.5f;
+constexpr int kCalibCols = 32;  // columns per shared-memory pass
+
+__global__ void __launch_bounds__(kThreads) big_calib_kernel(SweepArgs A, BigArgs B, int64_t n_rows) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t* qs = reinterpret_cast<uint32_t*>(smem);  // [kCalibCols][kQ + 1]
+    uint32_t* hist = qs + kCalibCols * (kQ + 1);         // [kCalibCols][kQ + 1]
+    const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    for (int64_t r = blockIdx.x; r < n_rows; r += gridDim.x) {
+        const int row = B.rows[r];
+        const int64_t lo = A.ptr[row];
+        const int n = (int)(A.ptr[row + 1] - lo);
+        const int s = A.budget[row];
+        if (s >= n) continue;
+        const int m = min(n, kCalibSamples);
+        const double p = (double)s / (double)n;
+        const double sig = sqrt(p * (1.0 - p) / (double)m * (double)(n - m) / (double)max(n - 1, 1));
+        const int t_lo = (int)floor((p - kCalibZ * sig) * (double)m);
+        const int t_hi = (int)ceil((p + kCalibZ * sig) * (double)m);
+        for (int c0 = 0; c0 < nf; c0 += kCalibCols) {
+            const int gc = min(kCalibCols, nf - c0);
+            __syncthreads();
+            for (int e = tid; e < gc * (kQ + 1); e += nt) {
+                qs[e] = A.qtab[(size_t)c0 * (kQ + 1) + e];
+                hist[e] = 0;
+            }
+            __syncthreads();
+            for (int j = tid; j < m; j += nt) {
+                const int k = (int)(((2 * (int64_t)j + 1) * n) / (2 * (int64_t)m));
+                const float* xr = A.src + (int64_t)__ldg(A.idx + lo + k) * A.ld_src + c0;
+                for (int g = 0; g < gc; ++g) {
+                    const uint32_t v = abs_bits(__ldg(xr + g));
+                    const uint32_t* q = qs + g * (kQ + 1);
+                    int a = 1, b = kQ;  // first level L with q[L] <= v (q descending, q[kQ] = 0)
+                    while (a < b) {
+                        const int mid = (a + b) >> 1;
+                        if (q[mid] <= v) b = mid; else a = mid + 1;
+                    }
+                    atomicAdd(&hist[g * (kQ + 1) + a], 1u);
+                }
+            }
+            __syncthreads();
+            for (int g = warp; g < gc; g += nt >> 5) {
+                // cnt(j) = sample values >= q[j] = sum_{L <= j} hist[L] (nondecreasing in j)
+                int run = 0, n_le = 0, n_lt = 0;
+                for (int j0 = 0; j0 <= kQ; j0 += 32) {
+                    const int j = j0 + lane;
+                    int v = j <= kQ ? (int)hist[g * (kQ + 1) + j] : 0;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int t2 = __shfl_up_sync(CALS_FULL_MASK, v, o);
+                        if (lane >= o) v += t2;
+                    }
+                    const int cnt = run + v;
+                    n_le += __popc(__ballot_sync(CALS_FULL_MASK, j <= kQ && cnt <= t_lo));
+                    n_lt += __popc(__ballot_sync(CALS_FULL_MASK, j <= kQ && cnt < t_hi));
+                    run += __shfl_sync(CALS_FULL_MASK, v, 31);
+                }
+                if (lane == 0) {
+                    const int jhi = t_lo < 0 ? 0 : n_le - 1;
+                    const int jlo = t_hi > m ? kQ : min(n_lt, kQ);
+                    ((uint32_t*)B.brk)[(size_t)r * nf + c0 + g] = (uint32_t)jhi | ((uint32_t)jlo << 16);
+                }
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs B) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_above[CALS_MAX_NF_DEV], s_base[CALS_MAX_NF_DEV], s_slot[CALS_MAX_NF_DEV];
@@ -56,7 +133,7 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
         __syncthreads();
         if (tid < nf) {
             uint32_t hib, lob;
-            table_bracket(A.qtab + (size_t)tid * (kQ + 1), n, s, A.delta_tab, hib, lob);
+            big_bracket(A, B, r, tid, n, s, hib, lob);
             s_hib[tid] = hib;
             s_lob[tid] = lob;
             s_above[tid] = 0;
@@ -153,7 +230,7 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
             const int capB = (int)((B.cand_ptr[r + 1] - B.cand_ptr[r]) / nf);
             uint64_t* cl = B.cand + cbase + (int64_t)c * capB;
             uint32_t hib, lob;
-            table_bracket(A.qtab + (size_t)c * (kQ + 1), n, s, A.delta_tab, hib, lob);
+            big_bracket(A, B, r, c, n, s, hib, lob);
             const uint64_t hik = hi_key_of(hib), lok = (uint64_t)lob << 32;
             if (above < s && s <= above + in && in <= capB && lok < hik) {
                 // bucket holding the target rank: inclusive scan of the histogram from the top
@@ -188,7 +265,11 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
                 if (lane == 0) stat_add(A, kStBigColumns, 1);
                 T = warp_select_keys(KeyList{cl}, m, need - before, blo, bhi, lane);
             } else {
-                if (lane == 0) stat_add(A, kStBigFallback, 1);
+                if (lane == 0) {
+                    stat_add(A, kStBigFallback, 1);
+                    stat_add(A, above >= s ? kStBigMissAbove : (above + in < s ? kStBigMissBelow : kStBigOverflow), 1);
+                    stat_add(A, kStBigFallbackN, (unsigned long long)n);
+                }
                 uint64_t rlo, rhi;
                 int m, need;
                 if (above >= s) { rlo = hik; rhi = ~0ull; m = above; need = s; }

@@ -41,7 +41,8 @@ struct SweepArgs {
 
 // Debug counters (only when A.stats != nullptr): see cals_debug_stats.
 enum StatId { kStColumns = 0, kStFallback, kStCandidates, kStAfterPrenarrow, kStSelectRounds, kStRows,
-              kStBigColumns, kStBigFallback, kStSmallOver, kStSmallMiss, kStFinalOver, kStCount = 16 };
+              kStBigColumns, kStBigFallback, kStSmallOver, kStSmallMiss, kStFinalOver, kStBigMissAbove,
+              kStBigMissBelow, kStBigOverflow, kStBigFallbackN, kStCount = 16 };
 __device__ __forceinline__ void stat_add(const SweepArgs& A, int id, unsigned long long v) {
     if (A.stats != nullptr) atomicAdd(A.stats + id, v);
 }
@@ -69,6 +70,7 @@ struct BigArgs {
     float* wbig;              // [n_big][nf]
     double* rss_part;         // [n_tiles]
     int* hist;                // [n_big][nf][kHB] in-bracket counts per sub-bucket
+    const uint32_t* brk;      // [n_big][nf] calibrated levels jhi | jlo << 16, or ~0u (use the table margin)
 };
 
 constexpr int kHB = 32;  // sub-buckets of a big row's bracket (linear in abs-bit space)
@@ -112,6 +114,20 @@ __device__ __forceinline__ void table_bracket(const uint32_t* qtab_c, int n, int
     table_levels(n, s, delta_tab, jhi, jlo);
     hib = qtab_c[jhi];
     lob = qtab_c[jlo];
+}
+
+// Bracket of big row r (batch-relative), column c: the row's own calibrated
+// table levels when it has them (big_calib_kernel), else the table margin.
+__device__ __forceinline__ void big_bracket(const SweepArgs& A, const BigArgs& B, int r, int c, int n, int s,
+                                            uint32_t& hib, uint32_t& lob) {
+    const uint32_t* q = A.qtab + (size_t)c * (kQ + 1);
+    const uint32_t v = B.brk != nullptr ? B.brk[(size_t)r * A.nf + c] : ~0u;
+    if (v != ~0u) {
+        hib = q[v & 0xFFFFu];
+        lob = q[v >> 16];
+    } else {
+        table_bracket(q, n, s, A.delta_tab, hib, lob);
+    }
 }
 
 __device__ __forceinline__ uint64_t hi_key_of(uint32_t hib) {

@@ -17,13 +17,16 @@ eng.set_factors(np.zeros((d.n_users, spec["n_f"])), synth.init_m(d.n_items, spec
 for it in range(2):
     eng.step("user")
 st = torch.zeros(16, dtype=torch.int64, device="cuda")
-_lib.load().cals_debug_stats(st.data_ptr())
-eng.step("user")
-torch.cuda.synchronize()
-_lib.load().cals_debug_stats(None)
-v = st.cpu().numpy()
-print(cfg, "rows(small, table)", v[0], "fallback", v[1], "cand/col", v[2] / max(v[0], 1),
-      "small over", v[8], "small miss", v[9], "final over", v[10], "big cols", v[6], "big fallback", v[7])
+for s in ("user", "item"):
+    st.zero_()
+    _lib.load().cals_debug_stats(st.data_ptr())
+    eng.half(s)
+    torch.cuda.synchronize()
+    _lib.load().cals_debug_stats(None)
+    v = st.cpu().numpy()
+    print(cfg, s, "rows(small, table)", v[0], "fallback", v[1], "cand/col", v[2] / max(v[0], 1),
+          "small over", v[8], "small miss", v[9], "final over", v[10], "big cols", v[6], "big fallback", v[7],
+          "miss above/below/overflow", v[11], v[12], v[13], "mean n of fallbacks", v[14] / max(v[7], 1))
 for side in (eng.user, eng.item):
     c = side.counts[side.counts > 0]
     print("rows", c.size, "n mean", round(float(c.mean()), 1), "max", c.max(), "small", side.plan.n_small,
