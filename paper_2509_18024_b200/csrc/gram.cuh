@@ -301,6 +301,100 @@ __device__ __forceinline__ void sparse_gram_owned(uint32_t xs, int sx, uint32_t 
     }
 }
 
+// Register-resident variant for a warp owning n_cols <= 32/LPC columns: the
+// accumulators persist across staged chunks (OwnedAcc), so the reduction and
+// the write-out happen once per work item (owned_flush) instead of per chunk.
+__host__ __device__ inline bool owned_single_round(int nf, int nwarps) {
+    const int nq = xs_chunks(nf);
+    const int lpc = nq < 4 ? nq : 4;
+    return (nf + nwarps - 1) / nwarps <= 32 / lpc;
+}
+
+template <int CPL>
+struct OwnedAcc {
+    float acc[4 * CPL];
+    float accb;
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i < 4 * CPL; ++i) acc[i] = 0.f;
+        accb = 0.f;
+    }
+};
+
+struct OwnedMap {
+    int LPC, QG, cs, qg, fl, c;
+    bool cvalid;
+    __device__ __forceinline__ OwnedMap(int nf, int c_first, int c_step, int n_cols, int lane) {
+        const int nq = xs_chunks(nf);
+        LPC = nq < 4 ? nq : 4;
+        int CT = 1;
+        while (CT < n_cols) CT <<= 1;
+        QG = 32 / (CT * LPC);
+        cs = lane / (QG * LPC);
+        qg = (lane / LPC) % QG;
+        fl = lane % LPC;
+        cvalid = cs < n_cols;
+        c = c_first + (cvalid ? cs : 0) * c_step;
+    }
+};
+
+// Accumulate one staged chunk: column M.c over its kept-row list (len rows,
+// or all rows when full).
+template <int CPL>
+__device__ __forceinline__ void owned_accumulate(OwnedAcc<CPL>& S, const OwnedMap& M, uint32_t xs, int sx,
+                                                 uint32_t ys, int nf, int len, bool full, uint32_t lists,
+                                                 int Smax) {
+    const int nq = xs_chunks(nf);
+    const uint32_t rowb = 4u * (uint32_t)sx;
+    const uint32_t L = lists + 2u * (uint32_t)(M.c * Smax);
+    const uint32_t xcol = xs + 4u * (uint32_t)M.c;
+    const bool chunk_ok_last = (M.fl + (CPL - 1) * M.LPC) < nq;
+    const int n = M.cvalid ? len : 0;
+    for (int q = M.qg; q < n; q += M.QG) {
+        const uint32_t k = full ? (uint32_t)q : lds_u16(L + 2u * (uint32_t)q);
+        const uint32_t rb = k * rowb;
+        const float xc = lds_f32(xcol + rb);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            if (i < CPL - 1 || chunk_ok_last) {
+                const float4 v = lds_f128(xs + rb + 16u * (uint32_t)(M.fl + i * M.LPC));
+                S.acc[4 * i + 0] = fmaf(xc, v.x, S.acc[4 * i + 0]);
+                S.acc[4 * i + 1] = fmaf(xc, v.y, S.acc[4 * i + 1]);
+                S.acc[4 * i + 2] = fmaf(xc, v.z, S.acc[4 * i + 2]);
+                S.acc[4 * i + 3] = fmaf(xc, v.w, S.acc[4 * i + 3]);
+            }
+        }
+        if (M.fl == 0) S.accb = fmaf(xc, lds_f32(ys + 4u * k), S.accb);
+    }
+}
+
+// Fixed-order reduction over the q-groups; row M.c of out (stride nf+1).
+template <int CPL>
+__device__ __forceinline__ void owned_flush(OwnedAcc<CPL>& S, const OwnedMap& M, int nf, float* __restrict__ out) {
+    const int nq = xs_chunks(nf);
+    const int gs = nf + 1;
+    for (int o = M.LPC; o < M.LPC * M.QG; o <<= 1) {
+#pragma unroll
+        for (int i = 0; i < 4 * CPL; ++i) S.acc[i] += __shfl_xor_sync(CALS_FULL_MASK, S.acc[i], o);
+        S.accb += __shfl_xor_sync(CALS_FULL_MASK, S.accb, o);
+    }
+    if (M.cvalid && M.qg == 0) {
+        float* grow = out + (size_t)M.c * gs;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            const int ch = M.fl + i * M.LPC;
+            if (ch < nq) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int f = 4 * ch + t;
+                    if (f < nf) grow[f] = S.acc[4 * i + t];
+                }
+            }
+        }
+        if (M.fl == 0) grow[nf] = S.accb;
+    }
+}
+
 __device__ __forceinline__ void sparse_gram_owned_any(uint32_t xs, int sx, uint32_t ys, int nf, int len, bool full,
                                                       uint32_t lists, int Smax, int c_first, int c_step, int n_cols,
                                                       float lam_n, float* Gout, int lane) {

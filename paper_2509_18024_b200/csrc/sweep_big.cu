@@ -287,7 +287,9 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
 
 // Partial normal equations of one work item: per staged chunk, warp w builds
 // the kept-row lists of its columns (ballots on key >= T) and accumulates
-// their sparse Gram rows in shared memory; the item's partial goes to global.
+// their sparse Gram rows -- in registers across the item's chunks when the
+// warp's columns fit one lane-group round (nf <= 64), else in shared memory;
+// the item's partial goes to global.
 template <int CPL>
 __global__ void __launch_bounds__(kThreads) big_gram_kernel(SweepArgs A, BigArgs B) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -297,16 +299,20 @@ __global__ void __launch_bounds__(kThreads) big_gram_kernel(SweepArgs A, BigArgs
     const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const int sx = xs_stride(nf), gs = nf + 1;
     const int CH = B.chunk;
+    const bool persist = owned_single_round(nf, nwarps);
     float* Xs = reinterpret_cast<float*>(smem);
     float* ys = reinterpret_cast<float*>(smem + align16((size_t)CH * sx * 4));
     unsigned char* after_ys = reinterpret_cast<unsigned char*>(ys) + align16((size_t)CH * 4);
-    float* G = reinterpret_cast<float*>(after_ys);
-    unsigned char* after_g = after_ys + align16((size_t)nf * gs * 4);
+    float* G = reinterpret_cast<float*>(after_ys);  // shared-memory accumulation (!persist only)
+    unsigned char* after_g = after_ys + (persist ? 0 : align16((size_t)nf * gs * 4));
     const uint32_t s_xs = smem_u32(Xs), s_ys = smem_u32(ys);
-    const uint32_t s_lists = smem_u32(after_g);  // [nf][CH] u16
+    const uint32_t s_lists = smem_u32(after_g);  // [nf][CH] u16, then [nf] u32 lengths
+    const uint32_t s_lens = s_lists + 2u * (uint32_t)(nf * CH);
     const uint32_t rowb = 4u * (uint32_t)sx;
     const FastDiv fq((uint32_t)xs_chunks(nf));
     const int my_cols = warp < nf ? (nf - 1 - warp) / nwarps + 1 : 0;
+    const OwnedMap M(nf, warp, nwarps, my_cols, lane);
+    OwnedAcc<CPL> S;
     for (int64_t t = blockIdx.x; t < B.n_tiles; t += gridDim.x) {
         const int64_t T_abs = B.tile_base + t;
         const int r = find_row(B.tile_ptr, B.n_big, T_abs);
@@ -321,6 +327,7 @@ __global__ void __launch_bounds__(kThreads) big_gram_kernel(SweepArgs A, BigArgs
             s_thr[tid] = B.thr[(size_t)r * nf + tid];
             if (A.tgt_old != nullptr) wold[tid] = A.tgt_old[(int64_t)row * A.ld_old + tid];
         }
+        S.zero();
         double racc = 0.0;
         for (int k0 = kbeg; k0 < kend; k0 += CH) {
             const int kn = min(CH, kend - k0);
@@ -336,10 +343,8 @@ __global__ void __launch_bounds__(kThreads) big_gram_kernel(SweepArgs A, BigArgs
                     racc = fma(d, d, racc);
                 }
             }
-            int len = kn;
             if (!full) {
-                // kept-row lists of the owned columns (ascending k), same length
-                // for all columns only when complete, so each column keeps its own
+                // kept-row lists of the owned columns (ascending k)
                 for (int j = 0; j < my_cols; ++j) {
                     const int c = warp + j * nwarps;
                     const uint64_t T = s_thr[c];
@@ -353,22 +358,29 @@ __global__ void __launch_bounds__(kThreads) big_gram_kernel(SweepArgs A, BigArgs
                         if (keep) sts_u16(L + 2u * (uint32_t)(w + __popc(bal & lanemask_lt())), (uint32_t)k);
                         w += __popc(bal);
                     }
-                    if (lane == 0) sts_u32(s_lists + 2u * (uint32_t)(nf * CH) + 4u * c, (uint32_t)w);
+                    if (lane == 0) sts_u32(s_lens + 4u * c, (uint32_t)w);
                 }
                 __syncwarp();
             }
-            // sparse accumulate (columns may have different list lengths here)
-            for (int j = 0; j < my_cols; ++j) {
-                const int c = warp + j * nwarps;
-                const int lc = full ? kn : (int)lds_u32(s_lists + 2u * (uint32_t)(nf * CH) + 4u * c);
-                sparse_gram_owned<CPL>(s_xs, sx, s_ys, nf, lc, full, s_lists, CH, c, nwarps, 1, 0.f, G, lane,
-                                       k0 != kbeg);
+            if (persist) {
+                const int lc = full ? kn : (M.cvalid ? (int)lds_u32(s_lens + 4u * M.c) : 0);
+                owned_accumulate<CPL>(S, M, s_xs, sx, s_ys, nf, lc, full, s_lists, CH);
+            } else {
+                for (int j = 0; j < my_cols; ++j) {
+                    const int c = warp + j * nwarps;
+                    const int lc = full ? kn : (int)lds_u32(s_lens + 4u * c);
+                    sparse_gram_owned<CPL>(s_xs, sx, s_ys, nf, lc, full, s_lists, CH, c, nwarps, 1, 0.f, G, lane,
+                                           k0 != kbeg);
+                }
             }
-            (void)len;
         }
-        __syncthreads();
         float* out = B.part + (size_t)t * nf * gs;
-        for (int e = tid; e < nf * gs; e += nt) out[e] = G[e];
+        if (persist) {
+            owned_flush<CPL>(S, M, nf, out);
+        } else {
+            __syncthreads();
+            for (int e = tid; e < nf * gs; e += nt) out[e] = G[e];
+        }
         if (A.rss_rows != nullptr) {
             racc = block_sum_d(racc, red);
             if (tid == 0) B.rss_part[t] = racc;

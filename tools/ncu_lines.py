@@ -1,7 +1,11 @@
 """Aggregate ncu source-page warp-stall samples per CUDA source line."""
 import csv, sys, subprocess, io, collections
 rep = sys.argv[1]
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
+kfilt = sys.argv[3] if len(sys.argv) > 3 else None
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"]
+if kfilt:
+    cmd[3:3] = ["-k", f"regex:{kfilt}", "-c", "1"]
+out = subprocess.run(cmd,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 fname = None
