@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kThreads) big_calib_kernel(SweepArgs A, BigArg
         const int n = (int)(A.ptr[row + 1] - lo);
         const int s = A.budget[row];
         if (s >= n) continue;
-        const int m = min(n, kCalibSamples);
+        const int m = min(kCalibSamples, max(1024, n / 4));  // n > 4096 here
         const double p = (double)s / (double)n;
         const double sig = sqrt(p * (1.0 - p) / (double)m * (double)(n - m) / (double)max(n - 1, 1));
         const int t_lo = (int)floor((p - kCalibZ * sig) * (double)m);
@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(kThreads) big_calib_kernel(SweepArgs A, BigArg
             for (int j = tid; j < m; j += nt) {
                 const int k = (int)(((2 * (int64_t)j + 1) * n) / (2 * (int64_t)m));
                 const float* xr = A.src + (int64_t)__ldg(A.idx + lo + k) * A.ld_src + c0;
+#pragma unroll 4
                 for (int g = 0; g < gc; ++g) {
                     const uint32_t v = abs_bits(__ldg(xr + g));
                     const uint32_t* q = qs + g * (kQ + 1);
@@ -151,13 +152,14 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
             int my_in = 0, my_above = 0;
             const int c = tid % nf, j = tid / nf;
             if (tid < per * nf) {
-                const uint32_t hib = s_hib[c], lob = s_lob[c], span = hib - lob;
+                const uint32_t hib = s_hib[c], lob = s_lob[c];
+                const int sh = hb_shift(hib - lob);
                 for (int k = j; k < kn; k += per) {
                     const uint32_t a = __float_as_uint(lds_f32(s_xs + (uint32_t)k * rowb + 4u * c)) & 0x7FFFFFFFu;
                     my_above += (a >= hib);
                     if (a >= lob && a < hib) {
                         ++my_in;
-                        atomicAdd(&s_hist[c * kHB + hb_bucket(a, lob, span)], 1);
+                        atomicAdd(&s_hist[c * kHB + hb_bucket(a, lob, sh)], 1);
                     }
                 }
                 atomicAdd(&s_above[c], my_above);
@@ -247,9 +249,9 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
                 const int L = __ffs(hit) - 1;  // first lane whose prefix reaches need
                 const int before = __shfl_sync(CALS_FULL_MASK, incl - cnt_b, L);
                 const int bT = kHB - 1 - L;
-                const uint32_t span = hib - lob;
-                const uint64_t blo = (uint64_t)hb_lower(bT, lob, span) << 32;
-                const uint64_t bhi = bT == kHB - 1 ? hik : ((uint64_t)hb_lower(bT + 1, lob, span) << 32);
+                const int sh = hb_shift(hib - lob);
+                const uint64_t blo = hb_lower_key(bT, lob, sh);
+                const uint64_t bhi = min(hb_lower_key(bT + 1, lob, sh), hik);
                 // keep that bucket's keys (in place), then select among them
                 int m = 0;
                 for (int i0 = 0; i0 < in; i0 += 32) {

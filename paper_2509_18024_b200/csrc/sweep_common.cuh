@@ -75,13 +75,17 @@ struct BigArgs {
 
 constexpr int kHB = 32;  // sub-buckets of a big row's bracket (linear in abs-bit space)
 
-// Sub-bucket of an in-bracket abs value a in [lob, hib): floor((a - lob) * kHB / span).
-__device__ __forceinline__ int hb_bucket(uint32_t a, uint32_t lob, uint32_t span) {
-    return (int)(((uint64_t)(a - lob) * kHB) / span);
+// Sub-buckets of a bracket [lob, hib) are power-of-two wide: width 2^sh with
+// sh the smallest shift mapping span - 1 below kHB (so 16..32 buckets are used).
+__device__ __forceinline__ int hb_shift(uint32_t span) {
+    const int bits = span > 1 ? 32 - __clz((int)(span - 1)) : 0;
+    return bits > 5 ? bits - 5 : 0;  // kHB == 32
 }
-// Smallest abs value of sub-bucket b: lob + ceil(b * span / kHB).
-__device__ __forceinline__ uint32_t hb_lower(int b, uint32_t lob, uint32_t span) {
-    return lob + (uint32_t)(((uint64_t)b * span + kHB - 1) / kHB);
+// Sub-bucket of an in-bracket abs value a.
+__device__ __forceinline__ int hb_bucket(uint32_t a, uint32_t lob, int sh) { return (int)((a - lob) >> sh); }
+// Key range [lo, hi) of sub-bucket b (hi capped at the bracket's top key).
+__device__ __forceinline__ uint64_t hb_lower_key(int b, uint32_t lob, int sh) {
+    return ((uint64_t)lob + ((uint64_t)b << sh)) << 32;
 }
 
 __host__ __device__ inline int round_up4(int x) { return (x + 3) & ~3; }
