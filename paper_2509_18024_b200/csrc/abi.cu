@@ -99,9 +99,11 @@ int big_chunk(int nf) {
 
 size_t big_gram_smem(int nf, int chunk) {
     const int sx = xs_stride(nf);
-    const size_t g = owned_single_round(nf, kThreads / 32) ? 0 : align16((size_t)nf * (nf + 1) * 4);
+    const bool persist = owned_single_round(nf, kThreads / 32);
+    const size_t g = persist ? 0 : align16((size_t)nf * (nf + 1) * 4);
+    const size_t lists = persist ? 0 : (size_t)nf * chunk * 2 + (size_t)nf * 4;
     return align16((size_t)chunk * sx * 4) + align16((size_t)chunk * 4) + g +
-           align16((size_t)nf * chunk * 2 + (size_t)nf * 4);
+           align16((size_t)nf * (chunk / 32) * 4 + lists);
 }
 
 size_t big_scan_smem(int nf, int chunk) {

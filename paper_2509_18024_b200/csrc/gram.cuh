@@ -338,20 +338,29 @@ struct OwnedMap {
     }
 };
 
-// Accumulate one staged chunk: column M.c over its kept-row list (len rows,
-// or all rows when full).
+// Accumulate one staged chunk of kn rows: column M.c over the set bits of its
+// kept-row bitmap words (bits[c][w], nw words per column), or over all rows
+// when full.  q-group g takes words g, g + QG, ...
 template <int CPL>
 __device__ __forceinline__ void owned_accumulate(OwnedAcc<CPL>& S, const OwnedMap& M, uint32_t xs, int sx,
-                                                 uint32_t ys, int nf, int len, bool full, uint32_t lists,
-                                                 int Smax) {
+                                                 uint32_t ys, int nf, int kn, bool full, uint32_t bits, int nw) {
     const int nq = xs_chunks(nf);
     const uint32_t rowb = 4u * (uint32_t)sx;
-    const uint32_t L = lists + 2u * (uint32_t)(M.c * Smax);
+    const uint32_t W = bits + 4u * (uint32_t)(M.c * nw);
     const uint32_t xcol = xs + 4u * (uint32_t)M.c;
     const bool chunk_ok_last = (M.fl + (CPL - 1) * M.LPC) < nq;
-    const int n = M.cvalid ? len : 0;
-    for (int q = M.qg; q < n; q += M.QG) {
-        const uint32_t k = full ? (uint32_t)q : lds_u16(L + 2u * (uint32_t)q);
+    const int nwk = M.cvalid ? (kn + 31) >> 5 : 0;
+    for (int wd = M.qg; wd < nwk; wd += M.QG) {
+      uint32_t word;
+      if (full) {
+          const int rem = kn - 32 * wd;
+          word = rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
+      } else {
+          word = lds_u32(W + 4u * (uint32_t)wd);
+      }
+      while (word) {
+        const uint32_t k = 32u * (uint32_t)wd + (uint32_t)(__ffs(word) - 1);
+        word &= word - 1u;
         const uint32_t rb = k * rowb;
         const float xc = lds_f32(xcol + rb);
 #pragma unroll
@@ -365,6 +374,7 @@ __device__ __forceinline__ void owned_accumulate(OwnedAcc<CPL>& S, const OwnedMa
             }
         }
         if (M.fl == 0) S.accb = fmaf(xc, lds_f32(ys + 4u * k), S.accb);
+      }
     }
 }
 

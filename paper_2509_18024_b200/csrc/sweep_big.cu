@@ -293,14 +293,14 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
 // warp's columns fit one lane-group round (nf <= 64), else in shared memory;
 // the item's partial goes to global.
 template <int CPL>
-__global__ void __launch_bounds__(kThreads) big_gram_kernel(SweepArgs A, BigArgs B) {
+__global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(SweepArgs A, BigArgs B) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t s_thr[CALS_MAX_NF_DEV];
     __shared__ float wold[CALS_MAX_NF_DEV];
     __shared__ double red[32];
     const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
     const int sx = xs_stride(nf), gs = nf + 1;
-    const int CH = B.chunk;
+    const int CH = B.chunk, nw = CH / 32;
     const bool persist = owned_single_round(nf, nwarps);
     float* Xs = reinterpret_cast<float*>(smem);
     float* ys = reinterpret_cast<float*>(smem + align16((size_t)CH * sx * 4));
@@ -308,8 +308,9 @@ __global__ void __launch_bounds__(kThreads) big_gram_kernel(SweepArgs A, BigArgs
     float* G = reinterpret_cast<float*>(after_ys);  // shared-memory accumulation (!persist only)
     unsigned char* after_g = after_ys + (persist ? 0 : align16((size_t)nf * gs * 4));
     const uint32_t s_xs = smem_u32(Xs), s_ys = smem_u32(ys);
-    const uint32_t s_lists = smem_u32(after_g);  // [nf][CH] u16, then [nf] u32 lengths
-    const uint32_t s_lens = s_lists + 2u * (uint32_t)(nf * CH);
+    const uint32_t s_bits = smem_u32(after_g);                       // [nf][nw] kept-row bitmap words
+    const uint32_t s_lists = s_bits + 4u * (uint32_t)(nf * nw);      // [nf][CH] u16 (!persist only)
+    const uint32_t s_lens = s_lists + 2u * (uint32_t)(nf * CH);      // [nf] u32 (!persist only)
     const uint32_t rowb = 4u * (uint32_t)sx;
     const FastDiv fq((uint32_t)xs_chunks(nf));
     const int my_cols = warp < nf ? (nf - 1 - warp) / nwarps + 1 : 0;
@@ -346,27 +347,35 @@ __global__ void __launch_bounds__(kThreads) big_gram_kernel(SweepArgs A, BigArgs
                 }
             }
             if (!full) {
-                // kept-row lists of the owned columns (ascending k)
+                // kept-row bitmap words of the owned columns: key >= T, i.e.
+                // abs > Ta, or abs == Ta with (global) row index <= Tk
+                const int nwk = (kn + 31) >> 5;
                 for (int j = 0; j < my_cols; ++j) {
                     const int c = warp + j * nwarps;
                     const uint64_t T = s_thr[c];
+                    const uint32_t Ta = (uint32_t)(T >> 32), Tk = 0xFFFFFFFFu - (uint32_t)T;
                     const uint32_t xcol = s_xs + 4u * (uint32_t)c;
-                    const uint32_t L = s_lists + 2u * (uint32_t)(c * CH);
-                    int w = 0;
-                    for (int kk0 = 0; kk0 < kn; kk0 += 32) {
-                        const int k = kk0 + lane;
-                        const bool keep = k < kn && make_key(lds_f32(xcol + (uint32_t)k * rowb), (uint32_t)(k0 + k)) >= T;
+                    for (int wd = 0; wd < nwk; ++wd) {
+                        const int k = 32 * wd + lane;
+                        const uint32_t a = k < kn ? abs_bits(lds_f32(xcol + (uint32_t)k * rowb)) : 0u;
+                        const bool keep = k < kn && (a > Ta || (a == Ta && (uint32_t)(k0 + k) <= Tk));
                         const uint32_t bal = __ballot_sync(CALS_FULL_MASK, keep);
-                        if (keep) sts_u16(L + 2u * (uint32_t)(w + __popc(bal & lanemask_lt())), (uint32_t)k);
-                        w += __popc(bal);
+                        if (lane == 0) sts_u32(s_bits + 4u * (uint32_t)(c * nw + wd), bal);
                     }
-                    if (lane == 0) sts_u32(s_lens + 4u * c, (uint32_t)w);
+                    if (!persist) {
+                        __syncwarp();
+                        bitmap_to_list(s_bits + 4u * (uint32_t)(c * nw), nwk, s_lists + 2u * (uint32_t)(c * CH), lane);
+                        if (lane == 0) {
+                            int w = 0;
+                            for (int wd = 0; wd < nwk; ++wd) w += __popc(lds_u32(s_bits + 4u * (uint32_t)(c * nw + wd)));
+                            sts_u32(s_lens + 4u * c, (uint32_t)w);
+                        }
+                    }
                 }
                 __syncwarp();
             }
             if (persist) {
-                const int lc = full ? kn : (M.cvalid ? (int)lds_u32(s_lens + 4u * M.c) : 0);
-                owned_accumulate<CPL>(S, M, s_xs, sx, s_ys, nf, lc, full, s_lists, CH);
+                owned_accumulate<CPL>(S, M, s_xs, sx, s_ys, nf, kn, full, s_bits, nw);
             } else {
                 for (int j = 0; j < my_cols; ++j) {
                     const int c = warp + j * nwarps;
