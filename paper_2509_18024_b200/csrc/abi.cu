@@ -134,6 +134,7 @@ struct Carve {
 
 struct Device {
     int sms = 148;
+    size_t smem_optin = 227 * 1024;
     bool init = false;
 };
 Device& dev() {
@@ -144,6 +145,9 @@ Device& dev() {
         int id = 0;
         cudaGetDevice(&id);
         cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, id);
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, id);
+        if (optin > 0) d.smem_optin = (size_t)optin;
         d.init = true;
     }
     return d;
@@ -311,6 +315,14 @@ int gram_grid(size_t smem, int64_t cnt, int threads) {
 }
 
 template <int CPL>
+int gram_occ(int threads, size_t smem) {
+    allow_smem(small_gram_kernel<CPL>);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, small_gram_kernel<CPL>, threads, smem);
+    return occ;
+}
+
+template <int CPL>
 void launch_tiny(const SweepArgs& A, const int32_t* rows, int64_t cnt, cudaStream_t st) {
     const size_t smem = tiny_warp_bytes(A.nf) * kTinyWarps;
     allow_smem(tiny_gram_kernel<CPL>);
@@ -348,6 +360,24 @@ int launch_small(SweepArgs A, const cals_plan* P, const Work& w, cudaStream_t st
         // one big CTA per SM when two would not fit in shared memory
         int threads = N <= 256 ? 128 : 256;
         if (threads == 256 && T1Layout(N, S, A.nf, 256).total > 112 * 1024) threads = 512;
+        {
+            // wide ranks: more threads per CTA when that raises the resident warps
+            auto warps_for = [&](int t) {
+                const size_t sm = T1Layout(N, S, A.nf, t).total;
+                if (sm > dev().smem_optin) return 0;
+                if (CPL == 1) return gram_occ<1>(t, sm) * t / 32;
+                if (CPL == 2) return gram_occ<2>(t, sm) * t / 32;
+                if (CPL == 4) return gram_occ<4>(t, sm) * t / 32;
+                return gram_occ<8>(t, sm) * t / 32;
+            };
+            const int base = warps_for(threads);
+            int best = base, pick = threads;
+            for (int t : {256, 512}) {
+                const int wv = t > threads ? warps_for(t) : 0;
+                if (wv > best) { best = wv; pick = t; }
+            }
+            if (best >= 2 * base) threads = pick;  // only when occupancy was the limiter
+        }
         const size_t smem = T1Layout(N, S, A.nf, threads).total;
         for (int64_t b0 = b; b0 < e; b0 += w.gbuf_rows) {
             const int64_t cnt = std::min<int64_t>(w.gbuf_rows, e - b0);
