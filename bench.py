@@ -36,7 +36,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-DEFAULT_CONFIG = "medium"
+DEFAULT_CONFIG = "large"
 METRIC = "observed ratings processed/sec per ALS iteration"
 UNIT = "ratings/s/iter"
 

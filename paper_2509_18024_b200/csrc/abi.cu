@@ -189,6 +189,13 @@ int cuda_status(const char* where) {
     return CALS_OK;
 }
 
+// Normal-equation batch: rows solved per phase-A/phase-B launch pair (<= ~1 GiB).
+int64_t gbuf_rows_for(int nf, int64_t rows) {
+    const int64_t per = (int64_t)nf * (nf + 1) * 4;
+    const int64_t cap = std::max<int64_t>(4096, ((int64_t)1 << 30) / per);
+    return std::max<int64_t>(1, std::min<int64_t>(cap, rows));
+}
+
 // Tiled-tier batches: rows [r[i], r[i+1]) share one scan/resolve/gram pass,
 // bounded so candidate keys and partial normal equations fit the workspace.
 struct BigBatches {
@@ -212,9 +219,12 @@ BigBatches big_batches(const cals_plan* P) {
                                     : std::max<int64_t>(1, ((int64_t)1 << 30) / ((int64_t)nf * (nf + 1) * 4));
     const int64_t* tp = P->big_tile_ptr_host;
     const int64_t* cp = P->big_cand_ptr_host;
+    // a batch's normal equations must fit one gbuf pass (single-item rows are written there directly)
+    const int64_t row_budget = gbuf_rows_for(nf, P->n_small + P->n_big);
     int64_t start = 0;
     for (int64_t r = 0; r < P->n_big; ++r) {
-        const bool over = (cp[r + 1] - cp[start] > cand_budget) || (tp[r + 1] - tp[start] > tile_budget);
+        const bool over = (cp[r + 1] - cp[start] > cand_budget) || (tp[r + 1] - tp[start] > tile_budget) ||
+                          (r + 1 - start > row_budget);
         if (over && r > start) {
             b.r.push_back(r);
             start = r;
@@ -246,13 +256,6 @@ struct Work {
 constexpr int kMaxGrid = 160 * 16;  // grid_for never exceeds min(SMs, 160) * 16 CTAs
 inline int retry_stride(int nf) { return ((nf * (nf + 1) + nf) + 31) & ~31; }
 constexpr int64_t kMaxSolveWarps = 160 * 64;  // solve_warp_kernel grid cap (64 warps per SM)
-
-// Normal-equation batch: rows solved per phase-A/phase-B launch pair (<= ~1 GiB).
-int64_t gbuf_rows_for(int nf, int64_t rows) {
-    const int64_t per = (int64_t)nf * (nf + 1) * 4;
-    const int64_t cap = std::max<int64_t>(4096, ((int64_t)1 << 30) / per);
-    return std::max<int64_t>(1, std::min<int64_t>(cap, rows));
-}
 
 Work carve(const cals_plan* P, void* ws, size_t* total) {
     Carve c(ws);
@@ -428,10 +431,13 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
         B.brk = w.brk;
         cudaMemsetAsync(w.cnt, 0, sizeof(int) * (size_t)B.n_big * nf * 2, st);
         cudaMemsetAsync(w.brk, 0xFF, sizeof(uint32_t) * (size_t)B.n_big * nf, st);
-        // rows spanning >= 2 work items get row-local bracket levels (rows are sorted by length)
+        // rows spanning >= 2 work items (a prefix: rows are sorted by length) get row-local
+        // bracket levels, and their partial normal equations are reduced by big_reduce;
+        // single-item rows write theirs straight into gbuf
         int64_t n_calib = 0;
         if (tp)
             while (n_calib < B.n_big && tp[r0 + n_calib + 1] - tp[r0 + n_calib] >= 2) ++n_calib;
+        B.n_multi = tp ? n_calib : B.n_big;  // without host offsets every row takes the partial path
         if (n_calib > 0) {
             const size_t smem = (size_t)2 * kCalibCols * (kQ + 1) * sizeof(uint32_t);
             allow_smem(big_calib_kernel);
@@ -461,15 +467,13 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
             else if (nq <= 16) launch_big_gram<4>(A, B, gram_smem, st);
             else launch_big_gram<8>(A, B, gram_smem, st);
         }
-        for (int64_t q0 = 0; q0 < B.n_big; q0 += w.gbuf_rows) {
-            const int64_t cnt = std::min<int64_t>(w.gbuf_rows, B.n_big - q0);
-            {
-                ProfScope ps("big_reduce_kernel", st);
-                big_reduce_kernel<<<(int)std::min<int64_t>(cnt, (int64_t)dev().sms * 8), kThreads, 0, st>>>(A, B, q0,
-                                                                                                         cnt);
-            }
-            launch_solve<NFP>(A, B.rows + q0, cnt, st);
+        if (B.n_big > w.gbuf_rows) return CALS_ERR_WORKSPACE;  // big_batches bounds rows per batch
+        if (B.n_multi > 0) {
+            ProfScope ps("big_reduce_kernel", st);
+            big_reduce_kernel<<<(int)std::min<int64_t>(B.n_multi, (int64_t)dev().sms * 8), kThreads, 0, st>>>(
+                A, B, 0, B.n_multi);
         }
+        launch_solve<NFP>(A, B.rows, B.n_big, st);
         const int rc = cuda_status("big-row kernels");
         if (rc) return rc;
     }

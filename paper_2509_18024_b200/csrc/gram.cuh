@@ -380,7 +380,8 @@ __device__ __forceinline__ void owned_accumulate(OwnedAcc<CPL>& S, const OwnedMa
 
 // Fixed-order reduction over the q-groups; row M.c of out (stride nf+1).
 template <int CPL>
-__device__ __forceinline__ void owned_flush(OwnedAcc<CPL>& S, const OwnedMap& M, int nf, float* __restrict__ out) {
+__device__ __forceinline__ void owned_flush(OwnedAcc<CPL>& S, const OwnedMap& M, int nf, float* __restrict__ out,
+                                            float lam_n = 0.f) {
     const int nq = xs_chunks(nf);
     const int gs = nf + 1;
     for (int o = M.LPC; o < M.LPC * M.QG; o <<= 1) {
@@ -397,7 +398,7 @@ __device__ __forceinline__ void owned_flush(OwnedAcc<CPL>& S, const OwnedMap& M,
 #pragma unroll
                 for (int t = 0; t < 4; ++t) {
                     const int f = 4 * ch + t;
-                    if (f < nf) grow[f] = S.acc[4 * i + t];
+                    if (f < nf) grow[f] = S.acc[4 * i + t] + ((f == M.c) ? lam_n : 0.f);
                 }
             }
         }

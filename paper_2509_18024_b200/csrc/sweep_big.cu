@@ -385,16 +385,25 @@ __global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(Sw
                 }
             }
         }
-        float* out = B.part + (size_t)t * nf * gs;
+        // single-item rows: finished normal equations (+ lam*n*I) straight into gbuf
+        const bool direct = r >= B.n_multi;
+        float* out = direct ? A.gbuf + (size_t)r * nf * gs : B.part + (size_t)t * nf * gs;
+        const float lam_n = direct ? (float)(A.lam * (double)n) : 0.f;
         if (persist) {
-            owned_flush<CPL>(S, M, nf, out);
+            owned_flush<CPL>(S, M, nf, out, lam_n);
         } else {
             __syncthreads();
-            for (int e = tid; e < nf * gs; e += nt) out[e] = G[e];
+            for (int e = tid; e < nf * gs; e += nt) {
+                const int c = e / gs, f = e - c * gs;
+                out[e] = G[e] + ((c == f) ? lam_n : 0.f);
+            }
         }
         if (A.rss_rows != nullptr) {
             racc = block_sum_d(racc, red);
-            if (tid == 0) B.rss_part[t] = racc;
+            if (tid == 0) {
+                if (direct) A.rss_rows[row] = racc;
+                else B.rss_part[t] = racc;
+            }
         }
     }
 }

@@ -58,6 +58,8 @@ struct BigArgs {
     const int64_t* tile_ptr;  // [n_big + 1] item prefix per row
     const int64_t* cand_ptr;  // [n_big + 1] candidate key offsets (nf equal column regions)
     int64_t n_big;            // rows of this batch
+    int64_t n_multi;          // rows [0, n_multi) span >= 2 work items (partials + big_reduce); the
+                              // rest write their normal equations straight into gbuf slot r
     int64_t n_tiles;          // work items of this batch
     int64_t tile_base;        // absolute index of the batch's first work item
     int64_t cand_base;        // absolute offset of the batch's first candidate key
