@@ -173,14 +173,16 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
             }
             __syncthreads();
             if (tid < per * nf && my_in) {
+                // one slot reservation per thread, then its keys in a contiguous run
                 const uint32_t hib = s_hib[c], lob = s_lob[c];
                 uint64_t* cl = B.cand + cbase + (int64_t)c * capB;
+                int pos = s_base[c] + atomicAdd(&s_slot[c], my_in);
                 for (int k = j; k < kn; k += per) {
                     const float x = lds_f32(s_xs + (uint32_t)k * rowb + 4u * c);
                     const uint32_t a = abs_bits(x);
                     if (a >= lob && a < hib) {
-                        const int pos = s_base[c] + atomicAdd(&s_slot[c], 1);
                         if (pos < capB) cl[pos] = make_key(x, (uint32_t)(k0 + k));
+                        ++pos;
                     }
                 }
             }
@@ -347,23 +349,28 @@ __global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(Sw
                 }
             }
             if (!full) {
-                // kept-row bitmap words of the owned columns: key >= T, i.e.
-                // abs > Ta, or abs == Ta with (global) row index <= Tk
+                // kept-row bitmap words: thread (c, wd) builds word wd of column c from 32
+                // sequential rows (a warp reads 32 adjacent columns of one row: no bank
+                // conflicts); keep <=> key >= T <=> abs > Ta, or abs == Ta and row <= Tk
                 const int nwk = (kn + 31) >> 5;
-                for (int j = 0; j < my_cols; ++j) {
-                    const int c = warp + j * nwarps;
+                for (int e = tid; e < nf * nwk; e += nt) {
+                    const int wd = e / nf, c = e - wd * nf;
                     const uint64_t T = s_thr[c];
                     const uint32_t Ta = (uint32_t)(T >> 32), Tk = 0xFFFFFFFFu - (uint32_t)T;
-                    const uint32_t xcol = s_xs + 4u * (uint32_t)c;
-                    for (int wd = 0; wd < nwk; ++wd) {
-                        const int k = 32 * wd + lane;
-                        const uint32_t a = k < kn ? abs_bits(lds_f32(xcol + (uint32_t)k * rowb)) : 0u;
-                        const bool keep = k < kn && (a > Ta || (a == Ta && (uint32_t)(k0 + k) <= Tk));
-                        const uint32_t bal = __ballot_sync(CALS_FULL_MASK, keep);
-                        if (lane == 0) sts_u32(s_bits + 4u * (uint32_t)(c * nw + wd), bal);
+                    const int kb = 32 * wd, ke = min(kn, kb + 32);
+                    uint32_t addr = s_xs + (uint32_t)kb * rowb + 4u * (uint32_t)c;
+                    uint32_t word = 0u;
+                    for (int k = kb; k < ke; ++k, addr += rowb) {
+                        const uint32_t a = abs_bits(lds_f32(addr));
+                        const bool keep = a > Ta || (a == Ta && (uint32_t)(k0 + k) <= Tk);
+                        word |= (uint32_t)keep << (k - kb);
                     }
-                    if (!persist) {
-                        __syncwarp();
+                    sts_u32(s_bits + 4u * (uint32_t)(c * nw + wd), word);
+                }
+                __syncthreads();
+                if (!persist) {
+                    for (int j = 0; j < my_cols; ++j) {
+                        const int c = warp + j * nwarps;
                         bitmap_to_list(s_bits + 4u * (uint32_t)(c * nw), nwk, s_lists + 2u * (uint32_t)(c * CH), lane);
                         if (lane == 0) {
                             int w = 0;
@@ -371,8 +378,8 @@ __global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(Sw
                             sts_u32(s_lens + 4u * c, (uint32_t)w);
                         }
                     }
+                    __syncwarp();
                 }
-                __syncwarp();
             }
             if (persist) {
                 owned_accumulate<CPL>(S, M, s_xs, sx, s_ys, nf, kn, full, s_bits, nw);
