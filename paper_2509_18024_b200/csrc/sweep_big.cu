@@ -148,20 +148,23 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
             stage_slice(A, lo, k0, kn, Xs, nullptr, fq);
             if (tid < nf) s_slot[tid] = 0;
             __syncthreads();
-            const int per = nt / nf;
+            const int per = nt / nf;  // threads per column; each scans <= 64 rows (big_chunk)
             int my_in = 0, my_above = 0;
+            uint64_t inmask = 0;      // bit i: row j + i * per is inside the bracket
             const int c = tid % nf, j = tid / nf;
             if (tid < per * nf) {
                 const uint32_t hib = s_hib[c], lob = s_lob[c];
                 const int sh = hb_shift(hib - lob);
-                for (int k = j; k < kn; k += per) {
+                int i = 0;
+                for (int k = j; k < kn; k += per, ++i) {
                     const uint32_t a = __float_as_uint(lds_f32(s_xs + (uint32_t)k * rowb + 4u * c)) & 0x7FFFFFFFu;
                     my_above += (a >= hib);
-                    if (a >= lob && a < hib) {
-                        ++my_in;
+                    if (a - lob < hib - lob) {  // lob <= a < hib
+                        inmask |= 1ull << i;
                         atomicAdd(&s_hist[c * kHB + hb_bucket(a, lob, sh)], 1);
                     }
                 }
+                my_in = __popcll(inmask);
                 atomicAdd(&s_above[c], my_above);
                 if (my_in) atomicAdd(&s_slot[c], my_in);
             }
@@ -174,16 +177,14 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
             __syncthreads();
             if (tid < per * nf && my_in) {
                 // one slot reservation per thread, then its keys in a contiguous run
-                const uint32_t hib = s_hib[c], lob = s_lob[c];
                 uint64_t* cl = B.cand + cbase + (int64_t)c * capB;
                 int pos = s_base[c] + atomicAdd(&s_slot[c], my_in);
-                for (int k = j; k < kn; k += per) {
-                    const float x = lds_f32(s_xs + (uint32_t)k * rowb + 4u * c);
-                    const uint32_t a = abs_bits(x);
-                    if (a >= lob && a < hib) {
-                        if (pos < capB) cl[pos] = make_key(x, (uint32_t)(k0 + k));
-                        ++pos;
-                    }
+                while (inmask) {
+                    const int i = __ffsll((long long)inmask) - 1;
+                    inmask &= inmask - 1;
+                    const int k = j + i * per;
+                    if (pos < capB) cl[pos] = make_key(lds_f32(s_xs + (uint32_t)k * rowb + 4u * c), (uint32_t)(k0 + k));
+                    ++pos;
                 }
             }
         }
