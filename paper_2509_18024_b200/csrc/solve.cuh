@@ -248,18 +248,15 @@ __device__ __forceinline__ void wide_step(WideLU<NF>& S, bool spd, int lane) {
     const int r0 = lane, r1 = lane + 32;
     int p = K;
     if (!spd) {
-        float best = S.ua ? -1.f : fabsf(S.a[K]);
-        int bi = r0;
-        const float vb = S.ub ? -1.f : fabsf(S.b[K]);
-        if (vb > best) { best = vb; bi = r1; }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const float obst = __shfl_xor_sync(CALS_FULL_MASK, best, o);
-            const int oi = __shfl_xor_sync(CALS_FULL_MASK, bi, o);
-            if (obst > best || (obst == best && oi < bi)) { best = obst; bi = oi; }
-        }
-        S.fail |= !(best > 0.f);
-        p = bi;
+        // one warp max-reduction of (|pivot| bits with the low 6 mantissa bits
+        // replaced by 63 - row): largest magnitude, ties (to 2^-17 relative)
+        // to the smallest row -- partial pivoting needs a large pivot, not the
+        // exact maximum
+        const uint32_t ka = S.ua ? (uint32_t)(63 - r0) : ((__float_as_uint(S.a[K]) & 0x7FFFFFC0u) | (uint32_t)(63 - r0));
+        const uint32_t kb = S.ub ? (uint32_t)(63 - r1) : ((__float_as_uint(S.b[K]) & 0x7FFFFFC0u) | (uint32_t)(63 - r1));
+        const uint32_t best = __reduce_max_sync(CALS_FULL_MASK, ka > kb ? ka : kb);
+        S.fail |= (best >> 6) == 0u;
+        p = 63 - (int)(best & 63u);
     }
     const bool hi = p >= 32;
     const int pl = p & 31;
