@@ -242,41 +242,58 @@ struct WideLU {
     int oa, ob;
 };
 
-// Elimination step K (compile-time, so every register index is static).
-template <int NF, int K>
-__device__ __forceinline__ void wide_step(WideLU<NF>& S, bool spd, int lane) {
+// Elimination steps K in [B0, B0 + 16) (a runtime loop: the fully unrolled
+// elimination is ~20k instructions and thrashes the instruction cache).  The
+// column-K entries come from a 16-way register select; the update sweeps
+// columns j >= B0 (compile-time), which also rewrites the block's columns
+// left of K in still-unused rows -- entries no later step or the back
+// substitution reads -- and leaves used rows alone (zero multiplier).
+template <int NF, int B0>
+__device__ __forceinline__ void wide_block(WideLU<NF>& S, bool spd, int lane) {
+    constexpr int BE = (B0 + 16 < NF) ? B0 + 16 : NF;
     const int r0 = lane, r1 = lane + 32;
-    int p = K;
-    if (!spd) {
-        // one warp max-reduction of (|pivot| bits with the low 6 mantissa bits
-        // replaced by 63 - row): largest magnitude, ties (to 2^-17 relative)
-        // to the smallest row -- partial pivoting needs a large pivot, not the
-        // exact maximum
-        const uint32_t ka = S.ua ? (uint32_t)(63 - r0) : ((__float_as_uint(S.a[K]) & 0x7FFFFFC0u) | (uint32_t)(63 - r0));
-        const uint32_t kb = S.ub ? (uint32_t)(63 - r1) : ((__float_as_uint(S.b[K]) & 0x7FFFFFC0u) | (uint32_t)(63 - r1));
-        const uint32_t best = __reduce_max_sync(CALS_FULL_MASK, ka > kb ? ka : kb);
-        S.fail |= (best >> 6) == 0u;
-        p = 63 - (int)(best & 63u);
-    }
-    const bool hi = p >= 32;
-    const int pl = p & 31;
-    const float d = __shfl_sync(CALS_FULL_MASK, sel_f32(hi, S.b[K], S.a[K]), pl);
-    S.fail |= spd ? !(d > 0.f) : !(d == d);
-    if (lane == pl) {
-        if (hi) { S.ub = true; S.ob = K; } else { S.ua = true; S.oa = K; }
-    }
-    const float inv = __frcp_rn(d);
-    const float fa = S.ua ? 0.f : S.a[K] * inv;
-    const float fb = S.ub ? 0.f : S.b[K] * inv;
+#pragma unroll 1
+    for (int K = B0; K < BE; ++K) {
+        float ca = S.a[B0], cb = S.b[B0];
 #pragma unroll
-    for (int j = K + 1; j < NF; ++j) {
-        const float vp = __shfl_sync(CALS_FULL_MASK, sel_f32(hi, S.b[j], S.a[j]), pl);
-        S.a[j] = fmaf(-fa, vp, S.a[j]);
-        S.b[j] = fmaf(-fb, vp, S.b[j]);
+        for (int i = 1; i < BE - B0; ++i) {
+            if (K == B0 + i) {
+                ca = S.a[B0 + i];
+                cb = S.b[B0 + i];
+            }
+        }
+        int p = K;
+        if (!spd) {
+            // one warp max-reduction of (|pivot| bits with the low 6 mantissa bits
+            // replaced by 63 - row): largest magnitude, ties (to 2^-17 relative)
+            // to the smallest row -- partial pivoting needs a large pivot, not the
+            // exact maximum
+            const uint32_t ka = S.ua ? (uint32_t)(63 - r0) : ((__float_as_uint(ca) & 0x7FFFFFC0u) | (uint32_t)(63 - r0));
+            const uint32_t kb = S.ub ? (uint32_t)(63 - r1) : ((__float_as_uint(cb) & 0x7FFFFFC0u) | (uint32_t)(63 - r1));
+            const uint32_t best = __reduce_max_sync(CALS_FULL_MASK, ka > kb ? ka : kb);
+            S.fail |= (best >> 6) == 0u;
+            p = 63 - (int)(best & 63u);
+        }
+        const bool hi = p >= 32;
+        const int pl = p & 31;
+        const float d = __shfl_sync(CALS_FULL_MASK, sel_f32(hi, cb, ca), pl);
+        S.fail |= spd ? !(d > 0.f) : !(d == d);
+        if (lane == pl) {
+            if (hi) { S.ub = true; S.ob = K; } else { S.ua = true; S.oa = K; }
+        }
+        const float inv = __frcp_rn(d);
+        const float fa = S.ua ? 0.f : ca * inv;
+        const float fb = S.ub ? 0.f : cb * inv;
+#pragma unroll
+        for (int j = B0; j < NF; ++j) {
+            const float vp = __shfl_sync(CALS_FULL_MASK, sel_f32(hi, S.b[j], S.a[j]), pl);
+            S.a[j] = fmaf(-fa, vp, S.a[j]);
+            S.b[j] = fmaf(-fb, vp, S.b[j]);
+        }
+        const float bp = __shfl_sync(CALS_FULL_MASK, sel_f32(hi, S.rb, S.ra), pl);
+        S.ra = fmaf(-fa, bp, S.ra);
+        S.rb = fmaf(-fb, bp, S.rb);
     }
-    const float bp = __shfl_sync(CALS_FULL_MASK, sel_f32(hi, S.rb, S.ra), pl);
-    S.ra = fmaf(-fa, bp, S.ra);
-    S.rb = fmaf(-fb, bp, S.rb);
 }
 
 // Back-substitution step K (pivot order): unknown K from the row pivoted at step K.
@@ -295,10 +312,10 @@ __device__ __forceinline__ void wide_back(WideLU<NF>& S, float& x0, float& x1, i
     if (S.ob >= 0 && S.ob < K) S.rb = fmaf(-S.b[K], xk, S.rb);
 }
 
-template <int NF, int... K>
+template <int NF, int... Q>
 __device__ __forceinline__ void wide_eliminate(WideLU<NF>& S, bool spd, int lane,
-                                               std::integer_sequence<int, K...>) {
-    (wide_step<NF, K>(S, spd, lane), ...);
+                                               std::integer_sequence<int, Q...>) {
+    (wide_block<NF, 16 * Q>(S, spd, lane), ...);
 }
 template <int NF, int... K>
 __device__ __forceinline__ void wide_substitute(WideLU<NF>& S, float& x0, float& x1, int lane,
@@ -328,7 +345,7 @@ __device__ __forceinline__ bool wide_lu_solve(const float* __restrict__ W, int n
     S.oa = -1;
     S.ob = -1;
     S.fail = false;
-    wide_eliminate<NF>(S, spd, lane, std::make_integer_sequence<int, NF>{});
+    wide_eliminate<NF>(S, spd, lane, std::make_integer_sequence<int, (NF + 15) / 16>{});
     x0 = 0.f;
     x1 = 0.f;
     wide_substitute<NF>(S, x0, x1, lane, std::make_integer_sequence<int, NF>{});
