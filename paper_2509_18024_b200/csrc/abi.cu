@@ -94,8 +94,8 @@ int big_chunk(int nf) {
     const size_t per = (size_t)xs_stride(nf) * 4 + 4 + (size_t)nf * 2;
     int ch = 1024;
     while (ch > 64 && (size_t)ch * per > 96 * 1024) ch >>= 1;
-    // big_scan: a thread scans chunk / (kThreads / nf) rows, at most 64 (one bit each)
-    while (ch > 32 && ch / std::max(1, kThreads / nf) > 64) ch >>= 1;
+    // big_scan: a thread scans chunk / (kThreads / nf) rows, at most 32 (one mask bit each)
+    while (ch > 32 && ch / std::max(1, kThreads / nf) > 32) ch >>= 1;
     return ch;
 }
 

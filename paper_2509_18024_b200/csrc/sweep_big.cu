@@ -148,23 +148,23 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
             stage_slice(A, lo, k0, kn, Xs, nullptr, fq);
             if (tid < nf) s_slot[tid] = 0;
             __syncthreads();
-            const int per = nt / nf;  // threads per column; each scans <= 64 rows (big_chunk)
+            const int per = nt / nf;  // threads per column; each scans <= 32 rows (big_chunk)
             int my_in = 0, my_above = 0;
-            uint64_t inmask = 0;      // bit i: row j + i * per is inside the bracket
+            uint32_t inmask = 0;      // bit i: row j + i * per is inside the bracket
             const int c = tid % nf, j = tid / nf;
             if (tid < per * nf) {
-                const uint32_t hib = s_hib[c], lob = s_lob[c];
-                const int sh = hb_shift(hib - lob);
-                int i = 0;
-                for (int k = j; k < kn; k += per, ++i) {
-                    const uint32_t a = __float_as_uint(lds_f32(s_xs + (uint32_t)k * rowb + 4u * c)) & 0x7FFFFFFFu;
-                    my_above += (a >= hib);
-                    if (a - lob < hib - lob) {  // lob <= a < hib
-                        inmask |= 1ull << i;
-                        atomicAdd(&s_hist[c * kHB + hb_bucket(a, lob, sh)], 1);
-                    }
+                const uint32_t hib = s_hib[c], lob = s_lob[c], span = hib - lob;
+                const uint32_t colb = s_xs + 4u * (uint32_t)c + (uint32_t)j * rowb, stepb = (uint32_t)per * rowb;
+                // branchless count pass (a warp spans 32 columns: any per-element branch
+                // would be taken by some lane almost always)
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int k = j + i * per;
+                    const uint32_t a = k < kn ? abs_bits(lds_f32(colb + (uint32_t)i * stepb)) : 0u;
+                    my_above += (k < kn && a >= hib) ? 1 : 0;
+                    inmask |= (k < kn && a - lob < span) ? (1u << i) : 0u;
                 }
-                my_in = __popcll(inmask);
+                my_in = __popc(inmask);
                 atomicAdd(&s_above[c], my_above);
                 if (my_in) atomicAdd(&s_slot[c], my_in);
             }
@@ -179,11 +179,15 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
                 // one slot reservation per thread, then its keys in a contiguous run
                 uint64_t* cl = B.cand + cbase + (int64_t)c * capB;
                 int pos = s_base[c] + atomicAdd(&s_slot[c], my_in);
+                const uint32_t lob = s_lob[c];
+                const int sh = hb_shift(s_hib[c] - lob);
                 while (inmask) {
-                    const int i = __ffsll((long long)inmask) - 1;
+                    const int i = __ffs(inmask) - 1;
                     inmask &= inmask - 1;
                     const int k = j + i * per;
-                    if (pos < capB) cl[pos] = make_key(lds_f32(s_xs + (uint32_t)k * rowb + 4u * c), (uint32_t)(k0 + k));
+                    const float x = lds_f32(s_xs + (uint32_t)k * rowb + 4u * c);
+                    atomicAdd(&s_hist[c * kHB + (int)((abs_bits(x) - lob) >> sh)], 1);
+                    if (pos < capB) cl[pos] = make_key(x, (uint32_t)(k0 + k));
                     ++pos;
                 }
             }

@@ -173,6 +173,39 @@ __device__ __forceinline__ void stage_slice(const SweepArgs& A, int64_t lo, int 
     cp_async_wait_all();
 }
 
+__device__ __forceinline__ void cp_async4(uint32_t saddr, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(saddr), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Asynchronous variant for double-buffered chunk loops: issue the copies of
+// slice rows [k0, k0 + kn) (X into xs_base, y into ys_base unless 0) as one
+// cp.async group and return; the caller waits with cp_async_wait<N>() and
+// synchronises the block before reading.
+__device__ __forceinline__ void stage_slice_issue(const SweepArgs& A, int64_t lo, int k0, int kn, uint32_t xs_base,
+                                                  uint32_t ys_base, const FastDiv& fq) {
+    const int sx = xs_stride(A.nf), nq = xs_chunks(A.nf);
+    const int nt = blockDim.x;
+    const int nel = kn * nq;
+    const int32_t* idx = A.idx + lo + k0;
+    const float* src = A.src;
+    const int64_t ld = A.ld_src;
+#pragma unroll 4
+    for (int e = threadIdx.x; e < nel; e += nt) {
+        const int k = (int)fq.div((uint32_t)e);
+        const int q = e - k * nq;
+        const int64_t r = __ldg(idx + k);
+        cp_async16(xs_base + (uint32_t)((k * sx + 4 * q) * 4), src + r * ld + 4 * q);
+    }
+    if (ys_base != 0u)
+        for (int k = threadIdx.x; k < kn; k += nt) cp_async4(ys_base + 4u * (uint32_t)k, A.val + lo + k0 + k);
+    cp_async_commit();
+}
+
 // Column lanes / slots of the staged-slice kernel: thread t handles column
 // t % NFP over the k-range of slot t / NFP (ranges are multiples of 32 rows,
 // so every bitmap word has a single owner).
