@@ -69,6 +69,19 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 }
 
 // Bitonic sort of one 64-bit key per lane; result descending (lane 0 = max).
+// need-th largest (1-based) of the unique keys held by lanes [0, m), m <= 32,
+// by counting: each lane counts the keys above its own (m broadcast rounds;
+// cheaper than a 32-wide bitonic sort for the small m of a final sub-bucket).
+__device__ __forceinline__ uint64_t warp_kth_desc(uint64_t v, int m, int need, int lane) {
+    int gt = 0;
+    for (int j = 0; j < m; ++j) {
+        const uint64_t o = __shfl_sync(0xffffffffu, v, j);
+        gt += (o > v) ? 1 : 0;
+    }
+    const uint32_t hit = __ballot_sync(0xffffffffu, lane < m && gt == need - 1);
+    return __shfl_sync(0xffffffffu, v, __ffs(hit) - 1);
+}
+
 __device__ __forceinline__ uint64_t warp_sort_desc(uint64_t v, int lane) {
 #pragma unroll
     for (int size = 2; size <= 32; size <<= 1) {

@@ -55,11 +55,7 @@ __device__ __forceinline__ void choose_bracket(int m, int need, int& a, int& b) 
 // (1 <= need <= m) among the m listed candidates, all inside [lo, hi).
 __device__ uint64_t warp_select_idx(IdxList L, int m, int need, uint64_t lo, uint64_t hi, int lane) {
     while (true) {
-        if (m <= 32) {
-            uint64_t v = lane < m ? L.key(lane) : 0ull;
-            v = warp_sort_desc(v, lane);
-            return __shfl_sync(CALS_FULL_MASK, v, need - 1);
-        }
+        if (m <= 32) return warp_kth_desc(lane < m ? L.key(lane) : 0ull, m, need, lane);
         int pos = (int)(((2ll * lane + 1) * (long long)m) >> 6);
         uint64_t smp = warp_sort_desc(L.key(pos), lane);
         int a, b;
@@ -156,11 +152,7 @@ __device__ void warp_prenarrow(IdxList& L, int& m, int& need, uint64_t& lo, uint
 // Warp-level select on a key list (in place).
 __device__ uint64_t warp_select_keys(KeyList L, int m, int need, uint64_t lo, uint64_t hi, int lane) {
     while (true) {
-        if (m <= 32) {
-            uint64_t v = lane < m ? L.key(lane) : 0ull;
-            v = warp_sort_desc(v, lane);
-            return __shfl_sync(CALS_FULL_MASK, v, need - 1);
-        }
+        if (m <= 32) return warp_kth_desc(lane < m ? L.key(lane) : 0ull, m, need, lane);
         int pos = (int)(((2ll * lane + 1) * (long long)m) >> 6);
         uint64_t smp = warp_sort_desc(L.key(pos), lane);
         int a, b;

@@ -295,9 +295,8 @@ __global__ void __launch_bounds__(512, 1) small_gram_kernel(SweepArgs A, const i
                 if (!exact) {
                     const int need = c_need[c];
                     if (m <= 32) {
-                        uint64_t v = lane < m ? keyat((int)lds_u16(s_fb + 2u * (uint32_t)(c * kFinalCap + (lane & 31)))) : 0ull;
-                        v = m <= 16 ? warp_sort_desc_w<16>(v, lane) : warp_sort_desc(v, lane);
-                        T = __shfl_sync(CALS_FULL_MASK, v, need - 1);
+                        const uint64_t v = lane < m ? keyat((int)lds_u16(s_fb + 2u * (uint32_t)(c * kFinalCap + (lane & 31)))) : 0ull;
+                        T = warp_kth_desc(v, m, need, lane);
                     } else {
                         for (int i = lane; i < m; i += 32)
                             wscr[i] = keyat((int)lds_u16(s_fb + 2u * (uint32_t)(c * kFinalCap + i)));
