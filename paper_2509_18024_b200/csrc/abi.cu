@@ -271,7 +271,7 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
     w.part = c.take<float>((size_t)bb.max_tiles * nf * (nf + 1));
     w.rss_part = c.take<double>((size_t)bb.max_tiles);
     w.hist = c.take<int>((size_t)bb.max_rows * nf * kHB);
-    w.brk = c.take<uint32_t>((size_t)bb.max_rows * nf);
+    w.brk = c.take<uint32_t>((size_t)std::max<int64_t>(P->n_big, 1) * nf);  // all big rows (one calibration pass)
     w.retry = c.take<double>((size_t)std::max<int64_t>(kMaxGrid, kMaxSolveWarps) * retry_stride(nf));
     w.gbuf_rows = gbuf_rows_for(nf, P->n_small + P->n_big);
     w.gbuf = c.take<float>((size_t)w.gbuf_rows * nf * (nf + 1));
@@ -412,6 +412,25 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
     const BigBatches bb = big_batches(P);
     const int64_t* tp = P->big_tile_ptr_host;
     const int64_t* cp = P->big_cand_ptr_host;
+    // row-local bracket levels of every multi-item row, in one launch (the long rows
+    // are few per batch, so per-batch launches would leave most SMs idle)
+    cudaMemsetAsync(w.brk, 0xFF, sizeof(uint32_t) * (size_t)P->n_big * nf, st);
+    {
+        int64_t n_calib = 0;
+        if (tp)
+            while (n_calib < P->n_big && tp[n_calib + 1] - tp[n_calib] >= 2) ++n_calib;
+        if (n_calib > 0) {
+            BigArgs C{};
+            C.rows = P->big_rows;
+            C.n_big = n_calib;
+            C.brk = w.brk;
+            const size_t smem = (size_t)2 * kCalibCols * (kQ + 1) * sizeof(uint32_t);
+            allow_smem(big_calib_kernel);
+            ProfScope ps("big_calib_kernel", st);
+            big_calib_kernel<<<(int)std::min<int64_t>(n_calib, (int64_t)dev().sms * 16), kThreads, smem, st>>>(A, C,
+                                                                                                       n_calib);
+        }
+    }
     for (size_t bi = 0; bi + 1 < bb.r.size(); ++bi) {
         const int64_t r0 = bb.r[bi], r1 = bb.r[bi + 1];
         BigArgs B{};
@@ -430,23 +449,15 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
         B.part = w.part;
         B.rss_part = w.rss_part;
         B.hist = w.hist;
-        B.brk = w.brk;
+        B.brk = w.brk + (size_t)r0 * nf;
         cudaMemsetAsync(w.cnt, 0, sizeof(int) * (size_t)B.n_big * nf * 2, st);
-        cudaMemsetAsync(w.brk, 0xFF, sizeof(uint32_t) * (size_t)B.n_big * nf, st);
-        // rows spanning >= 2 work items (a prefix: rows are sorted by length) get row-local
-        // bracket levels, and their partial normal equations are reduced by big_reduce;
-        // single-item rows write theirs straight into gbuf
+        // rows spanning >= 2 work items (a prefix: rows are sorted by length) had their
+        // bracket levels calibrated above, and their partial normal equations are reduced
+        // by big_reduce; single-item rows write theirs straight into gbuf
         int64_t n_calib = 0;
         if (tp)
             while (n_calib < B.n_big && tp[r0 + n_calib + 1] - tp[r0 + n_calib] >= 2) ++n_calib;
         B.n_multi = tp ? n_calib : B.n_big;  // without host offsets every row takes the partial path
-        if (n_calib > 0) {
-            const size_t smem = (size_t)2 * kCalibCols * (kQ + 1) * sizeof(uint32_t);
-            allow_smem(big_calib_kernel);
-            ProfScope ps("big_calib_kernel", st);
-            big_calib_kernel<<<(int)std::min<int64_t>(n_calib, (int64_t)dev().sms * 3), kThreads, smem, st>>>(A, B,
-                                                                                                      n_calib);
-        }
         cudaMemsetAsync(w.hist, 0, sizeof(int) * (size_t)B.n_big * nf * kHB, st);
         const size_t scan_smem = big_scan_smem(nf, B.chunk);
         allow_smem(big_scan_kernel);

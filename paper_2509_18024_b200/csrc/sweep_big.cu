@@ -74,13 +74,13 @@ __global__ void __launch_bounds__(kThreads) big_calib_kernel(SweepArgs A, BigArg
 #pragma unroll 4
                 for (int g = 0; g < gc; ++g) {
                     const uint32_t v = abs_bits(__ldg(xr + g));
-                    const uint32_t* q = qs + g * (kQ + 1);
-                    int a = 1, b = kQ;  // first level L with q[L] <= v (q descending, q[kQ] = 0)
-                    while (a < b) {
-                        const int mid = (a + b) >> 1;
-                        if (q[mid] <= v) b = mid; else a = mid + 1;
-                    }
-                    atomicAdd(&hist[g * (kQ + 1) + a], 1u);
+                    const uint32_t q = smem_u32(qs + g * (kQ + 1));
+                    // branchless search for the last level with q[pos] > v (q[0] = inf, q[kQ] = 0)
+                    int pos = 0;
+#pragma unroll
+                    for (int step = kQ / 2; step > 0; step >>= 1)
+                        pos += (lds_u32(q + 4u * (uint32_t)(pos + step)) > v) ? step : 0;
+                    atomicAdd(&hist[g * (kQ + 1) + pos + 1], 1u);
                 }
             }
             __syncthreads();
