@@ -69,6 +69,17 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 }
 
 // Bitonic sort of one 64-bit key per lane; result descending (lane 0 = max).
+// (d0, d1) += (a0, a1) * s as ONE packed FFMA2 (sm_100: fma.rn.f32x2; each
+// lane is an IEEE fmaf, so results are bit-identical to two fmaf calls).
+__device__ __forceinline__ void ffma2_bcast(float& d0, float& d1, float a0, float a1, float s) {
+    unsigned long long acc, av, sv;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(acc) : "f"(d0), "f"(d1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(av) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(sv) : "f"(s));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(av), "l"(sv));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(acc));
+}
+
 // need-th largest (1-based) of the unique keys held by lanes [0, m), m <= 32,
 // by counting: each lane counts the keys above its own (m broadcast rounds;
 // cheaper than a 32-wide bitonic sort for the small m of a final sub-bucket).

@@ -184,10 +184,8 @@ __device__ __forceinline__ void sparse_gram_warp(uint32_t xs, int sx, uint32_t y
                 const int ch = fl + i * LPC;
                 if (i < CPL - 1 || chunk_ok_last) {
                     const float4 v = lds_f128(xs + rb + 16u * (uint32_t)ch);
-                    acc[4 * i + 0] = fmaf(xc, v.x, acc[4 * i + 0]);
-                    acc[4 * i + 1] = fmaf(xc, v.y, acc[4 * i + 1]);
-                    acc[4 * i + 2] = fmaf(xc, v.z, acc[4 * i + 2]);
-                    acc[4 * i + 3] = fmaf(xc, v.w, acc[4 * i + 3]);
+                    ffma2_bcast(acc[4 * i + 0], acc[4 * i + 1], v.x, v.y, xc);
+                    ffma2_bcast(acc[4 * i + 2], acc[4 * i + 3], v.z, v.w, xc);
                 }
             }
             if (fl == 0) accb = fmaf(xc, lds_f32(ys + 4u * k), accb);
@@ -269,10 +267,8 @@ __device__ __forceinline__ void sparse_gram_owned(uint32_t xs, int sx, uint32_t 
             for (int i = 0; i < CPL; ++i) {
                 if (i < CPL - 1 || chunk_ok_last) {
                     const float4 v = lds_f128(xs + rb + 16u * (uint32_t)(fl + i * LPC));
-                    acc[4 * i + 0] = fmaf(xc, v.x, acc[4 * i + 0]);
-                    acc[4 * i + 1] = fmaf(xc, v.y, acc[4 * i + 1]);
-                    acc[4 * i + 2] = fmaf(xc, v.z, acc[4 * i + 2]);
-                    acc[4 * i + 3] = fmaf(xc, v.w, acc[4 * i + 3]);
+                    ffma2_bcast(acc[4 * i + 0], acc[4 * i + 1], v.x, v.y, xc);
+                    ffma2_bcast(acc[4 * i + 2], acc[4 * i + 3], v.z, v.w, xc);
                 }
             }
             if (fl == 0) accb = fmaf(xc, lds_f32(ys + 4u * k), accb);
@@ -367,10 +363,8 @@ __device__ __forceinline__ void owned_accumulate(OwnedAcc<CPL>& S, const OwnedMa
         for (int i = 0; i < CPL; ++i) {
             if (i < CPL - 1 || chunk_ok_last) {
                 const float4 v = lds_f128(xs + rb + 16u * (uint32_t)(M.fl + i * M.LPC));
-                S.acc[4 * i + 0] = fmaf(xc, v.x, S.acc[4 * i + 0]);
-                S.acc[4 * i + 1] = fmaf(xc, v.y, S.acc[4 * i + 1]);
-                S.acc[4 * i + 2] = fmaf(xc, v.z, S.acc[4 * i + 2]);
-                S.acc[4 * i + 3] = fmaf(xc, v.w, S.acc[4 * i + 3]);
+                ffma2_bcast(S.acc[4 * i + 0], S.acc[4 * i + 1], v.x, v.y, xc);
+                ffma2_bcast(S.acc[4 * i + 2], S.acc[4 * i + 3], v.z, v.w, xc);
             }
         }
         if (M.fl == 0) S.accb = fmaf(xc, lds_f32(ys + 4u * k), S.accb);

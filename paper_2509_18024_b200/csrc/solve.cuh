@@ -287,12 +287,10 @@ __device__ __forceinline__ void wide_block(WideLU<NF>& S, bool spd, int lane) {
 #pragma unroll
         for (int j = B0; j < NF; ++j) {
             const float vp = __shfl_sync(CALS_FULL_MASK, sel_f32(hi, S.b[j], S.a[j]), pl);
-            S.a[j] = fmaf(-fa, vp, S.a[j]);
-            S.b[j] = fmaf(-fb, vp, S.b[j]);
+            ffma2_bcast(S.a[j], S.b[j], -fa, -fb, vp);  // both rows in one FFMA2
         }
         const float bp = __shfl_sync(CALS_FULL_MASK, sel_f32(hi, S.rb, S.ra), pl);
-        S.ra = fmaf(-fa, bp, S.ra);
-        S.rb = fmaf(-fb, bp, S.rb);
+        ffma2_bcast(S.ra, S.rb, -fa, -fb, bp);
     }
 }
 
