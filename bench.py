@@ -360,12 +360,16 @@ def e2e(data, spec, M0, steps):
         wall = time.perf_counter() - t0
     nnz = R.n_entries
     n_f = spec["n_f"]
-    h2d = (R.row_ptr.nbytes + R.col_ptr.nbytes + 2 * nnz * 4 + 2 * nnz * 4 + (R.n_users + R.n_items) * n_f * 4)
-    d2h = (R.n_users + R.n_items) * n_f * 4 + rep.iters_run * 5 * 8
+    # copied tensors: both indexes (int64 pointers, int32 indices, float64 values -- narrowed to fp32 on
+    # the device), the fp32 item init (user rows start at zero on the device); back: float64 factors and
+    # 5 float64 objective terms per iteration
+    h2d = (R.row_ptr.nbytes + R.col_ptr.nbytes + 2 * nnz * 4 + 2 * nnz * 8 + R.n_items * n_f * 4)
+    d2h = (R.n_users + R.n_items) * n_f * 8 + rep.iters_run * 5 * 8
     return {"value": nnz * rep.iters_run / wall, "unit": UNIT, "h2d_bytes_per_step": h2d / rep.iters_run,
             "d2h_bytes_per_step": d2h / rep.iters_run, "wall_s": wall, "iters": rep.iters_run,
-            "how": "paper_2509_18024_b200.fit_core(RatingMatrix of numpy arrays) incl. plan, H2D (pageable), "
-                   "all iterations, D2H of float64 factors; per-step bytes amortised over the fit"}
+            "how": "paper_2509_18024_b200.fit_core(RatingMatrix of numpy arrays) incl. plan, H2D (pageable; the "
+                   "item side's copies overlap the first user half-sweep), all iterations, D2H of float64 "
+                   "factors; per-step bytes amortised over the fit"}
 
 
 if __name__ == "__main__":

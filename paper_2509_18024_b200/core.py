@@ -187,10 +187,12 @@ def fit_core(R, cfg, *, init_u=None, init_m=None, items_first=False, engine=None
     torch = _lib.require_cuda()
     from .engine import CoreEngine
 
-    F0 = init_factors(R, cfg) if (init_u is None or init_m is None) else None
-    U0 = F0.user_factors if init_u is None else np.ascontiguousarray(init_u, dtype=np.float64)
-    M0 = F0.item_factors if init_m is None else np.ascontiguousarray(init_m, dtype=np.float64)
-    if U0.shape != (R.n_users, cfg.n_f) or M0.shape != (R.n_items, cfg.n_f):
+    # init_factors draws only the item rows (user rows start at zero, als.py:117-131),
+    # so an explicit init_m needs no draw at all, and zero user rows need no upload
+    M0 = (init_factors(R, cfg).item_factors if init_m is None
+          else np.ascontiguousarray(init_m, dtype=np.float64))
+    U0 = None if init_u is None else np.ascontiguousarray(init_u, dtype=np.float64)
+    if (U0 is not None and U0.shape != (R.n_users, cfg.n_f)) or M0.shape != (R.n_items, cfg.n_f):
         raise ConfigError("initial factor shapes do not match the rating matrix")
 
     row_counts = np.diff(_host(R.row_ptr))
@@ -209,19 +211,21 @@ def fit_core(R, cfg, *, init_u=None, init_m=None, items_first=False, engine=None
 
     eng = engine if engine is not None else CoreEngine(R, cfg.n_f, cfg.rate, cfg.lam)
     eng.set_factors(U0, M0)
+    if U0 is None:
+        eng.zero_factors("user")
     ssq = eng.ssq
     obj_trace, rmse_trace = [], []
     converged = False
     first = "item" if items_first else "user"
     second = "user" if items_first else "item"
-    sides = {"user": eng.user, "item": eng.item}
+    sides = eng._side  # side objects by name (built lazily by the engine)
     prev = [None]
 
     def consume(t):
         """obj/rmse of iteration t (als.py:299-307); True when converged there."""
         terms = eng.terms(t)
-        _raise_for(terms.status_first, first, sides[first], t)
-        _raise_for(terms.status_second, second, sides[second], t)
+        _raise_for(terms.status_first, first, sides(first), t)
+        _raise_for(terms.status_second, second, sides(second), t)
         obj = terms.rss + (cfg.lam * terms.pen if cfg.lam != 0.0 else 0.0)
         obj_trace.append(obj)
         rmse_trace.append(np.sqrt(terms.rss / ssq) if ssq > 0 else 0.0)

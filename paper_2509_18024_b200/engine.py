@@ -23,6 +23,8 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass
 
+import threading
+
 import numpy as np
 
 from . import _lib
@@ -165,8 +167,13 @@ class CoreEngine:
         self.n_users, self.n_items = int(R.n_users), int(R.n_items)
         ur = user_range or (0, self.n_users)
         ir = item_range or (0, self.n_items)
-        self.user = DeviceSide(R.row_ptr, R.row_items, R.row_vals, self.n_items, n_f, rate, device, *ur)
-        self.item = DeviceSide(R.col_ptr, R.col_users, R.col_vals, self.n_users, n_f, rate, device, *ir)
+        # each side (plan + uploads) is built on first use, so the second side's
+        # host->device copies overlap the first half-sweep already on the GPU
+        self._side_args = {
+            "user": (R.row_ptr, R.row_items, R.row_vals, self.n_items, n_f, rate, device, *ur),
+            "item": (R.col_ptr, R.col_users, R.col_vals, self.n_users, n_f, rate, device, *ir),
+        }
+        self._sides = {}
         # factor rows padded to a multiple of 4 floats (16-byte gathers); padding stays zero
         self.ld = (self.n_f + 3) // 4 * 4
         self.Ub = [torch.zeros((self.n_users, self.ld), dtype=torch.float32, device=device) for _ in range(2)]
@@ -177,10 +184,42 @@ class CoreEngine:
         self.slots = torch.zeros((2, 5), dtype=torch.float64, device=device)
         self.host_slots = torch.zeros((2, 5), dtype=torch.float64).pin_memory()
         self.events = [torch.cuda.Event(), torch.cuda.Event()]
-        vals = R.row_vals if torch.is_tensor(R.row_vals) else torch.from_numpy(np.asarray(R.row_vals))
-        vals = vals.to(device=device, dtype=torch.float64)
-        self.ssq = float(torch.dot(vals, vals).item()) if vals.numel() else 0.0
+        # sum of squared ratings in float64 (relative RMSE denominator): on the
+        # device for device data, else on the host in a background thread
+        vals = R.row_vals
+        if torch.is_tensor(vals):
+            v = vals.to(device=device, dtype=torch.float64)
+            self._ssq = float(torch.dot(v, v).item()) if v.numel() else 0.0
+            self._ssq_thread = None
+        else:
+            v = np.asarray(vals, dtype=np.float64)
+            self._ssq = None
+            self._ssq_box = [0.0]
+            self._ssq_thread = threading.Thread(
+                target=lambda: self._ssq_box.__setitem__(0, float(np.dot(v, v)) if v.size else 0.0), daemon=True)
+            self._ssq_thread.start()
         self.iters_done = 0
+
+    @property
+    def ssq(self):
+        if self._ssq is None:
+            self._ssq_thread.join()
+            self._ssq = self._ssq_box[0]
+        return self._ssq
+
+    def _side(self, name):
+        s = self._sides.get(name)
+        if s is None:
+            s = self._sides[name] = DeviceSide(*self._side_args[name])
+        return s
+
+    @property
+    def user(self):
+        return self._side("user")
+
+    @property
+    def item(self):
+        return self._side("item")
 
     # -- factor buffers ------------------------------------------------------
     @property
@@ -210,6 +249,12 @@ class CoreEngine:
             m = torch.as_tensor(np.asarray(M, dtype=np.float32)).to(self.device)
             for b in self.Mb:
                 b[:, :self.n_f].copy_(m)
+        self.iters_done = 0
+
+    def zero_factors(self, side):
+        """Zero rows for one side in both buffers (the reference's user init)."""
+        for b in (self.Ub if side == "user" else self.Mb):
+            b.zero_()
         self.iters_done = 0
 
     def _exchange(self, side):  # all-gather of the new rows (sharded engine)
@@ -246,8 +291,9 @@ class CoreEngine:
         torch = _lib.require_cuda()
         t = self.iters_done
         second = "item" if first == "user" else "user"
-        sf, ss = (self.user, self.item) if first == "user" else (self.item, self.user)
+        sf = self._side(first)
         self.half(first, rss=t > 0)
+        ss = self._side(second)  # built here on the first step: overlaps the first half-sweep
         if t > 0:
             self._sum(sf.rss_rows, self.slots[(t - 1) % 2, 0:1].data_ptr())
             self._reduce_scalars((t - 1) % 2, (0,))
@@ -294,4 +340,5 @@ class CoreEngine:
         self.iters_done -= 1
 
     def factors_host(self):
+        # widen on the device: the float64 copy-out is cheaper than a host conversion
         return self.U_view.double().cpu().numpy(), self.M_view.double().cpu().numpy()
