@@ -183,6 +183,24 @@ def fit_core(R, cfg, *, init_u=None, init_m=None, items_first=False, engine=None
         warnings.warn("per-regression diagnostics are not available on the GPU path; ignoring the flag",
                       stacklevel=2)
         cfg = replace(cfg, diagnostics=False)
+    return _fit_gpu(R, cfg, cfg.rate, init_u, init_m, items_first, engine)
+
+
+def fit(R, cfg, *, init_u=None, init_m=None, items_first=False, engine=None):
+    """Exact full-sample ALS (method 'full', als.py:326-336) on the GPU.
+
+    Every regression is the exact ridge X^T X + lam*n_i*I (als.py:200-205) --
+    the same kernels with a complete budget (s_i = n_i: no selection, identity
+    kept-row lists, the SPD elimination with the reference's Cholesky failure
+    point and jitter retry, als.py:184-197).  Reference semantics otherwise as
+    fit_core; the report's sketch_time is 0 as in _FullSweeper.
+    """
+    if cfg.method != "full":
+        raise ConfigError(f"als.fit handles method 'full', got {cfg.method!r}")
+    return _fit_gpu(R, cfg, 1.0, init_u, init_m, items_first, engine)
+
+
+def _fit_gpu(R, cfg, rate, init_u, init_m, items_first, engine):
     start = time.perf_counter()
     torch = _lib.require_cuda()
     from .engine import CoreEngine
@@ -209,7 +227,7 @@ def fit_core(R, cfg, *, init_u=None, init_m=None, items_first=False, engine=None
             f"n_f={cfg.n_f} exceeds the smallest user rating count; "
             "the penalty term is doing the disambiguation", stacklevel=2)
 
-    eng = engine if engine is not None else CoreEngine(R, cfg.n_f, cfg.rate, cfg.lam)
+    eng = engine if engine is not None else CoreEngine(R, cfg.n_f, rate, cfg.lam)
     eng.set_factors(U0, M0)
     if U0 is None:
         eng.zero_factors("user")

@@ -1,17 +1,18 @@
 """Method dispatch (the reference's single public seam, driver.py:10-25).
 
-``fit_method(R, cfg)`` routes method "core" to the GPU fit.  The reference's
-other estimators (full, fast_core, unif, blev) are outside this package's
-scope; they raise ConfigError naming the supported method, so a caller can
-keep dispatching those to the reference.
+``fit_method(R, cfg)`` routes methods "core" and "full" (the exact ALS the
+core estimator is measured against) to the GPU fits.  The
+reference's other estimators (fast_core, unif, blev) are outside this
+package's scope; they raise ConfigError naming the supported methods, so a
+caller can keep dispatching those to the reference.
 """
 
-from .core import fit_core
+from .core import fit, fit_core
 from .errors import ConfigError
 
 __all__ = ["fit_method"]
 
-_DISPATCH = {"core": fit_core}
+_DISPATCH = {"core": fit_core, "full": fit}
 
 
 def fit_method(R, cfg, **kwargs):

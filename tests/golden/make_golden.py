@@ -24,6 +24,7 @@ import numpy as np  # noqa: E402
 
 import coreals  # noqa: E402
 from coreals import RatingMatrix, SolverConfig, ces_sketch, fit_core, update_user_core  # noqa: E402
+from coreals.als import fit as fit_full  # noqa: E402
 from coreals.core import sketch_budget  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -176,7 +177,30 @@ def fit_case(name, seed, n_users, n_items, density, n_f, lam, rate, iters, ties=
     )
 
 
+def full_case(name, seed, n_users, n_items, density, n_f, lam, iters, drop_user=None):
+    """The reference's exact ALS (method 'full', als.py:326-336)."""
+    users, items, vals = make_matrix(seed, n_users, n_items, density, max(2, n_f // 2), 0.5)
+    if drop_user is not None:
+        keep = users != drop_user
+        users, items, vals = users[keep], items[keep], vals[keep]
+    R = RatingMatrix(users, items, vals, n_users=n_users, n_items=n_items)
+    M0 = f32(np.random.default_rng(seed + 1).normal(0.0, 0.1, size=(n_items, n_f)))
+    cfg = SolverConfig(method="full", n_f=n_f, lam=lam, max_iters=iters, tol=1e-15)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        F, rep = fit_full(R, cfg, init_m=M0)
+    np.savez_compressed(
+        os.path.join(OUT, f"fit_{name}.npz"),
+        users=users, items=items, vals=vals, n_users=n_users, n_items=n_items, n_f=n_f, lam=lam, iters=iters,
+        M0=M0, objN=rep.objective_trace, rmseN=rep.rmse_trace, UN=F.user_factors, MN=F.item_factors,
+        skipped_users=rep.skipped_users, skipped_items=rep.skipped_items,
+    )
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["full"]:
+        full_case("full", 4, 120, 90, 0.3, 8, 0.1, 4, drop_user=7)
+        sys.exit(0)
     sketch_cases()
     update_cases()
     # config-1 shape scaled down (BASELINE configs[0]: n_f=5, lam=0.1, r=0.3)
@@ -187,4 +211,6 @@ if __name__ == "__main__":
     fit_case("ties_wide", 2, 90, 70, 0.15, 32, 0.05, 0.2, 3, ties=True, drop_user=3, drop_item=5)
     # rate 1: every row takes the exact SPD path
     fit_case("rate1", 3, 50, 40, 0.4, 4, 0.1, 1.0, 3)
+    # exact ALS (method 'full')
+    full_case("full", 4, 120, 90, 0.3, 8, 0.1, 4, drop_user=7)
     print("golden fixtures written to", OUT)

@@ -82,6 +82,22 @@ def test_golden_half_sweeps(name):
     assert row_rel_err(M, g["M1_from_U1"], act) <= FACTOR_TOL
 
 
+def test_golden_full_als():
+    """Method 'full' (exact ALS, every row SPD) against the reference's als.fit."""
+    g = load_golden("fit_full.npz")
+    R = cb.RatingMatrix(g["users"], g["items"], g["vals"], n_users=int(g["n_users"]), n_items=int(g["n_items"]))
+    cfg = cb.SolverConfig(method="full", n_f=int(g["n_f"]), lam=float(g["lam"]), max_iters=int(g["iters"]),
+                          tol=1e-15)
+    with _nowarn():
+        F, rep = cb.fit_method(R, cfg, init_m=g["M0"])
+    assert rep.method == "full" and rep.iters_run == int(g["iters"])
+    assert abs(rep.rmse_trace[-1] - g["rmseN"][-1]) <= 1e-3
+    np.testing.assert_allclose(rep.objective_trace, g["objN"], rtol=1e-3)
+    act = np.diff(R.row_ptr) > 0
+    assert row_rel_err(F.user_factors, g["UN"], act) <= 1e-3
+    assert rep.skipped_users == int(g["skipped_users"])
+
+
 @pytest.mark.parametrize("name", ["small", "medium", "ties_wide", "rate1"])
 def test_golden_fit_rmse(name):
     g, R, _ = golden_engine(name)

@@ -82,6 +82,21 @@ def test_half_sweeps_and_fit_match_reference(name):
     np.testing.assert_allclose(U, g["UN"], rtol=1e-7, atol=1e-9)
 
 
+def test_oracle_rate1_matches_reference_full_als():
+    """The reference's exact ALS (method 'full') is the rate-1 collapse of the
+    core estimator (test_acceptance.py:54-73): the oracle at rate 1 reproduces
+    the reference's `als.fit` fixture."""
+    g = load_golden("fit_full.npz")
+    n_f, lam = int(g["n_f"]), float(g["lam"])
+    csr, csc = csr_csc(g["users"], g["items"], g["vals"], int(g["n_users"]), int(g["n_items"]))
+    U0 = np.zeros((int(g["n_users"]), n_f))
+    U, M, rep = oracle.fit_core(csr, csc, n_f, lam, 1.0, int(g["iters"]), 1e-15, U0, g["M0"])
+    np.testing.assert_allclose(rep.objective_trace, g["objN"], rtol=1e-9)
+    np.testing.assert_allclose(rep.rmse_trace, g["rmseN"], rtol=1e-9)
+    np.testing.assert_allclose(U, g["UN"], rtol=1e-7, atol=1e-9)
+    np.testing.assert_allclose(M, g["MN"], rtol=1e-7, atol=1e-9)
+
+
 def test_multithreaded_oracle_is_deterministic():
     g = load_golden("fit_medium.npz")
     n_f, lam, rate = int(g["n_f"]), float(g["lam"]), float(g["rate"])
