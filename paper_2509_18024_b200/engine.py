@@ -122,8 +122,13 @@ class DeviceSide:
         torch = _lib.require_cuda()
         if stream is None:
             stream = torch.cuda.current_stream(self.device).cuda_stream
-        _lib.check(_lib.load().cals_residual(ctypes.byref(self.side), source.data_ptr(), source.stride(0), self.n_f,
-                                             rows_w.data_ptr(), rows_w.stride(0), self.rss_rows.data_ptr(), stream),
+        # this shard's rows only: a view of the side starting at row_begin
+        r0, r1 = self.row_range
+        view = _lib.cals_side(self.ptr.data_ptr() + 8 * r0, self.idx.data_ptr(), self.val.data_ptr(), r1 - r0,
+                              self.side.nnz)
+        _lib.check(_lib.load().cals_residual(ctypes.byref(view), source.data_ptr(), source.stride(0), self.n_f,
+                                             rows_w[r0:].data_ptr(), rows_w.stride(0),
+                                             self.rss_rows[r0:].data_ptr(), stream),
                    "cals_residual")
 
 

@@ -51,7 +51,14 @@ def allgather_rows(F, ranges, rank, group=None, scratch=None):
     recv = scratch[maxr * nf:(world + 1) * maxr * nf].view(world, maxr, nf)
     r0, r1 = ranges[rank]
     send[:r1 - r0].copy_(F[r0:r1])
-    dist.all_gather_into_tensor(recv.view(-1), send.view(-1), group=group)
+    if F.is_cuda and dist.get_backend(group) != "nccl":
+        # host-staged exchange for CPU backends (gloo): functional tests of the
+        # sharded engine with several ranks on one device
+        rc = recv.cpu()
+        dist.all_gather_into_tensor(rc.view(-1), send.cpu().view(-1), group=group)
+        recv.copy_(rc)
+    else:
+        dist.all_gather_into_tensor(recv.view(-1), send.view(-1), group=group)
     for q, (q0, q1) in enumerate(ranges):
         if q != rank and q1 > q0:
             F[q0:q1].copy_(recv[q, :q1 - q0])
@@ -79,14 +86,17 @@ class ShardedEngine:
                 row = self.slots[parity]
                 sums = [c for c in cols if c <= 2]
                 maxes = [c for c in cols if c >= 3]
+                host = dist.get_backend(group) != "nccl"  # gloo: reduce host copies
                 if sums:
                     t = row[sums[0]:sums[-1] + 1].clone()
+                    t = t.cpu() if host else t
                     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
                     row[sums[0]:sums[-1] + 1].copy_(t)
                 if maxes:
                     t = row[maxes[0]:maxes[-1] + 1].view(torch.int64).clone()
+                    t = t.cpu() if host else t
                     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-                    row[maxes[0]:maxes[-1] + 1].copy_(t.view(torch.float64))
+                    row[maxes[0]:maxes[-1] + 1].copy_(t.view(torch.float64).to(row.device))
 
         eng = _Sharded(R, n_f, rate, lam, device=device, user_range=user_ranges[rank], item_range=item_ranges[rank])
         eng._scratch = None
