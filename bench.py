@@ -226,10 +226,17 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CALS_BENCH_BACKEND=gloo: functional check of the N > 1 code path with several ranks on one
+    # device (host-staged exchange); never a measurement -- the line is tagged "functional_only"
+    backend = os.environ.get("CALS_BENCH_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     from paper_2509_18024_b200 import _lib, synth
     from paper_2509_18024_b200.engine import CoreEngine
     from paper_2509_18024_b200.shard import ShardedEngine
@@ -273,12 +280,15 @@ def main():
     _lib.profile_enable(False)
     total_ms = float(sum(times))
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     nnz = data.nnz
     value = nnz * args.steps / (total_ms / 1e3)
 
+    e2e_line = None
+    if not args.no_e2e:
+        e2e_line = e2e(data, spec, M0, args.steps, rank, world)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -286,7 +296,7 @@ def main():
         return
 
     hbm, peak_kind = measured_peaks()
-    core = eng.eng if world > 1 else eng
+    core = eng  # ShardedEngine is a CoreEngine restricted to this rank's rows
     sb_u, bb_u = tier_bytes(core.user, n_f)
     sb_i, bb_i = tier_bytes(core.item, n_f)
     kbytes = {"small_gram_kernel": (sb_u + sb_i) * args.steps, "big_gram_kernel": (bb_u + bb_i) * args.steps,
@@ -329,47 +339,67 @@ def main():
         line["cpu_baseline"] = cpu_baseline_port(R_host, spec, M0, args.cpu_seconds)
     else:
         line["cpu_baseline"] = None
-    if not args.no_e2e and world == 1:
-        line["e2e"] = e2e(data, spec, M0, args.steps)
+    if e2e_line is not None:
+        line["e2e"] = e2e_line
+    if backend != "nccl":
+        line["functional_only"] = f"{backend} backend, ranks share a device: not a measurement"
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     print(json.dumps(line), flush=True)
 
 
-def e2e(data, spec, M0, steps):
+def e2e(data, spec, M0, steps, rank=0, world=1):
     """fit_core through the public API from host (numpy) arrays: H2D of both
-    indexes and the init, `steps` iterations, D2H of both factor matrices."""
+    indexes and the init, `steps` iterations, D2H of both factor matrices.
+    With N > 1 ranks every rank runs fit_core on its row shard (ShardedEngine,
+    NCCL all-gather per half-sweep); wall = max over ranks."""
     import warnings
 
     import torch
+    import torch.distributed as dist
 
     import paper_2509_18024_b200 as cb
+    from paper_2509_18024_b200.shard import ShardedEngine
 
     R = data.rating_matrix()
     cfg = cb.SolverConfig(method="core", n_f=spec["n_f"], lam=spec["lam"], rate=spec["rate"], max_iters=steps,
                           tol=1e-15)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def engine():
+        if world == 1:
+            return None  # fit_core builds its own CoreEngine
+        return ShardedEngine(R, spec["n_f"], spec["rate"], spec["lam"], rank, world, device=dev)
+
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
         cb.fit_core(R, cb.SolverConfig(method="core", n_f=spec["n_f"], lam=spec["lam"], rate=spec["rate"],
-                                       max_iters=1, tol=1e-15), init_m=M0)  # warm (allocator, module load)
+                                       max_iters=1, tol=1e-15), init_m=M0, engine=engine())  # warm
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        F, rep = cb.fit_core(R, cfg, init_m=M0)
+        F, rep = cb.fit_core(R, cfg, init_m=M0, engine=engine())  # sides (and their H2D) built inside
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
+    if world > 1:
+        w = torch.tensor([wall], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(w, op=dist.ReduceOp.MAX)
+        wall = float(w.item())
     nnz = R.n_entries
     n_f = spec["n_f"]
     # copied tensors: both indexes (int64 pointers, int32 indices, float64 values -- narrowed to fp32 on
     # the device), the fp32 item init (user rows start at zero on the device); back: float64 factors and
-    # 5 float64 objective terms per iteration
-    h2d = (R.row_ptr.nbytes + R.col_ptr.nbytes + 2 * nnz * 4 + 2 * nnz * 8 + R.n_items * n_f * 4)
-    d2h = (R.n_users + R.n_items) * n_f * 8 + rep.iters_run * 5 * 8
+    # 5 float64 objective terms per iteration (per rank at N > 1: each rank uploads the full index)
+    h2d = (R.row_ptr.nbytes + R.col_ptr.nbytes + 2 * nnz * 4 + 2 * nnz * 8 + R.n_items * n_f * 4) * world
+    d2h = ((R.n_users + R.n_items) * n_f * 8 + rep.iters_run * 5 * 8) * world
     return {"value": nnz * rep.iters_run / wall, "unit": UNIT, "h2d_bytes_per_step": h2d / rep.iters_run,
             "d2h_bytes_per_step": d2h / rep.iters_run, "wall_s": wall, "iters": rep.iters_run,
             "how": "paper_2509_18024_b200.fit_core(RatingMatrix of numpy arrays) incl. plan, H2D (pageable; the "
                    "item side's copies overlap the first user half-sweep), all iterations, D2H of float64 "
-                   "factors; per-step bytes amortised over the fit"}
+                   "factors; per-step bytes amortised over the fit" + (
+                       f"; {world} ranks, ShardedEngine, max wall over ranks" if world > 1 else "")}
 
 
 if __name__ == "__main__":
