@@ -259,20 +259,46 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
                 const int sh = hb_shift(hib - lob);
                 const uint64_t blo = hb_lower_key(bT, lob, sh);
                 const uint64_t bhi = min(hb_lower_key(bT + 1, lob, sh), hik);
-                // keep that bucket's keys (in place), then select among them
+                // keep that bucket's keys, then select among them: in registers (one key
+                // per lane) while they fit, else compacted in place in the candidate list.
+                // Four 32-key loads are in flight per round (the list streams from HBM).
                 int m = 0;
-                for (int i0 = 0; i0 < in; i0 += 32) {
-                    const int i = i0 + lane;
-                    const uint64_t kk = i < in ? cl[i] : 0ull;
-                    const bool keep = i < in && kk >= blo && kk < bhi;
-                    const uint32_t bal = __ballot_sync(CALS_FULL_MASK, keep);
-                    __syncwarp();
-                    if (keep) cl[m + __popc(bal & lanemask_lt())] = kk;
-                    m += __popc(bal);
+                bool spill = false;
+                uint64_t v = 0ull;
+                for (int i0 = 0; i0 < in; i0 += 128) {
+                    uint64_t kk[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = i0 + 32 * u + lane;
+                        kk[u] = i < in ? cl[i] : 0ull;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = i0 + 32 * u + lane;
+                        const bool keep = i < in && kk[u] >= blo && kk[u] < bhi;
+                        const uint32_t bal = __ballot_sync(CALS_FULL_MASK, keep);
+                        const int cnt = __popc(bal);
+                        if (!spill && m + cnt <= 32) {
+                            const int p = lane - m;
+                            const bool mine = p >= 0 && p < cnt;
+                            const uint64_t got = __shfl_sync(CALS_FULL_MASK, kk[u], mine ? (int)__fns(bal, 0, p + 1) : 0);
+                            if (mine) v = got;
+                        } else {
+                            if (!spill) {
+                                __syncwarp();
+                                if (lane < m) cl[lane] = v;
+                                spill = true;
+                            }
+                            __syncwarp();
+                            if (keep) cl[m + __popc(bal & lanemask_lt())] = kk[u];
+                        }
+                        m += cnt;
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) stat_add(A, kStBigColumns, 1);
-                T = warp_select_keys(KeyList{cl}, m, need - before, blo, bhi, lane);
+                T = spill ? warp_select_keys(KeyList{cl}, m, need - before, blo, bhi, lane)
+                          : warp_kth_desc(v, m, need - before, lane);
             } else {
                 if (lane == 0) {
                     stat_add(A, kStBigFallback, 1);
