@@ -83,6 +83,7 @@ typedef struct cals_plan {
     int32_t n_f;                  /* rank the plan was built for */
     const int64_t* big_tile_ptr_host;  /* host copies (caller-owned) used to batch the tiled tier */
     const int64_t* big_cand_ptr_host;
+    const int32_t* big_tile_row;  /* optional device [n_big_tiles]: big row of each work item (else searched) */
 } cals_plan;
 
 /* Host: reference budget rule for every row (core.py:48-54), fp64, no FMA. */

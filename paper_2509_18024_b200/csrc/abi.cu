@@ -450,6 +450,8 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
         B.rss_part = w.rss_part;
         B.hist = w.hist;
         B.brk = w.brk + (size_t)r0 * nf;
+        B.tile_row = P->big_tile_row;
+        B.row_base = r0;
         cudaMemsetAsync(w.cnt, 0, sizeof(int) * (size_t)B.n_big * nf * 2, st);
         // rows spanning >= 2 work items (a prefix: rows are sorted by length) had their
         // bracket levels calibrated above, and their partial normal equations are reduced

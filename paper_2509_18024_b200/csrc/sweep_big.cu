@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
     const FastDiv fq((uint32_t)xs_chunks(nf));
     for (int64_t t = blockIdx.x; t < B.n_tiles; t += gridDim.x) {
         const int64_t T_abs = B.tile_base + t;
-        const int r = find_row(B.tile_ptr, B.n_big, T_abs);
+        const int r = B.tile_row != nullptr ? (int)(__ldg(B.tile_row + T_abs) - B.row_base)
+                                            : find_row(B.tile_ptr, B.n_big, T_abs);
         const int row = B.rows[r];
         const int64_t lo = A.ptr[row];
         const int n = (int)(A.ptr[row + 1] - lo);
@@ -351,7 +352,8 @@ __global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(Sw
     OwnedAcc<CPL> S;
     for (int64_t t = blockIdx.x; t < B.n_tiles; t += gridDim.x) {
         const int64_t T_abs = B.tile_base + t;
-        const int r = find_row(B.tile_ptr, B.n_big, T_abs);
+        const int r = B.tile_row != nullptr ? (int)(__ldg(B.tile_row + T_abs) - B.row_base)
+                                            : find_row(B.tile_ptr, B.n_big, T_abs);
         const int row = B.rows[r];
         const int64_t lo = A.ptr[row];
         const int n = (int)(A.ptr[row + 1] - lo);

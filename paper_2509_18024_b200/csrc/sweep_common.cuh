@@ -73,6 +73,8 @@ struct BigArgs {
     double* rss_part;         // [n_tiles]
     int* hist;                // [n_big][nf][kHB] in-bracket counts per sub-bucket
     const uint32_t* brk;      // [n_big][nf] calibrated levels jhi | jlo << 16, or ~0u (use the table margin)
+    const int32_t* tile_row;  // nullable: absolute big row of each absolute work item
+    int64_t row_base;         // absolute index of the batch's first big row
 };
 
 constexpr int kHB = 32;  // sub-buckets of a big row's bracket (linear in abs-bit space)

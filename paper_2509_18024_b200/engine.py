@@ -91,6 +91,11 @@ class DeviceSide:
         meta.big_cand_ptr = self.cand_ptr.data_ptr()
         self.tile_ptr_host = np.ascontiguousarray(tile_ptr[:meta.n_big + 1])
         self.cand_ptr_host = np.ascontiguousarray(cand_ptr[:meta.n_big + 1])
+        # work item -> big row (saves each item a binary search over tile_ptr)
+        tp = self.tile_ptr_host
+        self.tile_row = t(np.repeat(np.arange(meta.n_big, dtype=np.int32), np.diff(tp)) if meta.n_big
+                          else np.zeros(1, np.int32), torch.int32)
+        meta.big_tile_row = self.tile_row.data_ptr()
         meta.big_tile_ptr_host = self.tile_ptr_host.ctypes.data
         meta.big_cand_ptr_host = self.cand_ptr_host.ctypes.data
         self.plan = meta
