@@ -25,6 +25,7 @@ import numpy as np  # noqa: E402
 import coreals  # noqa: E402
 from coreals import RatingMatrix, SolverConfig, ces_sketch, fit_core, update_user_core  # noqa: E402
 from coreals.als import fit as fit_full  # noqa: E402
+from coreals.core import fit_fast_core  # noqa: E402
 from coreals.core import sketch_budget  # noqa: E402
 
 OUT = os.path.dirname(os.path.abspath(__file__))
@@ -197,9 +198,50 @@ def full_case(name, seed, n_users, n_items, density, n_f, lam, iters, drop_user=
     )
 
 
+def fast_case(name, seed, n_users, n_items, density, n_f, lam, rate, iters, drop_user=None, ties=False):
+    """The reference's whole-matrix sketch variant (method 'fast_core', core.py:255-324):
+    per-half-sweep global ces_sketch of the source, row-sketched Gram with the
+    empty-slice-column fallback (_kernels.py:172-216).  One-iteration factors
+    (from M0, and the item half from a fp32 snapshot of U1) plus N-iteration traces."""
+    users, items, vals = make_matrix(seed, n_users, n_items, density, max(2, n_f // 2), 0.5, ties)
+    if drop_user is not None:
+        keep = users != drop_user
+        users, items, vals = users[keep], items[keep], vals[keep]
+    R = RatingMatrix(users, items, vals, n_users=n_users, n_items=n_items)
+    M0 = np.random.default_rng(seed + 1).normal(0.0, 0.1, size=(n_items, n_f))
+    if ties:
+        M0 = np.round(M0, 2)
+    M0 = f32(M0)
+    cfg1 = SolverConfig(method="fast_core", n_f=n_f, lam=lam, rate=rate, max_iters=1, tol=1e-15)
+    cfgN = SolverConfig(method="fast_core", n_f=n_f, lam=lam, rate=rate, max_iters=iters, tol=1e-15)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        F1, rep1 = fit_fast_core(R, cfg1, init_m=M0)
+        U1 = f32(F1.user_factors)
+        F1b, _ = fit_fast_core(R, cfg1, init_u=U1, items_first=True)
+        FN, repN = fit_fast_core(R, cfgN, init_m=M0)
+    np.savez_compressed(
+        os.path.join(OUT, f"fast_{name}.npz"),
+        users=users, items=items, vals=vals, n_users=n_users, n_items=n_items, n_f=n_f, lam=lam, rate=rate,
+        iters=iters, M0=M0, U1=F1.user_factors, U1_f32=U1, M1_from_U1=F1b.item_factors,
+        objN=repN.objective_trace, rmseN=repN.rmse_trace, UN=FN.user_factors, MN=FN.item_factors,
+        skipped_users=repN.skipped_users, skipped_items=repN.skipped_items,
+    )
+
+
+def fast_cases():
+    fast_case("small", 5, 200, 150, 0.2, 8, 0.1, 0.3, 4)
+    # sparse slices (empty sketched columns -> fallback), ties, an empty user
+    fast_case("sparse_ties", 6, 300, 120, 0.05, 16, 0.05, 0.1, 3, drop_user=2, ties=True)
+    fast_case("rate1", 7, 60, 50, 0.4, 4, 0.1, 1.0, 3)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["full"]:
         full_case("full", 4, 120, 90, 0.3, 8, 0.1, 4, drop_user=7)
+        sys.exit(0)
+    if sys.argv[1:] == ["fast"]:
+        fast_cases()
         sys.exit(0)
     sketch_cases()
     update_cases()
@@ -213,4 +255,5 @@ if __name__ == "__main__":
     fit_case("rate1", 3, 50, 40, 0.4, 4, 0.1, 1.0, 3)
     # exact ALS (method 'full')
     full_case("full", 4, 120, 90, 0.3, 8, 0.1, 4, drop_user=7)
+    fast_cases()
     print("golden fixtures written to", OUT)

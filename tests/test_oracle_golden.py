@@ -97,6 +97,27 @@ def test_oracle_rate1_matches_reference_full_als():
     np.testing.assert_allclose(M, g["MN"], rtol=1e-7, atol=1e-9)
 
 
+@pytest.mark.parametrize("name", ["small", "sparse_ties", "rate1"])
+def test_oracle_fast_core_matches_reference(name):
+    """Method 'fast_core' (whole-matrix sketch + row-sketched Gram with the
+    empty-column fallback): the oracle reproduces the reference's fixtures."""
+    g = load_golden(f"fast_{name}.npz")
+    n_f, lam, rate = int(g["n_f"]), float(g["lam"]), float(g["rate"])
+    csr, csc = csr_csc(g["users"], g["items"], g["vals"], int(g["n_users"]), int(g["n_items"]))
+    U = np.zeros((int(g["n_users"]), n_f))
+    oracle.fast_half_sweep(*csr, g["M0"], n_f, lam, rate, U)
+    act = np.diff(csr[0]) > 0
+    np.testing.assert_allclose(U[act], g["U1"][act], rtol=1e-8, atol=1e-9)
+    M = g["M0"].astype(np.float64).copy()
+    oracle.fast_half_sweep(*csc, g["U1_f32"], n_f, lam, rate, M)
+    act = np.diff(csc[0]) > 0
+    np.testing.assert_allclose(M[act], g["M1_from_U1"][act], rtol=1e-8, atol=1e-9)
+    U0 = np.zeros((int(g["n_users"]), n_f))
+    U, M, rep = oracle.fit_fast_core(csr, csc, n_f, lam, rate, int(g["iters"]), 1e-15, U0, g["M0"])
+    np.testing.assert_allclose(rep.objective_trace, g["objN"], rtol=1e-9)
+    np.testing.assert_allclose(U, g["UN"], rtol=1e-7, atol=1e-9)
+
+
 def test_multithreaded_oracle_is_deterministic():
     g = load_golden("fit_medium.npz")
     n_f, lam, rate = int(g["n_f"]), float(g["lam"]), float(g["rate"])
