@@ -166,6 +166,32 @@ int cals_predict_entries(const float* U, const float* M, int n_f, int ld_u, int 
                          const int64_t* users, const int64_t* items, int64_t n, double* out,
                          void* stream);
 
+/*
+ * Method 'fast_core' (core.py:255-298): ONE sketch of the whole source per
+ * half-sweep instead of one per regression.
+ *   cals_plan_build_fast: every active row becomes a work-item row (sorted by
+ *     length); budget = n_i for a complete sketch (exact SPD rows), else 0
+ *     (every row solved by LU, _solve_sketched).  rows_host [n_rows],
+ *     tile_ptr_host / cand_ptr_host [n_rows + 1].
+ *   cals_fast_sketch: thr[c] = key of the s-th largest |source[:, c]| (s =
+ *     sketch_budget(n_src, rate), ties to the smaller row; key as thr_keys
+ *     below with the source row as index), and the kept mask
+ *     gmask[j * ceil(n_f/32) + c/32] bit c%32 = (key(j, c) >= thr[c])
+ *     (ces_sketch of the whole matrix, core.py:95-115).
+ *   cals_fast_half_sweep: per row G[c] sums the slice rows kept for column c
+ *     by gmask; a column with none takes the slice's first largest-|x| row
+ *     (gram_rhs_rowsketch, _kernels.py:172-216); G += lam*n_i*I; solve and
+ *     write as cals_core_half_sweep (rss: use cals_residual).
+ */
+int cals_plan_build_fast(const int64_t* counts_host, int64_t n_rows, int n_f, int complete, int32_t* budget_host,
+                         int32_t* rows_host, int64_t* tile_ptr_host, int64_t* cand_ptr_host, cals_plan* meta);
+size_t cals_fast_sketch_workspace_bytes(int n_f);
+int cals_fast_sketch(const float* source, int64_t n_src, int ld_src, int n_f, int64_t s, uint64_t* thr,
+                     uint32_t* gmask, void* ws, size_t ws_bytes, void* stream);
+int cals_fast_half_sweep(const cals_side* side, const cals_plan* plan, const float* source, int64_t n_src, int ld_src,
+                         int n_f, double lam, const uint32_t* gmask, float* target, int ld_tgt, double* pen_rows,
+                         int32_t* row_status, uint64_t* status_summary, void* ws, size_t ws_bytes, void* stream);
+
 /* Optional per-kernel timing with CUDA events recorded on the launch stream
  * (for bench.py's roofline numbers).  collect() synchronises on the recorded
  * events, writes "name launches total_ms" lines into buf, and resets. */

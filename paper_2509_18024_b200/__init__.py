@@ -5,14 +5,14 @@ hand-written sm_100a CUDA kernels behind the C ABI in include/coreals_b200.h.
 """
 
 from .als import FactorPair, FitReport, SolverConfig, init_factors, predict, predict_entries, predict_full
-from .core import SparseSketch, ces_sketch, fit, fit_core, sketch_budget, update_item_core, update_user_core
+from .core import SparseSketch, ces_sketch, fit, fit_core, fit_fast_core, sketch_budget, update_item_core, update_user_core
 from .driver import fit_method
 from .errors import ConfigError, DataError, NumericalError
 from .ratings import RatingMatrix
 
 __all__ = [
     "FactorPair", "FitReport", "SolverConfig", "init_factors", "predict", "predict_entries", "predict_full",
-    "SparseSketch", "ces_sketch", "fit", "fit_core", "sketch_budget", "update_item_core", "update_user_core",
+    "SparseSketch", "ces_sketch", "fit", "fit_core", "fit_fast_core", "sketch_budget", "update_item_core", "update_user_core",
     "fit_method", "ConfigError", "DataError", "NumericalError", "RatingMatrix",
 ]
 

@@ -200,6 +200,28 @@ def fit(R, cfg, *, init_u=None, init_m=None, items_first=False, engine=None):
     return _fit_gpu(R, cfg, 1.0, init_u, init_m, items_first, engine)
 
 
+def fit_fast_core(R, cfg, *, init_u=None, init_m=None, items_first=False, engine=None):
+    """Alternating fit sketching each whole factor matrix once per half-iteration
+    (method 'fast_core', core.py:314-324) on the GPU: per half-sweep one
+    whole-source element sketch (ces_sketch of the full source, core.py:276-286),
+    then every regression's Gram sums the slice rows that sketch kept for each
+    column, an empty column falling back to the slice's first largest-|x| row
+    (gram_rhs_rowsketch, _kernels.py:172-216), solved by LU (or the exact SPD
+    row when the sketch is complete).  ``cfg.diagnostics`` is warned about and
+    ignored, as the reference does (core.py:319-322).
+    """
+    if cfg.method != "fast_core":
+        raise ConfigError(f"fit_fast_core handles method 'fast_core', got {cfg.method!r}")
+    if cfg.diagnostics:
+        warnings.warn("per-regression diagnostics are only instrumented for method 'core'; ignoring the flag",
+                      stacklevel=2)
+        cfg = replace(cfg, diagnostics=False)
+    if engine is None:
+        from .engine import CoreEngine
+        engine = CoreEngine(R, cfg.n_f, cfg.rate, cfg.lam, fast=True)
+    return _fit_gpu(R, cfg, cfg.rate, init_u, init_m, items_first, engine)
+
+
 def _fit_gpu(R, cfg, rate, init_u, init_m, items_first, engine):
     start = time.perf_counter()
     torch = _lib.require_cuda()

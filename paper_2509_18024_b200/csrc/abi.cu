@@ -99,13 +99,13 @@ int big_chunk(int nf) {
     return ch;
 }
 
-size_t big_gram_smem(int nf, int chunk) {
+size_t big_gram_smem(int nf, int chunk, int gwords = 0) {
     const int sx = xs_stride(nf);
     const bool persist = owned_single_round(nf, kThreads / 32);
     const size_t g = persist ? 0 : align16((size_t)nf * (nf + 1) * 4);
     const size_t lists = persist ? 0 : (size_t)nf * chunk * 2 + (size_t)nf * 4;
     return align16((size_t)chunk * sx * 4) + align16((size_t)chunk * 4) + g +
-           align16((size_t)nf * (chunk / 32) * 4 + lists);
+           align16((size_t)nf * (chunk / 32) * 4 + lists + (size_t)chunk * gwords * 4);
 }
 
 size_t big_scan_smem(int nf, int chunk) {
@@ -250,6 +250,8 @@ struct Work {
     double* rss_part;
     int* hist;
     uint32_t* brk;
+    int* fcnt;
+    unsigned long long* famax;
     double* retry;
     float* gbuf;
     int64_t gbuf_rows;
@@ -272,6 +274,8 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
     w.rss_part = c.take<double>((size_t)bb.max_tiles);
     w.hist = c.take<int>((size_t)bb.max_rows * nf * kHB);
     w.brk = c.take<uint32_t>((size_t)std::max<int64_t>(P->n_big, 1) * nf);  // all big rows (one calibration pass)
+    w.fcnt = c.take<int>((size_t)bb.max_rows * nf);                      // fast_core: kept counts (multi-item rows)
+    w.famax = c.take<unsigned long long>((size_t)bb.max_rows * nf);      // fast_core: fallback keys
     w.retry = c.take<double>((size_t)std::max<int64_t>(kMaxGrid, kMaxSolveWarps) * retry_stride(nf));
     w.gbuf_rows = gbuf_rows_for(nf, P->n_small + P->n_big);
     w.gbuf = c.take<float>((size_t)w.gbuf_rows * nf * (nf + 1));
@@ -400,10 +404,73 @@ int launch_small(SweepArgs A, const cals_plan* P, const Work& w, cudaStream_t st
     return cuda_status("small tier");
 }
 
-template <int CPL>
+template <int CPL, bool FAST = false>
 void launch_big_gram(const SweepArgs& A, const BigArgs& B, size_t smem, cudaStream_t st) {
-    allow_smem(big_gram_kernel<CPL>);
-    big_gram_kernel<CPL><<<grid_for(big_gram_kernel<CPL>, smem, B.n_tiles), kThreads, smem, st>>>(A, B);
+    allow_smem(big_gram_kernel<CPL, FAST>);
+    big_gram_kernel<CPL, FAST><<<grid_for(big_gram_kernel<CPL, FAST>, smem, B.n_tiles), kThreads, smem, st>>>(A, B);
+}
+
+// method 'fast_core': every row is a tiled row whose kept bits come from the
+// whole-source mask; no calibration / scan / resolve.
+template <int NFP>
+int launch_fast(const SweepArgs& A, const cals_plan* P, const Work& w, const uint32_t* gmask, int gwords,
+                cudaStream_t st) {
+    const int nf = A.nf;
+    const BigBatches bb = big_batches(P);
+    const int64_t* tp = P->big_tile_ptr_host;
+    for (size_t bi = 0; bi + 1 < bb.r.size(); ++bi) {
+        const int64_t r0 = bb.r[bi], r1 = bb.r[bi + 1];
+        BigArgs B{};
+        B.rows = P->big_rows + r0;
+        B.tile_ptr = P->big_tile_ptr + r0;
+        B.cand_ptr = P->big_cand_ptr + r0;
+        B.n_big = r1 - r0;
+        B.tile_base = tp ? tp[r0] : 0;
+        B.n_tiles = tp ? tp[r1] - tp[r0] : P->n_big_tiles;
+        B.item_rows = P->item_rows;
+        B.chunk = big_chunk(nf);
+        B.part = w.part;
+        B.rss_part = w.rss_part;
+        B.tile_row = P->big_tile_row;
+        B.row_base = r0;
+        B.gmask = gmask;
+        B.gwords = gwords;
+        B.fcnt = w.fcnt;
+        B.famax = w.famax;
+        int64_t n_multi = 0;
+        if (tp)
+            while (n_multi < B.n_big && tp[r0 + n_multi + 1] - tp[r0 + n_multi] >= 2) ++n_multi;
+        B.n_multi = tp ? n_multi : B.n_big;
+        if (B.n_multi > 0) {
+            cudaMemsetAsync(w.fcnt, 0, sizeof(int) * (size_t)B.n_multi * nf, st);
+            cudaMemsetAsync(w.famax, 0, sizeof(unsigned long long) * (size_t)B.n_multi * nf, st);
+        }
+        const size_t gram_smem = big_gram_smem(nf, B.chunk, gwords);
+        {
+            ProfScope ps("fast_gram_kernel", st);
+            const int nq = xs_chunks(nf);
+            if (nq <= 4) launch_big_gram<1, true>(A, B, gram_smem, st);
+            else if (nq <= 8) launch_big_gram<2, true>(A, B, gram_smem, st);
+            else if (nq <= 16) launch_big_gram<4, true>(A, B, gram_smem, st);
+            else launch_big_gram<8, true>(A, B, gram_smem, st);
+        }
+        if (B.n_big > w.gbuf_rows) return CALS_ERR_WORKSPACE;
+        if (B.n_multi > 0) {
+            {
+                ProfScope ps("big_reduce_kernel", st);
+                big_reduce_kernel<<<(int)std::min<int64_t>(B.n_multi, (int64_t)dev().sms * 8), kThreads, 0, st>>>(
+                    A, B, 0, B.n_multi);
+            }
+            const int64_t warps = B.n_multi * nf;
+            ProfScope ps("fast_fix_kernel", st);
+            fast_fix_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)dev().sms * 8)),
+                              kThreads, 0, st>>>(A, B);
+        }
+        launch_solve<NFP>(A, B.rows, B.n_big, st);
+        const int rc = cuda_status("fast_core kernels");
+        if (rc) return rc;
+    }
+    return CALS_OK;
 }
 
 template <int NFP>
@@ -646,6 +713,104 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
         else rc = launch_big<0>(A, P, w, st);
     }
     return rc;
+}
+
+int cals_plan_build_fast(const int64_t* counts, int64_t n_rows, int n_f, int complete, int32_t* budget,
+                         int32_t* rows, int64_t* tile_ptr, int64_t* cand_ptr, cals_plan* meta) {
+    if (!counts || !budget || !rows || !tile_ptr || !cand_ptr || !meta) return CALS_ERR_ARG;
+    if (n_f < 1 || n_f > CALS_MAX_NF || n_rows < 0 || n_rows > 0x7fffffff) return CALS_ERR_ARG;
+    std::memset(meta, 0, sizeof(*meta));
+    meta->n_f = n_f;
+    std::vector<int32_t> act;
+    for (int64_t i = 0; i < n_rows; ++i) {
+        if (counts[i] > 0x7fffffffLL) return CALS_ERR_UNSUPPORTED;
+        // the solve takes the exact SPD row only for a complete whole-source sketch
+        budget[i] = complete ? (int32_t)counts[i] : 0;
+        if (counts[i] > 0) act.push_back((int32_t)i);
+    }
+    std::stable_sort(act.begin(), act.end(),
+                     [counts](int32_t a, int32_t b) { return counts[a] != counts[b] ? counts[a] > counts[b] : a < b; });
+    std::copy(act.begin(), act.end(), rows);
+    meta->n_big = (int64_t)act.size();
+    meta->item_rows = std::max(kItemRowsMin, big_chunk(n_f));
+    tile_ptr[0] = 0;
+    cand_ptr[0] = 0;
+    for (size_t r = 0; r < act.size(); ++r) {
+        tile_ptr[r + 1] = tile_ptr[r] + (counts[act[r]] + meta->item_rows - 1) / meta->item_rows;
+        cand_ptr[r + 1] = 0;
+    }
+    meta->n_big_tiles = tile_ptr[act.size()];
+    return CALS_OK;
+}
+
+size_t cals_fast_sketch_workspace_bytes(int n_f) {
+    return (size_t)n_f * (2 * sizeof(unsigned long long) + 256 * sizeof(unsigned int)) + 256;
+}
+
+int cals_fast_sketch(const float* source, int64_t n_src, int ld_src, int n_f, int64_t s, uint64_t* thr,
+                     uint32_t* gmask, void* ws, size_t ws_bytes, void* stream) {
+    if (!source || !thr || !gmask || n_f < 1 || n_f > CALS_MAX_NF || ld_src < n_f || n_src < 1 || s < 1 ||
+        s > n_src || n_src > 0xFFFFFFFFLL)
+        return CALS_ERR_ARG;
+    if (!ws || ws_bytes < cals_fast_sketch_workspace_bytes(n_f)) return CALS_ERR_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long* prefix = reinterpret_cast<unsigned long long*>(thr);
+    unsigned long long* above = reinterpret_cast<unsigned long long*>(ws);
+    unsigned int* hist = reinterpret_cast<unsigned int*>(above + n_f);
+    cudaMemsetAsync(prefix, 0, sizeof(unsigned long long) * n_f, st);
+    cudaMemsetAsync(above, 0, sizeof(unsigned long long) * n_f, st);
+    cudaMemsetAsync(hist, 0, sizeof(unsigned int) * 256 * n_f, st);
+    const int gwords = (n_f + 31) / 32;
+    const dim3 hgrid((unsigned)std::min<int64_t>((n_src + 7) / 8, (int64_t)dev().sms * 4), (unsigned)gwords);
+    ProfScope ps("fast_sketch_kernels", st);
+    for (int pass = 0; pass < 8; ++pass) {
+        fast_hist_kernel<<<hgrid, 256, 0, st>>>(source, n_src, ld_src, n_f, pass, prefix, hist);
+        fast_pick_kernel<<<(n_f + 7) / 8, 256, 0, st>>>(n_f, s, pass, prefix, above, hist);
+    }
+    fast_mask_kernel<<<(int)std::min<int64_t>((n_src * gwords + 255) / 256, (int64_t)dev().sms * 16), 256, 0, st>>>(
+        source, n_src, ld_src, n_f, prefix, gwords, gmask);
+    return cuda_status("cals_fast_sketch");
+}
+
+int cals_fast_half_sweep(const cals_side* side, const cals_plan* P, const float* source, int64_t n_src, int ld_src,
+                         int n_f, double lam, const uint32_t* gmask, float* target, int ld_tgt, double* pen_rows,
+                         int32_t* row_status, uint64_t* status_summary, void* ws, size_t ws_bytes, void* stream) {
+    if (!side || !P || !source || !target || !row_status || !gmask) return CALS_ERR_ARG;
+    if (n_f < 1 || n_f > CALS_MAX_NF || n_f != P->n_f || ld_src < 4 * xs_chunks(n_f) || (ld_src & 3) || ld_tgt < n_f ||
+        lam < 0 || ((uintptr_t)source & 15) || P->n_small != 0)
+        return CALS_ERR_ARG;
+    if (P->n_big && (!P->big_rows || !P->big_tile_ptr || !P->big_cand_ptr || !P->budget)) return CALS_ERR_ARG;
+    size_t need = 0;
+    Work w = carve(P, ws, &need);
+    if (ws_bytes < need || (!ws && need > 256)) return CALS_ERR_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    (void)dev();
+    if (status_summary) cudaMemsetAsync(status_summary, 0, sizeof(uint64_t), st);
+    SweepArgs A{};
+    A.ptr = side->ptr;
+    A.idx = side->idx;
+    A.val = side->val;
+    A.budget = P->budget;
+    A.src = source;
+    A.n_src = n_src;
+    A.ld_src = ld_src;
+    A.nf = n_f;
+    A.tgt = target;
+    A.ld_tgt = ld_tgt;
+    A.lam = lam;
+    A.pen_rows = pen_rows;
+    A.gbuf = w.gbuf;
+    A.stats = g_stats;
+    A.status = row_status;
+    A.summary = reinterpret_cast<unsigned long long*>(status_summary);
+    A.retry_ws = w.retry;
+    A.retry_stride = retry_stride(n_f);
+    if (P->n_big == 0) return CALS_OK;
+    const int gwords = (n_f + 31) / 32;
+    if (n_f <= 8) return launch_fast<8>(A, P, w, gmask, gwords, st);
+    if (n_f <= 16) return launch_fast<16>(A, P, w, gmask, gwords, st);
+    if (n_f <= 32) return launch_fast<32>(A, P, w, gmask, gwords, st);
+    return launch_fast<0>(A, P, w, gmask, gwords, st);
 }
 
 int cals_residual(const cals_side* side, const float* source, int ld_src, int n_f, const float* rows_w, int ld_w,

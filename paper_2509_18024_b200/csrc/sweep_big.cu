@@ -326,10 +326,12 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
 // their sparse Gram rows -- in registers across the item's chunks when the
 // warp's columns fit one lane-group round (nf <= 64), else in shared memory;
 // the item's partial goes to global.
-template <int CPL>
+template <int CPL, bool FAST>
 __global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(SweepArgs A, BigArgs B) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t s_thr[CALS_MAX_NF_DEV];
+    __shared__ unsigned long long s_amax[FAST ? CALS_MAX_NF_DEV : 1];
+    __shared__ int s_cnt[FAST ? CALS_MAX_NF_DEV : 1];
     __shared__ float wold[CALS_MAX_NF_DEV];
     __shared__ double red[32];
     const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
@@ -345,6 +347,8 @@ __global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(Sw
     const uint32_t s_bits = smem_u32(after_g);                       // [nf][nw] kept-row bitmap words
     const uint32_t s_lists = s_bits + 4u * (uint32_t)(nf * nw);      // [nf][CH] u16 (!persist only)
     const uint32_t s_lens = s_lists + 2u * (uint32_t)(nf * CH);      // [nf] u32 (!persist only)
+    // FAST: staged global-sketch mask words of the chunk's rows, [CH][gwords]
+    const uint32_t s_gm = persist ? s_bits + 4u * (uint32_t)(nf * nw) : s_lens + 4u * (uint32_t)nf;
     const uint32_t rowb = 4u * (uint32_t)sx;
     const FastDiv fq((uint32_t)xs_chunks(nf));
     const int my_cols = warp < nf ? (nf - 1 - warp) / nwarps + 1 : 0;
@@ -362,8 +366,12 @@ __global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(Sw
         const int kend = min(n, kbeg + B.item_rows);
         __syncthreads();
         if (tid < nf) {
-            s_thr[tid] = B.thr[(size_t)r * nf + tid];
+            if (!FAST) s_thr[tid] = B.thr[(size_t)r * nf + tid];
             if (A.tgt_old != nullptr) wold[tid] = A.tgt_old[(int64_t)row * A.ld_old + tid];
+            if (FAST) {
+                s_cnt[tid] = 0;
+                s_amax[tid] = 0ull;
+            }
         }
         S.zero();
         double racc = 0.0;
@@ -371,6 +379,13 @@ __global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(Sw
             const int kn = min(CH, kend - k0);
             __syncthreads();
             stage_slice(A, lo, k0, kn, Xs, ys, fq);
+            if (FAST && !full) {
+                for (int e = tid; e < kn * B.gwords; e += nt) {
+                    const int k = e / B.gwords, wi = e - k * B.gwords;
+                    sts_u32(s_gm + 4u * (uint32_t)e,
+                            __ldg(B.gmask + (int64_t)__ldg(A.idx + lo + k0 + k) * B.gwords + wi));
+                }
+            }
             __syncthreads();
             if (A.rss_rows != nullptr) {
                 for (int k = tid; k < kn; k += nt) {
@@ -388,15 +403,30 @@ __global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(Sw
                 const int nwk = (kn + 31) >> 5;
                 for (int e = tid; e < nf * nwk; e += nt) {
                     const int wd = e / nf, c = e - wd * nf;
-                    const uint64_t T = s_thr[c];
-                    const uint32_t Ta = (uint32_t)(T >> 32), Tk = 0xFFFFFFFFu - (uint32_t)T;
                     const int kb = 32 * wd, ke = min(kn, kb + 32);
                     uint32_t addr = s_xs + (uint32_t)kb * rowb + 4u * (uint32_t)c;
                     uint32_t word = 0u;
-                    for (int k = kb; k < ke; ++k, addr += rowb) {
-                        const uint32_t a = abs_bits(lds_f32(addr));
-                        const bool keep = a > Ta || (a == Ta && (uint32_t)(k0 + k) <= Tk);
-                        word |= (uint32_t)keep << (k - kb);
+                    if (FAST) {
+                        // kept bits from the whole-source sketch; the column's largest key
+                        // (first largest |x|) is the fallback row of an empty column
+                        unsigned long long kmax = 0ull;
+                        const uint32_t gm = s_gm + 4u * (uint32_t)(c >> 5), gsh = (uint32_t)(c & 31);
+                        for (int k = kb; k < ke; ++k, addr += rowb) {
+                            const uint32_t a = abs_bits(lds_f32(addr));
+                            const unsigned long long kk = ((unsigned long long)a << 32) | (0xFFFFFFFFu - (uint32_t)(k0 + k));
+                            kmax = kk > kmax ? kk : kmax;
+                            word |= ((lds_u32(gm + 4u * (uint32_t)(k * B.gwords)) >> gsh) & 1u) << (k - kb);
+                        }
+                        atomicMax(&s_amax[c], kmax);
+                        if (word) atomicAdd(&s_cnt[c], __popc(word));
+                    } else {
+                        const uint64_t T = s_thr[c];
+                        const uint32_t Ta = (uint32_t)(T >> 32), Tk = 0xFFFFFFFFu - (uint32_t)T;
+                        for (int k = kb; k < ke; ++k, addr += rowb) {
+                            const uint32_t a = abs_bits(lds_f32(addr));
+                            const bool keep = a > Ta || (a == Ta && (uint32_t)(k0 + k) <= Tk);
+                            word |= (uint32_t)keep << (k - kb);
+                        }
                     }
                     sts_u32(s_bits + 4u * (uint32_t)(c * nw + wd), word);
                 }
@@ -445,13 +475,144 @@ __global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(Sw
                 else B.rss_part[t] = racc;
             }
         }
+        if (FAST && !full) {
+            __syncthreads();  // flushed rows (global) and the column counts are complete
+            if (direct) {
+                // empty sketched columns: the first largest-|x| slice row alone (_kernels.py:196-211)
+                for (int c = warp; c < nf; c += nwarps) {
+                    if (s_cnt[c] != 0) continue;
+                    const int k = (int)(0xFFFFFFFFu - (uint32_t)s_amax[c]);
+                    const float* xr = A.src + (int64_t)__ldg(A.idx + lo + k) * A.ld_src;
+                    const float v = __ldg(xr + c);
+                    float* grow = out + (size_t)c * gs;
+                    for (int f = lane; f < nf; f += 32) grow[f] = fmaf(v, __ldg(xr + f), grow[f]);
+                    if (lane == 0) grow[nf] = fmaf(v, __ldg(A.val + lo + k), grow[nf]);
+                }
+            } else if (tid < nf) {
+                atomicAdd(&B.fcnt[(size_t)r * nf + tid], s_cnt[tid]);
+                atomicMax(&B.famax[(size_t)r * nf + tid], s_amax[tid]);
+            }
+        }
     }
 }
 
-template __global__ void big_gram_kernel<1>(SweepArgs, BigArgs);
-template __global__ void big_gram_kernel<2>(SweepArgs, BigArgs);
-template __global__ void big_gram_kernel<4>(SweepArgs, BigArgs);
-template __global__ void big_gram_kernel<8>(SweepArgs, BigArgs);
+// fast_core, multi-item rows [0, n_multi): the empty-column fallback on the
+// reduced normal equations (gbuf slot r), warp per (row, column).
+__global__ void __launch_bounds__(kThreads) fast_fix_kernel(SweepArgs A, BigArgs B) {
+    const int nf = A.nf, gs = nf + 1;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w = gw; w < B.n_multi * nf; w += wstride) {
+        const int r = (int)(w / nf), c = (int)(w % nf);
+        if (B.fcnt[(size_t)r * nf + c] != 0) continue;
+        const int row = B.rows[r];
+        const int64_t lo = A.ptr[row];
+        const int k = (int)(0xFFFFFFFFu - (uint32_t)B.famax[(size_t)r * nf + c]);
+        const float* xr = A.src + (int64_t)__ldg(A.idx + lo + k) * A.ld_src;
+        const float v = __ldg(xr + c);
+        float* grow = A.gbuf + (size_t)r * nf * gs + (size_t)c * gs;
+        for (int f = lane; f < nf; f += 32) grow[f] = fmaf(v, __ldg(xr + f), grow[f]);
+        if (lane == 0) grow[nf] = fmaf(v, __ldg(A.val + lo + k), grow[nf]);
+    }
+}
+
+// ---- whole-source sketch (method 'fast_core', core.py:276-286) ---------------
+// Per column the s-th largest key (abs_bits << 32 | ~row) of the source by an
+// 8-pass MSD radix select (8 bits per pass): histogram of the undecided byte of
+// the keys that match the decided prefix, then one warp per column picks the
+// byte holding rank s.  Columns in groups of 32 per block (32 x 256 counters).
+__global__ void __launch_bounds__(256) fast_hist_kernel(const float* __restrict__ src, int64_t n_src, int ld, int nf,
+                                                       int pass, const unsigned long long* __restrict__ prefix,
+                                                       unsigned int* __restrict__ hist) {
+    __shared__ unsigned int h[32 * 256];
+    __shared__ unsigned long long pre[32];
+    const int c0 = blockIdx.y * 32, gc = min(32, nf - c0);
+    const int sh = 56 - 8 * pass;
+    for (int e = threadIdx.x; e < 32 * 256; e += blockDim.x) h[e] = 0u;
+    if (threadIdx.x < gc) pre[threadIdx.x] = prefix[c0 + threadIdx.x];
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    if (lane < gc) {
+        const unsigned long long p = pre[lane];
+        for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < n_src;
+             j += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+            const unsigned long long key =
+                ((unsigned long long)abs_bits(__ldg(src + j * ld + c0 + lane)) << 32) | (0xFFFFFFFFu - (uint32_t)j);
+            if (pass == 0 || (key >> (sh + 8)) == (p >> (sh + 8)))
+                atomicAdd(&h[lane * 256 + (int)((key >> sh) & 255u)], 1u);
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < gc * 256; e += blockDim.x)
+        if (h[e]) atomicAdd(&hist[(size_t)c0 * 256 + e], h[e]);
+}
+
+__global__ void __launch_bounds__(256) fast_pick_kernel(int nf, int64_t s, int pass, unsigned long long* prefix,
+                                                       unsigned long long* above, unsigned int* hist) {
+    const int lane = threadIdx.x & 31;
+    const int c = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (c >= nf) return;
+    const int sh = 56 - 8 * pass;
+    unsigned int* hc = hist + (size_t)c * 256;
+    unsigned long long ab = above[c];
+    // bins from the top: lane l owns bins 255 - 8l .. 248 - 8l
+    unsigned long long part = 0;
+    unsigned int cnt[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        cnt[i] = hc[255 - 8 * lane - i];
+        part += cnt[i];
+    }
+    unsigned long long incl = part;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    const unsigned long long before = incl - part;  // keys in higher bins (this pass)
+    const bool here = ab + before < (unsigned long long)s && (unsigned long long)s <= ab + incl;
+    const uint32_t who = __ballot_sync(0xffffffffu, here);
+    if (who && lane == __ffs(who) - 1) {
+        unsigned long long acc = ab + before;
+        int bin = 255 - 8 * lane;
+        for (int i = 0; i < 8; ++i) {
+            if (acc + cnt[i] >= (unsigned long long)s) { bin = 255 - 8 * lane - i; break; }
+            acc += cnt[i];
+        }
+        prefix[c] |= (unsigned long long)bin << sh;
+        above[c] = acc;
+    }
+    __syncwarp();
+    for (int i = lane; i < 256; i += 32) hc[i] = 0u;
+}
+
+__global__ void __launch_bounds__(256) fast_mask_kernel(const float* __restrict__ src, int64_t n_src, int ld, int nf,
+                                                       const unsigned long long* __restrict__ thr, int gwords,
+                                                       uint32_t* __restrict__ gmask) {
+    const int64_t total = n_src * gwords;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e / gwords;
+        const int wi = (int)(e - j * gwords);
+        uint32_t word = 0u;
+        const int cb = 32 * wi, ce = min(nf, cb + 32);
+        for (int c = cb; c < ce; ++c) {
+            const unsigned long long key =
+                ((unsigned long long)abs_bits(__ldg(src + j * ld + c)) << 32) | (0xFFFFFFFFu - (uint32_t)j);
+            word |= (key >= __ldg(thr + c) ? 1u : 0u) << (c - cb);
+        }
+        gmask[e] = word;
+    }
+}
+
+template __global__ void big_gram_kernel<1, false>(SweepArgs, BigArgs);
+template __global__ void big_gram_kernel<2, false>(SweepArgs, BigArgs);
+template __global__ void big_gram_kernel<4, false>(SweepArgs, BigArgs);
+template __global__ void big_gram_kernel<8, false>(SweepArgs, BigArgs);
+template __global__ void big_gram_kernel<1, true>(SweepArgs, BigArgs);
+template __global__ void big_gram_kernel<2, true>(SweepArgs, BigArgs);
+template __global__ void big_gram_kernel<4, true>(SweepArgs, BigArgs);
+template __global__ void big_gram_kernel<8, true>(SweepArgs, BigArgs);
 
 // Big rows [r0, r0 + count): fixed-order float64 sum of the item partials,
 // + lam*n*I on the diagonal -> A.gbuf slot (r - r0); residual partial sums.

@@ -75,6 +75,12 @@ struct BigArgs {
     const uint32_t* brk;      // [n_big][nf] calibrated levels jhi | jlo << 16, or ~0u (use the table margin)
     const int32_t* tile_row;  // nullable: absolute big row of each absolute work item
     int64_t row_base;         // absolute index of the batch's first big row
+    // method 'fast_core' (big_gram_kernel<CPL, true>): kept bits come from one sketch of
+    // the whole source instead of per-row thresholds
+    const uint32_t* gmask;    // [n_src][gwords] bit c%32 of word c/32: source row kept for column c
+    int gwords;
+    int* fcnt;                // [n_big][nf] kept slice rows per column (multi-item rows)
+    unsigned long long* famax;  // [n_big][nf] max key (abs_bits << 32 | ~k) per column (fallback row)
 };
 
 constexpr int kHB = 32;  // sub-buckets of a big row's bracket (linear in abs-bit space)

@@ -33,11 +33,17 @@ from .errors import ConfigError
 __all__ = ["DeviceSide", "CoreEngine", "IterationTerms"]
 
 
+def _budget(n, rate):
+    """sketch_budget (core.py:48-54) for one count."""
+    s = int(np.floor(np.float64(n) * np.float64(rate) + 1e-9))
+    return max(1, min(s, int(n)))
+
+
 class DeviceSide:
     """One side of the rating matrix (CSR over users or CSC over items) on the
     device, with its static schedule (budgets, tiers) and workspace."""
 
-    def __init__(self, ptr, idx, val, n_src, n_f, rate, device, row_begin=0, row_end=None):
+    def __init__(self, ptr, idx, val, n_src, n_f, rate, device, row_begin=0, row_end=None, fast=False):
         torch = _lib.require_cuda()
         L = _lib.load()
         ptr_dev = ptr if torch.is_tensor(ptr) else None
@@ -62,10 +68,20 @@ class DeviceSide:
         tile_ptr = np.zeros(n_rows + 1, np.int64)
         cand_ptr = np.zeros(n_rows + 1, np.int64)
         meta = _lib.cals_plan()
-        rc = L.cals_plan_build(sched.ctypes.data, n_rows, self.n_f, float(rate), budget.ctypes.data,
-                               small.ctypes.data, big.ctypes.data, tile_ptr.ctypes.data, cand_ptr.ctypes.data,
-                               ctypes.byref(meta))
-        _lib.check(rc, "cals_plan_build")
+        self.fast = bool(fast)
+        if self.fast:
+            # method 'fast_core': one whole-source sketch per half-sweep; every row a work-item row
+            self.fast_s = _budget(self.n_src, rate)
+            complete = int(self.fast_s >= self.n_src)
+            rc = L.cals_plan_build_fast(sched.ctypes.data, n_rows, self.n_f, complete, budget.ctypes.data,
+                                        big.ctypes.data, tile_ptr.ctypes.data, cand_ptr.ctypes.data,
+                                        ctypes.byref(meta))
+            _lib.check(rc, "cals_plan_build_fast")
+        else:
+            rc = L.cals_plan_build(sched.ctypes.data, n_rows, self.n_f, float(rate), budget.ctypes.data,
+                                   small.ctypes.data, big.ctypes.data, tile_ptr.ctypes.data, cand_ptr.ctypes.data,
+                                   ctypes.byref(meta))
+            _lib.check(rc, "cals_plan_build")
         self.budget_host = budget
         self.small_host = small[:meta.n_small].copy()
         self.big_host = big[:meta.n_big].copy()
@@ -107,12 +123,31 @@ class DeviceSide:
         self.pen_rows = torch.zeros(n_rows, dtype=torch.float64, device=device)
         self.summary = torch.zeros(1, dtype=torch.int64, device=device)
         self.nnz = nnz
+        if self.fast:
+            self.gwords = (self.n_f + 31) // 32
+            self.fast_thr = torch.zeros(self.n_f, dtype=torch.int64, device=device)
+            self.gmask = torch.zeros(max(self.n_src, 1) * self.gwords, dtype=torch.int32, device=device)
+            self.fast_ws = torch.empty(int(L.cals_fast_sketch_workspace_bytes(self.n_f)), dtype=torch.uint8,
+                                       device=device)
 
     def half_sweep(self, source, target, target_old=None, want_rss=False, thr_keys=None, lam=0.0, stream=None):
         torch = _lib.require_cuda()
         if stream is None:
             stream = torch.cuda.current_stream(self.device).cuda_stream
         L = _lib.load()
+        if self.fast:
+            if want_rss:  # residual of the previous rows before they are replaced
+                self.residual(source, target_old, stream)
+            if self.plan.n_big:
+                _lib.check(L.cals_fast_sketch(source.data_ptr(), self.n_src, source.stride(0), self.n_f, self.fast_s,
+                                              self.fast_thr.data_ptr(), self.gmask.data_ptr(), self.fast_ws.data_ptr(),
+                                              self.fast_ws.numel(), stream), "cals_fast_sketch")
+            _lib.check(L.cals_fast_half_sweep(
+                ctypes.byref(self.side), ctypes.byref(self.plan), source.data_ptr(), source.shape[0], source.stride(0),
+                self.n_f, float(lam), self.gmask.data_ptr(), target.data_ptr(), target.stride(0),
+                self.pen_rows.data_ptr(), self.status.data_ptr(), self.summary.data_ptr(), self.ws.data_ptr(),
+                self.ws.numel(), stream), "cals_fast_half_sweep")
+            return
         rc = L.cals_core_half_sweep(
             ctypes.byref(self.side), ctypes.byref(self.plan), source.data_ptr(), source.shape[0],
             source.stride(0), self.n_f, float(lam), target.data_ptr(), target.stride(0),
@@ -166,7 +201,7 @@ class CoreEngine:
         eng.finish(first); terms = eng.terms(max_iters - 1)
     """
 
-    def __init__(self, R, n_f, rate, lam, device=None, user_range=None, item_range=None):
+    def __init__(self, R, n_f, rate, lam, device=None, user_range=None, item_range=None, fast=False):
         torch = _lib.require_cuda()
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
@@ -180,8 +215,8 @@ class CoreEngine:
         # each side (plan + uploads) is built on first use, so the second side's
         # host->device copies overlap the first half-sweep already on the GPU
         self._side_args = {
-            "user": (R.row_ptr, R.row_items, R.row_vals, self.n_items, n_f, rate, device, *ur),
-            "item": (R.col_ptr, R.col_users, R.col_vals, self.n_users, n_f, rate, device, *ir),
+            "user": (R.row_ptr, R.row_items, R.row_vals, self.n_items, n_f, rate, device, *ur, fast),
+            "item": (R.col_ptr, R.col_users, R.col_vals, self.n_users, n_f, rate, device, *ir, fast),
         }
         self._sides = {}
         # factor rows padded to a multiple of 4 floats (16-byte gathers); padding stays zero

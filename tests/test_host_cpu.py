@@ -117,7 +117,7 @@ def test_rating_matrix_layout_matches_reference_index():
 def test_driver_dispatch_scope():
     g = load_golden("fit_rate1.npz")
     R = cb.RatingMatrix(g["users"], g["items"], g["vals"])
-    for m in ("fast_core", "unif", "blev"):  # outside this package: the reference keeps serving them
+    for m in ("unif", "blev"):  # outside this package: the reference keeps serving them
         with pytest.raises(cb.ConfigError):
             cb.fit_method(R, cb.SolverConfig(method=m))
     with pytest.raises(cb.ConfigError):
@@ -125,7 +125,9 @@ def test_driver_dispatch_scope():
     with pytest.raises(cb.ConfigError):
         cb.fit(R, cb.SolverConfig(method="core", rate=0.5))
     from paper_2509_18024_b200 import driver
-    assert driver._DISPATCH == {"core": cb.fit_core, "full": cb.fit}
+    assert driver._DISPATCH == {"core": cb.fit_core, "full": cb.fit, "fast_core": cb.fit_fast_core}
+    with pytest.raises(cb.ConfigError):
+        cb.fit_fast_core(R, cb.SolverConfig(method="core", rate=0.5))
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
