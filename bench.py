@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
+    ap.add_argument("--method", default="core", choices=["core", "full", "fast_core"],
+                    help="estimator (core = the BASELINE metric; full / fast_core for comparison lines)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
@@ -248,8 +250,9 @@ def main():
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
     M0 = synth.init_m(data.n_items, n_f)
-    eng = (ShardedEngine(data, n_f, rate, lam, rank, world, device=dev) if world > 1
-           else CoreEngine(data, n_f, rate, lam, device=dev))
+    eff_rate = 1.0 if args.method == "full" else rate  # full ALS = complete budgets on every row
+    eng = (ShardedEngine(data, n_f, eff_rate, lam, rank, world, device=dev, fast=args.method == "fast_core")
+           if world > 1 else CoreEngine(data, n_f, eff_rate, lam, device=dev, fast=args.method == "fast_core"))
     eng.set_factors(np.zeros((data.n_users, n_f), np.float32), M0)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
@@ -288,7 +291,7 @@ def main():
 
     e2e_line = None
     if not args.no_e2e:
-        e2e_line = e2e(data, spec, M0, args.steps, rank, world)
+        e2e_line = e2e(data, spec, M0, args.steps, rank, world, args.method)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -300,7 +303,7 @@ def main():
     sb_u, bb_u = tier_bytes(core.user, n_f)
     sb_i, bb_i = tier_bytes(core.item, n_f)
     kbytes = {"small_gram_kernel": (sb_u + sb_i) * args.steps, "big_gram_kernel": (bb_u + bb_i) * args.steps,
-              "big_scan_kernel": (bb_u + bb_i) * args.steps}
+              "big_scan_kernel": (bb_u + bb_i) * args.steps, "fast_gram_kernel": (bb_u + bb_i) * args.steps}
     dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (0, 0.0))
     dom_name, (dom_cnt, dom_ms) = dom
     dom_bytes = kbytes.get(dom_name)
@@ -317,7 +320,8 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-        "config": {"workload": args.config, "nnz": nnz, "n_users": data.n_users, "n_items": data.n_items,
+        "config": {"workload": args.config, "method": args.method, "nnz": nnz, "n_users": data.n_users,
+                   "n_items": data.n_items,
                    "n_f": n_f, "lam": lam, "rate": rate, "parallelism": f"row-shard x{world}",
                    "l2": "512 MiB flush before every timed step (outside its events)",
                    "init": "M0 ~ N(0, 0.1^2) numpy seed 0, fp32; U0 = 0"},
@@ -349,7 +353,7 @@ def main():
     print(json.dumps(line), flush=True)
 
 
-def e2e(data, spec, M0, steps, rank=0, world=1):
+def e2e(data, spec, M0, steps, rank=0, world=1, method="core"):
     """fit_core through the public API from host (numpy) arrays: H2D of both
     indexes and the init, `steps` iterations, D2H of both factor matrices.
     With N > 1 ranks every rank runs fit_core on its row shard (ShardedEngine,
@@ -363,24 +367,25 @@ def e2e(data, spec, M0, steps, rank=0, world=1):
     from paper_2509_18024_b200.shard import ShardedEngine
 
     R = data.rating_matrix()
-    cfg = cb.SolverConfig(method="core", n_f=spec["n_f"], lam=spec["lam"], rate=spec["rate"], max_iters=steps,
-                          tol=1e-15)
+    rate = 1.0 if method == "full" else spec["rate"]
+    cfg = cb.SolverConfig(method=method, n_f=spec["n_f"], lam=spec["lam"], rate=rate, max_iters=steps, tol=1e-15)
+    cfg1 = cb.SolverConfig(method=method, n_f=spec["n_f"], lam=spec["lam"], rate=rate, max_iters=1, tol=1e-15)
+    fit = {"core": cb.fit_core, "full": cb.fit, "fast_core": cb.fit_fast_core}[method]
     dev = torch.device("cuda", torch.cuda.current_device())
 
     def engine():
         if world == 1:
-            return None  # fit_core builds its own CoreEngine
-        return ShardedEngine(R, spec["n_f"], spec["rate"], spec["lam"], rank, world, device=dev)
+            return None  # the fit builds its own engine
+        return ShardedEngine(R, spec["n_f"], rate, spec["lam"], rank, world, device=dev, fast=method == "fast_core")
 
     with warnings.catch_warnings():
         warnings.simplefilter("ignore")
-        cb.fit_core(R, cb.SolverConfig(method="core", n_f=spec["n_f"], lam=spec["lam"], rate=spec["rate"],
-                                       max_iters=1, tol=1e-15), init_m=M0, engine=engine())  # warm
+        fit(R, cfg1, init_m=M0, engine=engine())  # warm
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        F, rep = cb.fit_core(R, cfg, init_m=M0, engine=engine())  # sides (and their H2D) built inside
+        F, rep = fit(R, cfg, init_m=M0, engine=engine())  # sides (and their H2D) built inside
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
     if world > 1:
@@ -396,7 +401,7 @@ def e2e(data, spec, M0, steps, rank=0, world=1):
     d2h = ((R.n_users + R.n_items) * n_f * 8 + rep.iters_run * 5 * 8) * world
     return {"value": nnz * rep.iters_run / wall, "unit": UNIT, "h2d_bytes_per_step": h2d / rep.iters_run,
             "d2h_bytes_per_step": d2h / rep.iters_run, "wall_s": wall, "iters": rep.iters_run,
-            "how": "paper_2509_18024_b200.fit_core(RatingMatrix of numpy arrays) incl. plan, H2D (pageable; the "
+            "how": f"paper_2509_18024_b200.{fit.__name__}(RatingMatrix of numpy arrays) incl. plan, H2D (pageable; the "
                    "item side's copies overlap the first user half-sweep), all iterations, D2H of float64 "
                    "factors; per-step bytes amortised over the fit" + (
                        f"; {world} ranks, ShardedEngine, max wall over ranks" if world > 1 else "")}

@@ -181,7 +181,8 @@ int cals_predict_entries(const float* U, const float* M, int n_f, int ld_u, int 
  *   cals_fast_half_sweep: per row G[c] sums the slice rows kept for column c
  *     by gmask; a column with none takes the slice's first largest-|x| row
  *     (gram_rhs_rowsketch, _kernels.py:172-216); G += lam*n_i*I; solve and
- *     write as cals_core_half_sweep (rss: use cals_residual).
+ *     write as cals_core_half_sweep (rss_rows / target_old: the fused residual
+ *     of the previous rows, as there).
  */
 int cals_plan_build_fast(const int64_t* counts_host, int64_t n_rows, int n_f, int complete, int32_t* budget_host,
                          int32_t* rows_host, int64_t* tile_ptr_host, int64_t* cand_ptr_host, cals_plan* meta);
@@ -189,7 +190,8 @@ size_t cals_fast_sketch_workspace_bytes(int n_f);
 int cals_fast_sketch(const float* source, int64_t n_src, int ld_src, int n_f, int64_t s, uint64_t* thr,
                      uint32_t* gmask, void* ws, size_t ws_bytes, void* stream);
 int cals_fast_half_sweep(const cals_side* side, const cals_plan* plan, const float* source, int64_t n_src, int ld_src,
-                         int n_f, double lam, const uint32_t* gmask, float* target, int ld_tgt, double* pen_rows,
+                         int n_f, double lam, const uint32_t* gmask, float* target, int ld_tgt,
+                         const float* target_old, int ld_old, double* rss_rows, double* pen_rows,
                          int32_t* row_status, uint64_t* status_summary, void* ws, size_t ws_bytes, void* stream);
 
 /* Optional per-kernel timing with CUDA events recorded on the launch stream

@@ -47,7 +47,7 @@ SIGNATURES = {
     "cals_fast_sketch_workspace_bytes": (ctypes.c_size_t, [i32]),
     "cals_fast_sketch": (i32, [P, i64, i32, i32, i64, P, P, P, ctypes.c_size_t, P]),
     "cals_fast_half_sweep": (i32, [ctypes.POINTER(cals_side), ctypes.POINTER(cals_plan), P, i64, i32, i32, f64, P, P,
-                                   i32, P, P, P, P, ctypes.c_size_t, P]),
+                                   i32, P, i32, P, P, P, P, P, ctypes.c_size_t, P]),
     "cals_sum_f64": (i32, [P, i64, P, P, sz, P]),
     "cals_weighted_sqnorm": (i32, [P, i64, i32, i32, P, P, P, sz, P]),
     "cals_ces_sketch": (i32, [P, i64, i32, ctypes.c_int32, P, P, P, sz, P]),

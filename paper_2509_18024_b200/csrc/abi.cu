@@ -773,9 +773,11 @@ int cals_fast_sketch(const float* source, int64_t n_src, int ld_src, int n_f, in
 }
 
 int cals_fast_half_sweep(const cals_side* side, const cals_plan* P, const float* source, int64_t n_src, int ld_src,
-                         int n_f, double lam, const uint32_t* gmask, float* target, int ld_tgt, double* pen_rows,
+                         int n_f, double lam, const uint32_t* gmask, float* target, int ld_tgt,
+                         const float* target_old, int ld_old, double* rss_rows, double* pen_rows,
                          int32_t* row_status, uint64_t* status_summary, void* ws, size_t ws_bytes, void* stream) {
     if (!side || !P || !source || !target || !row_status || !gmask) return CALS_ERR_ARG;
+    if (rss_rows && (!target_old || ld_old < n_f)) return CALS_ERR_ARG;
     if (n_f < 1 || n_f > CALS_MAX_NF || n_f != P->n_f || ld_src < 4 * xs_chunks(n_f) || (ld_src & 3) || ld_tgt < n_f ||
         lam < 0 || ((uintptr_t)source & 15) || P->n_small != 0)
         return CALS_ERR_ARG;
@@ -798,6 +800,9 @@ int cals_fast_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.tgt = target;
     A.ld_tgt = ld_tgt;
     A.lam = lam;
+    A.tgt_old = target_old;
+    A.ld_old = ld_old;
+    A.rss_rows = rss_rows;
     A.pen_rows = pen_rows;
     A.gbuf = w.gbuf;
     A.stats = g_stats;
@@ -815,7 +820,9 @@ int cals_fast_half_sweep(const cals_side* side, const cals_plan* P, const float*
 
 int cals_residual(const cals_side* side, const float* source, int ld_src, int n_f, const float* rows_w, int ld_w,
                   double* rss_rows, void* stream) {
-    if (!side || !source || !rows_w || !rss_rows || n_f < 1 || ld_src < n_f || ld_w < n_f) return CALS_ERR_ARG;
+    if (!side || !source || !rows_w || !rss_rows || n_f < 1 || n_f > CALS_MAX_NF || ld_src < 4 * xs_chunks(n_f) ||
+        (ld_src & 3) || ((uintptr_t)source & 15) || ld_w < n_f)
+        return CALS_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((side->n_rows + 7) / 8, (int64_t)dev().sms * 16));
     ProfScope ps("residual_kernel", st);

@@ -55,17 +55,32 @@ __global__ void __launch_bounds__(256) residual_kernel(const int64_t* __restrict
                                                        const float* __restrict__ val, int64_t n_rows,
                                                        const float* __restrict__ src, int ld_src, int nf,
                                                        const float* __restrict__ w, int ld_w, double* rss_rows) {
-    const int lane = threadIdx.x & 31;
+    // the warp's row of w in shared memory (16-byte rows: ld_src is a multiple of 4 and the
+    // padding of w is zero or never read), source rows gathered as 16-byte chunks
+    __shared__ __align__(16) float ws[8][CALS_MAX_NF_DEV];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nq = (nf + 3) >> 2;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t stride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    float* wr = ws[warp];
     for (int64_t r = gw; r < n_rows; r += stride) {
         const int64_t lo = ptr[r], hi = ptr[r + 1];
+        __syncwarp();
+        for (int f = lane; f < 4 * nq; f += 32) wr[f] = f < nf ? w[r * ld_w + f] : 0.f;
+        __syncwarp();
         double acc = 0.0;
         for (int64_t e = lo + lane; e < hi; e += 32) {
-            const float* x = src + (int64_t)idx[e] * ld_src;
+            const float4* x = reinterpret_cast<const float4*>(src + (int64_t)__ldg(idx + e) * ld_src);
             double pred = 0.0;
-            for (int f = 0; f < nf; ++f) pred = fma((double)x[f], (double)w[r * ld_w + f], pred);
-            const double d = (double)val[e] - pred;
+            for (int q = 0; q < nq; ++q) {
+                const float4 v = __ldg(x + q);
+                const float4 u = *reinterpret_cast<const float4*>(wr + 4 * q);
+                pred = fma((double)v.x, (double)u.x, pred);
+                pred = fma((double)v.y, (double)u.y, pred);
+                pred = fma((double)v.z, (double)u.z, pred);
+                pred = fma((double)v.w, (double)u.w, pred);
+            }
+            const double d = (double)__ldg(val + e) - pred;
             acc = fma(d, d, acc);
         }
         acc = warp_sum_d(acc);

@@ -136,8 +136,6 @@ class DeviceSide:
             stream = torch.cuda.current_stream(self.device).cuda_stream
         L = _lib.load()
         if self.fast:
-            if want_rss:  # residual of the previous rows before they are replaced
-                self.residual(source, target_old, stream)
             if self.plan.n_big:
                 _lib.check(L.cals_fast_sketch(source.data_ptr(), self.n_src, source.stride(0), self.n_f, self.fast_s,
                                               self.fast_thr.data_ptr(), self.gmask.data_ptr(), self.fast_ws.data_ptr(),
@@ -145,6 +143,9 @@ class DeviceSide:
             _lib.check(L.cals_fast_half_sweep(
                 ctypes.byref(self.side), ctypes.byref(self.plan), source.data_ptr(), source.shape[0], source.stride(0),
                 self.n_f, float(lam), self.gmask.data_ptr(), target.data_ptr(), target.stride(0),
+                target_old.data_ptr() if target_old is not None else None,
+                target_old.stride(0) if target_old is not None else 0,
+                self.rss_rows.data_ptr() if want_rss else None,
                 self.pen_rows.data_ptr(), self.status.data_ptr(), self.summary.data_ptr(), self.ws.data_ptr(),
                 self.ws.numel(), stream), "cals_fast_half_sweep")
             return

@@ -69,7 +69,7 @@ class ShardedEngine:
     """Factory returning a CoreEngine restricted to this rank's row blocks,
     with the per-half-sweep exchange and the objective all-reduce hooked in."""
 
-    def __new__(cls, R, n_f, rate, lam, rank, world, group=None, device=None):
+    def __new__(cls, R, n_f, rate, lam, rank, world, group=None, device=None, fast=False):
         from .engine import CoreEngine
 
         user_ranges = nnz_balanced_ranges(R.row_ptr, world)
@@ -98,7 +98,8 @@ class ShardedEngine:
                     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
                     row[maxes[0]:maxes[-1] + 1].copy_(t.view(torch.float64).to(row.device))
 
-        eng = _Sharded(R, n_f, rate, lam, device=device, user_range=user_ranges[rank], item_range=item_ranges[rank])
+        eng = _Sharded(R, n_f, rate, lam, device=device, user_range=user_ranges[rank], item_range=item_ranges[rank],
+                       fast=fast)
         eng._scratch = None
         eng.rank, eng.world, eng.group = rank, world, group
         eng.user_ranges, eng.item_ranges = user_ranges, item_ranges
