@@ -165,6 +165,10 @@ int cals_update_core(const double* X, int64_t n, int p, const int64_t* col_ptr,
 int cals_predict_entries(const float* U, const float* M, int n_f, int ld_u, int ld_m,
                          const int64_t* users, const int64_t* items, int64_t n, double* out,
                          void* stream);
+/* Same with float64 factors (FactorPair precision; the evaluation metrics rank by these scores,
+ * metrics.py:64-160). */
+int cals_predict_entries_f64(const double* U, const double* M, int n_f, int ld_u, int ld_m, const int64_t* users,
+                             const int64_t* items, int64_t n, double* out, void* stream);
 
 /*
  * Method 'fast_core' (core.py:255-298): ONE sketch of the whole source per

@@ -55,6 +55,7 @@ SIGNATURES = {
     "cals_ces_sketch_f64": (i32, [P, i64, i32, ctypes.c_int32, P, P, sz, P]),
     "cals_update_core": (i32, [P, i64, i32, P, P, P, f64, i32, P, P, P]),
     "cals_predict_entries": (i32, [P, P, i32, i32, i32, P, P, i64, P, P]),
+    "cals_predict_entries_f64": (i32, [P, P, i32, i32, i32, P, P, i64, P, P]),
     "cals_profile_enable": (None, [i32]),
     "cals_debug_stats": (None, [P]),
     "cals_debug_big_batch": (None, [ctypes.c_int64, ctypes.c_int64]),

@@ -122,7 +122,9 @@ def predict(F, i, j):
 
 def predict_entries(F, users, items, chunk=1 << 18):
     """Predicted ratings for parallel index arrays (als.py:143-152), evaluated on
-    the GPU by the gather-dot kernel (cals_predict_entries), float64 accumulation."""
+    the GPU by the float64 gather-dot kernel (cals_predict_entries_f64) on the
+    FactorPair's float64 rows, so scores match the reference's einsum up to the
+    summation order (rankings in the evaluation metrics depend on them)."""
     from . import _lib
     torch = _lib.require_cuda()
     users = np.asarray(users, dtype=np.int64)
@@ -131,20 +133,22 @@ def predict_entries(F, users, items, chunk=1 << 18):
         raise ValueError("users and items must have the same shape")
     if users.size == 0:
         return np.empty(0, dtype=np.float64)
-    dev = torch.device("cuda")
-    U = torch.from_numpy(np.ascontiguousarray(F.user_factors, dtype=np.float32)).to(dev)
-    M = torch.from_numpy(np.ascontiguousarray(F.item_factors, dtype=np.float32)).to(dev)
-    if users.min() < 0 or users.max() >= U.shape[0] or items.min() < 0 or items.max() >= M.shape[0]:
+    U_h = np.ascontiguousarray(F.user_factors, dtype=np.float64)
+    M_h = np.ascontiguousarray(F.item_factors, dtype=np.float64)
+    if users.min() < 0 or users.max() >= U_h.shape[0] or items.min() < 0 or items.max() >= M_h.shape[0]:
         raise IndexError("entry index out of range")
-    uu = torch.from_numpy(users).to(dev)
-    ii = torch.from_numpy(items).to(dev)
+    dev = torch.device("cuda")
+    U = torch.from_numpy(U_h).to(dev)
+    M = torch.from_numpy(M_h).to(dev)
+    uu = torch.from_numpy(users.reshape(-1)).to(dev)
+    ii = torch.from_numpy(items.reshape(-1)).to(dev)
     out = torch.empty(users.size, dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream().cuda_stream
     nf = F.n_f
-    _lib.check(_lib.load().cals_predict_entries(U.data_ptr(), M.data_ptr(), nf, nf, nf, uu.data_ptr(),
-                                                ii.data_ptr(), users.size, out.data_ptr(), st),
-               "cals_predict_entries")
-    return out.cpu().numpy()
+    _lib.check(_lib.load().cals_predict_entries_f64(U.data_ptr(), M.data_ptr(), nf, nf, nf, uu.data_ptr(),
+                                                    ii.data_ptr(), users.size, out.data_ptr(), st),
+               "cals_predict_entries_f64")
+    return out.cpu().numpy().reshape(users.shape)
 
 
 def predict_full(F):

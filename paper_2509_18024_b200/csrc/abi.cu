@@ -898,6 +898,16 @@ int cals_predict_entries(const float* U, const float* M, int n_f, int ld_u, int 
     return cuda_status("cals_predict_entries");
 }
 
+int cals_predict_entries_f64(const double* U, const double* M, int n_f, int ld_u, int ld_m, const int64_t* users,
+                             const int64_t* items, int64_t n, double* out, void* stream) {
+    if (!U || !M || !users || !items || !out || n_f < 1 || ld_u < n_f || ld_m < n_f) return CALS_ERR_ARG;
+    if (n == 0) return CALS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, (int64_t)dev().sms * 16);
+    predict_entries_f64_kernel<<<(int)blocks, 256, 0, st>>>(U, M, n_f, ld_u, ld_m, users, items, n, out);
+    return cuda_status("cals_predict_entries_f64");
+}
+
 void cals_debug_stats(void* device_counters) { g_stats = (unsigned long long*)device_counters; }
 void cals_debug_big_batch(int64_t cand_keys, int64_t tiles) {
     g_big_cand_budget = cand_keys;

@@ -249,4 +249,20 @@ __global__ void __launch_bounds__(256) predict_entries_kernel(const float* __res
     }
 }
 
+// float64 factors (the reference's FactorPair precision, als.py:40-49): the
+// evaluation metrics rank by these scores, so they are not narrowed to fp32.
+__global__ void __launch_bounds__(256) predict_entries_f64_kernel(const double* __restrict__ U,
+                                                                  const double* __restrict__ M, int nf, int ldu,
+                                                                  int ldm, const int64_t* __restrict__ users,
+                                                                  const int64_t* __restrict__ items, int64_t n,
+                                                                  double* __restrict__ out) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const double* u = U + users[e] * ldu;
+        const double* m = M + items[e] * ldm;
+        double acc = 0.0;
+        for (int f = 0; f < nf; ++f) acc = fma(u[f], m[f], acc);
+        out[e] = acc;
+    }
+}
+
 }  // namespace cals

@@ -229,6 +229,33 @@ def fast_case(name, seed, n_users, n_items, density, n_f, lam, rate, iters, drop
     )
 
 
+def metric_cases():
+    """The reference's evaluation metrics (metrics.py:64-160) on a fitted model:
+    train RMSE, held-out PRMSE, hit@k and NDCG@k (with and without an explicit
+    relevance threshold), for the device-side evaluation path."""
+    from coreals import metrics
+    users, items, vals = make_matrix(9, 150, 120, 0.3, 4, 0.5)
+    rng = np.random.default_rng(10)
+    test = rng.random(users.size) < 0.2
+    R = RatingMatrix(users[~test], items[~test], vals[~test], n_users=150, n_items=120)
+    M0 = f32(np.random.default_rng(11).normal(0.0, 0.1, size=(120, 6)))
+    cfg = SolverConfig(method="core", n_f=6, lam=0.1, rate=0.3, max_iters=4, tol=1e-15)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        F, _ = fit_core(R, cfg, init_m=M0)
+    held = (users[test], items[test], vals[test])
+    np.savez_compressed(
+        os.path.join(OUT, "metrics.npz"),
+        users=users[~test], items=items[~test], vals=vals[~test], n_users=150, n_items=120,
+        hu=held[0], hi=held[1], hr=held[2], U=F.user_factors, M=F.item_factors,
+        rmse=metrics.rmse(R, F), prmse=metrics.prmse(held, F),
+        thr95=metrics.relevance_threshold(held[2], 95.0),
+        hit5=metrics.hit_at_k(held, F, 5), hit3_t0=metrics.hit_at_k(held, F, 3, threshold=0.0),
+        hit1_p80=metrics.hit_at_k(held, F, 1, percentile=80.0), hit2_t1=metrics.hit_at_k(held, F, 2, threshold=1.0),
+        ndcg10=metrics.ndcg_at_k(held, F, 10), ndcg3=metrics.ndcg_at_k(held, F, 3),
+    )
+
+
 def fast_cases():
     fast_case("small", 5, 200, 150, 0.2, 8, 0.1, 0.3, 4)
     # sparse slices (empty sketched columns -> fallback), ties, an empty user
@@ -243,6 +270,9 @@ if __name__ == "__main__":
     if sys.argv[1:] == ["fast"]:
         fast_cases()
         sys.exit(0)
+    if sys.argv[1:] == ["metrics"]:
+        metric_cases()
+        sys.exit(0)
     sketch_cases()
     update_cases()
     # config-1 shape scaled down (BASELINE configs[0]: n_f=5, lam=0.1, r=0.3)
@@ -256,4 +286,5 @@ if __name__ == "__main__":
     # exact ALS (method 'full')
     full_case("full", 4, 120, 90, 0.3, 8, 0.1, 4, drop_user=7)
     fast_cases()
+    metric_cases()
     print("golden fixtures written to", OUT)

@@ -367,3 +367,25 @@ def test_fit_method_dispatch_and_zero_iters():
     F, rep = cb.fit_method(R, cfg, init_m=g["M0"])
     assert rep.iters_run == 0 and rep.objective_trace.size == 0
     np.testing.assert_array_equal(F.item_factors, g["M0"])
+
+
+def test_evaluation_metrics_match_reference():
+    """metrics.rmse / prmse / hit_at_k / ndcg_at_k (metrics.py:64-160) on the
+    reference's own fitted factors, scored by the float64 GPU gather-dot."""
+    g = load_golden("metrics.npz")
+    R = cb.RatingMatrix(g["users"], g["items"], g["vals"], n_users=int(g["n_users"]), n_items=int(g["n_items"]))
+    F = cb.FactorPair(g["U"], g["M"])
+    held = (g["hu"], g["hi"], g["hr"])
+    assert cb.rmse(R, F) == pytest.approx(float(g["rmse"]), rel=1e-12)
+    assert cb.prmse(held, F) == pytest.approx(float(g["prmse"]), rel=1e-12)
+    assert cb.relevance_threshold(g["hr"], 95.0) == float(g["thr95"])
+    assert cb.hit_at_k(held, F, 5) == float(g["hit5"])
+    assert cb.hit_at_k(held, F, 3, threshold=0.0) == float(g["hit3_t0"])
+    assert cb.hit_at_k(held, F, 1, percentile=80.0) == float(g["hit1_p80"])
+    assert cb.hit_at_k(held, F, 2, threshold=1.0) == float(g["hit2_t1"])
+    assert cb.ndcg_at_k(held, F, 10) == pytest.approx(float(g["ndcg10"]), rel=1e-12)
+    assert cb.ndcg_at_k(held, F, 3) == pytest.approx(float(g["ndcg3"]), rel=1e-12)
+    ev = cb.evaluate(R, held, F)
+    assert ev.hit_at_k == float(g["hit5"]) and ev.ndcg_at_k == pytest.approx(float(g["ndcg10"]), rel=1e-12)
+    with pytest.raises(cb.DataError):
+        cb.prmse(([], [], []), F)
