@@ -332,6 +332,11 @@ __global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(Sw
     __shared__ uint64_t s_thr[CALS_MAX_NF_DEV];
     __shared__ unsigned long long s_amax[FAST ? CALS_MAX_NF_DEV : 1];
     __shared__ int s_cnt[FAST ? CALS_MAX_NF_DEV : 1];
+    __shared__ __align__(8) unsigned long long s_mbar;
+    const uint32_t mbar = smem_u32(&s_mbar);
+    uint32_t phase = 0;
+    if (threadIdx.x == 0) mbar_init(mbar, 1);
+    __syncthreads();
     __shared__ float wold[CALS_MAX_NF_DEV];
     __shared__ double red[32];
     const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
@@ -378,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(Sw
         for (int k0 = kbeg; k0 < kend; k0 += CH) {
             const int kn = min(CH, kend - k0);
             __syncthreads();
-            stage_slice(A, lo, k0, kn, Xs, ys, fq);
+            stage_slice_bulk(A, lo, k0, kn, s_xs, ys, mbar, phase);
             if (FAST && !full) {
                 for (int e = tid; e < kn * B.gwords; e += nt) {
                     const int k = e / B.gwords, wi = e - k * B.gwords;

@@ -214,6 +214,51 @@ __device__ __forceinline__ void stage_slice_issue(const SweepArgs& A, int64_t lo
     cp_async_commit();
 }
 
+// ---- 1-D bulk (TMA) staging of gathered rows ----------------------------------
+// One cp.async.bulk per slice row (its 16*nq data bytes), all completing on one
+// mbarrier: warp 0 issues, every thread waits on the barrier's phase.
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(mbar), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            mbar),
+        "r"(phase)
+        : "memory");
+}
+
+// Stage slice rows [k0, k0 + kn) like stage_slice, X by bulk copies (warp 0
+// issues one per row) and y by plain loads; returns after the copies landed.
+// `phase` is the barrier's current parity (flipped here).  The caller
+// synchronises the block before (buffer free) and after (y visible).
+__device__ __forceinline__ void stage_slice_bulk(const SweepArgs& A, int64_t lo, int k0, int kn, uint32_t xs_base,
+                                                 float* ys, uint32_t mbar, uint32_t& phase) {
+    const int sx = xs_stride(A.nf);
+    const uint32_t rowbytes = 16u * (uint32_t)xs_chunks(A.nf);
+    // every thread issues the copies of its rows; the barrier's single arrival (thread 0,
+    // with the expected byte count) may come before or after them: the phase cannot
+    // complete while that arrival is pending
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // prior generic reads of the buffer
+    if (threadIdx.x == 0) mbar_expect_tx(mbar, (uint32_t)kn * rowbytes);
+    const int32_t* idx = A.idx + lo + k0;
+    for (int k = threadIdx.x; k < kn; k += blockDim.x)
+        bulk_g2s(xs_base + (uint32_t)(k * sx * 4), A.src + (int64_t)__ldg(idx + k) * A.ld_src, rowbytes, mbar);
+    if (ys != nullptr)
+        for (int k = threadIdx.x; k < kn; k += blockDim.x) ys[k] = __ldg(A.val + lo + k0 + k);
+    mbar_wait(mbar, phase);
+    phase ^= 1u;
+}
+
 // Column lanes / slots of the staged-slice kernel: thread t handles column
 // t % NFP over the k-range of slot t / NFP (ranges are multiples of 32 rows,
 // so every bitmap word has a single owner).
