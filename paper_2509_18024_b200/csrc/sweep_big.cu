@@ -114,6 +114,11 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_above[CALS_MAX_NF_DEV], s_base[CALS_MAX_NF_DEV], s_slot[CALS_MAX_NF_DEV];
     __shared__ uint32_t s_hib[CALS_MAX_NF_DEV], s_lob[CALS_MAX_NF_DEV];
+    __shared__ __align__(8) unsigned long long s_mbar;
+    const uint32_t mbar = smem_u32(&s_mbar);
+    uint32_t phase = 0;
+    if (threadIdx.x == 0) mbar_init(mbar, 1);
+    __syncthreads();
     const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x;
     const int sx = xs_stride(nf);
     float* Xs = reinterpret_cast<float*>(smem);
@@ -146,7 +151,7 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
         for (int k0 = kbeg; k0 < kend; k0 += B.chunk) {
             const int kn = min(B.chunk, kend - k0);
             __syncthreads();
-            stage_slice(A, lo, k0, kn, Xs, nullptr, fq);
+            stage_slice_bulk(A, lo, k0, kn, s_xs, nullptr, mbar, phase);
             if (tid < nf) s_slot[tid] = 0;
             __syncthreads();
             const int per = nt / nf;  // threads per column; each scans <= 32 rows (big_chunk)
