@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
         for (int k0 = kbeg; k0 < kend; k0 += B.chunk) {
             const int kn = min(B.chunk, kend - k0);
             __syncthreads();
-            stage_slice_bulk(A, lo, k0, kn, s_xs, nullptr, mbar, phase);
+            if (xs_chunks(nf) >= 16) stage_slice_bulk(A, lo, k0, kn, s_xs, nullptr, mbar, phase);
+            else stage_slice(A, lo, k0, kn, Xs, nullptr, fq);
             if (tid < nf) s_slot[tid] = 0;
             __syncthreads();
             const int per = nt / nf;  // threads per column; each scans <= 32 rows (big_chunk)

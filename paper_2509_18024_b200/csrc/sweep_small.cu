@@ -77,6 +77,11 @@ __global__ void __launch_bounds__(512, 1) small_gram_kernel(SweepArgs A, const i
     __shared__ int c_need[CALS_MAX_NF_DEV], c_flag[CALS_MAX_NF_DEV], c_fc[CALS_MAX_NF_DEV];
     __shared__ float wold[CALS_MAX_NF_DEV];
     __shared__ double red[32];
+    __shared__ __align__(8) unsigned long long s_mbar;
+    const uint32_t mbar = smem_u32(&s_mbar);
+    uint32_t phase = 0;
+    if (threadIdx.x == 0) mbar_init(mbar, 1);
+    __syncthreads();
 
     const int nf = A.nf;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
@@ -113,7 +118,9 @@ __global__ void __launch_bounds__(512, 1) small_gram_kernel(SweepArgs A, const i
         if (use_tab) table_levels(n, s, A.delta_tab, jhi, jlo);
         const int chunk = SM.chunk(n);
 
-        stage_slice(A, lo, 0, n, Xs, ys, fq);
+        // 1-D bulk copies pay off for long rows (>= 256 B); short rows stay on cp.async
+        if (xs_chunks(nf) >= 16) stage_slice_bulk(A, lo, 0, n, s_xs, ys, mbar, phase);
+        else stage_slice(A, lo, 0, n, Xs, ys, fq);
         if (tid < nf && A.tgt_old != nullptr) wold[tid] = A.tgt_old[(int64_t)row * A.ld_old + tid];
         __syncthreads();
 
