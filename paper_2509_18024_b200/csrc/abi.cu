@@ -101,7 +101,9 @@ int big_chunk(int nf) {
 
 size_t big_gram_smem(int nf, int chunk, int gwords = 0) {
     const int sx = xs_stride(nf);
-    const bool persist = owned_single_round(nf, kThreads / 32);
+    const int nq = xs_chunks(nf);
+    const int threads = big_gram_threads(nq <= 4 ? 1 : (nq <= 8 ? 2 : (nq <= 16 ? 4 : 8)));
+    const bool persist = owned_single_round(nf, threads / 32);
     const size_t g = persist ? 0 : align16((size_t)nf * (nf + 1) * 4);
     const size_t lists = persist ? 0 : (size_t)nf * chunk * 2 + (size_t)nf * 4;
     return align16((size_t)chunk * sx * 4) + align16((size_t)chunk * 4) + g +
@@ -302,6 +304,13 @@ void launch_solve(const SweepArgs& A, const int32_t* rows, int64_t count, cudaSt
             allow_smem(solve_wide_kernel<64>);
             solve_wide_kernel<64><<<(int)blocks, 128, smem, st>>>(A, rows, count);
         }
+    } else if (A.nf <= 128) {
+        // one CTA of NF threads per system, rows in registers
+        const int64_t cap = (int64_t)dev().sms * 3;
+        if (A.nf <= 96)
+            solve_rows_kernel<96><<<(int)std::min<int64_t>(count, cap), 96, 0, st>>>(A, rows, count);
+        else
+            solve_rows_kernel<128><<<(int)std::min<int64_t>(count, cap), 128, 0, st>>>(A, rows, count);
     } else {
         const size_t smem = align16((size_t)A.nf * (A.nf + 1) * 4);
         allow_smem(solve_block_kernel);
@@ -406,8 +415,10 @@ int launch_small(SweepArgs A, const cals_plan* P, const Work& w, cudaStream_t st
 
 template <int CPL, bool FAST = false>
 void launch_big_gram(const SweepArgs& A, const BigArgs& B, size_t smem, cudaStream_t st) {
+    constexpr int threads = big_gram_threads(CPL);
     allow_smem(big_gram_kernel<CPL, FAST>);
-    big_gram_kernel<CPL, FAST><<<grid_for(big_gram_kernel<CPL, FAST>, smem, B.n_tiles), kThreads, smem, st>>>(A, B);
+    big_gram_kernel<CPL, FAST>
+        <<<grid_for(big_gram_kernel<CPL, FAST>, smem, B.n_tiles, 8, threads), threads, smem, st>>>(A, B);
 }
 
 // method 'fast_core': every row is a tiled row whose kept bits come from the

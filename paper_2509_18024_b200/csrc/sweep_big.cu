@@ -332,8 +332,12 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
 // their sparse Gram rows -- in registers across the item's chunks when the
 // warp's columns fit one lane-group round (nf <= 64), else in shared memory;
 // the item's partial goes to global.
+// n_f > 64 (CPL 8) runs 512-thread CTAs: 16 warps own <= 8 columns each, so the
+// accumulators stay register-resident (owned_single_round) instead of in shared memory.
+constexpr int big_gram_threads(int cpl) { return cpl >= 8 ? 512 : kThreads; }
+
 template <int CPL, bool FAST>
-__global__ void __launch_bounds__(kThreads, CPL <= 4 ? 3 : 1) big_gram_kernel(SweepArgs A, BigArgs B) {
+__global__ void __launch_bounds__(big_gram_threads(CPL), CPL <= 4 ? 3 : 1) big_gram_kernel(SweepArgs A, BigArgs B) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t s_thr[CALS_MAX_NF_DEV];
     __shared__ unsigned long long s_amax[FAST ? CALS_MAX_NF_DEV : 1];
