@@ -212,10 +212,8 @@ __device__ __forceinline__ void rows_block(float (&a)[NF], float& rhs, bool& use
 #pragma unroll
         for (int q = B0 / 4; q < NF / 4; ++q) {
             const float4 v = *reinterpret_cast<const float4*>(piv + 4 * q);
-            a[4 * q + 0] = fmaf(-f, v.x, a[4 * q + 0]);
-            a[4 * q + 1] = fmaf(-f, v.y, a[4 * q + 1]);
-            a[4 * q + 2] = fmaf(-f, v.z, a[4 * q + 2]);
-            a[4 * q + 3] = fmaf(-f, v.w, a[4 * q + 3]);
+            ffma2_bcast(a[4 * q + 0], a[4 * q + 1], v.x, v.y, -f);
+            ffma2_bcast(a[4 * q + 2], a[4 * q + 3], v.z, v.w, -f);
         }
         rhs = fmaf(-f, piv[NF], rhs);
         __syncthreads();  // piv is rewritten by the next step's owner
