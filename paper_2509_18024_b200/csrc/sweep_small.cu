@@ -446,6 +446,20 @@ __global__ void __launch_bounds__(kTinyWarps * 32) tiny_gram_kernel(SweepArgs A,
                     mn = t2 < mn ? t2 : mn;
                 }
                 T = mn;
+            } else if (s <= 8) {
+                // small budgets: extract the s largest keys one warp max at a time
+                uint64_t v0 = lane < n ? k0 : 0ull, v1 = lane + 32 < n ? k1 : 0ull;
+                for (int q = 0; q < s; ++q) {
+                    uint64_t m = v0 > v1 ? v0 : v1;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const uint64_t t2 = __shfl_xor_sync(CALS_FULL_MASK, m, o);
+                        m = t2 > m ? t2 : m;
+                    }
+                    T = m;  // keys are unique: exactly one lane holds m
+                    if (v0 == m) v0 = 0ull;
+                    if (v1 == m) v1 = 0ull;
+                }
             } else if (n <= 32) {
                 const uint64_t v = warp_sort_desc(k0, lane);
                 T = __shfl_sync(CALS_FULL_MASK, v, s - 1);
