@@ -51,7 +51,6 @@ __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v));
 }
 __device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v)); }
-__device__ __forceinline__ void atoms_or(uint32_t a, uint32_t v) { asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v)); }
 __device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
     unsigned short v;
     asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
@@ -108,22 +107,6 @@ __device__ __forceinline__ uint64_t warp_sort_desc(uint64_t v, int lane) {
     return v;
 }
 
-// Bitonic sort within aligned groups of W lanes (W <= 32), descending.
-template <int W>
-__device__ __forceinline__ uint64_t warp_sort_desc_w(uint64_t v, int lane) {
-#pragma unroll
-    for (int size = 2; size <= W; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            const uint64_t o = __shfl_xor_sync(CALS_FULL_MASK, v, stride);
-            const bool lower = (lane & stride) == 0;
-            const bool desc_block = (lane & size) == 0 || size == W;
-            const bool keep_max = (lower == desc_block);
-            v = keep_max ? (v > o ? v : o) : (v < o ? v : o);
-        }
-    }
-    return v;
-}
 
 // Bitonic sort of 64 keys held two per lane (element e = lane + 32*h), descending
 // by element index: after the call v0 = rank lane, v1 = rank lane + 32.

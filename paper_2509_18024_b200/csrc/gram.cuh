@@ -1,230 +1,17 @@
 // gram.cuh -- sketched normal equations from a staged slice.
 //
-// G[c][f] = sum_k P[k][c] * X[k][c] * X[k][f]   (f < nf)
-// G[c][nf] = sum_k P[k][c] * X[k][c] * y[k]      (the RHS b[c])
-// with P the selection mask (bit c of mb[k]).  This is the reference's
-// gram_rhs_global (_kernels.py:123-146) -- G row c sums over column c's
-// kept rows only, so G is generally non-symmetric -- written as a masked
-// dense contraction (P . X)^T [X | y] so that every thread runs a 4x4
-// register tile with vector shared-memory loads.  Partials over k-groups
+// G[c][f] = sum_{k kept for c} X[k][c] * X[k][f]   (f < nf)
+// G[c][nf] = sum_{k kept for c} X[k][c] * y[k]     (the RHS b[c])
+// This is the reference's gram_rhs_global (_kernels.py:123-146): G row c
+// sums over column c's kept rows only, so G is generally non-symmetric.  The
+// sum runs over the kept rows only (algorithmic flops): a few lanes own one
+// column and walk its kept-row list or bitmap, each lane accumulating a
+// 16-byte-chunk slice of [X | y] with packed FFMA2; partials over q-groups
 // are reduced in a fixed order, so results are deterministic.
 #pragma once
 #include "sweep_common.cuh"
 
 namespace cals {
-
-// One 4x4 tile (rows c0..c0+3, columns f0..f0+3 of [X | y]) over k = kbeg, kbeg+kstep, ...
-__device__ __forceinline__ void gram_tile(const float* __restrict__ Xs, int sx, const float* __restrict__ ys,
-                                          const uint32_t* __restrict__ mb, int mw, int n, int nf, int c0, int f0,
-                                          int kbeg, int kstep, float (&acc)[4][4]) {
-    const int wsel = c0 >> 5, sh = c0 & 31;
-    const int yslot = nf - f0;  // component of the B tile that is the response (if in [0, 4))
-    const bool bx = f0 < 4 * xs_chunks(nf);  // staged data chunks only (padding beyond is not staged)
-    (void)sx;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-#pragma unroll 4
-    for (int k = kbeg; k < n; k += kstep) {
-        const float4 av = *reinterpret_cast<const float4*>(Xs + (size_t)k * sx + c0);
-        float4 bv = bx ? *reinterpret_cast<const float4*>(Xs + (size_t)k * sx + f0) : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (yslot >= 0 && yslot < 4) {
-            const float yk = ys[k];
-            bv.x = yslot == 0 ? yk : bv.x;
-            bv.y = yslot == 1 ? yk : bv.y;
-            bv.z = yslot == 2 ? yk : bv.z;
-            bv.w = yslot == 3 ? yk : bv.w;
-        }
-        const uint32_t m = mb[k * mw + wsel] >> sh;
-        const float a[4] = {(m & 1u) ? av.x : 0.f, (m & 2u) ? av.y : 0.f, (m & 4u) ? av.z : 0.f,
-                            (m & 8u) ? av.w : 0.f};
-        const float b[4] = {bv.x, bv.y, bv.z, bv.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-    }
-}
-
-// Must be called by all threads of the block.  Xs: n rows, stride sx (zero
-// padding beyond nf), ys: n responses, mb: n * mw mask words.
-// Writes (or adds into) G (nf x (nf+1), row stride nf+1).  scratch: >= blockDim*16 floats.
-__device__ void tile_gram(const float* __restrict__ Xs, int sx, const float* __restrict__ ys,
-                          const uint32_t* __restrict__ mb, int mw, int n, int nf, float* __restrict__ G,
-                          float* __restrict__ scratch, bool accumulate = false) {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int gs = nf + 1;
-    const int RB = (nf + 3) >> 2, CB = (gs + 3) >> 2, NB = RB * CB;
-    if (NB <= nt) {
-        const int KG = nt / NB;
-        if (tid < NB * KG) {
-            const int bid = tid % NB, kg = tid / NB;
-            float acc[4][4];
-            gram_tile(Xs, sx, ys, mb, mw, n, nf, (bid / CB) * 4, (bid % CB) * 4, kg, KG, acc);
-            float* out = scratch + (size_t)(kg * NB + bid) * 16;
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) out[i * 4 + j] = acc[i][j];
-        }
-        __syncthreads();
-        for (int e = tid; e < nf * gs; e += nt) {
-            const int c = e / gs, f = e - c * gs;
-            const int bid = (c >> 2) * CB + (f >> 2);
-            const int slot = (c & 3) * 4 + (f & 3);
-            float v = 0.f;
-            for (int g = 0; g < KG; ++g) v += scratch[(size_t)(g * NB + bid) * 16 + slot];
-            G[c * gs + f] = accumulate ? G[c * gs + f] + v : v;
-        }
-        __syncthreads();
-    } else {
-        for (int bid = tid; bid < NB; bid += nt) {
-            const int c0 = (bid / CB) * 4, f0 = (bid % CB) * 4;
-            float acc[4][4];
-            gram_tile(Xs, sx, ys, mb, mw, n, nf, c0, f0, 0, 1, acc);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int c = c0 + i, f = f0 + j;
-                    if (c < nf && f < gs) G[c * gs + f] = accumulate ? G[c * gs + f] + acc[i][j] : acc[i][j];
-                }
-        }
-        __syncthreads();
-    }
-}
-
-// Selection bitmap: bit c of mb[k*mw + c/32] = (key(k0 + k, c) >= thr[c]).
-// Lanes run along columns (conflict-free row reads), ballots form the words;
-// for nf <= 16 several rows share a warp.
-__device__ void build_mask(const float* __restrict__ Xs, int sx, int n, int nf, const uint64_t* thr, bool full,
-                           uint32_t* __restrict__ mb, int mw, int k0 = 0) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    int P = 32;
-    if (nf <= 16) P = nf <= 1 ? 1 : (nf <= 2 ? 2 : (nf <= 4 ? 4 : (nf <= 8 ? 8 : 16)));
-    const int rpw = 32 / P, sub = lane / P, cl = lane - sub * P;
-    const uint32_t fieldmask = P == 32 ? 0xffffffffu : ((1u << P) - 1u);
-    for (int base = warp * rpw; base < n; base += nwarps * rpw) {
-        const int k = base + sub;
-        for (int w = 0; w < mw; ++w) {
-            const int c = w * 32 + cl;
-            bool bit = false;
-            if (k < n && c < nf)
-                bit = full || make_key(Xs[(size_t)k * sx + c], (uint32_t)(k0 + k)) >= thr[c];
-            const uint32_t bal = __ballot_sync(CALS_FULL_MASK, bit);
-            if (cl == 0 && k < n) mb[k * mw + w] = (bal >> (sub * P)) & fieldmask;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Sparse sketched normal equations (algorithmic flop count): for every column
-// c, G[c][:] = sum_{k in S_c} X[k][c] * [X[k][:] | y[k]] over the kept rows
-// S_c only (_kernels.py:132-145).  A warp task owns CT columns; its lanes are
-// (column slot, q-group, chunk lane): LPC lanes per column each own CPL
-// 16-byte chunks of the row (interleaved, so the lanes of one column read one
-// contiguous row segment), QG q-groups split the kept-row list round-robin and
-// are reduced with shuffles in a fixed order; lane (fl == 0) also owns b[c].
-// Kept-row lists (ascending k) are built from the selection bitmap by the
-// same warp.  Writes rows of G (+lam_n on the diagonal) to Gout (row stride nf+1).
-// ---------------------------------------------------------------------------
-template <int CPL>
-__device__ __forceinline__ void sparse_gram_warp(uint32_t xs, int sx, uint32_t ys, uint32_t mb, int mw, int n, int nf,
-                                                 int s, bool full, uint32_t lists, int Smax, float lam_n,
-                                                 float* __restrict__ Gout, int warp, int nwarps, int lane) {
-    const int nq = xs_chunks(nf);
-    const int LPC = nq < 4 ? nq : 4;
-    int CT = (nf + nwarps - 1) / nwarps;    // columns per task: power of two, CT * LPC <= 32
-    CT = CT <= 1 ? 1 : (CT <= 2 ? 2 : (CT <= 4 ? 4 : (CT <= 8 ? 8 : (CT <= 16 ? 16 : 32))));
-    while (CT * LPC > 32) CT >>= 1;
-    const int QG = 32 / (CT * LPC);         // power of two
-    const int cs = lane / (QG * LPC);
-    const int qg = (lane / LPC) % QG;
-    const int fl = lane % LPC;
-    const int gs = nf + 1;
-    const int ntask = (nf + CT - 1) / CT;
-    const uint32_t rowb = 4u * (uint32_t)sx;
-    for (int task = warp; task < ntask; task += nwarps) {
-        const int cbase = task * CT;
-        const int c = cbase + cs;
-        const bool cvalid = c < nf;
-        if (!full) {
-            // lists of the task's columns from the bitmap (CT columns share one word)
-            int cnt = 0;  // lane cc keeps column cbase+cc's running count
-            const int wsel = cbase >> 5, sh = cbase & 31;
-            for (int k0 = 0; k0 < n; k0 += 32) {
-                const int k = k0 + lane;
-                const uint32_t word = k < n ? (lds_u32(mb + 4u * (uint32_t)(k * mw + wsel)) >> sh) : 0u;
-                for (int cc = 0; cc < CT && cbase + cc < nf; ++cc) {
-                    const bool bit = (word >> cc) & 1u;
-                    const uint32_t bal = __ballot_sync(CALS_FULL_MASK, bit);
-                    const int base = __shfl_sync(CALS_FULL_MASK, cnt, cc);
-                    if (bit)
-                        sts_u16(lists + 2u * (uint32_t)((cbase + cc) * Smax + base + __popc(bal & lanemask_lt())), k);
-                    if (lane == cc) cnt += __popc(bal);
-                }
-            }
-            __syncwarp();
-        }
-        const int len = full ? n : s;
-        const uint32_t L = lists + 2u * (uint32_t)((cvalid ? c : cbase) * Smax);
-        const uint32_t xcol = xs + 4u * (uint32_t)(cvalid ? c : 0);
-        float acc[4 * CPL];
-#pragma unroll
-        for (int i = 0; i < 4 * CPL; ++i) acc[i] = 0.f;
-        float accb = 0.f;
-        const bool chunk_ok_last = (fl + (CPL - 1) * LPC) < nq;
-        for (int q = qg; q < len; q += QG) {
-            const uint32_t k = full ? (uint32_t)q : lds_u16(L + 2u * (uint32_t)q);
-            const uint32_t rb = k * rowb;
-            const float xc = lds_f32(xcol + rb);
-#pragma unroll
-            for (int i = 0; i < CPL; ++i) {
-                const int ch = fl + i * LPC;
-                if (i < CPL - 1 || chunk_ok_last) {
-                    const float4 v = lds_f128(xs + rb + 16u * (uint32_t)ch);
-                    ffma2_bcast(acc[4 * i + 0], acc[4 * i + 1], v.x, v.y, xc);
-                    ffma2_bcast(acc[4 * i + 2], acc[4 * i + 3], v.z, v.w, xc);
-                }
-            }
-            if (fl == 0) accb = fmaf(xc, lds_f32(ys + 4u * k), accb);
-        }
-        // fixed-order reduction over the q-groups (lane bits LPC .. LPC*QG)
-        for (int o = LPC; o < LPC * QG; o <<= 1) {
-#pragma unroll
-            for (int i = 0; i < 4 * CPL; ++i) acc[i] += __shfl_xor_sync(CALS_FULL_MASK, acc[i], o);
-            accb += __shfl_xor_sync(CALS_FULL_MASK, accb, o);
-        }
-        if (cvalid && qg == 0) {
-            float* grow = Gout + (size_t)c * gs;
-#pragma unroll
-            for (int i = 0; i < CPL; ++i) {
-                const int ch = fl + i * LPC;
-                if (ch < nq) {
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const int f = 4 * ch + t;
-                        if (f < nf) grow[f] = acc[4 * i + t] + ((f == c) ? lam_n : 0.f);
-                    }
-                }
-            }
-            if (fl == 0) grow[nf] = accb;
-        }
-        __syncwarp();
-    }
-}
-
-// CPL (16-byte chunks per lane) dispatch: nq <= 4 -> 1, <= 8 -> 2, <= 16 -> 4, else 8.
-__device__ __forceinline__ void sparse_gram(uint32_t xs, int sx, uint32_t ys, uint32_t mb, int mw, int n, int nf, int s,
-                                            bool full, uint32_t lists, int Smax, float lam_n, float* Gout, int warp,
-                                            int nwarps, int lane) {
-    const int nq = xs_chunks(nf);
-    if (nq <= 4) sparse_gram_warp<1>(xs, sx, ys, mb, mw, n, nf, s, full, lists, Smax, lam_n, Gout, warp, nwarps, lane);
-    else if (nq <= 8) sparse_gram_warp<2>(xs, sx, ys, mb, mw, n, nf, s, full, lists, Smax, lam_n, Gout, warp, nwarps, lane);
-    else if (nq <= 16) sparse_gram_warp<4>(xs, sx, ys, mb, mw, n, nf, s, full, lists, Smax, lam_n, Gout, warp, nwarps, lane);
-    else sparse_gram_warp<8>(xs, sx, ys, mb, mw, n, nf, s, full, lists, Smax, lam_n, Gout, warp, nwarps, lane);
-}
 
 // ---------------------------------------------------------------------------
 // Warp-owned variant: the calling warp owns columns c = c_first + j * c_step
@@ -398,16 +185,6 @@ __device__ __forceinline__ void owned_flush(OwnedAcc<CPL>& S, const OwnedMap& M,
         }
         if (M.fl == 0) grow[nf] = S.accb;
     }
-}
-
-__device__ __forceinline__ void sparse_gram_owned_any(uint32_t xs, int sx, uint32_t ys, int nf, int len, bool full,
-                                                      uint32_t lists, int Smax, int c_first, int c_step, int n_cols,
-                                                      float lam_n, float* Gout, int lane) {
-    const int nq = xs_chunks(nf);
-    if (nq <= 4) sparse_gram_owned<1>(xs, sx, ys, nf, len, full, lists, Smax, c_first, c_step, n_cols, lam_n, Gout, lane);
-    else if (nq <= 8) sparse_gram_owned<2>(xs, sx, ys, nf, len, full, lists, Smax, c_first, c_step, n_cols, lam_n, Gout, lane);
-    else if (nq <= 16) sparse_gram_owned<4>(xs, sx, ys, nf, len, full, lists, Smax, c_first, c_step, n_cols, lam_n, Gout, lane);
-    else sparse_gram_owned<8>(xs, sx, ys, nf, len, full, lists, Smax, c_first, c_step, n_cols, lam_n, Gout, lane);
 }
 
 // Kept-row list of one column from its column-major bitmap words (ascending k).

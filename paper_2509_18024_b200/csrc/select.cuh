@@ -17,22 +17,6 @@
 
 namespace cals {
 
-// Candidate list of slice-row indices (uint16, shared memory) into a staged
-// slice column; addresses are 32-bit shared-window addresses.
-struct IdxList {
-    uint32_t xs;     // staged slice base, row stride `stride` floats
-    int stride, c;
-    uint32_t buf;    // compaction buffer (uint16 entries, capacity >= current m)
-    bool identity;   // buf not yet materialised: element i is slice row i
-    __device__ __forceinline__ uint32_t elem(int i) const {
-        return identity ? (uint32_t)i : lds_u16(buf + 2u * (uint32_t)i);
-    }
-    __device__ __forceinline__ uint64_t key_of_elem(uint32_t e) const {
-        return make_key(lds_f32(xs + 4u * (e * (uint32_t)stride + (uint32_t)c)), e);
-    }
-    __device__ __forceinline__ uint64_t key(int i) const { return key_of_elem(elem(i)); }
-    __device__ __forceinline__ void put(int i, uint32_t e) { sts_u16(buf + 2u * (uint32_t)i, e); }
-};
 
 // Candidate list of explicit keys (big rows; may live in global memory).
 struct KeyList {
@@ -49,104 +33,6 @@ __device__ __forceinline__ void choose_bracket(int m, int need, int& a, int& b) 
     int D = (int)(2.5f * sig) + 1;
     a = e - D;
     b = e + D;
-}
-
-// Warp-level select on an index list: returns the need-th largest key
-// (1 <= need <= m) among the m listed candidates, all inside [lo, hi).
-__device__ uint64_t warp_select_idx(IdxList L, int m, int need, uint64_t lo, uint64_t hi, int lane) {
-    while (true) {
-        if (m <= 32) return warp_kth_desc(lane < m ? L.key(lane) : 0ull, m, need, lane);
-        int pos = (int)(((2ll * lane + 1) * (long long)m) >> 6);
-        uint64_t smp = warp_sort_desc(L.key(pos), lane);
-        int a, b;
-        choose_bracket(m, need, a, b);
-        uint64_t nhi = a >= 0 ? __shfl_sync(CALS_FULL_MASK, smp, a) : hi;
-        uint64_t nlo = b <= 31 ? __shfl_sync(CALS_FULL_MASK, smp, b) : lo;
-        int c_hi = 0, c_in = 0;
-        for (int i0 = 0; i0 < m; i0 += 32) {
-            int i = i0 + lane;
-            bool v = i < m;
-            uint64_t kk = v ? L.key(i) : 0ull;
-            c_hi += __popc(__ballot_sync(CALS_FULL_MASK, v && kk >= nhi));
-            c_in += __popc(__ballot_sync(CALS_FULL_MASK, v && kk >= nlo && kk < nhi));
-        }
-        uint64_t rlo, rhi;
-        int nneed;
-        if (c_hi < need && need <= c_hi + c_in) { rlo = nlo; rhi = nhi; nneed = need - c_hi; }
-        else if (c_hi >= need) { rlo = nhi; rhi = hi; nneed = need; }
-        else { rlo = lo; rhi = nlo; nneed = need - c_hi - c_in; }
-        int w = 0;
-        for (int i0 = 0; i0 < m; i0 += 32) {
-            int i = i0 + lane;
-            bool v = i < m;
-            uint32_t e = v ? L.elem(i) : 0u;
-            uint64_t kk = v ? L.key_of_elem(e) : 0ull;
-            bool in = v && kk >= rlo && kk < rhi;
-            uint32_t bal = __ballot_sync(CALS_FULL_MASK, in);
-            if (in) L.put(w + __popc(bal & lanemask_lt()), e);
-            w += __popc(bal);
-        }
-        __syncwarp();
-        L.identity = false;
-        m = w;
-        need = nneed;
-        lo = rlo;
-        hi = rhi;
-    }
-}
-
-// Pre-narrow an index list whose keys all lie in [lo, hi) using the quantile
-// table levels between jhi and jlo as ready-made splitters (no sampling or
-// sorting): one counting pass with kSub-1 ballots per chunk picks the
-// sub-bucket holding the target rank, one pass compacts it.
-__device__ void warp_prenarrow(IdxList& L, int& m, int& need, uint64_t& lo, uint64_t& hi,
-                               const uint32_t* qtab_c, int jhi, int jlo, int lane) {
-    const int span = jlo - jhi;
-    if (span < 2 || m <= 32) return;
-    uint32_t lev[kSub - 1];
-    int cnt[kSub - 1];
-#pragma unroll
-    for (int i = 0; i < kSub - 1; ++i) {
-        lev[i] = qtab_c[jhi + (span * (i + 1)) / kSub];
-        cnt[i] = 0;
-    }
-    for (int i0 = 0; i0 < m; i0 += 32) {
-        const int i = i0 + lane;
-        const bool v = i < m;
-        const uint32_t a = v ? (uint32_t)(L.key(i) >> 32) : 0u;
-#pragma unroll
-        for (int t = 0; t < kSub - 1; ++t) cnt[t] += __popc(__ballot_sync(CALS_FULL_MASK, v && a >= lev[t]));
-    }
-    int b = 0;
-#pragma unroll
-    for (int t = 0; t < kSub - 1; ++t) b += (cnt[t] < need) ? 1 : 0;  // counts are non-decreasing in t
-    int above = 0, upto = m;
-    uint64_t nhi = hi, nlo = lo;
-#pragma unroll
-    for (int t = 0; t < kSub - 1; ++t) {
-        if (t == b - 1) { above = cnt[t]; nhi = (uint64_t)lev[t] << 32; }
-        if (t == b) { upto = cnt[t]; nlo = (uint64_t)lev[t] << 32; }
-    }
-    if (nhi > hi) nhi = hi;
-    if (nlo < lo) nlo = lo;
-    int w = 0;
-    for (int i0 = 0; i0 < m; i0 += 32) {
-        const int i = i0 + lane;
-        const bool v = i < m;
-        const uint32_t e = v ? L.elem(i) : 0u;
-        const uint64_t kk = v ? L.key_of_elem(e) : 0ull;
-        const bool in = v && kk >= nlo && kk < nhi;
-        const uint32_t bal = __ballot_sync(CALS_FULL_MASK, in);
-        if (in) L.put(w + __popc(bal & lanemask_lt()), e);
-        w += __popc(bal);
-    }
-    __syncwarp();
-    L.identity = false;
-    m = w;
-    (void)upto;
-    need -= above;
-    lo = nlo;
-    hi = nhi;
 }
 
 // Warp-level select on a key list (in place).

@@ -17,69 +17,6 @@
 
 namespace cals {
 
-// One warp, lane r owns row r in registers; NFP >= nf (compile-time bound).
-// Pivot-row values are broadcast with shuffles inside the elimination loop,
-// so the only per-lane state is the row itself.
-// Returns 0 ok, 1 failure (zero / non-finite pivot; non-positive when spd).
-template <int NFP>
-__device__ int warp_lu_solve(const float* G, int gs, int nf, bool spd, float* x_out, int lane) {
-    float a[NFP];
-    float rhs = 0.f;
-#pragma unroll
-    for (int j = 0; j < NFP; ++j) a[j] = (lane < nf && j < nf) ? G[lane * gs + j] : ((lane == j) ? 1.f : 0.f);
-    if (lane < nf) rhs = G[lane * gs + nf];
-#pragma unroll
-    for (int k = 0; k < NFP; ++k) {
-        if (k < nf) {
-            int p = k;
-            if (!spd) {
-                float best = (lane >= k && lane < nf) ? fabsf(a[k]) : -1.f;
-                int bi = lane;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    const float ob = __shfl_xor_sync(CALS_FULL_MASK, best, o);
-                    const int oi = __shfl_xor_sync(CALS_FULL_MASK, bi, o);
-                    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-                }
-                if (!(best > 0.f)) return 1;
-                p = bi;
-            }
-            const float d = __shfl_sync(CALS_FULL_MASK, a[k], p);
-            if (spd ? !(d > 0.f) : !(d == d)) return 1;
-            const float rowk_k = __shfl_sync(CALS_FULL_MASK, a[k], k);
-            const float mine = (lane == p) ? rowk_k : a[k];  // column-k entry after the swap
-            const float f = (lane > k && lane < nf) ? mine / d : 0.f;
-#pragma unroll
-            for (int j = 0; j < NFP; ++j) {
-                if (j > k) {
-                    const float vp = __shfl_sync(CALS_FULL_MASK, a[j], p);
-                    const float vk = __shfl_sync(CALS_FULL_MASK, a[j], k);
-                    float v = (lane == k) ? vp : ((lane == p) ? vk : a[j]);
-                    a[j] = fmaf(-f, vp, v);
-                }
-            }
-            if (lane == k) a[k] = d;
-            const float bp = __shfl_sync(CALS_FULL_MASK, rhs, p);
-            const float bk = __shfl_sync(CALS_FULL_MASK, rhs, k);
-            const float bv = (lane == k) ? bp : ((lane == p) ? bk : rhs);
-            rhs = fmaf(-f, bp, bv);
-        }
-    }
-    float x = 0.f;
-#pragma unroll
-    for (int k = NFP - 1; k >= 0; --k) {
-        if (k < nf) {
-            float xk = (lane == k) ? rhs / a[k] : 0.f;
-            xk = __shfl_sync(CALS_FULL_MASK, xk, k);
-            if (lane == k) x = xk;
-            if (lane < k) rhs = fmaf(-a[k], xk, rhs);
-        }
-    }
-    if (lane < nf) x_out[lane] = x;
-    const bool bad = !(x == x) || (x - x != 0.f);
-    return __any_sync(CALS_FULL_MASK, lane < nf && bad) ? 1 : 0;
-}
-
 // Block-wide LU (nf <= 128) in shared memory, in place on W (stride nf+1),
 // working copy of G.  All threads of the block must call it.  Returns 0/1.
 template <typename T>
