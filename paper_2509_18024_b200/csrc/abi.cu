@@ -140,6 +140,8 @@ struct Device {
     int sms = 148;
     size_t smem_optin = 227 * 1024;
     bool init = false;
+    cudaStream_t side = nullptr;  // second stream: the staged tier beside the tiled tier
+    cudaEvent_t fork = nullptr, join = nullptr;
 };
 Device& dev() {
     static Device d;
@@ -152,6 +154,9 @@ Device& dev() {
         int optin = 0;
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, id);
         if (optin > 0) d.smem_optin = (size_t)optin;
+        cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming);
         d.init = true;
     }
     return d;
@@ -257,6 +262,8 @@ struct Work {
     double* retry;
     float* gbuf;
     int64_t gbuf_rows;
+    float* gbuf2;    // staged tier's own normal-equation buffer when both tiers run concurrently
+    double* retry2;  // and its jitter-retry scratch
 };
 
 constexpr int kMaxGrid = 160 * 16;  // grid_for never exceeds min(SMs, 160) * 16 CTAs
@@ -281,6 +288,10 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
     w.retry = c.take<double>((size_t)std::max<int64_t>(kMaxGrid, kMaxSolveWarps) * retry_stride(nf));
     w.gbuf_rows = gbuf_rows_for(nf, P->n_small + P->n_big);
     w.gbuf = c.take<float>((size_t)w.gbuf_rows * nf * (nf + 1));
+    if (P->n_small > 0 && P->n_big > 0) {  // the two tiers run on two streams
+        w.gbuf2 = c.take<float>((size_t)w.gbuf_rows * nf * (nf + 1));
+        w.retry2 = c.take<double>((size_t)std::max<int64_t>(kMaxGrid, kMaxSolveWarps) * retry_stride(nf));
+    }
     *total = c.off + 256;
     return w;
 }
@@ -710,12 +721,31 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
         if (rc) return rc;
     }
     int rc = CALS_OK;
+    // the staged and tiled tiers touch disjoint rows: with both present the staged
+    // tier runs on a second stream (own normal-equation buffer and retry scratch)
+    // beside the tiled tier, filling the SMs its low occupancy leaves idle
+    const bool both = P->n_small > 0 && P->n_big > 0;
+    SweepArgs As = A;
+    cudaStream_t ss = st;
+    if (both) {
+        As.gbuf = w.gbuf2;
+        As.retry_ws = w.retry2;
+        ss = dev().side;
+        cudaEventRecord(dev().fork, st);
+        cudaStreamWaitEvent(ss, dev().fork, 0);
+    }
     if (P->n_small > 0) {
-        if (n_f <= 8) rc = launch_small<8>(A, P, w, st);
-        else if (n_f <= 16) rc = launch_small<16>(A, P, w, st);
-        else if (n_f <= 32) rc = launch_small<32>(A, P, w, st);
-        else rc = launch_small<0>(A, P, w, st);
-        if (rc) return rc;
+        if (n_f <= 8) rc = launch_small<8>(As, P, w, ss);
+        else if (n_f <= 16) rc = launch_small<16>(As, P, w, ss);
+        else if (n_f <= 32) rc = launch_small<32>(As, P, w, ss);
+        else rc = launch_small<0>(As, P, w, ss);
+        if (both) {
+            cudaEventRecord(dev().join, ss);
+        }
+        if (rc) {
+            if (both) cudaStreamWaitEvent(st, dev().join, 0);
+            return rc;
+        }
     }
     if (P->n_big > 0) {
         if (n_f <= 8) rc = launch_big<8>(A, P, w, st);
@@ -723,6 +753,7 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
         else if (n_f <= 32) rc = launch_big<32>(A, P, w, st);
         else rc = launch_big<0>(A, P, w, st);
     }
+    if (both) cudaStreamWaitEvent(st, dev().join, 0);
     return rc;
 }
 
