@@ -250,6 +250,7 @@ def main():
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
     M0 = synth.init_m(data.n_items, n_f)
+    index_line = device_index_check(data, dev)
     eff_rate = 1.0 if args.method == "full" else rate  # full ALS = complete budgets on every row
     eng = (ShardedEngine(data, n_f, eff_rate, lam, rank, world, device=dev, fast=args.method == "fast_core")
            if world > 1 else CoreEngine(data, n_f, eff_rate, lam, device=dev, fast=args.method == "fast_core"))
@@ -337,6 +338,7 @@ def main():
         "clocks": clk.summary(),
         "rmse_prev_iter": float(np.sqrt(terms.rss / core.ssq)),
         "setup_s": {"generate": t_gen},
+        "device_index": index_line,
     }
     if not args.no_cpu and world == 1:
         R_host = data.rating_matrix()
@@ -351,6 +353,28 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     print(json.dumps(line), flush=True)
+
+
+def device_index_check(data, dev):
+    """The dual index built on the device (csrc/index.cu) from the workload's
+    CSR: its time, and that it equals the generator's CSC exactly (a full-size
+    parity property of ratings.py:86-92)."""
+    import torch
+
+    from paper_2509_18024_b200.ratings import csr_to_csc_device
+
+    csr_to_csc_device(data.row_ptr, data.row_items, data.row_vals, data.n_users, data.n_items)  # warm
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    cp, ci, cv = csr_to_csc_device(data.row_ptr, data.row_items, data.row_vals, data.n_users, data.n_items)
+    e1.record()
+    torch.cuda.synchronize()
+    same = bool(torch.equal(cp, data.col_ptr) and torch.equal(ci, data.col_users) and torch.equal(cv, data.col_vals))
+    del cp, ci, cv
+    torch.cuda.empty_cache()
+    return {"csr_to_csc_ms": e0.elapsed_time(e1), "equals_reference_order": same,
+            "ratings_per_s": data.nnz / (e0.elapsed_time(e1) / 1e3)}
 
 
 def e2e(data, spec, M0, steps, rank=0, world=1, method="core"):
@@ -394,15 +418,16 @@ def e2e(data, spec, M0, steps, rank=0, world=1, method="core"):
         wall = float(w.item())
     nnz = R.n_entries
     n_f = spec["n_f"]
-    # copied tensors: both indexes (int64 pointers, int32 indices, float64 values -- narrowed to fp32 on
-    # the device), the fp32 item init (user rows start at zero on the device); back: float64 factors and
-    # 5 float64 objective terms per iteration (per rank at N > 1: each rank uploads the full index)
-    h2d = (R.row_ptr.nbytes + R.col_ptr.nbytes + 2 * nnz * 4 + 2 * nnz * 8 + R.n_items * n_f * 4) * world
+    # copied tensors: the CSR only (int64 pointers, int32 indices, values narrowed to fp32 by torch's
+    # host-side conversion before the copy) -- the CSC is built on the device (csrc/index.cu) -- and the
+    # fp32 item init (user rows start at zero on the device); back: float64 factors and 5 float64
+    # objective terms per iteration (per rank at N > 1: each rank uploads the full CSR)
+    h2d = (R.row_ptr.nbytes + nnz * 4 + nnz * 4 + R.n_items * n_f * 4) * world
     d2h = ((R.n_users + R.n_items) * n_f * 8 + rep.iters_run * 5 * 8) * world
     return {"value": nnz * rep.iters_run / wall, "unit": UNIT, "h2d_bytes_per_step": h2d / rep.iters_run,
             "d2h_bytes_per_step": d2h / rep.iters_run, "wall_s": wall, "iters": rep.iters_run,
-            "how": f"paper_2509_18024_b200.{fit.__name__}(RatingMatrix of numpy arrays) incl. plan, H2D (pageable; the "
-                   "item side's copies overlap the first user half-sweep), all iterations, D2H of float64 "
+            "how": f"paper_2509_18024_b200.{fit.__name__}(RatingMatrix of numpy arrays) incl. plan, H2D of the CSR "
+                   "(pageable), the CSC built on the device beside the first user half-sweep, all iterations, D2H of float64 "
                    "factors; per-step bytes amortised over the fit" + (
                        f"; {world} ranks, ShardedEngine, max wall over ranks" if world > 1 else "")}
 

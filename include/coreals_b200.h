@@ -198,6 +198,31 @@ int cals_fast_half_sweep(const cals_side* side, const cals_plan* plan, const flo
                          const float* target_old, int ld_old, double* rss_rows, double* pen_rows,
                          int32_t* row_status, uint64_t* status_summary, void* ws, size_t ws_bytes, void* stream);
 
+/*
+ * Device dual index (RatingMatrix, ratings.py:54-92): the reference's two host
+ * lexsorts replaced by one device primitive, "group by key, order by
+ * secondary" (paper_2509_18024_b200/csrc/index.cu).  Integer work, exact.
+ *   cals_coo_to_csr: entries (keys[e], secs[e], vals[e]) -> ptr[n_keys + 1],
+ *     out_idx[nnz] = secondaries ascending within each key, out_val[nnz];
+ *     keys must lie in [0, n_keys) and secs in [0, n_sec) (validated by the
+ *     caller, as ratings.py:62-68 does).  dup_out (1 device uint64): the first
+ *     duplicated (key, sec) pair in (key, sec) order as (key << 32) | sec, or
+ *     all ones -- the pair ratings.py:77-82 names in its DataError.
+ *   cals_csr_to_csc: the dual (column-major) index of a CSR whose idx ascend
+ *     within rows: col_ptr[n_cols + 1], col_idx = rows ascending within each
+ *     column, col_val (ratings.py:86-92).
+ *   Workspace: cals_index_workspace_bytes(n_keys, n_sec, nnz) with (n_keys,
+ *   n_sec) = (n_rows, n_cols) for coo_to_csr and (n_cols, n_rows) for
+ *   csr_to_csc.
+ */
+size_t cals_index_workspace_bytes(int64_t n_keys, int64_t n_sec, int64_t nnz);
+int cals_coo_to_csr(const int32_t* keys, const int32_t* secs, const float* vals, int64_t nnz, int64_t n_keys,
+                    int64_t n_sec, int64_t* ptr, int32_t* out_idx, float* out_val, uint64_t* dup_out, void* ws,
+                    size_t ws_bytes, void* stream);
+int cals_csr_to_csc(const int64_t* ptr, const int32_t* idx, const float* val, int64_t n_rows, int64_t n_cols,
+                    int64_t nnz, int64_t* col_ptr, int32_t* col_idx, float* col_val, void* ws, size_t ws_bytes,
+                    void* stream);
+
 /* Optional per-kernel timing with CUDA events recorded on the launch stream
  * (for bench.py's roofline numbers).  collect() synchronises on the recorded
  * events, writes "name launches total_ms" lines into buf, and resets. */

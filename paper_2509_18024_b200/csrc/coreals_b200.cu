@@ -4,3 +4,4 @@
 #include "sweep_solve.cu"
 #include "misc.cu"
 #include "abi.cu"
+#include "index.cu"

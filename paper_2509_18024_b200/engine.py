@@ -43,10 +43,11 @@ class DeviceSide:
     """One side of the rating matrix (CSR over users or CSC over items) on the
     device, with its static schedule (budgets, tiers) and workspace."""
 
-    def __init__(self, ptr, idx, val, n_src, n_f, rate, device, row_begin=0, row_end=None, fast=False):
+    def __init__(self, ptr, idx, val, n_src, n_f, rate, device, row_begin=0, row_end=None, fast=False, ptr_dev=None):
         torch = _lib.require_cuda()
         L = _lib.load()
-        ptr_dev = ptr if torch.is_tensor(ptr) else None
+        if ptr_dev is None and torch.is_tensor(ptr):
+            ptr_dev = ptr
         ptr = np.ascontiguousarray(ptr.cpu().numpy() if torch.is_tensor(ptr) else ptr, dtype=np.int64)
         n_rows = ptr.size - 1
         self.n_rows = n_rows
@@ -220,6 +221,10 @@ class CoreEngine:
             "item": (R.col_ptr, R.col_users, R.col_vals, self.n_users, n_f, rate, device, *ir, fast),
         }
         self._sides = {}
+        # a host matrix ships its CSR only: the CSC (item side) is built from the
+        # device CSR (csrc/index.cu) on a side stream, beside the first half-sweep
+        self._csc_on_device = not torch.is_tensor(R.col_ptr)
+        self._user_ready = None
         # factor rows padded to a multiple of 4 floats (16-byte gathers); padding stays zero
         self.ld = (self.n_f + 3) // 4 * 4
         self.Ub = [torch.zeros((self.n_users, self.ld), dtype=torch.float32, device=device) for _ in range(2)]
@@ -256,8 +261,30 @@ class CoreEngine:
     def _side(self, name):
         s = self._sides.get(name)
         if s is None:
-            s = self._sides[name] = DeviceSide(*self._side_args[name])
+            if name == "item" and self._csc_on_device:
+                s = self._device_csc_side()
+            else:
+                s = DeviceSide(*self._side_args[name])
+            self._sides[name] = s
+            if name == "user":
+                torch = _lib.require_cuda()
+                self._user_ready = torch.cuda.Event()
+                self._user_ready.record(torch.cuda.current_stream(self.device))
         return s
+
+    def _device_csc_side(self):
+        """Item side from the device CSR: the transpose waits only for the user
+        side's uploads (not for a half-sweep already enqueued behind them)."""
+        torch = _lib.require_cuda()
+        from .ratings import csr_to_csc_device
+        u = self.user
+        side_st = torch.cuda.Stream(self.device)
+        side_st.wait_event(self._user_ready)
+        with torch.cuda.stream(side_st):
+            cp, ci, cv = csr_to_csc_device(u.ptr, u.idx, u.val, self.n_users, self.n_items)
+        torch.cuda.current_stream(self.device).wait_stream(side_st)
+        host_ptr, _, _, *rest = self._side_args["item"]
+        return DeviceSide(host_ptr, ci, cv, *rest, ptr_dev=cp)
 
     @property
     def user(self):

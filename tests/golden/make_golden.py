@@ -256,6 +256,49 @@ def metric_cases():
     )
 
 
+def index_cases():
+    """RatingMatrix dual index (ratings.py:54-92) on a shuffled COO with a
+    heavy item (rated by users spanning several 16384-id blocks), a heavy user,
+    empty rows/columns, plus the DataError messages of duplicate inputs."""
+    rng = np.random.default_rng(11)
+    n_users, n_items = 40000, 9000
+    u_heavy = rng.choice(n_users, 20000, replace=False)            # item 7: 20000 raters
+    i_heavy = rng.choice(np.setdiff1d(np.arange(n_items), [7]), 5000, replace=False)  # user 123: 5000 items
+    ru = rng.integers(0, n_users, 12000)
+    ri = rng.integers(0, n_items, 12000)
+    users = np.concatenate([u_heavy, np.full(5000, 123), ru])
+    items = np.concatenate([np.full(20000, 7), i_heavy, ri])
+    key = users * n_items + items
+    _, first = np.unique(key, return_index=True)
+    keep = np.sort(first)
+    users, items = users[keep], items[keep]
+    users[users == 5] = 6          # user 5: empty row
+    items[items == 11] = 12        # item 11: empty column
+    key = users * n_items + items
+    _, first = np.unique(key, return_index=True)
+    users, items = users[np.sort(first)], items[np.sort(first)]
+    perm = rng.permutation(users.size)
+    users, items = users[perm], items[perm]
+    vals = f32(np.round(rng.normal(3.0, 1.0, users.size), 1))
+    R = RatingMatrix(users, items, vals, n_users=n_users, n_items=n_items)
+    dups = {}
+    for name, (du, di) in {
+        "dup_simple": ([3, 1, 3, 0], [2, 4, 2, 9]),
+        "dup_two": ([9, 2, 5, 2, 9, 5], [1, 8, 3, 8, 1, 3]),   # (2,8) named, not (5,3) or (9,1)
+        "dup_many": ([4] * 40 + [1, 1], [7] * 40 + [0, 0]),    # first pair (1,0)
+    }.items():
+        try:
+            RatingMatrix(np.array(du), np.array(di), np.ones(len(du)))
+        except coreals.DataError as e:
+            dups[name] = str(e)
+    np.savez_compressed(os.path.join(OUT, "index_cases.npz"), users=users.astype(np.int32),
+                        items=items.astype(np.int32), vals=vals.astype(np.float32), n_users=n_users,
+                        n_items=n_items, row_ptr=R.row_ptr, row_items=R.row_items,
+                        row_vals=R.row_vals.astype(np.float32), col_ptr=R.col_ptr, col_users=R.col_users,
+                        col_vals=R.col_vals.astype(np.float32),
+                        dup_names=np.array(list(dups)), dup_msgs=np.array(list(dups.values())))
+
+
 def fast_cases():
     fast_case("small", 5, 200, 150, 0.2, 8, 0.1, 0.3, 4)
     # sparse slices (empty sketched columns -> fallback), ties, an empty user
@@ -269,6 +312,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if sys.argv[1:] == ["fast"]:
         fast_cases()
+        sys.exit(0)
+    if sys.argv[1:] == ["index"]:
+        index_cases()
         sys.exit(0)
     if sys.argv[1:] == ["metrics"]:
         metric_cases()
@@ -287,4 +333,5 @@ if __name__ == "__main__":
     full_case("full", 4, 120, 90, 0.3, 8, 0.1, 4, drop_user=7)
     fast_cases()
     metric_cases()
+    index_cases()
     print("golden fixtures written to", OUT)
