@@ -27,7 +27,7 @@ import threading
 
 import numpy as np
 
-from . import _lib
+from . import _lib, hostio
 from .errors import ConfigError
 
 __all__ = ["DeviceSide", "CoreEngine", "IterationTerms"]
@@ -91,7 +91,7 @@ class DeviceSide:
         def t(a, dt):
             if torch.is_tensor(a):
                 return a.to(device=device, dtype=dt).contiguous()
-            return torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dt)
+            return hostio.upload(a, dt, device)
 
         self.ptr = t(ptr_dev if ptr_dev is not None else ptr, torch.int64)
         self.idx = t(idx, torch.int32)
@@ -315,11 +315,13 @@ class CoreEngine:
         """Initial factors into BOTH buffers (rows without ratings never change)."""
         torch = _lib.require_cuda()
         if U is not None:
-            u = torch.as_tensor(np.asarray(U, dtype=np.float32)).to(self.device)
+            u = U.to(self.device, torch.float32) if torch.is_tensor(U) else hostio.upload(np.asarray(U), torch.float32,
+                                                                                         self.device)
             for b in self.Ub:
                 b[:, :self.n_f].copy_(u)
         if M is not None:
-            m = torch.as_tensor(np.asarray(M, dtype=np.float32)).to(self.device)
+            m = M.to(self.device, torch.float32) if torch.is_tensor(M) else hostio.upload(np.asarray(M), torch.float32,
+                                                                                         self.device)
             for b in self.Mb:
                 b[:, :self.n_f].copy_(m)
         self.iters_done = 0
@@ -414,4 +416,4 @@ class CoreEngine:
 
     def factors_host(self):
         # widen on the device: the float64 copy-out is cheaper than a host conversion
-        return self.U_view.double().cpu().numpy(), self.M_view.double().cpu().numpy()
+        return hostio.download_f64(self.U_view), hostio.download_f64(self.M_view)
