@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <numeric>
 #include <vector>
@@ -18,9 +19,19 @@ namespace {
 
 constexpr size_t kSmemBudget = 224 * 1024;  // dynamic shared memory per CTA (B200 opt-in max is 227 KB)
 constexpr int kQSsmall = 4096, kQSbig = 8192;
-constexpr int kItemRowsMin = 4096;
+constexpr int kItemRowsMin = 16384;  // slice rows per work item (sweep on the 500M config: 4096 -> 16384 = -2.4 %)
 
 thread_local char g_err[256] = "";
+
+// tuning overrides for experiments (unset: the built-in defaults)
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e != nullptr ? std::atoi(e) : dflt;
+}
+double env_double(const char* name, double dflt) {
+    const char* e = std::getenv(name);
+    return e != nullptr ? std::atof(e) : dflt;
+}
 int64_t g_big_cand_budget = 0, g_big_tile_budget = 0;  // debug overrides, see cals_debug_big_batch
 unsigned long long* g_stats = nullptr;  // debug counters (device), see cals_debug_stats
 
@@ -443,6 +454,8 @@ int launch_fast(const SweepArgs& A, const cals_plan* P, const Work& w, const uin
     for (size_t bi = 0; bi + 1 < bb.r.size(); ++bi) {
         const int64_t r0 = bb.r[bi], r1 = bb.r[bi + 1];
         BigArgs B{};
+        B.calib_samples = env_int("CALS_CALIB_M", 0);
+        B.calib_z = (float)env_double("CALS_CALIB_Z", 0.0);
         B.rows = P->big_rows + r0;
         B.tile_ptr = P->big_tile_ptr + r0;
         B.cand_ptr = P->big_cand_ptr + r0;
@@ -510,6 +523,8 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
             while (n_calib < P->n_big && tp[n_calib + 1] - tp[n_calib] >= 2) ++n_calib;
         if (n_calib > 0) {
             BigArgs C{};
+            C.calib_samples = env_int("CALS_CALIB_M", 0);
+            C.calib_z = (float)env_double("CALS_CALIB_Z", 0.0);
             C.rows = P->big_rows;
             C.n_big = n_calib;
             C.brk = w.brk;
@@ -523,6 +538,8 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
     for (size_t bi = 0; bi + 1 < bb.r.size(); ++bi) {
         const int64_t r0 = bb.r[bi], r1 = bb.r[bi + 1];
         BigArgs B{};
+        B.calib_samples = env_int("CALS_CALIB_M", 0);
+        B.calib_z = (float)env_double("CALS_CALIB_Z", 0.0);
         B.rows = P->big_rows + r0;
         B.tile_ptr = P->big_tile_ptr + r0;
         B.cand_ptr = P->big_cand_ptr + r0;
@@ -642,7 +659,7 @@ int cals_plan_build(const int64_t* counts, int64_t n_rows, int n_f, double rate,
     meta->small_seg[3] = pos;
     // big rows: work items and candidate buffers
     const int chunk = big_chunk(n_f);
-    meta->item_rows = std::max(kItemRowsMin, chunk);
+    meta->item_rows = std::max(env_int("CALS_ITEM_ROWS", kItemRowsMin), chunk);
     const float dtab = delta_tab_for(kQSbig);
     big_tile_ptr[0] = 0;
     big_cand_ptr[0] = 0;
@@ -774,7 +791,7 @@ int cals_plan_build_fast(const int64_t* counts, int64_t n_rows, int n_f, int com
                      [counts](int32_t a, int32_t b) { return counts[a] != counts[b] ? counts[a] > counts[b] : a < b; });
     std::copy(act.begin(), act.end(), rows);
     meta->n_big = (int64_t)act.size();
-    meta->item_rows = std::max(kItemRowsMin, big_chunk(n_f));
+    meta->item_rows = std::max(env_int("CALS_ITEM_ROWS", kItemRowsMin), big_chunk(n_f));
     tile_ptr[0] = 0;
     cand_ptr[0] = 0;
     for (size_t r = 0; r < act.size(); ++r) {

@@ -55,11 +55,12 @@ __global__ void __launch_bounds__(kThreads) big_calib_kernel(SweepArgs A, BigArg
         const int n = (int)(A.ptr[row + 1] - lo);
         const int s = A.budget[row];
         if (s >= n) continue;
-        const int m = min(kCalibSamples, max(1024, n / 4));  // n > 4096 here
+        const int m = min(B.calib_samples > 0 ? B.calib_samples : kCalibSamples, max(1024, n / 4));  // n > 4096 here
         const double p = (double)s / (double)n;
         const double sig = sqrt(p * (1.0 - p) / (double)m * (double)(n - m) / (double)max(n - 1, 1));
-        const int t_lo = (int)floor((p - kCalibZ * sig) * (double)m);
-        const int t_hi = (int)ceil((p + kCalibZ * sig) * (double)m);
+        const double z = B.calib_z > 0.f ? B.calib_z : kCalibZ;
+        const int t_lo = (int)floor((p - z * sig) * (double)m);
+        const int t_hi = (int)ceil((p + z * sig) * (double)m);
         for (int c0 = 0; c0 < nf; c0 += kCalibCols) {
             const int gc = min(kCalibCols, nf - c0);
             __syncthreads();

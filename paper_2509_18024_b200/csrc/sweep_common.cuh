@@ -79,6 +79,8 @@ struct BigArgs {
     // the whole source instead of per-row thresholds
     const uint32_t* gmask;    // [n_src][gwords] bit c%32 of word c/32: source row kept for column c
     int gwords;
+    int calib_samples;        // tuning overrides (0: defaults kCalibSamples / kCalibZ)
+    float calib_z;
     int* fcnt;                // [n_big][nf] kept slice rows per column (multi-item rows)
     unsigned long long* famax;  // [n_big][nf] max key (abs_bits << 32 | ~k) per column (fallback row)
 };
