@@ -292,7 +292,8 @@ def main():
 
     e2e_line = None
     if not args.no_e2e:
-        e2e_line = e2e(data, spec, M0, args.steps, rank, world, args.method)
+        # a whole fit of the workload as its config states it (large: 10 iterations), from host arrays
+        e2e_line = e2e(data, spec, M0, spec["iters"], rank, world, args.method)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -378,8 +379,9 @@ def device_index_check(data, dev):
 
 
 def e2e(data, spec, M0, steps, rank=0, world=1, method="core"):
-    """fit_core through the public API from host (numpy) arrays: H2D of both
-    indexes and the init, `steps` iterations, D2H of both factor matrices.
+    """fit_core through the public API from host (numpy) arrays: H2D of the
+    CSR and the init, `steps` iterations (the config's own count), D2H of both
+    factor matrices.
     With N > 1 ranks every rank runs fit_core on its row shard (ShardedEngine,
     NCCL all-gather per half-sweep); wall = max over ranks."""
     import warnings
