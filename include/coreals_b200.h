@@ -84,6 +84,7 @@ typedef struct cals_plan {
     const int64_t* big_tile_ptr_host;  /* host copies (caller-owned) used to batch the tiled tier */
     const int64_t* big_cand_ptr_host;
     const int32_t* big_tile_row;  /* optional device [n_big_tiles]: big row of each work item (else searched) */
+    int64_t n_rows;               /* rows of the side (sizes the per-row selection thresholds) */
 } cals_plan;
 
 /* Host: reference budget rule for every row (core.py:48-54), fp64, no FMA. */

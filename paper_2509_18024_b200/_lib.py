@@ -31,7 +31,7 @@ class cals_plan(ctypes.Structure):
         ("big_rows", P), ("n_big", i64), ("big_tile_ptr", P), ("n_big_tiles", i64),
         ("big_cand_ptr", P), ("big_cand_total", i64), ("item_rows", ctypes.c_int32),
         ("n_f", ctypes.c_int32),
-        ("big_tile_ptr_host", P), ("big_cand_ptr_host", P), ("big_tile_row", P),
+        ("big_tile_ptr_host", P), ("big_cand_ptr_host", P), ("big_tile_row", P), ("n_rows", i64),
     ]
 
 

@@ -117,8 +117,9 @@ size_t big_gram_smem(int nf, int chunk, int gwords = 0) {
     const bool persist = owned_single_round(nf, threads / 32);
     const size_t g = persist ? 0 : align16((size_t)nf * (nf + 1) * 4);
     const size_t lists = persist ? 0 : (size_t)nf * chunk * 2 + (size_t)nf * 4;
+    const size_t g64 = persist ? (size_t)nf * (nf + 1) * 8 : 0;  // float64 Gram accumulators
     return align16((size_t)chunk * sx * 4) + align16((size_t)chunk * 4) + g +
-           align16((size_t)nf * (chunk / 32) * 4 + lists + (size_t)chunk * gwords * 4);
+           align16((size_t)nf * (chunk / 32) * 4 + lists + (size_t)chunk * gwords * 4) + g64;
 }
 
 size_t big_scan_smem(int nf, int chunk) {
@@ -264,17 +265,20 @@ struct Work {
     int* cnt;
     uint64_t* cand;
     uint64_t* thr;
-    float* part;
+    double* part;
     double* rss_part;
     int* hist;
     uint32_t* brk;
     int* fcnt;
     unsigned long long* famax;
     double* retry;
-    float* gbuf;
+    double* gbuf;
     int64_t gbuf_rows;
-    float* gbuf2;    // staged tier's own normal-equation buffer when both tiers run concurrently
+    double* gbuf2;    // staged tier's own normal-equation buffer when both tiers run concurrently
     double* retry2;  // and its jitter-retry scratch
+    uint64_t* thr_all;  // [n_rows][nf] selection thresholds (when the caller asks for none)
+    int* rf_cnt;        // [2] rows deferred to the float64 refinement, per stream
+    int64_t* rf_list;   // [2][gbuf_rows] (row << 32 | gbuf slot)
 };
 
 constexpr int kMaxGrid = 160 * 16;  // grid_for never exceeds min(SMs, 160) * 16 CTAs
@@ -290,7 +294,7 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
     w.cnt = c.take<int>((size_t)bb.max_rows * nf * 2);
     w.cand = c.take<uint64_t>((size_t)bb.max_cand);
     w.thr = c.take<uint64_t>((size_t)bb.max_rows * nf);
-    w.part = c.take<float>((size_t)bb.max_tiles * nf * (nf + 1));
+    w.part = c.take<double>((size_t)bb.max_tiles * nf * (nf + 1));
     w.rss_part = c.take<double>((size_t)bb.max_tiles);
     w.hist = c.take<int>((size_t)bb.max_rows * nf * kHB);
     w.brk = c.take<uint32_t>((size_t)std::max<int64_t>(P->n_big, 1) * nf);  // all big rows (one calibration pass)
@@ -298,18 +302,45 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
     w.famax = c.take<unsigned long long>((size_t)bb.max_rows * nf);      // fast_core: fallback keys
     w.retry = c.take<double>((size_t)std::max<int64_t>(kMaxGrid, kMaxSolveWarps) * retry_stride(nf));
     w.gbuf_rows = gbuf_rows_for(nf, P->n_small + P->n_big);
-    w.gbuf = c.take<float>((size_t)w.gbuf_rows * nf * (nf + 1));
+    w.gbuf = c.take<double>((size_t)w.gbuf_rows * nf * (nf + 1));
     if (P->n_small > 0 && P->n_big > 0) {  // the two tiers run on two streams
-        w.gbuf2 = c.take<float>((size_t)w.gbuf_rows * nf * (nf + 1));
+        w.gbuf2 = c.take<double>((size_t)w.gbuf_rows * nf * (nf + 1));
         w.retry2 = c.take<double>((size_t)std::max<int64_t>(kMaxGrid, kMaxSolveWarps) * retry_stride(nf));
     }
+    w.thr_all = c.take<uint64_t>((size_t)std::max<int64_t>(P->n_rows, 1) * nf);
+    w.rf_cnt = c.take<int>(2);
+    w.rf_list = c.take<int64_t>((size_t)2 * w.gbuf_rows);
     *total = c.off + 256;
     return w;
 }
 
 template <int NFP>
-void launch_solve(const SweepArgs& A, const int32_t* rows, int64_t count, cudaStream_t st) {
+void launch_solve_fp32(const SweepArgs& A, const int32_t* rows, int64_t count, cudaStream_t st);
+
+// float64 recomputation of the systems the fp32 solve deferred (the count stays
+// on the device; one CTA per SM walks the list), then the list is reset
+void launch_refine(const SweepArgs& A, cudaStream_t st, int slice_ok) {
+    ProfScope ps("refine_kernel", st);
+    const size_t sm = refine_smem(A.nf);
+    if (refine_threads(A.nf) == 256) {
+        allow_smem(refine_kernel<256>);
+        refine_kernel<256><<<dev().sms * 4, 256, sm, st>>>(A, A.rf_cnt, A.rf_list, slice_ok);
+    } else {
+        allow_smem(refine_kernel<512>);
+        refine_kernel<512><<<dev().sms * 2, 512, sm, st>>>(A, A.rf_cnt, A.rf_list, slice_ok);
+    }
+    cudaMemsetAsync(A.rf_cnt, 0, sizeof(int), st);
+}
+
+template <int NFP>
+void launch_solve(const SweepArgs& A, const int32_t* rows, int64_t count, cudaStream_t st, int slice_ok = 1) {
     if (count <= 0) return;
+    launch_solve_fp32<NFP>(A, rows, count, st);
+    launch_refine(A, st, slice_ok);
+}
+
+template <int NFP>
+void launch_solve_fp32(const SweepArgs& A, const int32_t* rows, int64_t count, cudaStream_t st) {
     ProfScope ps("solve_kernel", st);
     if constexpr (NFP > 0) {
         const int64_t warps = (count + (32 / NFP) - 1) / (32 / NFP);
@@ -501,7 +532,7 @@ int launch_fast(const SweepArgs& A, const cals_plan* P, const Work& w, const uin
             fast_fix_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)dev().sms * 8)),
                               kThreads, 0, st>>>(A, B);
         }
-        launch_solve<NFP>(A, B.rows, B.n_big, st);
+        launch_solve<NFP>(A, B.rows, B.n_big, st, 0);
         const int rc = cuda_status("fast_core kernels");
         if (rc) return rc;
     }
@@ -628,6 +659,7 @@ int cals_plan_build(const int64_t* counts, int64_t n_rows, int n_f, double rate,
     if (rc) return rc;
     std::memset(meta, 0, sizeof(*meta));
     meta->n_f = n_f;
+    meta->n_rows = n_rows;
     const int nmax = small_nmax(n_f, rate);
     std::vector<int32_t> small, big;
     for (int64_t i = 0; i < n_rows; ++i) {
@@ -715,7 +747,16 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.ld_old = ld_old;
     A.rss_rows = rss_rows;
     A.pen_rows = pen_rows;
-    A.thr_keys = thr_keys;
+    A.thr_keys = thr_keys != nullptr ? thr_keys : w.thr_all;  // the float64 refinement reads them
+    {
+        static thread_local float ratio;  // host source of the async copy outlives the call
+        ratio = (float)env_double("CALS_ILL_RATIO", ill_ratio_for(n_f));
+        cudaMemcpyToSymbolAsync(g_ill_ratio, &ratio, sizeof(float), 0, cudaMemcpyHostToDevice, st);
+    }
+    A.rf_cnt = w.rf_cnt;
+    A.rf_list = w.rf_list;
+    A.rf_slice_max = env_int("CALS_RF_SLICE_MAX", 0);
+    cudaMemsetAsync(w.rf_cnt, 0, 2 * sizeof(int), st);
     A.gbuf = w.gbuf;
     A.stats = g_stats;
     A.status = row_status;
@@ -747,6 +788,8 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     if (both) {
         As.gbuf = w.gbuf2;
         As.retry_ws = w.retry2;
+        As.rf_cnt = w.rf_cnt + 1;
+        As.rf_list = w.rf_list + w.gbuf_rows;
         ss = dev().side;
         cudaEventRecord(dev().fork, st);
         cudaStreamWaitEvent(ss, dev().fork, 0);
@@ -780,6 +823,7 @@ int cals_plan_build_fast(const int64_t* counts, int64_t n_rows, int n_f, int com
     if (n_f < 1 || n_f > CALS_MAX_NF || n_rows < 0 || n_rows > 0x7fffffff) return CALS_ERR_ARG;
     std::memset(meta, 0, sizeof(*meta));
     meta->n_f = n_f;
+    meta->n_rows = n_rows;
     std::vector<int32_t> act;
     for (int64_t i = 0; i < n_rows; ++i) {
         if (counts[i] > 0x7fffffffLL) return CALS_ERR_UNSUPPORTED;
@@ -863,6 +907,16 @@ int cals_fast_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.ld_old = ld_old;
     A.rss_rows = rss_rows;
     A.pen_rows = pen_rows;
+    A.thr_keys = w.thr_all;
+    {
+        static thread_local float ratio;
+        ratio = (float)env_double("CALS_ILL_RATIO", ill_ratio_for(n_f));
+        cudaMemcpyToSymbolAsync(g_ill_ratio, &ratio, sizeof(float), 0, cudaMemcpyHostToDevice, st);
+    }
+    A.rf_cnt = w.rf_cnt;
+    A.rf_list = w.rf_list;
+    A.rf_slice_max = env_int("CALS_RF_SLICE_MAX", 0);
+    cudaMemsetAsync(w.rf_cnt, 0, 2 * sizeof(int), st);
     A.gbuf = w.gbuf;
     A.stats = g_stats;
     A.status = row_status;

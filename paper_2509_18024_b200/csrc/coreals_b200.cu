@@ -2,6 +2,7 @@
 #include "sweep_small.cu"
 #include "sweep_big.cu"
 #include "sweep_solve.cu"
+#include "sweep_refine.cu"
 #include "misc.cu"
 #include "abi.cu"
 #include "index.cu"

@@ -19,10 +19,10 @@ namespace cals {
 // processed in rounds of CT (power of two, CT * LPC <= 32); q-groups QG split
 // each list round-robin and are reduced with shuffles in a fixed order.
 // ---------------------------------------------------------------------------
-template <int CPL>
+template <int CPL, typename OT>
 __device__ __forceinline__ void sparse_gram_owned(uint32_t xs, int sx, uint32_t ys, int nf, int len, bool full,
                                                   uint32_t lists, int Smax, int c_first, int c_step, int n_cols,
-                                                  float lam_n, float* __restrict__ Gout, int lane,
+                                                  float lam_n, OT* __restrict__ Gout, int lane,
                                                   bool accumulate = false) {
     const int nq = xs_chunks(nf);
     const int LPC = nq < 4 ? nq : 4;
@@ -66,7 +66,7 @@ __device__ __forceinline__ void sparse_gram_owned(uint32_t xs, int sx, uint32_t 
             accb += __shfl_xor_sync(CALS_FULL_MASK, accb, o);
         }
         if (cvalid && qg == 0) {
-            float* grow = Gout + (size_t)c * gs;
+            OT* grow = Gout + (size_t)c * gs;
 #pragma unroll
             for (int i = 0; i < CPL; ++i) {
                 const int ch = fl + i * LPC;
@@ -74,11 +74,12 @@ __device__ __forceinline__ void sparse_gram_owned(uint32_t xs, int sx, uint32_t 
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
                         const int f = 4 * ch + t;
-                        if (f < nf) grow[f] = (accumulate ? grow[f] : 0.f) + acc[4 * i + t] + ((f == c) ? lam_n : 0.f);
+                        if (f < nf)
+                            grow[f] = (accumulate ? grow[f] : (OT)0) + (OT)acc[4 * i + t] + ((f == c) ? (OT)lam_n : (OT)0);
                     }
                 }
             }
-            if (fl == 0) grow[nf] = (accumulate ? grow[nf] : 0.f) + accb;
+            if (fl == 0) grow[nf] = (accumulate ? grow[nf] : (OT)0) + (OT)accb;
         }
         __syncwarp();
     }
@@ -184,6 +185,63 @@ __device__ __forceinline__ void owned_flush(OwnedAcc<CPL>& S, const OwnedMap& M,
             }
         }
         if (M.fl == 0) grow[nf] = S.accb;
+    }
+}
+
+// Fold the chunk's fp32 sums into float64 shared-memory accumulators G64
+// ([nf][nf+1] doubles) and restart them at zero: fp32 only ever sums one staged
+// chunk's kept rows (tens of terms), so the Gram of a long row carries float64
+// accumulation error instead of the fp32 error of a 16384-row sequential sum
+// (measured on the 500M config: that error dominated the factor error of
+// ill-conditioned long rows).  q-groups are reduced first (fixed order).
+template <int CPL>
+__device__ __forceinline__ void owned_fold(OwnedAcc<CPL>& S, const OwnedMap& M, int nf, double* __restrict__ G64) {
+    const int nq = xs_chunks(nf);
+    const int gs = nf + 1;
+    for (int o = M.LPC; o < M.LPC * M.QG; o <<= 1) {
+#pragma unroll
+        for (int i = 0; i < 4 * CPL; ++i) S.acc[i] += __shfl_xor_sync(CALS_FULL_MASK, S.acc[i], o);
+        S.accb += __shfl_xor_sync(CALS_FULL_MASK, S.accb, o);
+    }
+    if (M.cvalid && M.qg == 0) {
+        double* grow = G64 + (size_t)M.c * gs;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            const int ch = M.fl + i * M.LPC;
+            if (ch < nq) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int f = 4 * ch + t;
+                    if (f < nf) grow[f] += (double)S.acc[4 * i + t];
+                }
+            }
+        }
+        if (M.fl == 0) grow[nf] += (double)S.accb;
+    }
+    S.zero();
+}
+
+// Write row M.c of the normal equations from G64 (+ lam_n on the diagonal, in float64).
+template <int CPL>
+__device__ __forceinline__ void owned_flush64(const OwnedMap& M, int nf, const double* __restrict__ G64,
+                                              double* __restrict__ out, double lam_n) {
+    const int nq = xs_chunks(nf);
+    const int gs = nf + 1;
+    if (M.cvalid && M.qg == 0) {
+        const double* grow = G64 + (size_t)M.c * gs;
+        double* orow = out + (size_t)M.c * gs;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            const int ch = M.fl + i * M.LPC;
+            if (ch < nq) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int f = 4 * ch + t;
+                    if (f < nf) orow[f] = grow[f] + ((f == M.c) ? lam_n : 0.0);
+                }
+            }
+        }
+        if (M.fl == 0) orow[nf] = grow[nf];
     }
 }
 

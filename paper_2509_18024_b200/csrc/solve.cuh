@@ -92,21 +92,38 @@ __device__ int block_lu_solve(T* W, int nf, bool spd, T* x_out, int* s_piv) {
 // pivot row of step k is broadcast once and every unused row is eliminated
 // against it; back substitution walks the pivot order.  Same arithmetic as
 // row-swapping LU (first max |a| wins ties, like LAPACK idamax).
+// fp32 elimination accuracy guard: the fp32 LU's error grows like the system's
+// condition number (measured: ~6e-9 * cond), and the factor contract is 1e-4
+// relative to the reference's float64 solve.  A spread of pivot magnitudes
+// beyond the rank's ratio (a lower bound on cond) sends the system to the float64
+// path (warp_retry_f64: plain float64 first, the reference's jitter only if
+// that is singular too), exactly like an fp32 breakdown.
+// Ratio by rank (the fp32 elimination's error also grows with n_f): 100 up to
+// n_f = 20, then 2000 / n_f (31 at 64), and 1000 / n_f above 64 (8 at 128);
+// set per half-sweep (ill_ratio_for).  Measured on the 500M config at a later
+// iteration (tools/ill_diag.py) and on the wide config's short rows.
+__host__ inline float ill_ratio_for(int nf) {
+    return nf <= 20 ? 100.0f : (nf <= 64 ? 2000.0f / (float)nf : 1000.0f / (float)nf);
+}
+__device__ float g_ill_ratio = 100.0f;
+__device__ __forceinline__ bool ill_conditioned(float dmin, float dmax) { return dmax > g_ill_ratio * dmin; }
+
 // Returns, per lane, whether ITS system failed (uniform within a segment);
 // x: the lane's unknown (variable r of its system).
 template <int NFP>
-__device__ __forceinline__ bool seg_lu_solve(const float* __restrict__ Grow, int nf, bool spd, bool seg_valid,
+__device__ __forceinline__ bool seg_lu_solve(const double* __restrict__ Grow, int nf, bool spd, bool seg_valid,
                                              float& x, int lane) {
     const int r = lane & (NFP - 1);
     const bool rv = seg_valid && r < nf;
     float a[NFP];
     float rhs = 0.f;
 #pragma unroll
-    for (int j = 0; j < NFP; ++j) a[j] = (rv && j < nf) ? Grow[j] : 0.f;
-    if (rv) rhs = Grow[nf];
+    for (int j = 0; j < NFP; ++j) a[j] = (rv && j < nf) ? (float)Grow[j] : 0.f;
+    if (rv) rhs = (float)Grow[nf];
     bool used = !rv;
     int ord = -1;
     bool fail = !seg_valid;
+    float dmin = INFINITY, dmax = 0.f;  // pivot magnitudes: their spread flags ill-conditioning
 #pragma unroll
     for (int k = 0; k < NFP; ++k) {
         if (k < nf) {
@@ -123,6 +140,8 @@ __device__ __forceinline__ bool seg_lu_solve(const float* __restrict__ Grow, int
             if (!spd) fail |= !(best > 0.f);
             const float d = __shfl_sync(CALS_FULL_MASK, a[k], p, NFP);
             fail |= spd ? !(d > 0.f) : !(d == d);
+            dmin = fminf(dmin, fabsf(d));
+            dmax = fmaxf(dmax, fabsf(d));
             const bool me = (r == p);
             if (me) { used = true; ord = k; }
             const float f = (!used && !fail) ? a[k] / d : 0.f;
@@ -154,7 +173,7 @@ __device__ __forceinline__ bool seg_lu_solve(const float* __restrict__ Grow, int
     const bool bad = rv && (!(x == x) || (x - x != 0.f));
     const uint32_t anybad = __ballot_sync(CALS_FULL_MASK, bad);
     const uint32_t segm = (NFP == 32) ? 0xffffffffu : (((1u << NFP) - 1u) << seg_base);
-    return fail || (anybad & segm) != 0;
+    return fail || ill_conditioned(dmin, dmax) || (anybad & segm) != 0;
 }
 
 // Wide warp LU (32 < nf <= NF <= 64): lane owns rows `lane` and `lane + 32`
@@ -177,6 +196,7 @@ struct WideLU {
     float ra, rb;
     bool ua, ub, fail;
     int oa, ob;
+    float dmin, dmax;
 };
 
 // Elimination steps K in [B0, B0 + 16) (a runtime loop: the fully unrolled
@@ -215,6 +235,8 @@ __device__ __forceinline__ void wide_block(WideLU<NF>& S, bool spd, int lane) {
         const int pl = p & 31;
         const float d = __shfl_sync(CALS_FULL_MASK, sel_f32(hi, cb, ca), pl);
         S.fail |= spd ? !(d > 0.f) : !(d == d);
+        S.dmin = fminf(S.dmin, fabsf(d));
+        S.dmax = fmaxf(S.dmax, fabsf(d));
         if (lane == pl) {
             if (hi) { S.ub = true; S.ob = K; } else { S.ua = true; S.oa = K; }
         }
@@ -280,22 +302,26 @@ __device__ __forceinline__ bool wide_lu_solve(const float* __restrict__ W, int n
     S.oa = -1;
     S.ob = -1;
     S.fail = false;
+    S.dmin = INFINITY;
+    S.dmax = 0.f;
     wide_eliminate<NF>(S, spd, lane, std::make_integer_sequence<int, (NF + 15) / 16>{});
     x0 = 0.f;
     x1 = 0.f;
     wide_substitute<NF>(S, x0, x1, lane, std::make_integer_sequence<int, NF>{});
     const bool bad = (v0 && (!(x0 == x0) || (x0 - x0 != 0.f))) || (v1 && (!(x1 == x1) || (x1 - x1 != 0.f)));
-    return S.fail || __any_sync(CALS_FULL_MASK, bad);
+    return S.fail || ill_conditioned(S.dmin, S.dmax) || __any_sync(CALS_FULL_MASK, bad);
 }
 
-// Float64 retry of a failed system with the reference's diagonal jitter
-// 1e-10 * tr(G) / nf (core.py:126-131, als.py:191-197).  One warp, lanes over
+// Float64 solve of a system the fp32 path failed or flagged, optionally with the
+// reference's diagonal jitter 1e-10 * tr(G) / nf (core.py:126-131, als.py:191-197):
+// the callers run it plain first and jittered only when that is singular, as the
+// reference retries only after LinAlgError.  One warp, lanes over
 // columns, scratch W (nf*(nf+1) doubles, any memory).  Rare path.
-__device__ int warp_retry_f64(const float* G, int nf, bool spd, double* W, double* x, int lane) {
+__device__ int warp_retry_f64(const double* G, int nf, bool spd, double* W, double* x, int lane, bool jitter) {
     const int gs = nf + 1;
     double tr = 0.0;
     for (int c = 0; c < nf; ++c) tr += (double)G[c * gs + c];
-    const double jit = 1e-10 * tr / (double)nf;
+    const double jit = jitter ? 1e-10 * tr / (double)nf : 0.0;
     for (int e = lane; e < nf * gs; e += 32) {
         const int c = e / gs, f = e - c * gs;
         W[e] = (double)G[e] + ((c == f) ? jit : 0.0);
@@ -340,6 +366,14 @@ __device__ int warp_retry_f64(const float* G, int nf, bool spd, double* W, doubl
     }
     __syncwarp();
     return __shfl_sync(CALS_FULL_MASK, bad, 0);
+}
+
+// Plain float64 solve, then (if singular) the jittered retry.  Returns the
+// row status (CALS_ROW_OK / JITTERED / SINGULAR); x holds the solution.
+__device__ int warp_solve_f64(const double* G, int nf, bool spd, double* W, double* x, int lane) {
+    if (!warp_retry_f64(G, nf, spd, W, x, lane, false)) return CALS_ROW_OK;
+    __syncwarp();
+    return warp_retry_f64(G, nf, spd, W, x, lane, true) ? CALS_ROW_SINGULAR : CALS_ROW_JITTERED;
 }
 
 }  // namespace cals

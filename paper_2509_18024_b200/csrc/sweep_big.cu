@@ -336,6 +336,8 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
 // n_f > 64 (CPL 8) runs 512-thread CTAs: 16 warps own <= 8 columns each, so the
 // accumulators stay register-resident (owned_single_round) instead of in shared memory.
 constexpr int big_gram_threads(int cpl) { return cpl >= 8 ? 512 : kThreads; }
+// staged chunks summed in fp32 before a fold into the float64 accumulators (~50 kept terms at rate 0.1)
+constexpr int kFoldChunks = 4;
 
 template <int CPL, bool FAST>
 __global__ void __launch_bounds__(big_gram_threads(CPL), CPL <= 4 ? 3 : 1) big_gram_kernel(SweepArgs A, BigArgs B) {
@@ -365,6 +367,9 @@ __global__ void __launch_bounds__(big_gram_threads(CPL), CPL <= 4 ? 3 : 1) big_g
     const uint32_t s_lens = s_lists + 2u * (uint32_t)(nf * CH);      // [nf] u32 (!persist only)
     // FAST: staged global-sketch mask words of the chunk's rows, [CH][gwords]
     const uint32_t s_gm = persist ? s_bits + 4u * (uint32_t)(nf * nw) : s_lens + 4u * (uint32_t)nf;
+    // float64 accumulators of the work item's Gram (persist path only), after the FAST mask words
+    double* G64 = reinterpret_cast<double*>(after_g + align16((size_t)nf * nw * 4 +
+                                                              (FAST ? (size_t)CH * B.gwords * 4 : 0)));
     const uint32_t rowb = 4u * (uint32_t)sx;
     const FastDiv fq((uint32_t)xs_chunks(nf));
     const int my_cols = warp < nf ? (nf - 1 - warp) / nwarps + 1 : 0;
@@ -390,6 +395,8 @@ __global__ void __launch_bounds__(big_gram_threads(CPL), CPL <= 4 ? 3 : 1) big_g
             }
         }
         S.zero();
+        if (persist)
+            for (int e = tid; e < nf * gs; e += nt) G64[e] = 0.0;  // the tile-start barrier above orders the reuse
         double racc = 0.0;
         for (int k0 = kbeg; k0 < kend; k0 += CH) {
             const int kn = min(CH, kend - k0);
@@ -462,6 +469,9 @@ __global__ void __launch_bounds__(big_gram_threads(CPL), CPL <= 4 ? 3 : 1) big_g
             }
             if (persist) {
                 owned_accumulate<CPL>(S, M, s_xs, sx, s_ys, nf, kn, full, s_bits, nw);
+                // fold every kFoldChunks chunks and at the item's end (entries owned by this lane only)
+                if (((k0 - kbeg) / CH) % kFoldChunks == kFoldChunks - 1 || k0 + CH >= kend)
+                    owned_fold<CPL>(S, M, nf, G64);
             } else {
                 for (int j = 0; j < my_cols; ++j) {
                     const int c = warp + j * nwarps;
@@ -473,10 +483,10 @@ __global__ void __launch_bounds__(big_gram_threads(CPL), CPL <= 4 ? 3 : 1) big_g
         }
         // single-item rows: finished normal equations (+ lam*n*I) straight into gbuf
         const bool direct = r >= B.n_multi;
-        float* out = direct ? A.gbuf + (size_t)r * nf * gs : B.part + (size_t)t * nf * gs;
+        double* out = direct ? A.gbuf + (size_t)r * nf * gs : B.part + (size_t)t * nf * gs;
         const float lam_n = direct ? (float)(A.lam * (double)n) : 0.f;
         if (persist) {
-            owned_flush<CPL>(S, M, nf, out, lam_n);
+            owned_flush64<CPL>(M, nf, G64, out, direct ? A.lam * (double)n : 0.0);
         } else {
             __syncthreads();
             for (int e = tid; e < nf * gs; e += nt) {
@@ -500,9 +510,9 @@ __global__ void __launch_bounds__(big_gram_threads(CPL), CPL <= 4 ? 3 : 1) big_g
                     const int k = (int)(0xFFFFFFFFu - (uint32_t)s_amax[c]);
                     const float* xr = A.src + (int64_t)__ldg(A.idx + lo + k) * A.ld_src;
                     const float v = __ldg(xr + c);
-                    float* grow = out + (size_t)c * gs;
-                    for (int f = lane; f < nf; f += 32) grow[f] = fmaf(v, __ldg(xr + f), grow[f]);
-                    if (lane == 0) grow[nf] = fmaf(v, __ldg(A.val + lo + k), grow[nf]);
+                    double* grow = out + (size_t)c * gs;
+                    for (int f = lane; f < nf; f += 32) grow[f] = fma((double)v, (double)__ldg(xr + f), grow[f]);
+                    if (lane == 0) grow[nf] = fma((double)v, (double)__ldg(A.val + lo + k), grow[nf]);
                 }
             } else if (tid < nf) {
                 atomicAdd(&B.fcnt[(size_t)r * nf + tid], s_cnt[tid]);
@@ -527,9 +537,9 @@ __global__ void __launch_bounds__(kThreads) fast_fix_kernel(SweepArgs A, BigArgs
         const int k = (int)(0xFFFFFFFFu - (uint32_t)B.famax[(size_t)r * nf + c]);
         const float* xr = A.src + (int64_t)__ldg(A.idx + lo + k) * A.ld_src;
         const float v = __ldg(xr + c);
-        float* grow = A.gbuf + (size_t)r * nf * gs + (size_t)c * gs;
-        for (int f = lane; f < nf; f += 32) grow[f] = fmaf(v, __ldg(xr + f), grow[f]);
-        if (lane == 0) grow[nf] = fmaf(v, __ldg(A.val + lo + k), grow[nf]);
+        double* grow = A.gbuf + (size_t)r * nf * gs + (size_t)c * gs;
+        for (int f = lane; f < nf; f += 32) grow[f] = fma((double)v, (double)__ldg(xr + f), grow[f]);
+        if (lane == 0) grow[nf] = fma((double)v, (double)__ldg(A.val + lo + k), grow[nf]);
     }
 }
 
@@ -639,13 +649,13 @@ __global__ void __launch_bounds__(kThreads) big_reduce_kernel(SweepArgs A, BigAr
         const int row = B.rows[r];
         const int n = (int)(A.ptr[row + 1] - A.ptr[row]);
         const int64_t t0 = B.tile_ptr[r] - B.tile_base, t1 = B.tile_ptr[r + 1] - B.tile_base;
-        const float lam_n = (float)(A.lam * (double)n);
-        float* G = A.gbuf + (size_t)q * nout;
+        const double lam_n = A.lam * (double)n;
+        double* G = A.gbuf + (size_t)q * nout;
         for (int e = threadIdx.x; e < nout; e += blockDim.x) {
             double v = 0.0;
-            for (int64_t t = t0; t < t1; ++t) v += (double)B.part[(size_t)t * nout + e];
+            for (int64_t t = t0; t < t1; ++t) v += B.part[(size_t)t * nout + e];
             const int c = e / gs, f = e - c * gs;
-            G[e] = (float)v + ((c == f) ? lam_n : 0.f);
+            G[e] = v + ((c == f) ? lam_n : 0.0);
         }
         if (A.rss_rows != nullptr && threadIdx.x == 0) {
             double v = 0.0;

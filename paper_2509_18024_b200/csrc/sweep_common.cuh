@@ -35,14 +35,24 @@ struct SweepArgs {
     unsigned long long* summary;  // nullable: max over rows of (status << 32 | ~row)
     double* retry_ws;             // per-warp float64 jitter-retry scratch (retry_stride doubles each)
     int retry_stride;
-    float* gbuf;                  // normal equations of the current batch: [slot][nf][nf+1]
+    double* gbuf;                 // normal equations of the current batch: [slot][nf][nf+1], float64
+                                  // (the fp32 solve rounds them; the float64 refinement needs them exact)
     unsigned long long* stats;    // nullable debug counters (cals_debug_stats)
+    int* rf_cnt;                  // rows deferred to the float64 refinement (sweep_refine.cu) ...
+    int64_t* rf_list;             // ... as (row << 32 | normal-equation slot)
+    int rf_slice_max;             // tuning override of kRfSliceMax (0: default)
 };
+
+// Hand a system the fp32 solve cannot hold to the float64 refinement.
+__device__ __forceinline__ void defer_refine(const SweepArgs& A, int row, int64_t slot) {
+    const int at = atomicAdd(A.rf_cnt, 1);
+    A.rf_list[at] = ((int64_t)row << 32) | (int64_t)(uint32_t)slot;
+}
 
 // Debug counters (only when A.stats != nullptr): see cals_debug_stats.
 enum StatId { kStColumns = 0, kStFallback, kStCandidates, kStAfterPrenarrow, kStSelectRounds, kStRows,
               kStBigColumns, kStBigFallback, kStSmallOver, kStSmallMiss, kStFinalOver, kStBigMissAbove,
-              kStBigMissBelow, kStBigOverflow, kStBigFallbackN, kStCount = 16 };
+              kStBigMissBelow, kStBigOverflow, kStBigFallbackN, kStRefined, kStCount = 16 };
 __device__ __forceinline__ void stat_add(const SweepArgs& A, int id, unsigned long long v) {
     if (A.stats != nullptr) atomicAdd(A.stats + id, v);
 }
@@ -68,7 +78,7 @@ struct BigArgs {
     int* cnt;                 // [n_big][nf][2]  (above, in)
     uint64_t* cand;           // [cand_total]
     uint64_t* thr;            // [n_big][nf]
-    float* part;              // [n_tiles][nf][nf+1]
+    double* part;             // [n_tiles][nf][nf+1] float64 partial normal equations
     float* wbig;              // [n_big][nf]
     double* rss_part;         // [n_tiles]
     int* hist;                // [n_big][nf][kHB] in-bracket counts per sub-bucket

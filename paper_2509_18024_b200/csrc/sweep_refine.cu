@@ -1,0 +1,219 @@
+// sweep_refine.cu -- float64 solve of the normal equations the fp32 solve
+// kernels cannot hold to the reference's float64 answer.
+//
+// The fp32 solve kernels defer a system here when its elimination breaks down
+// (zero / non-finite pivot) or when the spread of its pivot magnitudes says it
+// is ill-conditioned (ill_ratio_for, solve.cuh): the fp32 LU's error grows like
+// cond * 6e-9 (measured), beyond the 1e-4 factor contract for cond >~ 1e4,
+// while a float64 solve of the same (fp32-stored) normal equations stays at
+// ~cond * 1e-9.  Like the reference (core.py:120-131, als.py:184-205): LU with
+// partial pivoting (first largest pivot, as LAPACK's idamax) or, for a
+// complete sketch, elimination without pivoting failing on a non-positive
+// pivot (Cholesky's condition); on a breakdown the reference's jitter
+// 1e-10 * tr(G) / n_f and one retry.  One CTA per deferred system, the
+// system in shared memory as float64.
+#include "solve.cuh"
+#include "sweep_common.cuh"
+
+namespace cals {
+
+constexpr int kRfChunk = 64;       // slice rows staged per pass of the float64 Gram
+constexpr int kRfSliceMax = 4096;  // rows up to this length rebuild their Gram in float64 from the slice
+
+__host__ __device__ inline int refine_threads(int nf) { return nf > 64 ? 512 : 256; }
+__host__ __device__ inline size_t refine_smem(int nf) {
+    return align16((size_t)nf * (nf + 1) * 8) + align16((size_t)kRfChunk * round_up4(nf) * 4) +
+           align16(kRfChunk * 4) + align16((size_t)nf * (kRfChunk / 32) * 4);
+}
+
+// Float64 Gram of one row from its slice: column c keeps the rows whose key
+// reaches the row's selection threshold (all rows for a complete sketch);
+// thread (c, fl) accumulates G[c][fl + j lpc] (f = nf: the right-hand side).
+// Products of two fp32 values are exact in float64.
+template <int NT>
+__device__ __forceinline__ void refine_slice_gram(const SweepArgs& A, int row, int64_t lo, int n, bool full,
+                                                  const uint64_t* s_thr, double* G, float* Xs, float* ys,
+                                                  uint32_t* bits) {
+    constexpr int kMaxAcc = NT == 256 ? 17 : 33;  // ceil((nf + 1) / lanes per column), lanes >= 4
+    const int nf = A.nf, gs = nf + 1, tid = threadIdx.x;
+    const int ldx = round_up4(nf), nq = xs_chunks(nf);
+    const int lpc = NT / nf;
+    const int c = tid / lpc, fl = tid - c * lpc;
+    double acc[kMaxAcc];
+#pragma unroll
+    for (int j = 0; j < kMaxAcc; ++j) acc[j] = 0.0;
+    for (int k0 = 0; k0 < n; k0 += kRfChunk) {
+        const int kn = min(kRfChunk, n - k0);
+        __syncthreads();  // previous chunk consumed
+        for (int q = tid; q < kn * nq; q += NT) {
+            const int k = q / nq, h = q - k * nq;
+            *reinterpret_cast<float4*>(Xs + k * ldx + 4 * h) = __ldg(
+                reinterpret_cast<const float4*>(A.src + (int64_t)__ldg(A.idx + lo + k0 + k) * A.ld_src + 4 * h));
+        }
+        for (int k = tid; k < kn; k += NT) ys[k] = __ldg(A.val + lo + k0 + k);
+        __syncthreads();
+        for (int q = tid; q < nf * (kRfChunk / 32); q += NT) {
+            const int cc = q % nf, w = q / nf;
+            uint32_t word = 0u;
+            for (int b = 0; b < 32; ++b) {
+                const int k = 32 * w + b;
+                if (k < kn && (full || make_key(Xs[k * ldx + cc], (uint32_t)(k0 + k)) >= s_thr[cc])) word |= 1u << b;
+            }
+            bits[cc * (kRfChunk / 32) + w] = word;
+        }
+        __syncthreads();
+        if (c < nf) {
+            for (int w = 0; w < kRfChunk / 32; ++w) {
+                uint32_t word = bits[c * (kRfChunk / 32) + w];
+                while (word) {
+                    const int k = 32 * w + __ffs(word) - 1;
+                    word &= word - 1u;
+                    const double xc = (double)Xs[k * ldx + c];
+#pragma unroll
+                    for (int j = 0; j < kMaxAcc; ++j) {
+                        const int f = fl + j * lpc;
+                        if (f < nf) acc[j] = fma(xc, (double)Xs[k * ldx + f], acc[j]);
+                        else if (f == nf) acc[j] = fma(xc, (double)ys[k], acc[j]);
+                    }
+                }
+            }
+        }
+    }
+    if (c < nf) {
+#pragma unroll
+        for (int j = 0; j < kMaxAcc; ++j) {
+            const int f = fl + j * lpc;
+            if (f <= nf) G[c * gs + f] = acc[j] + ((f == c) ? A.lam * (double)n : 0.0);
+        }
+    }
+}
+
+// slice_ok: the rows' kept sets are per-row thresholds (method 'core'; fast_core
+// rows use the stored normal equations, which hold its whole-source sketch).
+template <int NT>
+__global__ void __launch_bounds__(NT) refine_kernel(SweepArgs A, const int* __restrict__ count,
+                                                   const int64_t* __restrict__ list, int slice_ok) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double s_x[CALS_MAX_NF_DEV];
+    __shared__ double s_red[32];
+    __shared__ int s_piv, s_bad;
+    const int nf = A.nf, gs = nf + 1, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* G = reinterpret_cast<double*>(smem);
+    float* Xs = reinterpret_cast<float*>(smem + align16((size_t)nf * gs * 8));
+    float* ys = Xs + kRfChunk * round_up4(nf);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(ys) + align16(kRfChunk * 4));
+    __shared__ uint64_t s_thr[CALS_MAX_NF_DEV];
+    const int n_list = *count;
+    for (int64_t e = blockIdx.x; e < n_list; e += gridDim.x) {
+        const int row = (int)(list[e] >> 32);
+        const int64_t slot = (int64_t)(uint32_t)list[e];
+        const int n = (int)(A.ptr[row + 1] - A.ptr[row]);
+        const bool full = A.budget[row] >= n;
+        const double* Gf = A.gbuf + (size_t)slot * nf * gs;
+        // short rows rebuild their Gram in float64 (their fp32 sums are the error floor of an
+        // ill-conditioned system); long rows' stored equations are float64-folded already
+        const bool from_slice = slice_ok && n <= (A.rf_slice_max > 0 ? A.rf_slice_max : kRfSliceMax);
+        __syncthreads();
+        if (from_slice && tid < nf) s_thr[tid] = A.thr_keys[(int64_t)row * nf + tid];
+        int st = CALS_ROW_SINGULAR;
+        for (int attempt = 0; attempt < 2 && st == CALS_ROW_SINGULAR; ++attempt) {
+            __syncthreads();
+            if (from_slice) refine_slice_gram<NT>(A, row, A.ptr[row], n, full, s_thr, G, Xs, ys, bits);
+            else
+                for (int q = tid; q < nf * gs; q += NT) G[q] = Gf[q];
+            __syncthreads();
+            if (attempt == 1) {  // the reference's retry: G += 1e-10 * tr(G) / n_f * I (core.py:126-131)
+                if (warp == 0) {
+                    double tr = 0.0;
+                    for (int i = lane; i < nf; i += 32) tr += G[i * gs + i];
+                    tr = warp_sum_d(tr);
+                    if (lane == 0) s_red[0] = 1e-10 * tr / (double)nf;
+                }
+                __syncthreads();
+                for (int i = tid; i < nf; i += NT) G[i * gs + i] += s_red[0];
+                __syncthreads();
+            }
+            if (tid == 0) s_bad = 0;
+            // ---- float64 elimination on [G | b] ----
+            for (int k = 0; k < nf; ++k) {
+                if (warp == 0) {
+                    int p = k;
+                    if (!full) {
+                        // first row of the largest |G[i][k]|, i >= k (idamax)
+                        double best = -1.0;
+                        int bi = nf;
+                        for (int i = k + lane; i < nf; i += 32) {
+                            const double v = fabs(G[i * gs + k]);
+                            if (v > best) { best = v; bi = i; }
+                        }
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            const double ob = __shfl_xor_sync(CALS_FULL_MASK, best, o);
+                            const int oi = __shfl_xor_sync(CALS_FULL_MASK, bi, o);
+                            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+                        }
+                        p = bi;
+                        if (lane == 0 && !(best > 0.0)) s_bad = 1;
+                    } else if (lane == 0 && !(G[k * gs + k] > 0.0)) {
+                        s_bad = 1;
+                    }
+                    if (lane == 0) s_piv = p;
+                }
+                __syncthreads();
+                if (s_bad) break;
+                const int p = s_piv;
+                if (p != k)
+                    for (int j = tid; j < gs; j += NT) {
+                        const double t = G[k * gs + j];
+                        G[k * gs + j] = G[p * gs + j];
+                        G[p * gs + j] = t;
+                    }
+                __syncthreads();
+                const double d = G[k * gs + k];
+                for (int i = k + 1 + tid; i < nf; i += NT) G[i * gs + k] /= d;  // multipliers
+                __syncthreads();
+                const int w = gs - k - 1;
+                for (int q = tid; q < (nf - k - 1) * w; q += NT) {
+                    const int i = k + 1 + q / w, j = k + 1 + q % w;
+                    G[i * gs + j] = fma(-G[i * gs + k], G[k * gs + j], G[i * gs + j]);
+                }
+                __syncthreads();
+            }
+            if (s_bad) continue;  // singular: jittered retry (attempt 1) or give up
+            // back substitution (one warp): x_i = (b_i - sum_{j > i} U_ij x_j) / U_ii
+            if (warp == 0) {
+                for (int i = nf - 1; i >= 0; --i) {
+                    double t = 0.0;
+                    for (int j = i + 1 + lane; j < nf; j += 32) t += G[i * gs + j] * s_x[j];
+                    t = warp_sum_d(t);
+                    if (lane == 0) s_x[i] = (G[i * gs + nf] - t) / G[i * gs + i];
+                    __syncwarp();
+                }
+            }
+            __syncthreads();
+            st = attempt == 0 ? CALS_ROW_OK : CALS_ROW_JITTERED;
+        }
+        // write-out as the fp32 solve kernels do (als.py:286, penalty als.py:162-167)
+        if (st != CALS_ROW_SINGULAR)
+            for (int f = tid; f < nf; f += NT) A.tgt[(int64_t)row * A.ld_tgt + f] = (float)s_x[f];
+        if (A.pen_rows != nullptr && warp == 0) {
+            double p = 0.0;
+            for (int f = lane; f < nf; f += 32) {
+                const double xf = (double)(float)s_x[f];
+                p += xf * xf;
+            }
+            p = warp_sum_d(p);
+            if (lane == 0) A.pen_rows[row] = (st == CALS_ROW_SINGULAR) ? 0.0 : (double)n * p;
+        }
+        if (tid == 0) {
+            A.status[row] = st;
+            report_status(A, row, st);
+            stat_add(A, kStRefined, 1);
+        }
+    }
+}
+
+template __global__ void refine_kernel<256>(SweepArgs, const int*, const int64_t*, int);
+template __global__ void refine_kernel<512>(SweepArgs, const int*, const int64_t*, int);
+
+}  // namespace cals

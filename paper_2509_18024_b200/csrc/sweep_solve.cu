@@ -24,43 +24,21 @@ __global__ void __launch_bounds__(256, 3) solve_warp_kernel(SweepArgs A, const i
         const int row = sv ? rows[li] : 0;
         const int n = sv ? (int)(A.ptr[row + 1] - A.ptr[row]) : 1;
         const bool spd = sv && A.budget[row] >= n;
-        const float* G = A.gbuf + (size_t)(sv ? li : 0) * nf * gs;
+        const double* G = A.gbuf + (size_t)(sv ? li : 0) * nf * gs;
         float x;
         const bool bad = seg_lu_solve<NFP>(G + (size_t)(r < nf ? r : 0) * gs, nf, spd, sv, x, lane);
-        int st = CALS_ROW_OK;
-        // rare path: float64 retry with the reference's jitter, one system at a time
-        const uint32_t badmask = __ballot_sync(CALS_FULL_MASK, bad && sv && r == 0);
-        if (badmask) {
-            double* W = A.retry_ws + (size_t)gw * A.retry_stride;
-            double* xd = W + nf * gs;
-            uint32_t m = badmask;
-            while (m) {
-                const int sl = __ffs(m) - 1;
-                m &= m - 1;
-                const int q = sl / NFP;
-                const int64_t lq = b0 + q;
-                const int rq = rows[lq];
-                const int nq = (int)(A.ptr[rq + 1] - A.ptr[rq]);
-                const bool spdq = A.budget[rq] >= nq;
-                const int bq = warp_retry_f64(A.gbuf + (size_t)lq * nf * gs, nf, spdq, W, xd, lane);
-                __syncwarp();
-                if (seg == q) {
-                    if (r < nf) x = (float)xd[r];
-                    st = bq ? CALS_ROW_SINGULAR : CALS_ROW_JITTERED;
-                }
-                __syncwarp();
-            }
-        }
-        if (sv) {
-            if (st != CALS_ROW_SINGULAR && r < nf) A.tgt[(int64_t)row * A.ld_tgt + r] = x;
-        }
+        // fp32 breakdown or ill-conditioning: the float64 refinement owns the row
+        const bool deferred = bad && sv;
+        if (deferred && r == 0) defer_refine(A, row, li);
+        const int st = CALS_ROW_OK;
+        if (sv && !deferred && r < nf) A.tgt[(int64_t)row * A.ld_tgt + r] = x;
         if (A.pen_rows != nullptr) {
             double p = (sv && r < nf) ? (double)x * (double)x : 0.0;
 #pragma unroll
             for (int o = NFP / 2; o > 0; o >>= 1) p += __shfl_xor_sync(CALS_FULL_MASK, p, o, NFP);
-            if (sv && r == 0) A.pen_rows[row] = (st == CALS_ROW_SINGULAR) ? 0.0 : (double)n * p;
+            if (sv && !deferred && r == 0) A.pen_rows[row] = (double)n * p;
         }
-        if (sv && r == 0) {
+        if (sv && !deferred && r == 0) {
             A.status[row] = st;
             report_status(A, row, st);
         }
@@ -80,19 +58,19 @@ __global__ void __launch_bounds__(128) solve_block_kernel(SweepArgs A, const int
         const int row = rows[li];
         const int n = (int)(A.ptr[row + 1] - A.ptr[row]);
         const bool spd = A.budget[row] >= n;
-        const float* G = A.gbuf + (size_t)li * nout;
+        const double* G = A.gbuf + (size_t)li * nout;
         __syncthreads();
-        for (int e = tid; e < nout; e += blockDim.x) W[e] = G[e];
+        for (int e = tid; e < nout; e += blockDim.x) W[e] = (float)G[e];
         __syncthreads();
         int st = CALS_ROW_OK;
         if (block_lu_solve<float>(W, nf, spd, wv, s_piv)) {
             if (tid < 32) {
                 double* Wd = A.retry_ws + (size_t)blockIdx.x * A.retry_stride;
                 double* xd = Wd + nout;
-                const int bad = warp_retry_f64(G, nf, spd, Wd, xd, tid);
+                const int sq = warp_solve_f64(G, nf, spd, Wd, xd, tid);
                 if (tid < 32) {
                     for (int f = tid; f < nf; f += 32) wv[f] = (float)xd[f];
-                    if (tid == 0) s_flag[0] = bad ? CALS_ROW_SINGULAR : CALS_ROW_JITTERED;
+                    if (tid == 0) s_flag[0] = sq;
                 }
             }
             __syncthreads();
@@ -128,20 +106,15 @@ __global__ void __launch_bounds__(128, 3) solve_wide_kernel(SweepArgs A, const i
         const int row = rows[li];
         const int n = (int)(A.ptr[row + 1] - A.ptr[row]);
         const bool spd = A.budget[row] >= n;
-        const float* G = A.gbuf + (size_t)li * nout;
+        const double* G = A.gbuf + (size_t)li * nout;
         __syncwarp();
-        for (int e = lane; e < nout; e += 32) W[e] = __ldcs(G + e);
+        for (int e = lane; e < nout; e += 32) W[e] = (float)__ldcs(G + e);
         __syncwarp();
         float x0, x1;
-        int st = CALS_ROW_OK;
-        if (wide_lu_solve<NF>(W, nf, spd, x0, x1, lane)) {
-            double* Wd = A.retry_ws + (size_t)gw * A.retry_stride;
-            double* xd = Wd + nout;
-            const int bad = warp_retry_f64(G, nf, spd, Wd, xd, lane);
-            __syncwarp();
-            x0 = lane < nf ? (float)xd[lane] : 0.f;
-            x1 = lane + 32 < nf ? (float)xd[lane + 32] : 0.f;
-            st = bad ? CALS_ROW_SINGULAR : CALS_ROW_JITTERED;
+        const int st = CALS_ROW_OK;
+        if (wide_lu_solve<NF>(W, nf, spd, x0, x1, lane)) {  // the float64 refinement owns the row
+            if (lane == 0) defer_refine(A, row, li);
+            continue;
         }
         float* out = A.tgt + (int64_t)row * A.ld_tgt;
         if (st != CALS_ROW_SINGULAR) {
@@ -174,7 +147,8 @@ template __global__ void solve_wide_kernel<64>(SweepArgs, const int32_t*, int64_
 // against it (no row swaps; back substitution walks the pivot order).
 template <int NF, int B0>
 __device__ __forceinline__ void rows_block(float (&a)[NF], float& rhs, bool& used, int& ord, float& mydiag,
-                                           bool& fail, bool spd, int r, float* piv, uint32_t* wbest) {
+                                           bool& fail, float& dmin, float& dmax, bool spd, int r, float* piv,
+                                           uint32_t* wbest) {
     constexpr int BE = (B0 + 16 < NF) ? B0 + 16 : NF;
     const int lane = r & 31, warp = r >> 5;
 #pragma unroll 1
@@ -208,6 +182,8 @@ __device__ __forceinline__ void rows_block(float (&a)[NF], float& rhs, bool& use
         __syncthreads();
         const float d = piv[NF + 1];
         fail |= spd ? !(d > 0.f) : !(d == d);
+        dmin = fminf(dmin, fabsf(d));
+        dmax = fmaxf(dmax, fabsf(d));
         const float f = used ? 0.f : ck * __frcp_rn(d);
 #pragma unroll
         for (int q = B0 / 4; q < NF / 4; ++q) {
@@ -239,9 +215,9 @@ __device__ __forceinline__ void rows_back(const float (&a)[NF], float& rhs, int 
 
 template <int NF, int... Q>
 __device__ __forceinline__ void rows_eliminate(float (&a)[NF], float& rhs, bool& used, int& ord, float& mydiag,
-                                               bool& fail, bool spd, int r, float* piv, uint32_t* wbest,
-                                               std::integer_sequence<int, Q...>) {
-    (rows_block<NF, 16 * Q>(a, rhs, used, ord, mydiag, fail, spd, r, piv, wbest), ...);
+                                               bool& fail, float& dmin, float& dmax, bool spd, int r, float* piv,
+                                               uint32_t* wbest, std::integer_sequence<int, Q...>) {
+    (rows_block<NF, 16 * Q>(a, rhs, used, ord, mydiag, fail, dmin, dmax, spd, r, piv, wbest), ...);
 }
 template <int NF, int... Q>
 __device__ __forceinline__ void rows_substitute(const float (&a)[NF], float& rhs, int ord, float mydiag, int r,
@@ -263,34 +239,29 @@ __global__ void __launch_bounds__(NF, 3) solve_rows_kernel(SweepArgs A, const in
         const int row = rows[li];
         const int n = (int)(A.ptr[row + 1] - A.ptr[row]);
         const bool spd = A.budget[row] >= n;
-        const float* G = A.gbuf + (size_t)li * nf * gs;
+        const double* G = A.gbuf + (size_t)li * nf * gs;
         float a[NF];
 #pragma unroll
-        for (int j = 0; j < NF; ++j) a[j] = (r < nf && j < nf) ? __ldcs(G + (size_t)r * gs + j) : (j == r ? 1.f : 0.f);
-        float rhs = r < nf ? __ldcs(G + (size_t)r * gs + nf) : 0.f;
+        for (int j = 0; j < NF; ++j) a[j] = (r < nf && j < nf) ? (float)__ldcs(G + (size_t)r * gs + j) : (j == r ? 1.f : 0.f);
+        float rhs = r < nf ? (float)__ldcs(G + (size_t)r * gs + nf) : 0.f;
         bool used = false, fail = false;
         int ord = -1;
-        float mydiag = 1.f;
+        float mydiag = 1.f, dmin = INFINITY, dmax = 0.f;
         if (r == 0) s_bad = 0;
-        rows_eliminate<NF>(a, rhs, used, ord, mydiag, fail, spd, r, piv, wbest, std::make_integer_sequence<int, NF / 16>{});
+        rows_eliminate<NF>(a, rhs, used, ord, mydiag, fail, dmin, dmax, spd, r, piv, wbest,
+                           std::make_integer_sequence<int, NF / 16>{});
         rows_substitute<NF>(a, rhs, ord, mydiag, r, xs, std::make_integer_sequence<int, NF / 16>{});
         __syncthreads();
         // unknown r (solved from the row pivoted at step r)
         float x = r < nf ? xs[r] : 0.f;
-        const bool bad = fail || (r < nf && (!(x == x) || (x - x != 0.f)));
+        const bool bad = fail || ill_conditioned(dmin, dmax) || (r < nf && (!(x == x) || (x - x != 0.f)));
         if (bad) atomicOr(&s_bad, 1);
         __syncthreads();
-        int st = CALS_ROW_OK;
-        if (s_bad) {
-            if (r < 32) {
-                double* Wd = A.retry_ws + (size_t)blockIdx.x * A.retry_stride;
-                double* xd = Wd + nf * gs;
-                const int b = warp_retry_f64(G, nf, spd, Wd, xd, r);
-                if (r == 0) s_bad = b ? 2 : 1;
-            }
+        const int st = CALS_ROW_OK;
+        if (s_bad) {  // the float64 refinement owns the row
+            if (r == 0) defer_refine(A, row, li);
             __syncthreads();
-            st = s_bad == 2 ? CALS_ROW_SINGULAR : CALS_ROW_JITTERED;
-            if (r < nf) x = (float)A.retry_ws[(size_t)blockIdx.x * A.retry_stride + nf * gs + r];
+            continue;
         }
         if (st != CALS_ROW_SINGULAR && r < nf) A.tgt[(int64_t)row * A.ld_tgt + r] = x;
         if (A.pen_rows != nullptr) {

@@ -88,6 +88,13 @@ def _ptr_from_sorted(keys_major, n):
 def _finish(name, spec, users, items, vals, n_users, n_items):
     """users/items/vals sorted by (user, item) -> SynthData with both indexes."""
     row_ptr = _ptr_from_sorted(users, n_users)
+    if users.is_cuda and users.numel() > (1 << 30):
+        # past ~1G ratings: the CSC from the device dual index (csrc/index.cu, exact; a torch argsort of the keys needs 4x the memory)
+        from .ratings import csr_to_csc_device
+        row_items, row_vals = items.to(torch.int32), vals.float()
+        del users, items, vals
+        col_ptr, col_users, col_vals = csr_to_csc_device(row_ptr, row_items, row_vals, n_users, n_items)
+        return SynthData(name, n_users, n_items, row_ptr, row_items, row_vals, col_ptr, col_users, col_vals, spec)
     key2 = items.long() * n_users + users.long()
     order = torch.argsort(key2)
     col_ptr = _ptr_from_sorted(items[order], n_items)
@@ -149,6 +156,8 @@ def _powerlaw(name, spec, device, seed, nnz_target=None):
         k = torch.searchsorted(cdf, u).clamp_max(ni - 1)
         return perm[k]
 
+    if target > (1 << 30):
+        return _powerlaw_blocked(name, spec, device, g, counts, draw)
     users = torch.repeat_interleave(torch.arange(nu, device=device), counts)
     items = draw(users)
     for _ in range(8):
@@ -182,6 +191,58 @@ def _powerlaw(name, spec, device, seed, nnz_target=None):
     if spec.get("quantize"):
         z = vals / float(np.sqrt(r + spec["noise"] ** 2))
         vals = torch.clamp(torch.round((2.75 + z) * 2.0) / 2.0, 0.5, 5.0)
+    return _finish(name, spec, users, items, vals, nu, ni)
+
+
+def _powerlaw_blocked(name, spec, device, g, counts, draw):
+    """The power-law construction of _powerlaw over blocks of users (each block's
+    draws stay far below torch's 2^31-element sort limit): per block, draw,
+    dedupe, top up deficits, then drop overshoot at random -- the same steps,
+    block-local (every step is per user, so blocks are independent)."""
+    nu, ni, r = spec["n_users"], spec["n_items"], spec["rank"]
+    us, its = [], []
+    cum = torch.cumsum(counts, 0)
+    lo = 0
+    while lo < nu:
+        base = int(cum[lo - 1]) if lo else 0
+        hi = int(torch.searchsorted(cum, torch.tensor(base + (1 << 28), device=device, dtype=cum.dtype)))
+        hi = min(nu, max(hi, lo + 1))
+        c = counts[lo:hi]
+        n = hi - lo
+        users = torch.repeat_interleave(torch.arange(n, device=device), c)
+        items = draw(users)
+        for _ in range(8):
+            key = torch.unique(users * ni + items)
+            users, items = key // ni, key % ni
+            have = torch.bincount(users, minlength=n)
+            deficit = (c - have).clamp_min(0)
+            if int(deficit.sum()) == 0:
+                break
+            extra_u = torch.repeat_interleave(torch.arange(n, device=device), deficit * 2)
+            users = torch.cat([users, extra_u])
+            items = torch.cat([items, draw(extra_u)])
+        key = torch.unique(users * ni + items)
+        users, items = key // ni, key % ni
+        have = torch.bincount(users, minlength=n)
+        if bool((have > c).any()):
+            pri = torch.rand(users.numel(), generator=g, device=device)
+            order = torch.argsort(users.double() * 2.0 + pri.double())
+            users_o = users[order]
+            start = torch.zeros(n + 1, dtype=torch.int64, device=device)
+            start[1:] = torch.cumsum(have, 0)
+            pos = torch.arange(users_o.numel(), device=device) - start[users_o]
+            keep = order[pos < c[users_o]]
+            keep, _ = torch.sort(keep)
+            users, items = users[keep], items[keep]
+        us.append((users + lo).to(torch.int32))
+        its.append(items.to(torch.int32))
+        lo = hi
+    users = torch.cat(us)
+    items = torch.cat(its)
+    del us, its
+    Ut = torch.randn(nu, r, generator=g, device=device)
+    Vt = torch.randn(ni, r, generator=g, device=device)
+    vals = _truth_values(users, items, Ut, Vt, spec["noise"], g)
     return _finish(name, spec, users, items, vals, nu, ni)
 
 

@@ -1,5 +1,6 @@
-"""Parity at BASELINE.json's full sizes (configs 2-4: medium 10M, power-law 25M,
-large 500M ratings) on a stratified row sample, as SURVEY 8c.1-2 prescribe for
+"""Parity at BASELINE.json's full sizes (configs 2-5: medium 10M, power-law 25M,
+large 500M, wide 2B ratings at n_f = 128 -- the 8-GPU config, which fits one
+B200's 180 GB) on a stratified row sample, as SURVEY 8c.1-2 prescribe for
 sizes the float64 oracle cannot sweep whole: one GPU half-sweep per side (the
 item side fed the GPU's own user factors), then the oracle (a restatement of
 core.py:199-223, pinned to the reference's fixtures) on the sampled rows with
@@ -60,7 +61,7 @@ def half(eng, side, source):
     return tgt, keys
 
 
-@pytest.mark.parametrize("config", ["medium", "powerlaw", "large"])
+@pytest.mark.parametrize("config", ["medium", "powerlaw", "large", "wide"])
 def test_full_size_config_stratified_rows(config):
     spec = synth.CONFIGS[config]
     n_f, lam, rate = spec["n_f"], spec["lam"], spec["rate"]

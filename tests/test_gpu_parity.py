@@ -395,3 +395,40 @@ def test_evaluation_metrics_match_reference():
     assert ev.hit_at_k == float(g["hit5"]) and ev.ndcg_at_k == pytest.approx(float(g["ndcg10"]), rel=1e-12)
     with pytest.raises(cb.DataError):
         cb.prmse(([], [], []), F)
+
+
+@pytest.mark.parametrize("n_f", [8, 64, 128])
+def test_float64_path_on_every_system(n_f, monkeypatch):
+    """Every system forced through the float64 solve (CALS_ILL_RATIO=0), on all
+    tiers including multi-item rows: the float64 path alone matches the oracle."""
+    monkeypatch.setenv("CALS_ILL_RATIO", "0")
+    monkeypatch.setenv("CALS_ITEM_ROWS", "1024")
+    u, i, v = random_matrix(n_f, 3000, 400, 0.04, heavy_items=6, heavy_density=0.9)
+    R = cb.RatingMatrix(u, i, v, n_users=3000, n_items=400)
+    M0 = np.random.default_rng(1).normal(0, 0.1, (400, n_f)).astype(np.float32)
+    eng = check_against_oracle(R, n_f, 0.05, 0.2, M0)
+    assert eng.item.plan.n_big_tiles > eng.item.plan.n_big
+
+
+@pytest.mark.parametrize("item_rows", [None, 1024])
+@pytest.mark.parametrize("n_f", [8, 32, 64, 128])
+def test_oracle_parity_ill_conditioned(n_f, item_rows, monkeypatch):
+    """Large, nearly collinear source columns (like the factors of later
+    iterations) make many sketched systems ill-conditioned: the fp32 solve
+    defers them to the float64 solve (sweep_refine.cu), and rows still match the
+    float64 reference within 1e-4 on every tier."""
+    from paper_2509_18024_b200 import _lib
+    if item_rows is not None:
+        monkeypatch.setenv("CALS_ITEM_ROWS", str(item_rows))
+    u, i, v = random_matrix(n_f + 50, 3000, 400, 0.04, heavy_items=6, heavy_density=0.9)
+    R = cb.RatingMatrix(u, i, v, n_users=3000, n_items=400)
+    rng = np.random.default_rng(3)
+    base = rng.normal(0.0, 3.0, (400, 1))
+    M0 = (base + 0.05 * rng.normal(0.0, 3.0, (400, n_f))).astype(np.float32)
+    stats = torch.zeros(16, dtype=torch.int64, device="cuda")
+    _lib.load().cals_debug_stats(stats.data_ptr())
+    try:
+        check_against_oracle(R, n_f, 0.01, 0.1, M0)
+    finally:
+        _lib.load().cals_debug_stats(None)
+    assert int(stats[15]) > 0  # the float64 path was exercised

@@ -34,3 +34,4 @@ names = ["columns", "fallback", "candidates", "after_prenarrow", "select_rounds"
          "big_fallback", "small_over", "small_miss", "final_over", "big_miss_above", "big_miss_below",
          "big_overflow", "big_fallback_n"]
 print({n: int(v) for n, v in zip(names, st.cpu().tolist())})
+print("refined rows (item half):", int(st[15].item()))
