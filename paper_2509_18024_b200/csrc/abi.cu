@@ -277,8 +277,9 @@ struct Work {
     double* gbuf2;    // staged tier's own normal-equation buffer when both tiers run concurrently
     double* retry2;  // and its jitter-retry scratch
     uint64_t* thr_all;  // [n_rows][nf] selection thresholds (when the caller asks for none)
-    int* rf_cnt;        // [2] rows deferred to the float64 refinement, per stream
-    int64_t* rf_list;   // [2][gbuf_rows] (row << 32 | gbuf slot)
+    int* rf_cnt;        // [4]: per stream, rows deferred to the float64 refinement from the stored
+    int64_t* rf_list;   // equations [2][gbuf_rows] (row << 32 | slot), and from the slice:
+    int32_t* rs_list;   // [2][n_rows] rows
 };
 
 constexpr int kMaxGrid = 160 * 16;  // grid_for never exceeds min(SMs, 160) * 16 CTAs
@@ -308,8 +309,9 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
         w.retry2 = c.take<double>((size_t)std::max<int64_t>(kMaxGrid, kMaxSolveWarps) * retry_stride(nf));
     }
     w.thr_all = c.take<uint64_t>((size_t)std::max<int64_t>(P->n_rows, 1) * nf);
-    w.rf_cnt = c.take<int>(2);
+    w.rf_cnt = c.take<int>(4);
     w.rf_list = c.take<int64_t>((size_t)2 * w.gbuf_rows);
+    w.rs_list = c.take<int32_t>((size_t)2 * std::max<int64_t>(P->n_rows, 1));
     *total = c.off + 256;
     return w;
 }
@@ -319,24 +321,28 @@ void launch_solve_fp32(const SweepArgs& A, const int32_t* rows, int64_t count, c
 
 // float64 recomputation of the systems the fp32 solve deferred (the count stays
 // on the device; one CTA per SM walks the list), then the list is reset
-void launch_refine(const SweepArgs& A, cudaStream_t st, int slice_ok) {
+void launch_refine(const SweepArgs& A, cudaStream_t st, bool from_slice) {
     ProfScope ps("refine_kernel", st);
     const size_t sm = refine_smem(A.nf);
+    const int* cnt = from_slice ? A.rs_cnt : A.rf_cnt;
+    const void* list = from_slice ? static_cast<const void*>(A.rs_list) : static_cast<const void*>(A.rf_list);
+    // the per-batch list is usually empty (long rows rarely defer): one CTA per SM keeps that launch cheap
+    const int per_sm = from_slice ? (refine_threads(A.nf) == 256 ? 4 : 2) : 1;
     if (refine_threads(A.nf) == 256) {
         allow_smem(refine_kernel<256>);
-        refine_kernel<256><<<dev().sms * 4, 256, sm, st>>>(A, A.rf_cnt, A.rf_list, slice_ok);
+        refine_kernel<256><<<dev().sms * per_sm, 256, sm, st>>>(A, cnt, list, from_slice ? 1 : 0);
     } else {
         allow_smem(refine_kernel<512>);
-        refine_kernel<512><<<dev().sms * 2, 512, sm, st>>>(A, A.rf_cnt, A.rf_list, slice_ok);
+        refine_kernel<512><<<dev().sms * per_sm, 512, sm, st>>>(A, cnt, list, from_slice ? 1 : 0);
     }
-    cudaMemsetAsync(A.rf_cnt, 0, sizeof(int), st);
+    cudaMemsetAsync(const_cast<int*>(cnt), 0, sizeof(int), st);
 }
 
 template <int NFP>
-void launch_solve(const SweepArgs& A, const int32_t* rows, int64_t count, cudaStream_t st, int slice_ok = 1) {
+void launch_solve(const SweepArgs& A, const int32_t* rows, int64_t count, cudaStream_t st) {
     if (count <= 0) return;
     launch_solve_fp32<NFP>(A, rows, count, st);
-    launch_refine(A, st, slice_ok);
+    launch_refine(A, st, false);  // systems that need this batch's stored equations
 }
 
 template <int NFP>
@@ -532,7 +538,7 @@ int launch_fast(const SweepArgs& A, const cals_plan* P, const Work& w, const uin
             fast_fix_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, (int64_t)dev().sms * 8)),
                               kThreads, 0, st>>>(A, B);
         }
-        launch_solve<NFP>(A, B.rows, B.n_big, st, 0);
+        launch_solve<NFP>(A, B.rows, B.n_big, st);
         const int rc = cuda_status("fast_core kernels");
         if (rc) return rc;
     }
@@ -755,8 +761,10 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     }
     A.rf_cnt = w.rf_cnt;
     A.rf_list = w.rf_list;
-    A.rf_slice_max = env_int("CALS_RF_SLICE_MAX", 0);
-    cudaMemsetAsync(w.rf_cnt, 0, 2 * sizeof(int), st);
+    A.rs_cnt = w.rf_cnt + 2;
+    A.rs_list = w.rs_list;
+    A.rf_slice_max = env_int("CALS_RF_SLICE_MAX", kRfSliceMax);
+    cudaMemsetAsync(w.rf_cnt, 0, 4 * sizeof(int), st);
     A.gbuf = w.gbuf;
     A.stats = g_stats;
     A.status = row_status;
@@ -790,6 +798,8 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
         As.retry_ws = w.retry2;
         As.rf_cnt = w.rf_cnt + 1;
         As.rf_list = w.rf_list + w.gbuf_rows;
+        As.rs_cnt = w.rf_cnt + 3;
+        As.rs_list = w.rs_list + std::max<int64_t>(P->n_rows, 1);
         ss = dev().side;
         cudaEventRecord(dev().fork, st);
         cudaStreamWaitEvent(ss, dev().fork, 0);
@@ -799,6 +809,7 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
         else if (n_f <= 16) rc = launch_small<16>(As, P, w, ss);
         else if (n_f <= 32) rc = launch_small<32>(As, P, w, ss);
         else rc = launch_small<0>(As, P, w, ss);
+        launch_refine(As, ss, true);  // the tier's deferred short rows, from their slices
         if (both) {
             cudaEventRecord(dev().join, ss);
         }
@@ -812,6 +823,7 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
         else if (n_f <= 16) rc = launch_big<16>(A, P, w, st);
         else if (n_f <= 32) rc = launch_big<32>(A, P, w, st);
         else rc = launch_big<0>(A, P, w, st);
+        launch_refine(A, st, true);
     }
     if (both) cudaStreamWaitEvent(st, dev().join, 0);
     return rc;
@@ -915,8 +927,10 @@ int cals_fast_half_sweep(const cals_side* side, const cals_plan* P, const float*
     }
     A.rf_cnt = w.rf_cnt;
     A.rf_list = w.rf_list;
-    A.rf_slice_max = env_int("CALS_RF_SLICE_MAX", 0);
-    cudaMemsetAsync(w.rf_cnt, 0, 2 * sizeof(int), st);
+    A.rs_cnt = w.rf_cnt + 2;
+    A.rs_list = w.rs_list;
+    A.rf_slice_max = 0;  // fast_core rows keep their stored equations (whole-source sketch)
+    cudaMemsetAsync(w.rf_cnt, 0, 4 * sizeof(int), st);
     A.gbuf = w.gbuf;
     A.stats = g_stats;
     A.status = row_status;

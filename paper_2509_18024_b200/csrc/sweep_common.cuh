@@ -38,15 +38,22 @@ struct SweepArgs {
     double* gbuf;                 // normal equations of the current batch: [slot][nf][nf+1], float64
                                   // (the fp32 solve rounds them; the float64 refinement needs them exact)
     unsigned long long* stats;    // nullable debug counters (cals_debug_stats)
-    int* rf_cnt;                  // rows deferred to the float64 refinement (sweep_refine.cu) ...
-    int64_t* rf_list;             // ... as (row << 32 | normal-equation slot)
-    int rf_slice_max;             // tuning override of kRfSliceMax (0: default)
+    int* rf_cnt;                  // rows deferred to the float64 refinement (sweep_refine.cu) that
+    int64_t* rf_list;             // need their stored normal equations: (row << 32 | slot), per batch
+    int* rs_cnt;                  // rows deferred that rebuild their Gram from the slice: refined once
+    int32_t* rs_list;             // after the tier's last batch (one launch, no per-batch latency)
+    int rf_slice_max;             // rows up to this length rebuild from the slice (0: none)
 };
 
 // Hand a system the fp32 solve cannot hold to the float64 refinement.
 __device__ __forceinline__ void defer_refine(const SweepArgs& A, int row, int64_t slot) {
-    const int at = atomicAdd(A.rf_cnt, 1);
-    A.rf_list[at] = ((int64_t)row << 32) | (int64_t)(uint32_t)slot;
+    const int n = (int)(A.ptr[row + 1] - A.ptr[row]);
+    if (n <= A.rf_slice_max) {
+        A.rs_list[atomicAdd(A.rs_cnt, 1)] = row;
+    } else {
+        const int at = atomicAdd(A.rf_cnt, 1);
+        A.rf_list[at] = ((int64_t)row << 32) | (int64_t)(uint32_t)slot;
+    }
 }
 
 // Debug counters (only when A.stats != nullptr): see cals_debug_stats.

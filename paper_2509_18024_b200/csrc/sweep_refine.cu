@@ -90,9 +90,12 @@ __device__ __forceinline__ void refine_slice_gram(const SweepArgs& A, int row, i
 
 // slice_ok: the rows' kept sets are per-row thresholds (method 'core'; fast_core
 // rows use the stored normal equations, which hold its whole-source sketch).
+// from_slice: the list holds rows (int32) that rebuild their Gram from the slice
+// (method 'core', per-row thresholds); else (row << 32 | slot) entries solved
+// from the stored normal equations.
 template <int NT>
 __global__ void __launch_bounds__(NT) refine_kernel(SweepArgs A, const int* __restrict__ count,
-                                                   const int64_t* __restrict__ list, int slice_ok) {
+                                                   const void* __restrict__ list, int from_slice) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double s_x[CALS_MAX_NF_DEV];
     __shared__ double s_red[32];
@@ -105,14 +108,15 @@ __global__ void __launch_bounds__(NT) refine_kernel(SweepArgs A, const int* __re
     __shared__ uint64_t s_thr[CALS_MAX_NF_DEV];
     const int n_list = *count;
     for (int64_t e = blockIdx.x; e < n_list; e += gridDim.x) {
-        const int row = (int)(list[e] >> 32);
-        const int64_t slot = (int64_t)(uint32_t)list[e];
+        const int64_t ent = from_slice ? (int64_t)static_cast<const int32_t*>(list)[e] << 32
+                                       : static_cast<const int64_t*>(list)[e];
+        const int row = (int)(ent >> 32);
+        const int64_t slot = (int64_t)(uint32_t)ent;
         const int n = (int)(A.ptr[row + 1] - A.ptr[row]);
         const bool full = A.budget[row] >= n;
         const double* Gf = A.gbuf + (size_t)slot * nf * gs;
         // short rows rebuild their Gram in float64 (their fp32 sums are the error floor of an
         // ill-conditioned system); long rows' stored equations are float64-folded already
-        const bool from_slice = slice_ok && n <= (A.rf_slice_max > 0 ? A.rf_slice_max : kRfSliceMax);
         __syncthreads();
         if (from_slice && tid < nf) s_thr[tid] = A.thr_keys[(int64_t)row * nf + tid];
         int st = CALS_ROW_SINGULAR;
@@ -213,7 +217,7 @@ __global__ void __launch_bounds__(NT) refine_kernel(SweepArgs A, const int* __re
     }
 }
 
-template __global__ void refine_kernel<256>(SweepArgs, const int*, const int64_t*, int);
-template __global__ void refine_kernel<512>(SweepArgs, const int*, const int64_t*, int);
+template __global__ void refine_kernel<256>(SweepArgs, const int*, const void*, int);
+template __global__ void refine_kernel<512>(SweepArgs, const int*, const void*, int);
 
 }  // namespace cals
