@@ -9,5 +9,5 @@ ncu --kernel-name-base demangled -k regex:cals:: --metrics gpu__time_duration.su
     python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/f_ncu_launches.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:big_gram -c 1 -o gpurun_out/f_user_big_gram \
     python tools/prof_half.py large user 1 > gpurun_out/f_ncu_user.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:big_gram -c 1 -o gpurun_out/f_item_big_gram \
-    python tools/prof_half.py large item 1 > gpurun_out/f_ncu_item.log 2>&1
+ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "target/" -k regex:big_gram -c 1 \
+    -o gpurun_out/f_item_big_gram python tools/prof_half.py large item 1 > gpurun_out/f_ncu_item.log 2>&1

@@ -31,8 +31,9 @@ want = np.zeros((rows.size, n_f))
 _, _, ko = oracle.core_half_sweep(sp, si, sv, U.astype(np.float64), n_f, lam, rate, want, want_keys=True,
                                   threads=os.cpu_count())
 scale = np.maximum(np.abs(want).max(axis=1), 1e-2)
-for ratio in sys.argv[3:]:
-    os.environ["CALS_ILL_RATIO"] = ratio
+for ratio in sys.argv[3:] or ["default"]:
+    if ratio != "default":
+        os.environ["CALS_ILL_RATIO"] = ratio
     outs = []
     for rep in range(2):
         tgt, keys = half(eng, "item", U)
