@@ -754,11 +754,7 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.rss_rows = rss_rows;
     A.pen_rows = pen_rows;
     A.thr_keys = thr_keys != nullptr ? thr_keys : w.thr_all;  // the float64 refinement reads them
-    {
-        static thread_local float ratio;  // host source of the async copy outlives the call
-        ratio = (float)env_double("CALS_ILL_RATIO", ill_ratio_for(n_f));
-        cudaMemcpyToSymbolAsync(g_ill_ratio, &ratio, sizeof(float), 0, cudaMemcpyHostToDevice, st);
-    }
+    A.ill_ratio = (float)env_double("CALS_ILL_RATIO", ill_ratio_for(n_f));
     A.rf_cnt = w.rf_cnt;
     A.rf_list = w.rf_list;
     A.rs_cnt = w.rf_cnt + 2;
@@ -920,11 +916,7 @@ int cals_fast_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.rss_rows = rss_rows;
     A.pen_rows = pen_rows;
     A.thr_keys = w.thr_all;
-    {
-        static thread_local float ratio;
-        ratio = (float)env_double("CALS_ILL_RATIO", ill_ratio_for(n_f));
-        cudaMemcpyToSymbolAsync(g_ill_ratio, &ratio, sizeof(float), 0, cudaMemcpyHostToDevice, st);
-    }
+    A.ill_ratio = (float)env_double("CALS_ILL_RATIO", ill_ratio_for(n_f));
     A.rf_cnt = w.rf_cnt;
     A.rf_list = w.rf_list;
     A.rs_cnt = w.rf_cnt + 2;

@@ -105,13 +105,12 @@ __device__ int block_lu_solve(T* W, int nf, bool spd, T* x_out, int* s_piv) {
 __host__ inline float ill_ratio_for(int nf) {
     return nf <= 20 ? 100.0f : (nf <= 64 ? 2000.0f / (float)nf : 1000.0f / (float)nf);
 }
-__device__ float g_ill_ratio = 100.0f;
-__device__ __forceinline__ bool ill_conditioned(float dmin, float dmax) { return dmax > g_ill_ratio * dmin; }
+__device__ __forceinline__ bool ill_conditioned(float dmin, float dmax, float ratio) { return dmax > ratio * dmin; }
 
 // Returns, per lane, whether ITS system failed (uniform within a segment);
 // x: the lane's unknown (variable r of its system).
 template <int NFP>
-__device__ __forceinline__ bool seg_lu_solve(const double* __restrict__ Grow, int nf, bool spd, bool seg_valid,
+__device__ __forceinline__ bool seg_lu_solve(const double* __restrict__ Grow, int nf, bool spd, float ill_ratio, bool seg_valid,
                                              float& x, int lane) {
     const int r = lane & (NFP - 1);
     const bool rv = seg_valid && r < nf;
@@ -173,7 +172,7 @@ __device__ __forceinline__ bool seg_lu_solve(const double* __restrict__ Grow, in
     const bool bad = rv && (!(x == x) || (x - x != 0.f));
     const uint32_t anybad = __ballot_sync(CALS_FULL_MASK, bad);
     const uint32_t segm = (NFP == 32) ? 0xffffffffu : (((1u << NFP) - 1u) << seg_base);
-    return fail || ill_conditioned(dmin, dmax) || (anybad & segm) != 0;
+    return fail || ill_conditioned(dmin, dmax, ill_ratio) || (anybad & segm) != 0;
 }
 
 // Wide warp LU (32 < nf <= NF <= 64): lane owns rows `lane` and `lane + 32`
@@ -281,7 +280,7 @@ __device__ __forceinline__ void wide_substitute(WideLU<NF>& S, float& x0, float&
 }
 
 template <int NF>
-__device__ __forceinline__ bool wide_lu_solve(const float* __restrict__ W, int nf, bool spd, float& x0, float& x1,
+__device__ __forceinline__ bool wide_lu_solve(const float* __restrict__ W, int nf, bool spd, float ill_ratio, float& x0, float& x1,
                                               int lane) {
     static_assert(NF > 32 && NF <= 64, "two rows per lane");
     const int gs = nf + 1;
@@ -309,7 +308,7 @@ __device__ __forceinline__ bool wide_lu_solve(const float* __restrict__ W, int n
     x1 = 0.f;
     wide_substitute<NF>(S, x0, x1, lane, std::make_integer_sequence<int, NF>{});
     const bool bad = (v0 && (!(x0 == x0) || (x0 - x0 != 0.f))) || (v1 && (!(x1 == x1) || (x1 - x1 != 0.f)));
-    return S.fail || ill_conditioned(S.dmin, S.dmax) || __any_sync(CALS_FULL_MASK, bad);
+    return S.fail || ill_conditioned(S.dmin, S.dmax, ill_ratio) || __any_sync(CALS_FULL_MASK, bad);
 }
 
 // Float64 solve of a system the fp32 path failed or flagged, optionally with the

@@ -43,6 +43,7 @@ struct SweepArgs {
     int* rs_cnt;                  // rows deferred that rebuild their Gram from the slice: refined once
     int32_t* rs_list;             // after the tier's last batch (one launch, no per-batch latency)
     int rf_slice_max;             // rows up to this length rebuild from the slice (0: none)
+    float ill_ratio;              // pivot-magnitude spread that defers a system (ill_ratio_for)
 };
 
 // Hand a system the fp32 solve cannot hold to the float64 refinement.

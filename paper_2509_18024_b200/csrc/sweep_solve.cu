@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256, 3) solve_warp_kernel(SweepArgs A, const i
         const bool spd = sv && A.budget[row] >= n;
         const double* G = A.gbuf + (size_t)(sv ? li : 0) * nf * gs;
         float x;
-        const bool bad = seg_lu_solve<NFP>(G + (size_t)(r < nf ? r : 0) * gs, nf, spd, sv, x, lane);
+        const bool bad = seg_lu_solve<NFP>(G + (size_t)(r < nf ? r : 0) * gs, nf, spd, A.ill_ratio, sv, x, lane);
         // fp32 breakdown or ill-conditioning: the float64 refinement owns the row
         const bool deferred = bad && sv;
         if (deferred && r == 0) defer_refine(A, row, li);
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(128, 3) solve_wide_kernel(SweepArgs A, const i
         __syncwarp();
         float x0, x1;
         const int st = CALS_ROW_OK;
-        if (wide_lu_solve<NF>(W, nf, spd, x0, x1, lane)) {  // the float64 refinement owns the row
+        if (wide_lu_solve<NF>(W, nf, spd, A.ill_ratio, x0, x1, lane)) {  // the float64 refinement owns the row
             if (lane == 0) defer_refine(A, row, li);
             continue;
         }
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(NF, 3) solve_rows_kernel(SweepArgs A, const in
         __syncthreads();
         // unknown r (solved from the row pivoted at step r)
         float x = r < nf ? xs[r] : 0.f;
-        const bool bad = fail || ill_conditioned(dmin, dmax) || (r < nf && (!(x == x) || (x - x != 0.f)));
+        const bool bad = fail || ill_conditioned(dmin, dmax, A.ill_ratio) || (r < nf && (!(x == x) || (x - x != 0.f)));
         if (bad) atomicOr(&s_bad, 1);
         __syncthreads();
         const int st = CALS_ROW_OK;
