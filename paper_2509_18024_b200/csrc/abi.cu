@@ -271,11 +271,9 @@ struct Work {
     uint32_t* brk;
     int* fcnt;
     unsigned long long* famax;
-    double* retry;
     double* gbuf;
     int64_t gbuf_rows;
     double* gbuf2;    // staged tier's own normal-equation buffer when both tiers run concurrently
-    double* retry2;  // and its jitter-retry scratch
     uint64_t* thr_all;  // [n_rows][nf] selection thresholds (when the caller asks for none)
     int* rf_cnt;        // [4]: per stream, rows deferred to the float64 refinement from the stored
     int64_t* rf_list;   // equations [2][gbuf_rows] (row << 32 | slot), and from the slice:
@@ -283,7 +281,6 @@ struct Work {
 };
 
 constexpr int kMaxGrid = 160 * 16;  // grid_for never exceeds min(SMs, 160) * 16 CTAs
-inline int retry_stride(int nf) { return ((nf * (nf + 1) + nf) + 31) & ~31; }
 constexpr int64_t kMaxSolveWarps = 160 * 64;  // solve_warp_kernel grid cap (64 warps per SM)
 
 Work carve(const cals_plan* P, void* ws, size_t* total) {
@@ -301,12 +298,10 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
     w.brk = c.take<uint32_t>((size_t)std::max<int64_t>(P->n_big, 1) * nf);  // all big rows (one calibration pass)
     w.fcnt = c.take<int>((size_t)bb.max_rows * nf);                      // fast_core: kept counts (multi-item rows)
     w.famax = c.take<unsigned long long>((size_t)bb.max_rows * nf);      // fast_core: fallback keys
-    w.retry = c.take<double>((size_t)std::max<int64_t>(kMaxGrid, kMaxSolveWarps) * retry_stride(nf));
     w.gbuf_rows = gbuf_rows_for(nf, P->n_small + P->n_big);
     w.gbuf = c.take<double>((size_t)w.gbuf_rows * nf * (nf + 1));
     if (P->n_small > 0 && P->n_big > 0) {  // the two tiers run on two streams
         w.gbuf2 = c.take<double>((size_t)w.gbuf_rows * nf * (nf + 1));
-        w.retry2 = c.take<double>((size_t)std::max<int64_t>(kMaxGrid, kMaxSolveWarps) * retry_stride(nf));
     }
     w.thr_all = c.take<uint64_t>((size_t)std::max<int64_t>(P->n_rows, 1) * nf);
     w.rf_cnt = c.take<int>(4);
@@ -370,11 +365,6 @@ void launch_solve_fp32(const SweepArgs& A, const int32_t* rows, int64_t count, c
             solve_rows_kernel<96><<<(int)std::min<int64_t>(count, cap), 96, 0, st>>>(A, rows, count);
         else
             solve_rows_kernel<128><<<(int)std::min<int64_t>(count, cap), 128, 0, st>>>(A, rows, count);
-    } else {
-        const size_t smem = align16((size_t)A.nf * (A.nf + 1) * 4);
-        allow_smem(solve_block_kernel);
-        const int grid = grid_for(solve_block_kernel, smem, count, 16, 128);
-        solve_block_kernel<<<std::min(grid, kMaxGrid), 128, smem, st>>>(A, rows, count);
     }
 }
 
@@ -766,8 +756,6 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.status = row_status;
     A.summary = reinterpret_cast<unsigned long long*>(status_summary);
     A.qtab = nullptr;
-    A.retry_ws = w.retry;
-    A.retry_stride = retry_stride(n_f);
 
     const bool long_small = P->n_small > 0 && P->small_seg_maxn[0] > 16;
     if ((long_small || P->n_big > 0) && side->nnz > 0) {
@@ -784,14 +772,13 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     }
     int rc = CALS_OK;
     // the staged and tiled tiers touch disjoint rows: with both present the staged
-    // tier runs on a second stream (own normal-equation buffer and retry scratch)
+    // tier runs on a second stream (own normal-equation buffer and float64 refinement lists)
     // beside the tiled tier, filling the SMs its low occupancy leaves idle
     const bool both = P->n_small > 0 && P->n_big > 0;
     SweepArgs As = A;
     cudaStream_t ss = st;
     if (both) {
         As.gbuf = w.gbuf2;
-        As.retry_ws = w.retry2;
         As.rf_cnt = w.rf_cnt + 1;
         As.rf_list = w.rf_list + w.gbuf_rows;
         As.rs_cnt = w.rf_cnt + 3;
@@ -927,8 +914,6 @@ int cals_fast_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.stats = g_stats;
     A.status = row_status;
     A.summary = reinterpret_cast<unsigned long long*>(status_summary);
-    A.retry_ws = w.retry;
-    A.retry_stride = retry_stride(n_f);
     if (P->n_big == 0) return CALS_OK;
     const int gwords = (n_f + 31) / 32;
     if (n_f <= 8) return launch_fast<8>(A, P, w, gmask, gwords, st);

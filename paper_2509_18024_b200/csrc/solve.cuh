@@ -5,9 +5,10 @@
 // the reference does with LAPACK gesv (_kernels.py:233-236).  Rows whose
 // sketch is complete (s == n) take the exact SPD ridge path (core.py:206-207,
 // als.py:184-205): elimination without pivoting, failing on a non-positive
-// pivot exactly where Cholesky fails.  Either failure triggers the
-// reference's single jitter retry (+1e-10 * tr(G)/n_f on the diagonal,
-// core.py:126-131), done in float64 by the block solver (rare path).
+// pivot exactly where Cholesky fails.  A failure (or an ill-conditioned
+// system) is re-solved in float64 with the reference's single jitter retry
+// (+1e-10 * tr(G)/n_f on the diagonal, core.py:126-131) by sweep_refine.cu;
+// block_lu_solve below serves the public single-row update (misc.cu).
 //
 // Input: augmented matrix G[r * gs + j], j < nf the Gram, j == nf the RHS.
 #pragma once
@@ -18,7 +19,7 @@
 namespace cals {
 
 // Block-wide LU (nf <= 128) in shared memory, in place on W (stride nf+1),
-// working copy of G.  All threads of the block must call it.  Returns 0/1.
+// working copy of G (cals_update_core).  All threads of the block must call it.  Returns 0/1.
 template <typename T>
 __device__ int block_lu_solve(T* W, int nf, bool spd, T* x_out, int* s_piv) {
     const int gs = nf + 1;
@@ -96,8 +97,8 @@ __device__ int block_lu_solve(T* W, int nf, bool spd, T* x_out, int* s_piv) {
 // condition number (measured: ~6e-9 * cond), and the factor contract is 1e-4
 // relative to the reference's float64 solve.  A spread of pivot magnitudes
 // beyond the rank's ratio (a lower bound on cond) sends the system to the float64
-// path (warp_retry_f64: plain float64 first, the reference's jitter only if
-// that is singular too), exactly like an fp32 breakdown.
+// refinement (sweep_refine.cu: plain float64 first, the reference's jitter
+// only if that is singular too), exactly like an fp32 breakdown.
 // Ratio by rank (the fp32 elimination's error also grows with n_f): 100 up to
 // n_f = 20, then 2000 / n_f (31 at 64), and 1000 / n_f above 64 (8 at 128);
 // set per half-sweep (ill_ratio_for).  Measured on the 500M config at a later
@@ -309,70 +310,6 @@ __device__ __forceinline__ bool wide_lu_solve(const float* __restrict__ W, int n
     wide_substitute<NF>(S, x0, x1, lane, std::make_integer_sequence<int, NF>{});
     const bool bad = (v0 && (!(x0 == x0) || (x0 - x0 != 0.f))) || (v1 && (!(x1 == x1) || (x1 - x1 != 0.f)));
     return S.fail || ill_conditioned(S.dmin, S.dmax, ill_ratio) || __any_sync(CALS_FULL_MASK, bad);
-}
-
-// Float64 solve of a system the fp32 path failed or flagged, optionally with the
-// reference's diagonal jitter 1e-10 * tr(G) / nf (core.py:126-131, als.py:191-197):
-// the callers run it plain first and jittered only when that is singular, as the
-// reference retries only after LinAlgError.  One warp, lanes over
-// columns, scratch W (nf*(nf+1) doubles, any memory).  Rare path.
-__device__ int warp_retry_f64(const double* G, int nf, bool spd, double* W, double* x, int lane, bool jitter) {
-    const int gs = nf + 1;
-    double tr = 0.0;
-    for (int c = 0; c < nf; ++c) tr += (double)G[c * gs + c];
-    const double jit = jitter ? 1e-10 * tr / (double)nf : 0.0;
-    for (int e = lane; e < nf * gs; e += 32) {
-        const int c = e / gs, f = e - c * gs;
-        W[e] = (double)G[e] + ((c == f) ? jit : 0.0);
-    }
-    __syncwarp();
-    for (int k = 0; k < nf; ++k) {
-        int p = k;
-        if (!spd) {
-            double best = -1.0;
-            for (int r = k; r < nf; ++r) {
-                const double v = fabs(W[r * gs + k]);
-                if (v > best) { best = v; p = r; }
-            }
-            if (!(best > 0.0)) return 1;
-        } else if (!(W[k * gs + k] > 0.0)) {
-            return 1;
-        }
-        if (p != k) {
-            for (int jj = lane; jj < gs; jj += 32) {
-                const double t = W[k * gs + jj];
-                W[k * gs + jj] = W[p * gs + jj];
-                W[p * gs + jj] = t;
-            }
-            __syncwarp();
-        }
-        const double d = W[k * gs + k];
-        for (int r = k + 1; r < nf; ++r) {
-            const double f = W[r * gs + k] / d;
-            __syncwarp();
-            for (int jj = k + 1 + lane; jj < gs; jj += 32) W[r * gs + jj] -= f * W[k * gs + jj];
-            __syncwarp();
-        }
-    }
-    int bad = 0;
-    if (lane == 0) {
-        for (int r = nf - 1; r >= 0; --r) {
-            double acc = W[r * gs + nf];
-            for (int jj = r + 1; jj < nf; ++jj) acc -= W[r * gs + jj] * x[jj];
-            x[r] = acc / W[r * gs + r];
-            if (!(x[r] == x[r]) || (x[r] - x[r] != 0.0)) bad = 1;
-        }
-    }
-    __syncwarp();
-    return __shfl_sync(CALS_FULL_MASK, bad, 0);
-}
-
-// Plain float64 solve, then (if singular) the jittered retry.  Returns the
-// row status (CALS_ROW_OK / JITTERED / SINGULAR); x holds the solution.
-__device__ int warp_solve_f64(const double* G, int nf, bool spd, double* W, double* x, int lane) {
-    if (!warp_retry_f64(G, nf, spd, W, x, lane, false)) return CALS_ROW_OK;
-    __syncwarp();
-    return warp_retry_f64(G, nf, spd, W, x, lane, true) ? CALS_ROW_SINGULAR : CALS_ROW_JITTERED;
 }
 
 }  // namespace cals

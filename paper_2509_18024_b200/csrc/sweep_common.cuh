@@ -33,8 +33,6 @@ struct SweepArgs {
     const uint32_t* qtab;  // [nf][kQ+1] abs-bit quantiles of the source, or null
     float delta_tab;       // quantile-table sampling margin (rank units)
     unsigned long long* summary;  // nullable: max over rows of (status << 32 | ~row)
-    double* retry_ws;             // per-warp float64 jitter-retry scratch (retry_stride doubles each)
-    int retry_stride;
     double* gbuf;                 // normal equations of the current batch: [slot][nf][nf+1], float64
                                   // (the fp32 solve rounds them; the float64 refinement needs them exact)
     unsigned long long* stats;    // nullable debug counters (cals_debug_stats)

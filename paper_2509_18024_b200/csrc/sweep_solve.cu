@@ -1,8 +1,10 @@
 // sweep_solve.cu -- phase B of a half-sweep: solve a batch of sketched normal
-// equations written by phase A, with the reference's failure semantics
-// (LU with partial pivoting for sketched rows, SPD for complete sketches,
-// one float64 jitter retry; core.py:120-131, als.py:184-205), write the new
-// factor rows (als.py:286) and their penalty terms n_i*|w_i|^2 (als.py:162-167).
+// equations written by phase A in fp32 registers (LU with partial pivoting for
+// sketched rows, SPD elimination for complete sketches; core.py:120-131,
+// als.py:184-205), write the new factor rows (als.py:286) and their penalty
+// terms n_i*|w_i|^2 (als.py:162-167).  A breakdown or an ill-conditioned system
+// is deferred to the float64 refinement (sweep_refine.cu), which owns the
+// reference's plain-then-jittered retry semantics.
 #include "solve.cuh"
 #include "sweep_common.cuh"
 
@@ -39,52 +41,6 @@ __global__ void __launch_bounds__(256, 3) solve_warp_kernel(SweepArgs A, const i
             if (sv && !deferred && r == 0) A.pen_rows[row] = (double)n * p;
         }
         if (sv && !deferred && r == 0) {
-            A.status[row] = st;
-            report_status(A, row, st);
-        }
-    }
-}
-
-// One CTA per system (nf > 32): LU in shared memory.
-__global__ void __launch_bounds__(128) solve_block_kernel(SweepArgs A, const int32_t* __restrict__ rows,
-                                                          int64_t n_list) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ float wv[CALS_MAX_NF_DEV];
-    __shared__ double red[32];
-    __shared__ int s_piv[1], s_flag[1];
-    const int nf = A.nf, gs = nf + 1, nout = nf * gs, tid = threadIdx.x;
-    float* W = reinterpret_cast<float*>(smem);
-    for (int64_t li = blockIdx.x; li < n_list; li += gridDim.x) {
-        const int row = rows[li];
-        const int n = (int)(A.ptr[row + 1] - A.ptr[row]);
-        const bool spd = A.budget[row] >= n;
-        const double* G = A.gbuf + (size_t)li * nout;
-        __syncthreads();
-        for (int e = tid; e < nout; e += blockDim.x) W[e] = (float)G[e];
-        __syncthreads();
-        int st = CALS_ROW_OK;
-        if (block_lu_solve<float>(W, nf, spd, wv, s_piv)) {
-            if (tid < 32) {
-                double* Wd = A.retry_ws + (size_t)blockIdx.x * A.retry_stride;
-                double* xd = Wd + nout;
-                const int sq = warp_solve_f64(G, nf, spd, Wd, xd, tid);
-                if (tid < 32) {
-                    for (int f = tid; f < nf; f += 32) wv[f] = (float)xd[f];
-                    if (tid == 0) s_flag[0] = sq;
-                }
-            }
-            __syncthreads();
-            st = s_flag[0];
-        }
-        if (st != CALS_ROW_SINGULAR)
-            for (int f = tid; f < nf; f += blockDim.x) A.tgt[(int64_t)row * A.ld_tgt + f] = wv[f];
-        if (A.pen_rows != nullptr) {
-            double p = 0.0;
-            for (int f = tid; f < nf; f += blockDim.x) p += (double)wv[f] * (double)wv[f];
-            p = block_sum_d(p, red);
-            if (tid == 0) A.pen_rows[row] = (st == CALS_ROW_SINGULAR) ? 0.0 : (double)n * p;
-        }
-        if (tid == 0) {
             A.status[row] = st;
             report_status(A, row, st);
         }
