@@ -10,17 +10,17 @@
 //            and ptr[key] = offset of the key's first segment
 //   scatter  each entry to its segment (atomic slot; order inside the segment
 //            is arbitrary) as one 64-bit word (sec << 32 | value bits)
-//   sort     every segment by its words (at most 2^kSecShift distinct
-//            secondaries per segment: a warp sort up to 32 words, a
-//            shared-memory bitonic sort above), split into idx / val
+//   sort     every segment by its secondaries (at most 2^kSecShift distinct
+//            values per segment: a warp sort up to 32 words, a presence
+//            bitmap + popcount ranks above), split into idx / val
 //
 // Segments cover disjoint ascending secondary ranges, so each key's run is
 // sorted once its segments are.  COO -> CSR uses key = user, sec = item;
 // CSR -> CSC uses key = item, sec = user (the row of the CSR entry).  The
 // first duplicate pair in (key, sec) order -- the one the reference names --
 // is the minimum over duplicated pairs of (key << 32 | sec), found with
-// adjacent-word compares after the sort (or a shared-memory bitmap for a
-// segment that overflows the sort tier, which only duplicates can cause).
+// adjacent-word compares after a warp sort, or as an already-set bit of a
+// longer segment's presence bitmap.
 // Everything is integer work: results are exact and run-to-run identical.
 
 namespace cals {
@@ -232,17 +232,25 @@ __global__ void __launch_bounds__(256) ix_sort_small_kernel(const int64_t* __res
     }
 }
 
-// One CTA per queued segment (33 .. kSegMax words): shared-memory bitonic sort.
-// A longer segment can only hold duplicates: its smallest duplicated
-// secondary is found with a bitmap of the segment's secondary range.
+// One CTA per queued segment (> 32 words).  A segment's secondaries are
+// distinct values inside one kSegMax-wide block, so the segment is sorted by
+// presence: a kSegMax-bit bitmap of its secondaries (shared memory), an
+// exclusive prefix of the word popcounts, and every word goes straight to the
+// rank of its secondary -- O(len + kSegMax / 32), two passes over the words.
+// A bit found already set is a duplicate pair: the smallest one is reported
+// (the outputs of such a segment do not matter, the build fails).
 __global__ void __launch_bounds__(1024) ix_sort_big_kernel(const int64_t* __restrict__ off, int64_t nb,
                                                            const int64_t* __restrict__ big_list,
                                                            const unsigned long long* __restrict__ big_count,
                                                            const uint64_t* __restrict__ words,
                                                            int32_t* __restrict__ out_idx, float* __restrict__ out_val,
                                                            unsigned long long* __restrict__ dup) {
-    extern __shared__ __align__(16) uint64_t s_w[];  // [kSegMax]
-    const int tid = threadIdx.x, nt = blockDim.x;
+    constexpr int NW = kSegMax / 32;  // bitmap words
+    __shared__ uint32_t s_bits[NW];
+    __shared__ int s_pre[NW];
+    __shared__ int s_wsum[32];
+    __shared__ int s_dup;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int64_t n_big = (int64_t)*big_count;
     for (int64_t b = blockIdx.x; b < n_big; b += gridDim.x) {
         const int64_t seg = big_list[b];
@@ -250,41 +258,47 @@ __global__ void __launch_bounds__(1024) ix_sort_big_kernel(const int64_t* __rest
         const int64_t len = off[seg + 1] - lo;
         const uint64_t key_hi = (unsigned long long)(seg / nb) << 32;
         __syncthreads();
-        if (len > kSegMax) {
-            uint32_t* bits = reinterpret_cast<uint32_t*>(s_w);  // kSegMax bits
-            for (int i = tid; i < kSegMax / 32; i += nt) bits[i] = 0u;
-            __syncthreads();
-            for (int64_t i = tid; i < len; i += nt) {
-                const uint32_t sec = (uint32_t)(words[lo + i] >> 32);
-                const uint32_t rel = sec & (kSegMax - 1);
-                const uint32_t m = 1u << (rel & 31);
-                if (atomicOr(&bits[rel >> 5], m) & m) atomicMin(dup, key_hi | sec);
-            }
-            continue;
-        }
-        int n2 = 64;
-        while (n2 < len) n2 <<= 1;
-        for (int i = tid; i < n2; i += nt) s_w[i] = i < len ? words[lo + i] : ~0ull;
+        for (int i = tid; i < NW; i += nt) s_bits[i] = 0u;
+        if (tid == 0) s_dup = 0;
         __syncthreads();
-        for (int size = 2; size <= n2; size <<= 1) {
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                for (int t = tid; t < (n2 >> 1); t += nt) {
-                    const int i = 2 * t - (t & (stride - 1));  // lower element of the pair
-                    const int j = i + stride;
-                    const uint64_t a = s_w[i], c = s_w[j];
-                    const bool asc = (i & size) == 0;
-                    if ((a > c) == asc) {
-                        s_w[i] = c;
-                        s_w[j] = a;
-                    }
-                }
-                __syncthreads();
+        for (int64_t i = tid; i < len; i += nt) {
+            const uint32_t sec = (uint32_t)(words[lo + i] >> 32);
+            const uint32_t rel = sec & (kSegMax - 1);
+            const uint32_t m = 1u << (rel & 31);
+            if (atomicOr(&s_bits[rel >> 5], m) & m) {
+                atomicMin(dup, key_hi | sec);
+                s_dup = 1;
             }
         }
-        for (int i = tid; i < len; i += nt) {
-            const uint64_t v = s_w[i];
-            ix_emit(v, lo + i, out_idx, out_val);
-            if (i > 0 && (s_w[i - 1] >> 32) == (v >> 32)) atomicMin(dup, key_hi | (v >> 32));
+        __syncthreads();
+        if (s_dup) continue;  // uniform
+        // exclusive prefix of the popcounts (NW = 512 words, 1024 threads: one word per thread)
+        int v = tid < NW ? __popc(s_bits[tid]) : 0;
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(CALS_FULL_MASK, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            int w = lane < (nt >> 5) ? s_wsum[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(CALS_FULL_MASK, w, o);
+                if (lane >= o) w += t;
+            }
+            s_wsum[lane] = w;  // inclusive prefix over warps
+        }
+        __syncthreads();
+        if (tid < NW) s_pre[tid] = incl - v + (warp ? s_wsum[warp - 1] : 0);
+        __syncthreads();
+        for (int64_t i = tid; i < len; i += nt) {
+            const uint64_t w = words[lo + i];
+            const uint32_t rel = (uint32_t)(w >> 32) & (kSegMax - 1);
+            const int rank = s_pre[rel >> 5] + __popc(s_bits[rel >> 5] & ((1u << (rel & 31)) - 1u));
+            ix_emit(w, lo + rank, out_idx, out_val);
         }
     }
 }
@@ -358,14 +372,8 @@ int ix_group(Count count, Scatter scatter, int64_t n_keys, int64_t n_sec, int64_
         ProfScope ps("ix_sort", st);
         ix_sort_small_kernel<<<(unsigned)std::min<int64_t>((n_seg + 255) / 256, grid), 256, 0, st>>>(
             w.off, n_seg, nb, w.words, out_idx, out_val, w.big_list, w.counters, w.counters + 1);
-        const size_t smem = (size_t)kSegMax * 8;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(ix_sort_big_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
-        ix_sort_big_kernel<<<sms, 1024, smem, st>>>(w.off, nb, w.big_list, w.counters, w.words, out_idx, out_val,
-                                                    w.counters + 1);
+        ix_sort_big_kernel<<<sms * 2, 1024, 0, st>>>(w.off, nb, w.big_list, w.counters, w.words, out_idx, out_val,
+                                                  w.counters + 1);
     }
     return cuda_status("dual-index build");
 }
