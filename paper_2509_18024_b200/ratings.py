@@ -14,7 +14,8 @@ import numpy as np
 
 from .errors import DataError
 
-__all__ = ["RatingMatrix", "DeviceRatingMatrix", "coo_to_csr_device", "csr_to_csc_device"]
+__all__ = ["RatingMatrix", "DeviceRatingMatrix", "coo_to_csr_device", "csr_to_csc_device", "build_rating_matrix",
+           "read_ratings_csv", "write_ratings_csv"]
 
 
 class RatingMatrix:
@@ -283,3 +284,71 @@ class DeviceRatingMatrix:
 
     def __repr__(self):
         return f"DeviceRatingMatrix({self.n_users} users x {self.n_items} items, {self.n_entries} observed)"
+
+
+# ---------------------------------------------------------------------------
+# Ratings CSV (ratings.py:161-183, 253-291 of the reference): the same header,
+# error messages and id remapping (np.unique order of the external ids), with
+# the dual index optionally built on the device.
+# ---------------------------------------------------------------------------
+
+def build_rating_matrix(triples, device=None):
+    """(user_id, item_id, rating) triples -> RatingMatrix with external ids
+    remapped to dense indices in sorted-id order (ratings.py:161-181);
+    ``device`` (e.g. "cuda") builds a DeviceRatingMatrix instead."""
+    triples = list(triples)
+    if not triples:
+        raise DataError("no rating triples supplied")
+    raw_u = np.asarray([t[0] for t in triples])
+    raw_i = np.asarray([t[1] for t in triples])
+    vals = np.asarray([float(t[2]) for t in triples], dtype=np.float64)
+    user_ids, users = np.unique(raw_u, return_inverse=True)
+    item_ids, items = np.unique(raw_i, return_inverse=True)
+    cls = RatingMatrix if device is None else DeviceRatingMatrix
+    kw = {} if device is None else {"device": device}
+    return cls(users, items, vals, n_users=len(user_ids), n_items=len(item_ids), user_ids=user_ids,
+               item_ids=item_ids, **kw)
+
+
+def read_ratings_csv(path, device=None):
+    """Rating-triple CSV with header ``user,item,rating[,date]`` (ratings.py:253-276)."""
+    import csv
+
+    triples = []
+    with open(path, "r", encoding="utf-8", newline="") as fh:
+        reader = csv.reader(fh)
+        header = next(reader, None)
+        if header is None or [h.strip().lower() for h in header[:3]] != ["user", "item", "rating"]:
+            raise DataError(f"{path}: expected header 'user,item,rating[,date]', got {header}")
+        for lineno, row in enumerate(reader, start=2):
+            if not row:
+                continue
+            if len(row) < 3:
+                raise DataError(f"{path}:{lineno}: expected at least 3 fields, got {len(row)}")
+            try:
+                rating = float(row[2])
+            except ValueError as exc:
+                raise DataError(f"{path}:{lineno}: bad rating {row[2]!r}") from exc
+            triples.append((row[0], row[1], rating))
+    return build_rating_matrix(triples, device=device)
+
+
+def write_ratings_csv(path, R):
+    """Observed entries as ``user,item,rating`` in row-major order, external ids if
+    present, shortest round-trip decimals (ratings.py:284-291)."""
+    import csv
+
+    def host(a, dt):
+        return np.asarray(a.cpu().numpy() if hasattr(a, "cpu") else a, dtype=dt)
+
+    counts = np.diff(host(R.row_ptr, np.int64))
+    users = np.repeat(np.arange(R.n_users, dtype=np.int64), counts)
+    items = host(R.row_items, np.int64)
+    vals = host(R.row_vals, np.float64)
+    u_lab = R.user_ids[users] if R.user_ids is not None else users
+    i_lab = R.item_ids[items] if R.item_ids is not None else items
+    with open(path, "w", encoding="utf-8", newline="") as fh:
+        w = csv.writer(fh, lineterminator="\n")
+        w.writerow(["user", "item", "rating"])
+        for u, i, v in zip(u_lab, i_lab, vals):
+            w.writerow([u, i, repr(float(v))])

@@ -299,6 +299,32 @@ def index_cases():
                         dup_names=np.array(list(dups)), dup_msgs=np.array(list(dups.values())))
 
 
+def io_cases():
+    """CAMX factor container and ratings CSV written/read by the reference
+    (serialize.py:14-47, ratings.py:253-291): the files and what the reference
+    reads back from them."""
+    from coreals import serialize
+    from coreals.ratings import read_ratings_csv, write_ratings_csv
+    rng = np.random.default_rng(21)
+    F = rng.normal(size=(5, 3))
+    serialize.write_matrix(os.path.join(OUT, "factors.camx"), F)
+    # string ids (sorted lexicographically by the reference: "u10" < "u2"), a date column
+    rows = ["user,item,rating,date"]
+    users = ["u2", "u10", "u2", "alice", "u10", "bob"]
+    items = ["i1", "i1", "i3", "i3", "x", "i1"]
+    vals = ["4.5", "3", "1e0", "2.25", "5", "0.5"]
+    for u, i, v in zip(users, items, vals):
+        rows.append(f"{u},{i},{v},2020-01-0{len(u)}")
+    path = os.path.join(OUT, "ratings.csv")
+    with open(path, "w") as fh:
+        fh.write("\n".join(rows) + "\n")
+    R = read_ratings_csv(path)
+    write_ratings_csv(os.path.join(OUT, "ratings_written.csv"), R)
+    np.savez_compressed(os.path.join(OUT, "io_cases.npz"), F=F, row_ptr=R.row_ptr, row_items=R.row_items,
+                        row_vals=R.row_vals, col_ptr=R.col_ptr, col_users=R.col_users, col_vals=R.col_vals,
+                        user_ids=np.asarray(R.user_ids).astype(str), item_ids=np.asarray(R.item_ids).astype(str))
+
+
 def fast_cases():
     fast_case("small", 5, 200, 150, 0.2, 8, 0.1, 0.3, 4)
     # sparse slices (empty sketched columns -> fallback), ties, an empty user
@@ -312,6 +338,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if sys.argv[1:] == ["fast"]:
         fast_cases()
+        sys.exit(0)
+    if sys.argv[1:] == ["io"]:
+        io_cases()
         sys.exit(0)
     if sys.argv[1:] == ["index"]:
         index_cases()
@@ -334,4 +363,5 @@ if __name__ == "__main__":
     fast_cases()
     metric_cases()
     index_cases()
+    io_cases()
     print("golden fixtures written to", OUT)
