@@ -218,7 +218,7 @@ def check_against_oracle(R, n_f, lam, rate, source_item, seed=0, ties=False):
 
 
 @pytest.mark.parametrize("item_rows", [None, 1024])
-@pytest.mark.parametrize("n_f", [1, 3, 5, 8, 16, 24, 32, 48, 64, 128])
+@pytest.mark.parametrize("n_f", [1, 3, 5, 8, 16, 24, 32, 48, 64, 80, 100, 128])
 def test_oracle_parity_mixed_tiers(n_f, item_rows, monkeypatch):
     """Short rows (identity lists), table-bracket rows and big tiled rows."""
     u, i, v = random_matrix(n_f, 3000, 400, 0.04, heavy_items=6, heavy_density=0.9)
@@ -397,7 +397,7 @@ def test_evaluation_metrics_match_reference():
         cb.prmse(([], [], []), F)
 
 
-@pytest.mark.parametrize("n_f", [8, 64, 128])
+@pytest.mark.parametrize("n_f", [8, 48, 64, 100, 128])
 def test_float64_path_on_every_system(n_f, monkeypatch):
     """Every system forced through the float64 solve (CALS_ILL_RATIO=0), on all
     tiers including multi-item rows: the float64 path alone matches the oracle."""
