@@ -176,10 +176,12 @@ __global__ void __launch_bounds__(NT) refine_kernel(SweepArgs A, const int* __re
                 const double d = G[k * gs + k];
                 for (int i = k + 1 + tid; i < nf; i += NT) G[i * gs + k] /= d;  // multipliers
                 __syncthreads();
-                const int w = gs - k - 1;
-                for (int q = tid; q < (nf - k - 1) * w; q += NT) {
-                    const int i = k + 1 + q / w, j = k + 1 + q % w;
-                    G[i * gs + j] = fma(-G[i * gs + k], G[k * gs + j], G[i * gs + j]);
+                // rank-1 update of the trailing block: warps over rows, lanes over columns
+                // (consecutive doubles per warp, the pivot-row value kept per column)
+                for (int j = k + 1 + lane; j < gs; j += 32) {
+                    const double pj = G[k * gs + j];
+                    for (int i = k + 1 + warp; i < nf; i += NT / 32)
+                        G[i * gs + j] = fma(-G[i * gs + k], pj, G[i * gs + j]);
                 }
                 __syncthreads();
             }
