@@ -336,7 +336,13 @@ void launch_refine(const SweepArgs& A, cudaStream_t st, bool from_slice) {
 template <int NFP>
 void launch_solve(const SweepArgs& A, const int32_t* rows, int64_t count, cudaStream_t st) {
     if (count <= 0) return;
-    launch_solve_fp32<NFP>(A, rows, count, st);
+    if (A.nf > 64) {
+        ProfScope ps("solve_kernel", st);
+        defer_all_kernel<<<(int)std::min<int64_t>((count + 255) / 256, (int64_t)dev().sms * 8), 256, 0, st>>>(
+            A, rows, count);
+    } else {
+        launch_solve_fp32<NFP>(A, rows, count, st);
+    }
     launch_refine(A, st, false);  // systems that need this batch's stored equations
 }
 
