@@ -100,9 +100,10 @@ __device__ int block_lu_solve(T* W, int nf, bool spd, T* x_out, int* s_piv) {
 // refinement (sweep_refine.cu: plain float64 first, the reference's jitter
 // only if that is singular too), exactly like an fp32 breakdown.
 // Ratio by rank (the fp32 elimination's error also grows with n_f): 100 up to
-// n_f = 20, then 2000 / n_f (31 at 64), and 1000 / n_f above 64 (8 at 128);
-// set per half-sweep (ill_ratio_for).  Measured on the 500M config at a later
-// iteration (tools/ill_diag.py) and on the wide config's short rows.
+// n_f = 20, then 2000 / n_f (31 at 64); set per half-sweep (ill_ratio_for).
+// Measured on the 500M config at a later iteration (tools/ill_diag.py).  Above
+// n_f = 64 the fp32 LU is skipped (defer_all_kernel): 97 % of the wide config's
+// systems exceeded any useful ratio.
 __host__ inline float ill_ratio_for(int nf) {
     return nf <= 20 ? 100.0f : (nf <= 64 ? 2000.0f / (float)nf : 1000.0f / (float)nf);
 }
