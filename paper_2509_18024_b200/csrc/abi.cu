@@ -364,14 +364,8 @@ void launch_solve_fp32(const SweepArgs& A, const int32_t* rows, int64_t count, c
             allow_smem(solve_wide_kernel<64>);
             solve_wide_kernel<64><<<(int)blocks, 128, smem, st>>>(A, rows, count);
         }
-    } else if (A.nf <= 128) {
-        // one CTA of NF threads per system, rows in registers
-        const int64_t cap = (int64_t)dev().sms * 3;
-        if (A.nf <= 96)
-            solve_rows_kernel<96><<<(int)std::min<int64_t>(count, cap), 96, 0, st>>>(A, rows, count);
-        else
-            solve_rows_kernel<128><<<(int)std::min<int64_t>(count, cap), 128, 0, st>>>(A, rows, count);
     }
+    // n_f > 64: no fp32 LU, every system goes to the float64 pass (launch_solve)
 }
 
 template <int CPL>
