@@ -432,3 +432,28 @@ def test_oracle_parity_ill_conditioned(n_f, item_rows, monkeypatch):
     finally:
         _lib.load().cals_debug_stats(None)
     assert int(stats[15]) > 0  # the float64 path was exercised
+
+
+@pytest.mark.parametrize("n_f", [16, 64])
+def test_later_iteration_half_sweep_matches_oracle(n_f):
+    """After several iterations the factors are large and the sketched systems
+    ill-conditioned (the regime where an all-fp32 pipeline drifted from the
+    float64 reference): one more half-sweep from the GPU's own state
+    still matches the oracle fed the same state -- keys exactly, rows to 1e-4."""
+    u, i, v = random_matrix(n_f + 7, 3000, 400, 0.05, heavy_items=8, heavy_density=0.9)
+    R = cb.RatingMatrix(u, i, v, n_users=3000, n_items=400)
+    M0 = np.random.default_rng(2).normal(0, 0.1, (400, n_f)).astype(np.float32)
+    lam, rate = 0.02, 0.1
+    eng = CoreEngine(R, n_f, rate, lam)
+    eng.set_factors(np.zeros((R.n_users, n_f)), M0)
+    for _ in range(6):
+        eng.step("user")
+    eng.finish("user")
+    U = eng.U_view.contiguous().float().cpu().numpy()
+    M, keys = gpu_half(eng, "item", U)
+    Mo = np.zeros((R.n_items, n_f))
+    _, _, ko = oracle.core_half_sweep(R.col_ptr, R.col_users, R.col_vals, U.astype(np.float64), n_f, lam, rate, Mo,
+                                      want_keys=True, threads=8)
+    act = np.diff(R.col_ptr) > 0
+    np.testing.assert_array_equal(keys[act], ko[act])
+    assert row_rel_err(M, Mo, act) <= FACTOR_TOL
