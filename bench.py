@@ -373,9 +373,26 @@ def device_index_check(data, dev):
     torch.cuda.synchronize()
     same = bool(torch.equal(cp, data.col_ptr) and torch.equal(ci, data.col_users) and torch.equal(cv, data.col_vals))
     del cp, ci, cv
+    # COO (shuffled) -> CSR, the RatingMatrix constructor's sort (ratings.py:74-82)
+    from paper_2509_18024_b200.ratings import coo_to_csr_device
+
+    users = torch.repeat_interleave(torch.arange(data.n_users, device=dev, dtype=torch.int32),
+                                    data.row_ptr[1:] - data.row_ptr[:-1])
+    perm = torch.randperm(data.nnz, device=dev, generator=torch.Generator(device=dev).manual_seed(5))
+    ku, ki, kv = users[perm], data.row_items[perm], data.row_vals[perm]
+    del users, perm
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record()
+    rp, ri, rv, dup = coo_to_csr_device(ku, ki, kv, data.n_users, data.n_items)
+    e3.record()
+    torch.cuda.synchronize()
+    same_csr = dup is None and bool(torch.equal(rp, data.row_ptr) and torch.equal(ri, data.row_items)
+                                    and torch.equal(rv, data.row_vals))
+    del ku, ki, kv, rp, ri, rv
     torch.cuda.empty_cache()
     return {"csr_to_csc_ms": e0.elapsed_time(e1), "equals_reference_order": same,
-            "ratings_per_s": data.nnz / (e0.elapsed_time(e1) / 1e3)}
+            "ratings_per_s": data.nnz / (e0.elapsed_time(e1) / 1e3),
+            "coo_to_csr_ms": e2.elapsed_time(e3), "coo_equals_reference_order": same_csr}
 
 
 def e2e(data, spec, M0, steps, rank=0, world=1, method="core"):
