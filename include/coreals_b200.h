@@ -44,7 +44,11 @@ extern "C" {
 #define CALS_ERR_WORKSPACE 3
 #define CALS_ERR_UNSUPPORTED 4
 
-/* per-row status (core.py:120-131 / als.py:184-197 jitter semantics) */
+/* per-row status (core.py:120-131 / als.py:184-197 jitter semantics): a system the
+ * fp32 solve cannot hold (breakdown, or a pivot-magnitude spread marking it
+ * ill-conditioned) is re-solved in float64 inside the same call -- plain first
+ * (CALS_ROW_OK), then with the reference's 1e-10 * tr(G) / n_f jitter
+ * (CALS_ROW_JITTERED), else CALS_ROW_SINGULAR (row left untouched). */
 #define CALS_ROW_OK 0
 #define CALS_ROW_JITTERED 1
 #define CALS_ROW_SINGULAR 2
