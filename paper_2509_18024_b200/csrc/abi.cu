@@ -483,6 +483,7 @@ int launch_fast(const SweepArgs& A, const cals_plan* P, const Work& w, const uin
         BigArgs B{};
         B.calib_samples = env_int("CALS_CALIB_M", 0);
         B.calib_z = (float)env_double("CALS_CALIB_Z", 0.0);
+        B.fold_chunks = env_int("CALS_FOLD_CHUNKS", 0);
         B.rows = P->big_rows + r0;
         B.tile_ptr = P->big_tile_ptr + r0;
         B.cand_ptr = P->big_cand_ptr + r0;
@@ -567,6 +568,7 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
         BigArgs B{};
         B.calib_samples = env_int("CALS_CALIB_M", 0);
         B.calib_z = (float)env_double("CALS_CALIB_Z", 0.0);
+        B.fold_chunks = env_int("CALS_FOLD_CHUNKS", 0);
         B.rows = P->big_rows + r0;
         B.tile_ptr = P->big_tile_ptr + r0;
         B.cand_ptr = P->big_cand_ptr + r0;

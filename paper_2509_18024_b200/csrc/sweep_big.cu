@@ -470,7 +470,8 @@ __global__ void __launch_bounds__(big_gram_threads(CPL), CPL <= 4 ? 3 : 1) big_g
             if (persist) {
                 owned_accumulate<CPL>(S, M, s_xs, sx, s_ys, nf, kn, full, s_bits, nw);
                 // fold every kFoldChunks chunks and at the item's end (entries owned by this lane only)
-                if (((k0 - kbeg) / CH) % kFoldChunks == kFoldChunks - 1 || k0 + CH >= kend)
+                const int fold = B.fold_chunks > 0 ? B.fold_chunks : kFoldChunks;
+                if (((k0 - kbeg) / CH) % fold == fold - 1 || k0 + CH >= kend)
                     owned_fold<CPL>(S, M, nf, G64);
             } else {
                 for (int j = 0; j < my_cols; ++j) {

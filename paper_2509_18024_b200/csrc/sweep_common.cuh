@@ -95,6 +95,7 @@ struct BigArgs {
     // the whole source instead of per-row thresholds
     const uint32_t* gmask;    // [n_src][gwords] bit c%32 of word c/32: source row kept for column c
     int gwords;
+    int fold_chunks;          // big_gram: chunks summed in fp32 before a float64 fold (0: kFoldChunks)
     int calib_samples;        // tuning overrides (0: defaults kCalibSamples / kCalibZ)
     float calib_z;
     int* fcnt;                // [n_big][nf] kept slice rows per column (multi-item rows)
