@@ -94,17 +94,6 @@ __host__ __device__ inline bool owned_single_round(int nf, int nwarps) {
     return (nf + nwarps - 1) / nwarps <= 32 / lpc;
 }
 
-template <int CPL>
-struct OwnedAcc {
-    float acc[4 * CPL];
-    float accb;
-    __device__ __forceinline__ void zero() {
-#pragma unroll
-        for (int i = 0; i < 4 * CPL; ++i) acc[i] = 0.f;
-        accb = 0.f;
-    }
-};
-
 struct OwnedMap {
     int LPC, QG, cs, qg, fl, c;
     bool cvalid;
@@ -121,6 +110,86 @@ struct OwnedMap {
         c = c_first + (cvalid ? cs : 0) * c_step;
     }
 };
+
+template <int CPL, typename AT = float>
+struct OwnedAcc {
+    AT acc[4 * CPL];
+    AT accb;
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int i = 0; i < 4 * CPL; ++i) acc[i] = (AT)0;
+        accb = (AT)0;
+    }
+};
+
+// Float64 accumulation of one staged chunk (exact fp32 products, float64 sums):
+// the same walk as owned_accumulate with DFMA instead of packed FFMA2.
+template <int CPL>
+__device__ __forceinline__ void owned_accumulate_f64(OwnedAcc<CPL, double>& S, const OwnedMap& M, uint32_t xs, int sx,
+                                                     uint32_t ys, int nf, int kn, bool full, uint32_t bits, int nw) {
+    const int nq = xs_chunks(nf);
+    const uint32_t rowb = 4u * (uint32_t)sx;
+    const uint32_t W = bits + 4u * (uint32_t)(M.c * nw);
+    const uint32_t xcol = xs + 4u * (uint32_t)M.c;
+    const bool chunk_ok_last = (M.fl + (CPL - 1) * M.LPC) < nq;
+    const int nwk = M.cvalid ? (kn + 31) >> 5 : 0;
+    for (int wd = M.qg; wd < nwk; wd += M.QG) {
+        uint32_t word;
+        if (full) {
+            const int rem = kn - 32 * wd;
+            word = rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
+        } else {
+            word = lds_u32(W + 4u * (uint32_t)wd);
+        }
+        while (word) {
+            const uint32_t k = 32u * (uint32_t)wd + (uint32_t)(__ffs(word) - 1);
+            word &= word - 1u;
+            const uint32_t rb = k * rowb;
+            const double xc = (double)lds_f32(xcol + rb);
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) {
+                if (i < CPL - 1 || chunk_ok_last) {
+                    const float4 v = lds_f128(xs + rb + 16u * (uint32_t)(M.fl + i * M.LPC));
+                    S.acc[4 * i + 0] = fma((double)v.x, xc, S.acc[4 * i + 0]);
+                    S.acc[4 * i + 1] = fma((double)v.y, xc, S.acc[4 * i + 1]);
+                    S.acc[4 * i + 2] = fma((double)v.z, xc, S.acc[4 * i + 2]);
+                    S.acc[4 * i + 3] = fma((double)v.w, xc, S.acc[4 * i + 3]);
+                }
+            }
+            if (M.fl == 0) S.accb = fma(xc, (double)lds_f32(ys + 4u * k), S.accb);
+        }
+    }
+}
+
+// Row M.c of float64 normal equations straight from float64 register sums.
+template <int CPL>
+__device__ __forceinline__ void owned_flush_f64(OwnedAcc<CPL, double>& S, const OwnedMap& M, int nf,
+                                                double* __restrict__ out, double lam_n) {
+    const int nq = xs_chunks(nf);
+    const int gs = nf + 1;
+    for (int o = M.LPC; o < M.LPC * M.QG; o <<= 1) {
+#pragma unroll
+        for (int i = 0; i < 4 * CPL; ++i) S.acc[i] += __shfl_xor_sync(CALS_FULL_MASK, S.acc[i], o);
+        S.accb += __shfl_xor_sync(CALS_FULL_MASK, S.accb, o);
+    }
+    if (M.cvalid && M.qg == 0) {
+        double* grow = out + (size_t)M.c * gs;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            const int ch = M.fl + i * M.LPC;
+            if (ch < nq) {
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int f = 4 * ch + t;
+                    if (f < nf) grow[f] = S.acc[4 * i + t] + ((f == M.c) ? lam_n : 0.0);
+                }
+            }
+        }
+        if (M.fl == 0) grow[nf] = S.accb;
+    }
+}
+
+
 
 // Accumulate one staged chunk of kn rows: column M.c over the set bits of its
 // kept-row bitmap words (bits[c][w], nw words per column), or over all rows

@@ -339,8 +339,8 @@ constexpr int big_gram_threads(int cpl) { return cpl >= 8 ? 512 : kThreads; }
 // staged chunks summed in fp32 before a fold into the float64 accumulators (~50 kept terms at rate 0.1)
 constexpr int kFoldChunks = 4;
 
-template <int CPL, bool FAST>
-__global__ void __launch_bounds__(big_gram_threads(CPL), CPL <= 4 ? 3 : 1) big_gram_kernel(SweepArgs A, BigArgs B) {
+template <int CPL, bool FAST, bool F64 = false>
+__global__ void __launch_bounds__(big_gram_threads(CPL), CPL <= 4 ? (F64 ? 2 : 3) : 1) big_gram_kernel(SweepArgs A, BigArgs B) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ uint64_t s_thr[CALS_MAX_NF_DEV];
     __shared__ unsigned long long s_amax[FAST ? CALS_MAX_NF_DEV : 1];
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(big_gram_threads(CPL), CPL <= 4 ? 3 : 1) big_g
     const FastDiv fq((uint32_t)xs_chunks(nf));
     const int my_cols = warp < nf ? (nf - 1 - warp) / nwarps + 1 : 0;
     const OwnedMap M(nf, warp, nwarps, my_cols, lane);
-    OwnedAcc<CPL> S;
+    OwnedAcc<CPL, typename std::conditional<F64, double, float>::type> S;
     for (int64_t t = blockIdx.x; t < B.n_tiles; t += gridDim.x) {
         const int64_t T_abs = B.tile_base + t;
         const int r = B.tile_row != nullptr ? (int)(__ldg(B.tile_row + T_abs) - B.row_base)
@@ -468,11 +468,15 @@ __global__ void __launch_bounds__(big_gram_threads(CPL), CPL <= 4 ? 3 : 1) big_g
                 }
             }
             if (persist) {
+                if constexpr (F64) {
+                    owned_accumulate_f64<CPL>(S, M, s_xs, sx, s_ys, nf, kn, full, s_bits, nw);
+                } else {
                 owned_accumulate<CPL>(S, M, s_xs, sx, s_ys, nf, kn, full, s_bits, nw);
                 // fold every kFoldChunks chunks and at the item's end (entries owned by this lane only)
                 const int fold = B.fold_chunks > 0 ? B.fold_chunks : kFoldChunks;
                 if (((k0 - kbeg) / CH) % fold == fold - 1 || k0 + CH >= kend)
                     owned_fold<CPL>(S, M, nf, G64);
+                }
             } else {
                 for (int j = 0; j < my_cols; ++j) {
                     const int c = warp + j * nwarps;
@@ -487,7 +491,8 @@ __global__ void __launch_bounds__(big_gram_threads(CPL), CPL <= 4 ? 3 : 1) big_g
         double* out = direct ? A.gbuf + (size_t)r * nf * gs : B.part + (size_t)t * nf * gs;
         const float lam_n = direct ? (float)(A.lam * (double)n) : 0.f;
         if (persist) {
-            owned_flush64<CPL>(M, nf, G64, out, direct ? A.lam * (double)n : 0.0);
+            if constexpr (F64) owned_flush_f64<CPL>(S, M, nf, out, direct ? A.lam * (double)n : 0.0);
+            else owned_flush64<CPL>(M, nf, G64, out, direct ? A.lam * (double)n : 0.0);
         } else {
             __syncthreads();
             for (int e = tid; e < nf * gs; e += nt) {
@@ -640,6 +645,7 @@ template __global__ void big_gram_kernel<1, true>(SweepArgs, BigArgs);
 template __global__ void big_gram_kernel<2, true>(SweepArgs, BigArgs);
 template __global__ void big_gram_kernel<4, true>(SweepArgs, BigArgs);
 template __global__ void big_gram_kernel<8, true>(SweepArgs, BigArgs);
+template __global__ void big_gram_kernel<4, false, true>(SweepArgs, BigArgs);
 
 // Big rows [r0, r0 + count): fixed-order float64 sum of the item partials,
 // + lam*n*I on the diagonal -> A.gbuf slot (r - r0); residual partial sums.
