@@ -350,6 +350,14 @@ class CoreEngine:
             self.cm = 1 - self.cm
         self._exchange(side)
 
+    def undo_half(self, side):
+        """Make the buffer before the last half-sweep of `side` current again (its rows
+        are untouched: half-sweeps write the other buffer)."""
+        if side == "user":
+            self.cu = 1 - self.cu
+        else:
+            self.cm = 1 - self.cm
+
     def _sum(self, src, dst_ptr):
         torch = _lib.require_cuda()
         st = torch.cuda.current_stream(self.device).cuda_stream

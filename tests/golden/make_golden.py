@@ -332,6 +332,174 @@ def fast_cases():
     fast_case("rate1", 7, 60, 50, 0.4, 4, 0.1, 1.0, 3)
 
 
+# ---------------------------------------------------------------------------
+# Round 2: the BASELINE config 1 at its stated size, the reference's loop
+# semantics (items_first / init_u / tol convergence / seeded init) and its
+# acceptance cases c1, c6, c10 plus test_imaging's short-row restoration.
+# ---------------------------------------------------------------------------
+
+def _thr_rows(ptr, idx, source, n_f, rate):
+    """Per (row, column) the slice row of the sketch threshold element: the
+    last kept element of ces_sketch (core.py:95-115) in key order, i.e. the
+    kept element with the smallest (|x|, -row) key.  -1 for empty rows.  The
+    threshold key is (abs_bits(x) << 32) | (0xFFFFFFFF - k) of that element."""
+    n_rows = ptr.size - 1
+    out = np.full((n_rows, n_f), -1, dtype=np.int32)
+    for i in range(n_rows):
+        lo, hi = ptr[i], ptr[i + 1]
+        if hi == lo:
+            continue
+        X = source[idx[lo:hi]]
+        sk = ces_sketch(X, rate)
+        for c in range(n_f):
+            r, v = sk.column(c)
+            bits = np.abs(v).astype(np.float32).view(np.uint32).astype(np.uint64) & np.uint64(0x7FFFFFFF)
+            k = (bits << np.uint64(32)) | (np.uint64(0xFFFFFFFF) - r.astype(np.uint64))
+            out[i, c] = int(r[int(np.argmin(k))])
+    return out
+
+
+def config1_case():
+    """BASELINE configs[0] exactly: U* 1000x5, V* 800x5 i.i.d. N(0,1), R = U* V*^T +
+    N(0, 0.5^2), Bernoulli(0.2) mask, n_f 5, lam 0.1, rate 0.3, 10 iterations,
+    M0 ~ N(0, 0.1^2) seed 0.  Values are fp32 (upcast for the reference).
+    Besides the plain 10-iteration fit, the reference is run half-sweep by
+    half-sweep along its own trajectory with every input snapshot rounded to
+    fp32 (SURVEY 8c.1 injection): a GPU test feeds the same snapshots and
+    compares all 20 half-sweeps (threshold rows exactly, factors to 1e-4)."""
+    rng = np.random.default_rng(2025)
+    n_u, n_m, r, n_f, lam, rate, iters = 1000, 800, 5, 5, 0.1, 0.3, 10
+    Ut = rng.normal(size=(n_u, r))
+    Vt = rng.normal(size=(n_m, r))
+    mask = rng.random((n_u, n_m)) < 0.2
+    users, items = np.nonzero(mask)
+    vals = f32(np.einsum("ef,ef->e", Ut[users], Vt[items]) + 0.5 * rng.normal(size=users.size))
+    R = RatingMatrix(users, items, vals, n_users=n_u, n_items=n_m)
+    M0 = f32(np.random.default_rng(0).normal(0.0, 0.1, size=(n_m, n_f)))
+    cfgN = SolverConfig(method="core", n_f=n_f, lam=lam, rate=rate, max_iters=iters, tol=1e-15)
+    cfg1 = SolverConfig(method="core", n_f=n_f, lam=lam, rate=rate, max_iters=1, tol=1e-15)
+    out = {}
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        FN, repN = fit_core(R, cfgN, init_m=M0)
+        src = M0
+        for t in range(iters):
+            Fu, _ = fit_core(R, cfg1, init_m=src)                       # user half from the M snapshot
+            U32 = f32(Fu.user_factors)
+            Fm, _ = fit_core(R, cfg1, init_u=U32, items_first=True)      # item half from the U snapshot
+            out[f"Ut{t}"] = Fu.user_factors
+            out[f"Mt{t}"] = Fm.item_factors
+            out[f"ku{t}"] = _thr_rows(R.row_ptr, R.row_items, src, n_f, rate).astype(np.int16)
+            out[f"km{t}"] = _thr_rows(R.col_ptr, R.col_users, U32, n_f, rate).astype(np.int16)
+            src = f32(Fm.item_factors)
+    np.savez_compressed(
+        os.path.join(OUT, "config1.npz"), mask=np.packbits(mask), vals=vals.astype(np.float32), n_users=n_u,
+        n_items=n_m, n_f=n_f, lam=lam, rate=rate, iters=iters, M0=M0.astype(np.float32),
+        objN=repN.objective_trace, rmseN=repN.rmse_trace, UN=FN.user_factors, MN=FN.item_factors, **out)
+
+
+def semantics_case():
+    """Loop semantics of _alternate (als.py:243-323) through fit_core: items_first with
+    init_u, a tol-converged fit (iters_run / converged / traces / the factors of the
+    converged iteration), the seeded default init, init_u on a user-first fit."""
+    users, items, vals = make_matrix(12, 200, 150, 0.3, 4, 0.5)
+    R = RatingMatrix(users, items, vals, n_users=200, n_items=150)
+    rng = np.random.default_rng(13)
+    n_f, lam, rate = 8, 0.1, 0.3
+    M0 = f32(rng.normal(0.0, 0.1, size=(150, n_f)))
+    U0 = f32(rng.normal(0.0, 0.1, size=(200, n_f)))
+    out = dict(users=users, items=items, vals=vals, n_users=200, n_items=150, n_f=n_f, lam=lam, rate=rate,
+               M0=M0, U0=U0)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        cfg3 = SolverConfig(method="core", n_f=n_f, lam=lam, rate=rate, max_iters=3, tol=1e-15)
+        F, rep = fit_core(R, cfg3, init_u=U0, init_m=M0, items_first=True)
+        out.update(if_obj=rep.objective_trace, if_rmse=rep.rmse_trace, if_U=F.user_factors, if_M=F.item_factors)
+        F, rep = fit_core(R, cfg3, init_u=U0, init_m=M0)
+        out.update(iu_obj=rep.objective_trace, iu_U=F.user_factors, iu_M=F.item_factors)
+        cfgt = SolverConfig(method="core", n_f=n_f, lam=lam, rate=rate, max_iters=60, tol=2e-3)
+        F, rep = fit_core(R, cfgt, init_m=M0)
+        out.update(tol_obj=rep.objective_trace, tol_rmse=rep.rmse_trace, tol_iters=rep.iters_run,
+                   tol_conv=rep.converged, tol_U=F.user_factors, tol_M=F.item_factors)
+        cfgs = SolverConfig(method="core", n_f=n_f, lam=lam, rate=rate, max_iters=3, tol=1e-15, seed=7)
+        F, rep = fit_core(R, cfgs)
+        out.update(seed_obj=rep.objective_trace, seed_rmse=rep.rmse_trace)
+    np.savez_compressed(os.path.join(OUT, "semantics.npz"), **out)
+
+
+def acceptance_cases():
+    """The reference acceptance criteria c1 (rate-1 collapse, 20 seeds,
+    pkg/tests/test_acceptance.py:54-73), c6 (convergence regime, :195-209; the
+    first 12 of its 40 seeds) and c10 (image restoration, :414-429), and
+    test_imaging.py:84-95 (n_f 50 on rows shorter than n_f).  Inputs come from
+    the reference's own generators, values rounded to fp32; the initial item
+    factors are the reference's seeded init rounded to fp32 and passed
+    explicitly to both sides."""
+    import itertools
+    sys.path.insert(0, "/root/reference/pkg/tests")
+    from conftest import random_matrix  # reference test helper (generator wrapper)
+    from test_acceptance import _rank50_image
+    from coreals import GrayImage, mask_image, restore  # noqa: F401
+    from coreals.als import init_factors
+
+    def f32R(R):
+        u, i, v = R.entries()
+        return RatingMatrix(u, i, f32(v), n_users=R.n_users, n_items=R.n_items)
+
+    out = {}
+    combos = list(itertools.product(["normal", "lognormal", "t4"], [0.4, 0.7]))
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for seed in range(20):
+            dist, alpha = combos[seed % len(combos)]
+            n_u, n_m = 80 + 11 * (seed % 5), 70 + 7 * (seed % 4)
+            R0, _ = random_matrix(seed, n_users=n_u, n_items=n_m, alpha=alpha, dist=dist, n_f=5)
+            R = f32R(R0)
+            kw = dict(n_f=5, lam=0.1, rate=1.0, max_iters=4, tol=1e-12, seed=seed)
+            M0 = f32(init_factors(R, SolverConfig(method="full", **kw)).item_factors)
+            _, rf = fit_full(R, SolverConfig(method="full", **kw), init_m=M0)
+            u, i, v = R.entries()
+            out.update({f"c1_u{seed}": u.astype(np.int32), f"c1_i{seed}": i.astype(np.int32),
+                        f"c1_v{seed}": v.astype(np.float32), f"c1_shape{seed}": np.array([n_u, n_m]),
+                        f"c1_M0{seed}": M0.astype(np.float32), f"c1_obj{seed}": rf.objective_trace})
+        for j, seed in enumerate(range(12)):
+            R = f32R(random_matrix(200 + seed, n_users=300, n_items=300, alpha=0.4, dist="normal", n_f=20)[0])
+            cfg = SolverConfig(method="core", n_f=20, lam=0.1, rate=0.25, max_iters=50, tol=0.01, seed=seed)
+            M0 = f32(init_factors(R, cfg).item_factors)
+            F, rep = fit_core(R, cfg, init_m=M0)
+            u, i, v = R.entries()
+            out.update({f"c6_key{j}": (u * 300 + i).astype(np.int32), f"c6_v{j}": v.astype(np.float32),
+                        f"c6_M0{j}": M0.astype(np.float32), f"c6_obj{j}": rep.objective_trace,
+                        f"c6_iters{j}": rep.iters_run, f"c6_conv{j}": rep.converged})
+        for seed in (1, 2, 3):
+            img = GrayImage(f32(_rank50_image(seed).pixels))
+            masked = mask_image(img, 0.6, seed=seed)
+            common = dict(n_f=50, lam=0.01, max_iters=5, tol=1e-15, seed=seed)
+            M0 = f32(init_factors(masked, SolverConfig(method="full", **common)).item_factors)
+            res = {}
+            for meth, rate in (("full", 1.0), ("core", 0.15)):
+                cfg = SolverConfig(method=meth, rate=rate, **common)
+                F, rep = (fit_full if meth == "full" else fit_core)(masked, cfg, init_m=M0)
+                pred = np.clip(F.user_factors @ F.item_factors.T, 0.0, 1.0)
+                mse = float(np.mean((pred - img.pixels) ** 2))
+                res[meth] = (min(10.0 * np.log10(1.0 / mse), 100.0), rep.objective_trace)
+            u, i, _ = masked.entries()
+            out.update({f"c10_img{seed}": img.pixels.astype(np.float32), f"c10_key{seed}": (u * 256 + i).astype(np.int32),
+                        f"c10_M0{seed}": M0.astype(np.float32),
+                        f"c10_psnr_full{seed}": res["full"][0], f"c10_psnr_core{seed}": res["core"][0],
+                        f"c10_obj_full{seed}": res["full"][1], f"c10_obj_core{seed}": res["core"][1]})
+        img = GrayImage(f32(np.random.default_rng(5).uniform(size=(96, 96))))
+        masked = mask_image(img, 0.6, seed=5)
+        cfg = SolverConfig(method="core", n_f=50, lam=0.01, rate=0.15, max_iters=5, tol=1e-12, seed=1)
+        M0 = f32(init_factors(masked, cfg).item_factors)
+        F, rep = fit_core(masked, cfg, init_m=M0)
+        u, i, _ = masked.entries()
+        out.update(img96=img.pixels.astype(np.float32), img96_key=(u * 96 + i).astype(np.int32),
+                   img96_M0=M0.astype(np.float32), img96_obj=rep.objective_trace, img96_iters=rep.iters_run,
+                   img96_U=F.user_factors, img96_M=F.item_factors)
+    np.savez_compressed(os.path.join(OUT, "acceptance.npz"), **out)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["full"]:
         full_case("full", 4, 120, 90, 0.3, 8, 0.1, 4, drop_user=7)
@@ -344,6 +512,11 @@ if __name__ == "__main__":
         sys.exit(0)
     if sys.argv[1:] == ["index"]:
         index_cases()
+        sys.exit(0)
+    if sys.argv[1:] == ["r02"]:
+        config1_case()
+        semantics_case()
+        acceptance_cases()
         sys.exit(0)
     if sys.argv[1:] == ["metrics"]:
         metric_cases()
