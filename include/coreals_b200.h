@@ -240,6 +240,10 @@ void cals_debug_stats(void* device_counters);
  * batch; 0 = defaults of 2^27 keys and 1 GiB of partial normal equations).
  * Must stay in effect from sizing a workspace until its last half-sweep. */
 void cals_debug_big_batch(int64_t cand_keys, int64_t tiles);
+/* Comparison switch for the tiled tier's Gram at 32 < n_f <= 64: 0 (default) the
+ * tensor-core integer Gram (tcgen05 kind::i8, csrc/sweep_tc.cu), 1 the float64
+ * SIMT accumulate it replaced.  Both give float64-quality normal equations. */
+void cals_debug_gram_path(int path);
 int cals_profile_collect(char* buf, size_t len);
 
 const char* cals_strerror(int status);

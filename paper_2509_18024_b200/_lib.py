@@ -62,6 +62,7 @@ SIGNATURES = {
     "cals_profile_enable": (None, [i32]),
     "cals_debug_stats": (None, [P]),
     "cals_debug_big_batch": (None, [ctypes.c_int64, ctypes.c_int64]),
+    "cals_debug_gram_path": (None, [ctypes.c_int]),
     "cals_profile_collect": (i32, [ctypes.c_char_p, sz]),
     "cals_strerror": (ctypes.c_char_p, [i32]),
     "cals_build_info": (ctypes.c_char_p, []),

@@ -34,6 +34,7 @@ double env_double(const char* name, double dflt) {
 }
 int64_t g_big_cand_budget = 0, g_big_tile_budget = 0;  // debug overrides, see cals_debug_big_batch
 unsigned long long* g_stats = nullptr;  // debug counters (device), see cals_debug_stats
+int g_gram_path = 0;  // tiled-tier Gram at 32 < n_f <= 64: 0 tensor cores (default), 1 float64 SIMT (comparison)
 
 // ---- optional per-kernel timing (CUDA events on the launch stream) --------
 struct ProfRec {
@@ -275,6 +276,7 @@ struct Work {
     int64_t gbuf_rows;
     double* gbuf2;    // staged tier's own normal-equation buffer when both tiers run concurrently
     uint64_t* thr_all;  // [n_rows][nf] selection thresholds (when the caller asks for none)
+    unsigned int* colmax;  // [CALS_MAX_NF] |source| column maxima (tensor-core Gram digit scales)
     int* rf_cnt;        // [4]: per stream, rows deferred to the float64 refinement from the stored
     int64_t* rf_list;   // equations [2][gbuf_rows] (row << 32 | slot), and from the slice:
     int32_t* rs_list;   // [2][n_rows] rows
@@ -304,6 +306,7 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
         w.gbuf2 = c.take<double>((size_t)w.gbuf_rows * nf * (nf + 1));
     }
     w.thr_all = c.take<uint64_t>((size_t)std::max<int64_t>(P->n_rows, 1) * nf);
+    w.colmax = c.take<unsigned int>(CALS_MAX_NF);
     w.rf_cnt = c.take<int>(4);
     w.rf_list = c.take<int64_t>((size_t)2 * w.gbuf_rows);
     w.rs_list = c.take<int32_t>((size_t)2 * std::max<int64_t>(P->n_rows, 1));
@@ -574,6 +577,13 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
                                                                                                        n_calib);
         }
     }
+    // tensor-core Gram (sweep_tc.cu) at 32 < n_f <= 64: digit scales from the source's column maxima
+    const bool tc_gram = nf > 32 && nf <= 64 && g_gram_path == 0;
+    if (tc_gram && P->n_big > 0) {
+        cudaMemsetAsync(w.colmax, 0, sizeof(unsigned int) * CALS_MAX_NF, st);
+        ProfScope ps("col_absmax_kernel", st);
+        col_absmax_kernel<<<dev().sms * 2, 256, 0, st>>>(A.src, A.n_src, A.ld_src, nf, w.colmax);
+    }
     for (size_t bi = 0; bi + 1 < bb.r.size(); ++bi) {
         const int64_t r0 = bb.r[bi], r1 = bb.r[bi + 1];
         BigArgs B{};
@@ -620,7 +630,12 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
             big_resolve_kernel<<<(int)std::max<int64_t>(1, blocks), kThreads, 0, st>>>(A, B);
         }
         const size_t gram_smem = big_gram_smem(nf, B.chunk);
-        {
+        if (tc_gram) {
+            ProfScope ps("big_gram_tc_kernel", st);
+            allow_smem(big_gram_tc_kernel);
+            const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(B.n_tiles, dev().sms));
+            big_gram_tc_kernel<<<grid, kTcThreads, TcSmem::total, st>>>(A, B, w.colmax);
+        } else {
             ProfScope ps("big_gram_kernel", st);
             const int nq = xs_chunks(nf);
             if (nq <= 4) launch_big_gram<1>(A, B, gram_smem, st);
@@ -1030,6 +1045,7 @@ void cals_debug_big_batch(int64_t cand_keys, int64_t tiles) {
     g_big_cand_budget = cand_keys;
     g_big_tile_budget = tiles;
 }
+void cals_debug_gram_path(int path) { g_gram_path = path; }
 
 void cals_profile_enable(int on) {
     Prof& P = prof();

@@ -226,6 +226,59 @@ __global__ void __launch_bounds__(128, 1)
     if (warp == 0) tc::tmem_free<512>(tbase);
 }
 
+
+// MN-major (M / N contiguous) interleaved operands, as the integer Gram writes them:
+// byte (mn, k) of a [R x 32] K-step tile at (mn/16)*512 + (k/8)*128 + (k%8)*16 + mn%16
+__host__ __device__ constexpr uint32_t mn_off(uint32_t mn, uint32_t k) {
+    return (mn >> 4) * 512u + (k >> 3) * 128u + (k & 7u) * 16u + (mn & 15u);
+}
+__global__ void __launch_bounds__(128, 1)
+    k_mma_mn(const int8_t* __restrict__ Ag, const int8_t* __restrict__ Bg, int N, int ksteps, int32_t* __restrict__ Dout) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ uint32_t tslot;
+    __shared__ __align__(8) unsigned long long mbar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int KT = 32 * ksteps;
+    unsigned char* As = smem;                       // ksteps tiles of 128 x 32
+    unsigned char* Bs = smem + ksteps * 128 * 32;   // ksteps tiles of N x 32
+    for (int e = tid; e < 128 * KT; e += blockDim.x) {
+        const int m = e / KT, k = e % KT;
+        As[(k / 32) * 4096 + mn_off(m, k % 32)] = (unsigned char)Ag[m * KT + k];
+    }
+    const int btile = (N + 15) / 16 * 512;
+    for (int e = tid; e < N * KT; e += blockDim.x) {
+        const int n = e / KT, k = e % KT;
+        Bs[(k / 32) * btile + mn_off(n, k % 32)] = (unsigned char)Bg[n * KT + k];
+    }
+    if (warp == 0) tc::tmem_alloc<256>(&tslot);
+    if (tid == 0) tc::mbar_init(tc::smem_addr(&mbar), 1);
+    tc::fence_smem_async();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tbase = tslot;
+    const uint32_t idesc = tc::idesc_i8(128, N) | (1u << 15) | (1u << 16);  // A and B MN-major
+    if (tid == 0) {
+        for (int ks = 0; ks < ksteps; ++ks)
+            tc::mma_i8_ss(tbase, tc::sdesc(tc::smem_addr(As) + 4096u * ks, 128, 512),
+                          tc::sdesc(tc::smem_addr(Bs) + (uint32_t)btile * ks, 128, 512), idesc, ks > 0);
+        tc::commit(tc::smem_addr(&mbar));
+        tc::mbar_wait(tc::smem_addr(&mbar), 0);
+    }
+    __syncthreads();
+    tc::fence_after();
+    for (int c0 = 0; c0 < N; c0 += 8) {
+        uint32_t v[8];
+        tc::ld_32x32b_x8(tbase + ((uint32_t)(32 * warp) << 16) + c0, v);
+        tc::ld_wait();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) Dout[tid * N + c0 + j] = (int32_t)v[j];
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<256>(tbase);
+}
+
 static float time_launch(void (*launch)(void*), void* arg, int reps = 5) {
     cudaEvent_t a, b;
     CK(cudaEventCreate(&a));
@@ -349,6 +402,37 @@ int main() {
                  (double)mx / (c.rounds * (KB / 32)), bad);
         js += buf;
         fprintf(stderr, "%s N=%d ms=%.3f cycles=%lld bad=%ld\n", cs.name, cs.N, ms, mx, bad);
+    }
+
+    {
+        // MN-major layout check at N = 144 (64 + y + pad per level, two levels), 2 K-steps
+        const int N = 144, KS = 2, KT = 64;
+        std::vector<int8_t> a(128 * KT), b(N * KT);
+        for (auto& x : a) x = (int8_t)((rand() % 256) - 128);
+        for (auto& x : b) x = (int8_t)((rand() % 256) - 128);
+        int8_t *da, *db;
+        int32_t* dd;
+        CK(cudaMalloc(&da, a.size()));
+        CK(cudaMalloc(&db, b.size()));
+        CK(cudaMalloc(&dd, 128 * N * 4));
+        CK(cudaMemcpy(da, a.data(), a.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(db, b.data(), b.size(), cudaMemcpyHostToDevice));
+        const int sm = KS * 4096 + KS * 9 * 512;
+        CK(cudaFuncSetAttribute(k_mma_mn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        k_mma_mn<<<1, 128, sm>>>(da, db, N, KS, dd);
+        CK(cudaDeviceSynchronize());
+        std::vector<int32_t> d(128 * N);
+        CK(cudaMemcpy(d.data(), dd, d.size() * 4, cudaMemcpyDeviceToHost));
+        long bad = 0;
+        for (int m = 0; m < 128; ++m)
+            for (int n = 0; n < N; ++n) {
+                int32_t ref = 0;
+                for (int k = 0; k < KT; ++k) ref += (int32_t)a[m * KT + k] * (int32_t)b[n * KT + k];
+                bad += d[m * N + n] != ref;
+            }
+        snprintf(buf, sizeof buf, ", \"i8_mn_major_m128_n144_check_mismatches\": %ld", bad);
+        js += buf;
+        fprintf(stderr, "mn-major N=144 bad=%ld\n", bad);
     }
     js += "}";
     printf("%s\n", js.c_str());
