@@ -240,10 +240,32 @@ void cals_debug_stats(void* device_counters);
  * batch; 0 = defaults of 2^27 keys and 1 GiB of partial normal equations).
  * Must stay in effect from sizing a workspace until its last half-sweep. */
 void cals_debug_big_batch(int64_t cand_keys, int64_t tiles);
-/* Comparison switch for the tiled tier's Gram at 32 < n_f <= 64: 0 (default) the
- * tensor-core integer Gram (tcgen05 kind::i8, csrc/sweep_tc.cu), 1 the float64
- * SIMT accumulate it replaced.  Both give float64-quality normal equations. */
-void cals_debug_gram_path(int path);
+/*
+ * Explicit tuning (process-wide; set it before building plans and sizing
+ * workspaces, keep it until their last half-sweep).  NULL restores the
+ * defaults.  Zero / negative fields select the built-in defaults.
+ *   item_rows      slice rows per work item of a tiled row (default 16384)
+ *   ill_ratio      pivot-magnitude spread that defers a system to the float64
+ *                  solve (default rank-dependent; 0 = every system)
+ *   rf_slice_max   deferred rows up to this length rebuild their Gram in float64
+ *                  from the slice (default 4096)
+ *   gram_path      tiled Gram at 32 < n_f <= 64: 0 the tensor-core integer Gram
+ *                  (tcgen05 kind::i8, csrc/sweep_tc.cu), 1 the float64 SIMT
+ *                  accumulate it replaced (comparison); both float64-quality
+ *   calib_samples, calib_z   long-row bracket calibration (defaults 4096, 5.5)
+ *   fold_chunks    fp32 Gram (n_f > 64): staged chunks summed before a float64 fold (4)
+ */
+typedef struct cals_tuning {
+    int32_t item_rows;
+    float ill_ratio;
+    int32_t rf_slice_max;
+    int32_t gram_path;
+    int32_t calib_samples;
+    float calib_z;
+    int32_t fold_chunks;
+} cals_tuning;
+void cals_set_tuning(const cals_tuning* tuning);
+void cals_get_tuning(cals_tuning* tuning);
 int cals_profile_collect(char* buf, size_t len);
 
 const char* cals_strerror(int status);

@@ -35,6 +35,28 @@ class cals_plan(ctypes.Structure):
     ]
 
 
+class cals_tuning(ctypes.Structure):
+    _fields_ = [("item_rows", ctypes.c_int32), ("ill_ratio", ctypes.c_float), ("rf_slice_max", ctypes.c_int32),
+                ("gram_path", ctypes.c_int32), ("calib_samples", ctypes.c_int32), ("calib_z", ctypes.c_float),
+                ("fold_chunks", ctypes.c_int32)]
+
+
+TUNING_DEFAULTS = dict(item_rows=0, ill_ratio=-1.0, rf_slice_max=-1, gram_path=0, calib_samples=0, calib_z=0.0,
+                       fold_chunks=0)
+
+
+def set_tuning(**fields):
+    """Explicit tuning of the native path (cals_set_tuning); unnamed fields take the
+    defaults.  Returns the previous settings as a dict (pass them back to restore)."""
+    L = load()
+    prev = cals_tuning()
+    L.cals_get_tuning(ctypes.byref(prev))
+    old = {f: getattr(prev, f) for f, _ in cals_tuning._fields_}
+    t = cals_tuning(**{**TUNING_DEFAULTS, **fields})
+    L.cals_set_tuning(ctypes.byref(t))
+    return old
+
+
 # name -> (restype, argtypes): every symbol include/coreals_b200.h declares
 SIGNATURES = {
     "cals_budget_host": (i32, [P, i64, f64, P]),
@@ -62,7 +84,8 @@ SIGNATURES = {
     "cals_profile_enable": (None, [i32]),
     "cals_debug_stats": (None, [P]),
     "cals_debug_big_batch": (None, [ctypes.c_int64, ctypes.c_int64]),
-    "cals_debug_gram_path": (None, [ctypes.c_int]),
+    "cals_set_tuning": (None, [P]),
+    "cals_get_tuning": (None, [P]),
     "cals_profile_collect": (i32, [ctypes.c_char_p, sz]),
     "cals_strerror": (ctypes.c_char_p, [i32]),
     "cals_build_info": (ctypes.c_char_p, []),

@@ -23,18 +23,10 @@ constexpr int kItemRowsMin = 16384;  // slice rows per work item (sweep on the 5
 
 thread_local char g_err[256] = "";
 
-// tuning overrides for experiments (unset: the built-in defaults)
-int env_int(const char* name, int dflt) {
-    const char* e = std::getenv(name);
-    return e != nullptr ? std::atoi(e) : dflt;
-}
-double env_double(const char* name, double dflt) {
-    const char* e = std::getenv(name);
-    return e != nullptr ? std::atof(e) : dflt;
-}
+// explicit tuning (cals_set_tuning); zero / negative fields select the built-in defaults
+cals_tuning g_tuning = {0, -1.0f, -1, 0, 0, 0.0f, 0};
 int64_t g_big_cand_budget = 0, g_big_tile_budget = 0;  // debug overrides, see cals_debug_big_batch
 unsigned long long* g_stats = nullptr;  // debug counters (device), see cals_debug_stats
-int g_gram_path = 0;  // tiled-tier Gram at 32 < n_f <= 64: 0 tensor cores (default), 1 float64 SIMT (comparison)
 
 // ---- optional per-kernel timing (CUDA events on the launch stream) --------
 struct ProfRec {
@@ -276,7 +268,8 @@ struct Work {
     int64_t gbuf_rows;
     double* gbuf2;    // staged tier's own normal-equation buffer when both tiers run concurrently
     uint64_t* thr_all;  // [n_rows][nf] selection thresholds (when the caller asks for none)
-    unsigned int* colmax;  // [CALS_MAX_NF] |source| column maxima (tensor-core Gram digit scales)
+    float* tc_scale;    // [65] tensor-core Gram digit scales 2^(32 - E) (64 columns + ratings)
+    double* tc_alpha;   // [65] 2^E
     int* rf_cnt;        // [4]: per stream, rows deferred to the float64 refinement from the stored
     int64_t* rf_list;   // equations [2][gbuf_rows] (row << 32 | slot), and from the slice:
     int32_t* rs_list;   // [2][n_rows] rows
@@ -306,7 +299,8 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
         w.gbuf2 = c.take<double>((size_t)w.gbuf_rows * nf * (nf + 1));
     }
     w.thr_all = c.take<uint64_t>((size_t)std::max<int64_t>(P->n_rows, 1) * nf);
-    w.colmax = c.take<unsigned int>(CALS_MAX_NF);
+    w.tc_scale = c.take<float>(65);
+    w.tc_alpha = c.take<double>(65);
     w.rf_cnt = c.take<int>(4);
     w.rf_list = c.take<int64_t>((size_t)2 * w.gbuf_rows);
     w.rs_list = c.take<int32_t>((size_t)2 * std::max<int64_t>(P->n_rows, 1));
@@ -469,10 +463,9 @@ template <int CPL, bool FAST = false>
 void launch_big_gram(const SweepArgs& A, const BigArgs& B, size_t smem, cudaStream_t st) {
     constexpr int threads = big_gram_threads(CPL);
     if constexpr (CPL == 4 && !FAST) {
-        // float64 accumulation of the tiled Gram (default): long rows of later iterations reach cond ~1e6,
-        // where fp32 partial sums miss the 1e-4 contract; CALS_GRAM_F64=0 selects fp32 sums folded into
-        // float64 every 4 chunks (22 % faster on the 500M config, outliers up to ~6e-3 on such rows)
-        if (env_int("CALS_GRAM_F64", 1)) {
+        // float64 accumulation of the SIMT tiled Gram: long rows of later iterations reach cond ~1e6,
+        // where fp32 partial sums miss the 1e-4 contract (the tensor-core Gram is the default here)
+        {
             allow_smem(big_gram_kernel<4, false, true>);
             big_gram_kernel<4, false, true>
                 <<<grid_for(big_gram_kernel<4, false, true>, smem, B.n_tiles, 8, threads), threads, smem, st>>>(A, B);
@@ -495,9 +488,9 @@ int launch_fast(const SweepArgs& A, const cals_plan* P, const Work& w, const uin
     for (size_t bi = 0; bi + 1 < bb.r.size(); ++bi) {
         const int64_t r0 = bb.r[bi], r1 = bb.r[bi + 1];
         BigArgs B{};
-        B.calib_samples = env_int("CALS_CALIB_M", 0);
-        B.calib_z = (float)env_double("CALS_CALIB_Z", 0.0);
-        B.fold_chunks = env_int("CALS_FOLD_CHUNKS", 0);
+        B.calib_samples = g_tuning.calib_samples;
+        B.calib_z = g_tuning.calib_z;
+        B.fold_chunks = g_tuning.fold_chunks;
         B.rows = P->big_rows + r0;
         B.tile_ptr = P->big_tile_ptr + r0;
         B.cand_ptr = P->big_cand_ptr + r0;
@@ -565,8 +558,8 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
             while (n_calib < P->n_big && tp[n_calib + 1] - tp[n_calib] >= 2) ++n_calib;
         if (n_calib > 0) {
             BigArgs C{};
-            C.calib_samples = env_int("CALS_CALIB_M", 0);
-            C.calib_z = (float)env_double("CALS_CALIB_Z", 0.0);
+            C.calib_samples = g_tuning.calib_samples;
+            C.calib_z = g_tuning.calib_z;
             C.rows = P->big_rows;
             C.n_big = n_calib;
             C.brk = w.brk;
@@ -577,19 +570,19 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
                                                                                                        n_calib);
         }
     }
-    // tensor-core Gram (sweep_tc.cu) at 32 < n_f <= 64: digit scales from the source's column maxima
-    const bool tc_gram = nf > 32 && nf <= 64 && g_gram_path == 0;
+    // tensor-core Gram (sweep_tc.cu) at 32 < n_f <= 64: digit scales from the quantile table
+    const bool tc_gram = nf > 32 && nf <= 64 && g_tuning.gram_path == 0 && A.qtab != nullptr &&
+                         P->item_rows <= kTcMaxChunks * kTcKC;
     if (tc_gram && P->n_big > 0) {
-        cudaMemsetAsync(w.colmax, 0, sizeof(unsigned int) * CALS_MAX_NF, st);
-        ProfScope ps("col_absmax_kernel", st);
-        col_absmax_kernel<<<dev().sms * 2, 256, 0, st>>>(A.src, A.n_src, A.ld_src, nf, w.colmax);
+        ProfScope ps("tc_scales_kernel", st);
+        tc_scales_kernel<<<1, 256, 0, st>>>(A.qtab, nf, A.val, A.nnz, w.tc_scale, w.tc_alpha);
     }
     for (size_t bi = 0; bi + 1 < bb.r.size(); ++bi) {
         const int64_t r0 = bb.r[bi], r1 = bb.r[bi + 1];
         BigArgs B{};
-        B.calib_samples = env_int("CALS_CALIB_M", 0);
-        B.calib_z = (float)env_double("CALS_CALIB_Z", 0.0);
-        B.fold_chunks = env_int("CALS_FOLD_CHUNKS", 0);
+        B.calib_samples = g_tuning.calib_samples;
+        B.calib_z = g_tuning.calib_z;
+        B.fold_chunks = g_tuning.fold_chunks;
         B.rows = P->big_rows + r0;
         B.tile_ptr = P->big_tile_ptr + r0;
         B.cand_ptr = P->big_cand_ptr + r0;
@@ -634,7 +627,7 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
             ProfScope ps("big_gram_tc_kernel", st);
             allow_smem(big_gram_tc_kernel);
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(B.n_tiles, dev().sms));
-            big_gram_tc_kernel<<<grid, kTcThreads, TcSmem::total, st>>>(A, B, w.colmax);
+            big_gram_tc_kernel<<<grid, kTcThreads, TcSmem::total, st>>>(A, B, w.tc_scale, w.tc_alpha);
         } else {
             ProfScope ps("big_gram_kernel", st);
             const int nq = xs_chunks(nf);
@@ -715,7 +708,7 @@ int cals_plan_build(const int64_t* counts, int64_t n_rows, int n_f, double rate,
     meta->small_seg[3] = pos;
     // big rows: work items and candidate buffers
     const int chunk = big_chunk(n_f);
-    meta->item_rows = std::max(env_int("CALS_ITEM_ROWS", kItemRowsMin), chunk);
+    meta->item_rows = std::max(g_tuning.item_rows > 0 ? g_tuning.item_rows : kItemRowsMin, chunk);
     const float dtab = delta_tab_for(kQSbig);
     big_tile_ptr[0] = 0;
     big_cand_ptr[0] = 0;
@@ -759,6 +752,7 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.ptr = side->ptr;
     A.idx = side->idx;
     A.val = side->val;
+    A.nnz = side->nnz;
     A.budget = P->budget;
     A.src = source;
     A.n_src = n_src;
@@ -772,12 +766,12 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.rss_rows = rss_rows;
     A.pen_rows = pen_rows;
     A.thr_keys = thr_keys != nullptr ? thr_keys : w.thr_all;  // the float64 refinement reads them
-    A.ill_ratio = (float)env_double("CALS_ILL_RATIO", ill_ratio_for(n_f));
+    A.ill_ratio = g_tuning.ill_ratio >= 0.f ? g_tuning.ill_ratio : ill_ratio_for(n_f);
     A.rf_cnt = w.rf_cnt;
     A.rf_list = w.rf_list;
     A.rs_cnt = w.rf_cnt + 2;
     A.rs_list = w.rs_list;
-    A.rf_slice_max = env_int("CALS_RF_SLICE_MAX", kRfSliceMax);
+    A.rf_slice_max = g_tuning.rf_slice_max >= 0 ? g_tuning.rf_slice_max : kRfSliceMax;
     cudaMemsetAsync(w.rf_cnt, 0, 4 * sizeof(int), st);
     A.gbuf = w.gbuf;
     A.stats = g_stats;
@@ -858,7 +852,7 @@ int cals_plan_build_fast(const int64_t* counts, int64_t n_rows, int n_f, int com
                      [counts](int32_t a, int32_t b) { return counts[a] != counts[b] ? counts[a] > counts[b] : a < b; });
     std::copy(act.begin(), act.end(), rows);
     meta->n_big = (int64_t)act.size();
-    meta->item_rows = std::max(env_int("CALS_ITEM_ROWS", kItemRowsMin), big_chunk(n_f));
+    meta->item_rows = std::max(g_tuning.item_rows > 0 ? g_tuning.item_rows : kItemRowsMin, big_chunk(n_f));
     tile_ptr[0] = 0;
     cand_ptr[0] = 0;
     for (size_t r = 0; r < act.size(); ++r) {
@@ -918,6 +912,7 @@ int cals_fast_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.ptr = side->ptr;
     A.idx = side->idx;
     A.val = side->val;
+    A.nnz = side->nnz;
     A.budget = P->budget;
     A.src = source;
     A.n_src = n_src;
@@ -931,7 +926,7 @@ int cals_fast_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.rss_rows = rss_rows;
     A.pen_rows = pen_rows;
     A.thr_keys = w.thr_all;
-    A.ill_ratio = (float)env_double("CALS_ILL_RATIO", ill_ratio_for(n_f));
+    A.ill_ratio = g_tuning.ill_ratio >= 0.f ? g_tuning.ill_ratio : ill_ratio_for(n_f);
     A.rf_cnt = w.rf_cnt;
     A.rf_list = w.rf_list;
     A.rs_cnt = w.rf_cnt + 2;
@@ -1045,7 +1040,13 @@ void cals_debug_big_batch(int64_t cand_keys, int64_t tiles) {
     g_big_cand_budget = cand_keys;
     g_big_tile_budget = tiles;
 }
-void cals_debug_gram_path(int path) { g_gram_path = path; }
+void cals_set_tuning(const cals_tuning* t) {
+    static const cals_tuning defaults = {0, -1.0f, -1, 0, 0, 0.0f, 0};
+    g_tuning = t != nullptr ? *t : defaults;
+}
+void cals_get_tuning(cals_tuning* t) {
+    if (t != nullptr) *t = g_tuning;
+}
 
 void cals_profile_enable(int on) {
     Prof& P = prof();

@@ -16,6 +16,7 @@ struct SweepArgs {
     const int64_t* ptr;
     const int32_t* idx;
     const float* val;
+    int64_t nnz;
     const int32_t* budget;
     const float* src;
     int64_t n_src;

@@ -37,3 +37,20 @@ def csr_csc(users, items, vals, n_users, n_items):
     np.cumsum(np.bincount(items, minlength=n_items), out=col_ptr[1:])
     return ((row_ptr, items[o].astype(np.int32), vals[o]),
             (col_ptr, users[o2].astype(np.int32), vals[o2]))
+
+
+@pytest.fixture
+def tuning():
+    """Explicit native tuning for one test (cals_set_tuning), restored afterwards."""
+    from paper_2509_18024_b200 import _lib
+
+    prev = []
+
+    def set_(**fields):
+        old = _lib.set_tuning(**fields)
+        if not prev:
+            prev.append(old)
+
+    yield set_
+    if prev:
+        _lib.set_tuning(**prev[0])

@@ -211,8 +211,10 @@ def test_large_later_iterations_both_sides():
                                                want_keys=True, threads=THREADS)
             np.testing.assert_array_equal(gk, ko, err_msg=f"large iteration {t} {side}: keys")
             err = np.abs(got - want).max(axis=1) / np.maximum(np.abs(want).max(axis=1), 1e-2)
+            wr = int(np.argmax(err))
             report.append(f"it {t} {side}: rows {rows.size} (>100k: {(cnt[rows] > 100_000).sum()}) "
-                          f"max {err.max():.2e} median {np.median(err):.2e}")
+                          f"max {err.max():.2e} median {np.median(err):.2e}; worst row {rows[wr]} n {cnt[rows[wr]]} "
+                          f"|w| {np.abs(want[wr]).max():.3g} status {int(eng.user.status[rows[wr]] if side == 'user' else eng.item.status[rows[wr]])}")
             assert err.max() <= FACTOR_TOL, report[-1]
     print("\n".join(report))
     del eng, data

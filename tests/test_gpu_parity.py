@@ -129,11 +129,11 @@ def test_golden_fast_core(name):
 
 
 @pytest.mark.parametrize("n_f", [5, 16, 32, 64, 128])
-def test_fast_core_oracle_parity_tiers(n_f, monkeypatch):
+def test_fast_core_oracle_parity_tiers(n_f, tuning):
     """fast_core on long rows (multi-item work items, reduced partials and the
     fallback fix-up) and sparse rows (in-kernel fallback) vs the oracle."""
     from paper_2509_18024_b200.engine import CoreEngine
-    monkeypatch.setenv("CALS_ITEM_ROWS", "4096")  # work items small enough that the 7200-rating items span several
+    tuning(item_rows=4096)  # work items small enough that the 7200-rating items span several
     u, i, v = random_matrix(n_f, 9000, 300, 0.01, heavy_items=3, heavy_density=0.8)
     R = cb.RatingMatrix(u, i, v, n_users=9000, n_items=300)
     M0 = np.random.default_rng(8).normal(0, 0.1, (300, n_f)).astype(np.float32)
@@ -219,13 +219,13 @@ def check_against_oracle(R, n_f, lam, rate, source_item, seed=0, ties=False):
 
 @pytest.mark.parametrize("item_rows", [None, 1024])
 @pytest.mark.parametrize("n_f", [1, 3, 5, 8, 16, 24, 32, 48, 64, 80, 100, 128])
-def test_oracle_parity_mixed_tiers(n_f, item_rows, monkeypatch):
+def test_oracle_parity_mixed_tiers(n_f, item_rows, tuning):
     """Short rows (identity lists), table-bracket rows and big tiled rows."""
     u, i, v = random_matrix(n_f, 3000, 400, 0.04, heavy_items=6, heavy_density=0.9)
     R = cb.RatingMatrix(u, i, v, n_users=3000, n_items=400)
     M0 = np.random.default_rng(1).normal(0, 0.1, (400, n_f)).astype(np.float32)
     if item_rows is not None:  # small work items: every heavy item is a calibrated multi-item row
-        monkeypatch.setenv("CALS_ITEM_ROWS", str(item_rows))
+        tuning(item_rows=item_rows)
     eng = check_against_oracle(R, n_f, 0.05, 0.2, M0)
     assert eng.user.plan.n_small > 0
     if item_rows is not None and eng.item.plan.n_big:
@@ -398,11 +398,10 @@ def test_evaluation_metrics_match_reference():
 
 
 @pytest.mark.parametrize("n_f", [8, 48, 64, 100, 128])
-def test_float64_path_on_every_system(n_f, monkeypatch):
-    """Every system forced through the float64 solve (CALS_ILL_RATIO=0), on all
+def test_float64_path_on_every_system(n_f, tuning):
+    """Every system forced through the float64 solve (tuning ill_ratio=0), on all
     tiers including multi-item rows: the float64 path alone matches the oracle."""
-    monkeypatch.setenv("CALS_ILL_RATIO", "0")
-    monkeypatch.setenv("CALS_ITEM_ROWS", "1024")
+    tuning(ill_ratio=0.0, item_rows=1024)
     u, i, v = random_matrix(n_f, 3000, 400, 0.04, heavy_items=6, heavy_density=0.9)
     R = cb.RatingMatrix(u, i, v, n_users=3000, n_items=400)
     M0 = np.random.default_rng(1).normal(0, 0.1, (400, n_f)).astype(np.float32)
@@ -412,14 +411,14 @@ def test_float64_path_on_every_system(n_f, monkeypatch):
 
 @pytest.mark.parametrize("item_rows", [None, 1024])
 @pytest.mark.parametrize("n_f", [8, 32, 64, 128])
-def test_oracle_parity_ill_conditioned(n_f, item_rows, monkeypatch):
+def test_oracle_parity_ill_conditioned(n_f, item_rows, tuning):
     """Large, nearly collinear source columns (like the factors of later
     iterations) make many sketched systems ill-conditioned: the fp32 solve
     defers them to the float64 solve (sweep_refine.cu), and rows still match the
     float64 reference within 1e-4 on every tier."""
     from paper_2509_18024_b200 import _lib
     if item_rows is not None:
-        monkeypatch.setenv("CALS_ITEM_ROWS", str(item_rows))
+        tuning(item_rows=item_rows)
     u, i, v = random_matrix(n_f + 50, 3000, 400, 0.04, heavy_items=6, heavy_density=0.9)
     R = cb.RatingMatrix(u, i, v, n_users=3000, n_items=400)
     rng = np.random.default_rng(3)

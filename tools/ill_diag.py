@@ -1,5 +1,5 @@
 """Per-row error vs the oracle of ONE item half-sweep of the large config at a later
-iteration, under several float64-deferral ratios (CALS_ILL_RATIO), from the same state."""
+iteration, under several float64-deferral ratios (tuning ill_ratio), from the same state."""
 import os
 import sys
 
@@ -33,7 +33,8 @@ _, _, ko = oracle.core_half_sweep(sp, si, sv, U.astype(np.float64), n_f, lam, ra
 scale = np.maximum(np.abs(want).max(axis=1), 1e-2)
 for ratio in sys.argv[3:] or ["default"]:
     if ratio != "default":
-        os.environ["CALS_ILL_RATIO"] = ratio
+        from paper_2509_18024_b200 import _lib
+        _lib.set_tuning(ill_ratio=float(ratio))
     outs = []
     for rep in range(2):
         tgt, keys = half(eng, "item", U)
