@@ -254,6 +254,11 @@ void cals_debug_big_batch(int64_t cand_keys, int64_t tiles);
  *                  accumulate it replaced (comparison); both float64-quality
  *   calib_samples, calib_z   long-row bracket calibration (defaults 4096, 5.5)
  *   fold_chunks    fp32 Gram (n_f > 64): staged chunks summed before a float64 fold (4)
+ *   serial_tiers   1: the staged tier runs on the caller's stream before the tiled
+ *                  tier instead of beside it on a second stream (profiling)
+ *   tc_debug       profiling only (results are then wrong): bit 0 skips the
+ *                  tensor-core Gram's MMAs, bit 1 its digit pass, bit 2 its digit
+ *                  stores; 8 traces CTA 0 into the cals_debug_stats buffer
  */
 typedef struct cals_tuning {
     int32_t item_rows;
@@ -263,6 +268,8 @@ typedef struct cals_tuning {
     int32_t calib_samples;
     float calib_z;
     int32_t fold_chunks;
+    int32_t serial_tiers;
+    int32_t tc_debug;
 } cals_tuning;
 void cals_set_tuning(const cals_tuning* tuning);
 void cals_get_tuning(cals_tuning* tuning);

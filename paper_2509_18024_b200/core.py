@@ -160,7 +160,7 @@ def _raise_for(status, side, engine_side, it):
     st, row = status
     if st != _lib.CALS_ROW_SINGULAR:
         return
-    full = int(engine_side.budget_host[row]) == int(engine_side.counts[row])
+    full = engine_side.complete_row(row)
     if full:  # exact SPD row (core.py:206-207 -> als.py:197, no context passed)
         raise NumericalError("singular Gram matrix after jitter retry ")
     raise NumericalError(f"singular sketched system after jitter retry ({side} {row}, iteration {it})")

@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <numeric>
+#include <utility>
 #include <vector>
 
 #include "coreals_b200.h"
@@ -24,7 +25,7 @@ constexpr int kItemRowsMin = 16384;  // slice rows per work item (sweep on the 5
 thread_local char g_err[256] = "";
 
 // explicit tuning (cals_set_tuning); zero / negative fields select the built-in defaults
-cals_tuning g_tuning = {0, -1.0f, -1, 0, 0, 0.0f, 0};
+cals_tuning g_tuning = {0, -1.0f, -1, 0, 0, 0.0f, 0, 0, 0};
 int64_t g_big_cand_budget = 0, g_big_tile_budget = 0;  // debug overrides, see cals_debug_big_batch
 unsigned long long* g_stats = nullptr;  // debug counters (device), see cals_debug_stats
 
@@ -148,40 +149,45 @@ struct Device {
     cudaStream_t side = nullptr;  // second stream: the staged tier beside the tiled tier
     cudaEvent_t fork = nullptr, join = nullptr;
 };
+constexpr int kMaxDevices = 64;
+// per-device state (SM count, the side stream and its fork/join events), keyed by the
+// caller's current device; one host thread per device drives the half-sweeps
 Device& dev() {
-    static Device d;
+    static Device d[kMaxDevices];
     static std::mutex mu;
+    int id = 0;
+    cudaGetDevice(&id);
+    if (id < 0 || id >= kMaxDevices) id = 0;
     std::lock_guard<std::mutex> lk(mu);
-    if (!d.init) {
-        int id = 0;
-        cudaGetDevice(&id);
-        cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, id);
+    Device& D = d[id];
+    if (!D.init) {
+        cudaDeviceGetAttribute(&D.sms, cudaDevAttrMultiProcessorCount, id);
         int optin = 0;
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, id);
-        if (optin > 0) d.smem_optin = (size_t)optin;
-        cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking);
-        cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming);
-        d.init = true;
+        if (optin > 0) D.smem_optin = (size_t)optin;
+        cudaStreamCreateWithFlags(&D.side, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&D.fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&D.join, cudaEventDisableTiming);
+        D.init = true;
     }
-    return d;
+    return D;
 }
 
 template <typename K>
 void allow_smem(K kernel) {
     static std::mutex mu;
-    static std::vector<const void*> done;
+    static std::vector<std::pair<int, const void*>> done;  // the attribute is per device
     std::lock_guard<std::mutex> lk(mu);
     const void* k = reinterpret_cast<const void*>(kernel);
-    if (std::find(done.begin(), done.end(), k) == done.end()) {
-        int id = 0, optin = 0;
-        cudaGetDevice(&id);
+    int id = 0, optin = 0;
+    cudaGetDevice(&id);
+    if (std::find(done.begin(), done.end(), std::make_pair(id, k)) == done.end()) {
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, id);
         cudaFuncAttributes fa{};
         cudaFuncGetAttributes(&fa, k);
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
         cudaGetLastError();  // an attribute failure must not masquerade as a launch error
-        done.push_back(k);
+        done.push_back({id, k});
     }
 }
 
@@ -203,7 +209,8 @@ int cuda_status(const char* where) {
     return CALS_OK;
 }
 
-// Normal-equation batch: rows solved per phase-A/phase-B launch pair (<= ~1 GiB).
+// Normal-equation batch: rows solved per phase-A/phase-B launch pair.  The budget
+// counts 4 bytes per entry but the buffers hold float64: each is <= ~2 GiB.
 int64_t gbuf_rows_for(int nf, int64_t rows) {
     const int64_t per = (int64_t)nf * (nf + 1) * 4;
     const int64_t cap = std::max<int64_t>(4096, ((int64_t)1 << 30) / per);
@@ -270,6 +277,7 @@ struct Work {
     uint64_t* thr_all;  // [n_rows][nf] selection thresholds (when the caller asks for none)
     float* tc_scale;    // [65] tensor-core Gram digit scales 2^(32 - E) (64 columns + ratings)
     double* tc_alpha;   // [65] 2^E
+    int* item_ctr;      // big_gram_tc work-item counter
     int* rf_cnt;        // [4]: per stream, rows deferred to the float64 refinement from the stored
     int64_t* rf_list;   // equations [2][gbuf_rows] (row << 32 | slot), and from the slice:
     int32_t* rs_list;   // [2][n_rows] rows
@@ -301,6 +309,7 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
     w.thr_all = c.take<uint64_t>((size_t)std::max<int64_t>(P->n_rows, 1) * nf);
     w.tc_scale = c.take<float>(65);
     w.tc_alpha = c.take<double>(65);
+    w.item_ctr = c.take<int>(1);
     w.rf_cnt = c.take<int>(4);
     w.rf_list = c.take<int64_t>((size_t)2 * w.gbuf_rows);
     w.rs_list = c.take<int32_t>((size_t)2 * std::max<int64_t>(P->n_rows, 1));
@@ -627,7 +636,10 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
             ProfScope ps("big_gram_tc_kernel", st);
             allow_smem(big_gram_tc_kernel);
             const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(B.n_tiles, dev().sms));
-            big_gram_tc_kernel<<<grid, kTcThreads, TcSmem::total, st>>>(A, B, w.tc_scale, w.tc_alpha);
+            B.item_ctr = w.item_ctr;
+            cudaMemsetAsync(w.item_ctr, 0, sizeof(int), st);
+            big_gram_tc_kernel<<<grid, kTcThreads, TcSmem::total, st>>>(A, B, w.tc_scale, w.tc_alpha,
+                                                                            g_tuning.tc_debug);
         } else {
             ProfScope ps("big_gram_kernel", st);
             const int nq = xs_chunks(nf);
@@ -796,7 +808,7 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     // the staged and tiled tiers touch disjoint rows: with both present the staged
     // tier runs on a second stream (own normal-equation buffer and float64 refinement lists)
     // beside the tiled tier, filling the SMs its low occupancy leaves idle
-    const bool both = P->n_small > 0 && P->n_big > 0;
+    const bool both = P->n_small > 0 && P->n_big > 0 && g_tuning.serial_tiers == 0;
     SweepArgs As = A;
     cudaStream_t ss = st;
     if (both) {
@@ -1041,7 +1053,7 @@ void cals_debug_big_batch(int64_t cand_keys, int64_t tiles) {
     g_big_tile_budget = tiles;
 }
 void cals_set_tuning(const cals_tuning* t) {
-    static const cals_tuning defaults = {0, -1.0f, -1, 0, 0, 0.0f, 0};
+    static const cals_tuning defaults = {0, -1.0f, -1, 0, 0, 0.0f, 0, 0, 0};
     g_tuning = t != nullptr ? *t : defaults;
 }
 void cals_get_tuning(cals_tuning* t) {

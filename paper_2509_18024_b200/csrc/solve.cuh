@@ -198,6 +198,7 @@ struct WideLU {
     bool ua, ub, fail;
     int oa, ob;
     float dmin, dmax;
+    int nf;
 };
 
 // Elimination steps K in [B0, B0 + 16) (a runtime loop: the fully unrolled
@@ -236,8 +237,10 @@ __device__ __forceinline__ void wide_block(WideLU<NF>& S, bool spd, int lane) {
         const int pl = p & 31;
         const float d = __shfl_sync(CALS_FULL_MASK, sel_f32(hi, cb, ca), pl);
         S.fail |= spd ? !(d > 0.f) : !(d == d);
-        S.dmin = fminf(S.dmin, fabsf(d));
-        S.dmax = fmaxf(S.dmax, fabsf(d));
+        if (K < S.nf) {  // identity padding rows (K >= nf) pivot at 1.0: not a real pivot
+            S.dmin = fminf(S.dmin, fabsf(d));
+            S.dmax = fmaxf(S.dmax, fabsf(d));
+        }
         if (lane == pl) {
             if (hi) { S.ub = true; S.ob = K; } else { S.ua = true; S.oa = K; }
         }
@@ -305,6 +308,7 @@ __device__ __forceinline__ bool wide_lu_solve(const float* __restrict__ W, int n
     S.fail = false;
     S.dmin = INFINITY;
     S.dmax = 0.f;
+    S.nf = nf;
     wide_eliminate<NF>(S, spd, lane, std::make_integer_sequence<int, (NF + 15) / 16>{});
     x0 = 0.f;
     x1 = 0.f;

@@ -101,6 +101,7 @@ struct BigArgs {
     float calib_z;
     int* fcnt;                // [n_big][nf] kept slice rows per column (multi-item rows)
     unsigned long long* famax;  // [n_big][nf] max key (abs_bits << 32 | ~k) per column (fallback row)
+    int* item_ctr;            // big_gram_tc: next unclaimed work item (zeroed before the launch)
 };
 
 constexpr int kHB = 32;  // sub-buckets of a big row's bracket (linear in abs-bit space)
@@ -207,7 +208,7 @@ __device__ __forceinline__ void cp_async4(uint32_t saddr, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 // Asynchronous variant for double-buffered chunk loops: issue the copies of
@@ -248,6 +249,28 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
                  "l"(src), "r"(bytes), "r"(mbar)
                  : "memory");
+}
+// waiter for role warps that wait long (a whole work item): polls with a short sleep in
+// between so its spinning does not take issue slots from the warps doing the work
+__device__ __forceinline__ bool mbar_test(uint32_t mbar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(mbar), "r"(phase)
+        : "memory");
+    return ok != 0u;
+}
+// try_wait with a suspend-time hint: the thread may be suspended until the phase completes
+__device__ __forceinline__ void mbar_wait_hint(uint32_t mbar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            mbar),
+        "r"(phase), "r"(1000000u)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint32_t mbar, uint32_t phase) {
+    while (!mbar_test(mbar, phase)) __nanosleep(128);
 }
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
     asm volatile(

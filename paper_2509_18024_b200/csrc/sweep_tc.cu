@@ -26,53 +26,80 @@
 //
 // Numerically this is a float64-quality Gram (measured: 2^-31-relative inputs,
 // exact sums; a numpy emulation at cond ~1e6 gives ~5e-7 factor error where
-// fp32 products give ~2e-4, tools/ozaki_emul.py).
+// fp32 products give ~2e-4).
 //
-// Pipeline per CTA (one per SM, 16 warps): a 4-deep ring of fp32 slice chunks
-// (64 rows, one cp.async.bulk per gathered row, mbarrier completion) feeds a
-// digit pass (all warps: kept bits from the selection thresholds, digits,
-// masked copies -> two double-buffered K-step tile sets in shared memory), and
-// thread 0 issues the chunk's MMAs and commits them to that tile set's
-// mbarrier, so the tensor cores run one chunk behind the digit pass.
+// Pipeline per CTA (one per SM, 14 warps, warp-specialised, mbarrier handoffs):
+//   * warp 13, scheduler: resolves 32 work items at a time lane-parallel (row,
+//     rating range, slice rows) into an 8-deep item ring, and copies each
+//     item's selection thresholds and previous row into it with cp.async (the
+//     ring slot's barrier completes when they land: no warp waits on memory);
+//   * warps 0..7, digit pass: every lane gathers ITS OWN 64 bytes of a slice
+//     row (four 16-byte cp.async, three chunks ahead, swizzled lane-private
+//     staging) and its rating, then turns them into kept bits, fixed point and
+//     the 4 signed digits, written into one of two K-step tile sets;
+//   * warp 12, lane 0: issues the chunk's 3 MMAs per 32 rows once its tile
+//     set is complete and commits them to that set's "empty" barrier;
+//   * warps 8..11, epilogue (one TMEM lane quarter each): drain the
+//     accumulators into float64 (then the next item's MMAs may start), add
+//     the exception rows, write the normal equations, release the ring slot.
 #include "sweep_common.cuh"
 #include "tc.cuh"
 
 namespace cals {
 
-constexpr int kTcCW = 8;                      // compute warps: 8 whole slice rows each per chunk
-constexpr int kTcThreads = (kTcCW + 1) * 32;  // + the control warp (bulk-copy producer, MMA issue)
-constexpr int kTcKC = 64;                     // slice rows per chunk (two K-steps of 32)
-constexpr int kTcStages = 4;                  // fp32 staging ring depth
-constexpr int kTcSX = 80;                     // staged row stride in floats (320 B: conflict-free float4 reads)
-constexpr int kTcN = 144;                     // N side: two levels x (64 factor columns + y + 7 zero pad)
-constexpr int kTcLvl = 72;                    // N columns per level
-constexpr int kTcATile = 4096;                // M = 128 (two levels x 64 columns) x 32 K bytes
-constexpr int kTcBTile = 4608;                // N = 144 x 32 K bytes
+constexpr int kTcKC = 64;                       // slice rows per chunk (two K-steps of 32)
+constexpr int kTcCW = 16;                       // digit-pass warps
+constexpr int kTcRW = kTcKC / kTcCW;            // slice rows per digit-pass warp per chunk (4)
+constexpr int kTcLPR = 32 / kTcRW;              // lanes per slice row (8)
+constexpr int kTcNG = 64 / (4 * kTcLPR);        // groups of 4 columns per lane (2)
+constexpr int kTcEW = 4;                        // epilogue warps (TMEM lane quarters)
+constexpr int kTcMmaWarp = kTcCW + kTcEW;       // MMA issue
+constexpr int kTcSchedWarp = kTcMmaWarp + 1;    // work-item scheduler
+constexpr int kTcThreads = (kTcSchedWarp + 1) * 32;
+constexpr int kTcStages = 5;                    // lane-private cp.async staging ring
+constexpr int kTcAhead = kTcStages - 1;         // chunks gathered ahead of the digit pass
+constexpr int kTcRing = 16;                     // index ring slots (>= 2 kTcAhead + 1)
+constexpr int kTcStageX = kTcKC * 64 * 4;       // 64 rows x 64 floats (lane-private 64-byte segments)
+constexpr int kTcN = 144;                       // N side: two levels x (64 factor columns + y + 7 zero pad)
+constexpr int kTcLvl = 72;                      // N columns per level
+constexpr int kTcATile = 4096;                  // M = 128 (two levels x 64 columns) x 32 K bytes
+constexpr int kTcBTile = 4608;                  // N = 144 x 32 K bytes
 constexpr int kTcKStepBytes = 2 * kTcATile + 2 * kTcBTile;  // A12 A34 B12 B34
 constexpr int kTcDigitBuf = 2 * kTcKStepBytes;              // one chunk (two K-steps)
-constexpr int kTcAccB = 256;                  // TMEM column of the second accumulator (levels 4..6)
-constexpr int kTcSlots = 4;                   // work items in flight (finalize lags <= 2 chunks)
-constexpr int kTcMaxChunks = 256;             // chunks per work item (item_rows <= 16384)
-constexpr int kTcExcBatch = 64;               // exception rows staged per finalize round (one chunk)
-constexpr float kTcLimit = 2.13e9f;           // |x * 2^32 / alpha| below this keeps the top digit in int8
+constexpr int kTcAccB = 256;                    // TMEM column of the second accumulator (levels 4..6)
+constexpr int kTcItems = 16;                    // work-item ring
+constexpr int kTcGrab = 8;                      // work items claimed per counter increment
+constexpr int kTcExcSlots = 4;                  // exception masks: items in flight past the epilogue <= 3
+constexpr int kTcMaxChunks = 256;               // chunks per work item (item_rows <= 16384)
+constexpr int kTcExcBatch = 32;                 // exception rows staged per epilogue round (half a chunk)
+constexpr float kTcLimit = 2.13e9f;             // |x * 2^32 / alpha| below this keeps the top digit in int8
 
-struct TcMeta {             // per staged chunk: its work item's thresholds and previous rows
-    uint64_t T[64];
-    float wold[64];
+struct TcItem {             // one work item in the ring (written by the scheduler warp)
+    uint64_t T[64];         // selection thresholds (~0: padding column, never kept)
+    float wold[64];         // previous row (fused residual)
+    int64_t lo;             // first rating of the row
+    int64_t t;              // batch-relative work item; -1 ends the CTA's list
+    int n, kbeg, kend, r, row, pad[3];
 };
 
 struct TcSmem {
-    static constexpr int stage_x = 0;                                          // [4][64][kTcSX] f32
-    static constexpr int stage_y = stage_x + kTcStages * kTcKC * kTcSX * 4;     // [4][64] f32
-    static constexpr int meta = stage_y + kTcStages * kTcKC * 4;               // [4] TcMeta
-    static constexpr int digits = (meta + kTcStages * (int)sizeof(TcMeta) + 1023) & ~1023;  // [2] tile sets
+    static constexpr int stage_x = 0;                                          // [4] lane-private rows
+    static constexpr int ring = stage_x + kTcStages * kTcStageX;               // [R][64] idx, [R][64] f32 y
+    static constexpr int digits = (ring + 2 * kTcRing * kTcKC * 4 + 1023) & ~1023;  // [2] tile sets
     static constexpr int xchg = digits + 2 * kTcDigitBuf;                      // [64][72] f64
-    static constexpr int exc_x = xchg + 64 * kTcLvl * 8;                       // [32][72] f32 (+ y, k)
-    static constexpr int exc_mask = exc_x + kTcExcBatch * kTcLvl * 4;          // [slots][256] u64
-    static constexpr int rss = exc_mask + kTcSlots * kTcMaxChunks * 8;         // [slots][kTcCW] f64
-    static constexpr int fin_T = rss + kTcSlots * kTcCW * 8;                   // [slots][64] u64
-    static constexpr int total = fin_T + kTcSlots * 64 * 8;
+    static constexpr int exc_x = xchg + 64 * kTcLvl * 8;                       // [64][72] f32 (+ y, k)
+    static constexpr int exc_mask = exc_x + kTcExcBatch * kTcLvl * 4;          // [4][256][2] u32
+    static constexpr int items = exc_mask + kTcExcSlots * kTcMaxChunks * 8;    // [8] TcItem
+    static constexpr int rss = items + kTcItems * (int)sizeof(TcItem);         // [8][kTcCW] f64
+    static constexpr int total = rss + kTcItems * kTcCW * 8;
 };
+static_assert(sizeof(TcItem) % 16 == 0, "item ring alignment");
+
+// item-ring threshold slot of column c: the digit pass reads columns 4q .. 4q+3 (q = 8g + lane
+// group) as two 16-byte words; lanes 0..7 of a row read 128 contiguous bytes per word
+__host__ __device__ constexpr int tperm(int c) {
+    return (((c >> 5) * 2 + ((c >> 1) & 1)) * 8 + ((c >> 2) & 7)) * 2 + (c & 1);
+}
 
 __host__ __device__ constexpr uint32_t tc_mn_off(uint32_t mn, uint32_t k) {
     return (mn >> 4) * 512u + (k >> 3) * 128u + (k & 7u) * 16u + (mn & 15u);
@@ -88,6 +115,14 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
 }
 __device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(mbar) : "memory");
+}
+// arrive on `mbar` once every cp.async this thread issued so far has landed (counts as one of
+// the barrier's expected arrivals)
+__device__ __forceinline__ void cp_async_mbar_arrive(uint32_t mbar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(mbar) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t saddr, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(saddr), "l"(gmem));
 }
 
 // Digit scales of one half-sweep.  Factor column c: alpha_c = 2^E with alpha_c > 32.25 q_c,
@@ -132,81 +167,87 @@ __global__ void __launch_bounds__(256) tc_scales_kernel(const uint32_t* __restri
     }
 }
 
-struct TcCursor {
-    int64_t t;   // work item index (batch-relative); >= n_tiles when done
+// profiling trace (tc_debug 8, CALS_TC_TRACE builds): timestamps of CTA 0 of launch A.stats[49149]
+// into A.stats (>= 49152 words; A.stats[49150] counts launches)
+#ifndef CALS_TC_TRACE
+#define CALS_TC_TRACE 0
+#endif
+#define TC_TRACE(slot, cond)                                                                   \
+    do {                                                                                       \
+        if (CALS_TC_TRACE && trace && (cond)) A.stats[(slot)] = (unsigned long long)clock64(); \
+    } while (0)
+
+// Work-item cursor of the digit-pass warps (item ring position + chunk start).
+struct TcCur {
+    int i;       // item sequence number (ring slot i % kTcItems)
     int k0;      // first slice row of the chunk
     int kbeg, kend;
-    int r, row;  // batch row, row id
-    int64_t lo;  // first rating of the row
-    int n;
+    int64_t lo;
+    bool ok;     // false past the CTA's last item
 };
 
-__device__ __forceinline__ void tc_cursor_item(const SweepArgs& A, const BigArgs& B, TcCursor& c) {
-    if (c.t >= B.n_tiles) return;
-    const int64_t T_abs = B.tile_base + c.t;
-    int r;
-    if (B.tile_row != nullptr) {
-        r = (int)(__ldg(B.tile_row + T_abs) - B.row_base);
-    } else {
-        int64_t lo = 0, hi = B.n_big - 1;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi + 1) >> 1;
-            if (B.tile_ptr[mid] <= T_abs) lo = mid; else hi = mid - 1;
-        }
-        r = (int)lo;
-    }
-    c.r = r;
-    c.row = B.rows[r];
-    c.lo = A.ptr[c.row];
-    c.n = (int)(A.ptr[c.row + 1] - c.lo);
-    c.kbeg = (int)(T_abs - B.tile_ptr[r]) * B.item_rows;
-    c.kend = min(c.n, c.kbeg + B.item_rows);
-    c.k0 = c.kbeg;
+__device__ __forceinline__ void tc_enter(TcCur& c, const TcItem* items, uint32_t full_base) {
+    const int sl = c.i % kTcItems;
+    mbar_wait(full_base + 8u * (uint32_t)sl, (uint32_t)((c.i / kTcItems) & 1));
+    const TcItem& d = items[sl];
+    c.ok = d.t >= 0;
+    c.kbeg = d.kbeg;
+    c.kend = d.kend;
+    c.k0 = d.kbeg;
+    c.lo = d.lo;
 }
-
-__device__ __forceinline__ void tc_cursor_next(const SweepArgs& A, const BigArgs& B, TcCursor& c) {
+__device__ __forceinline__ void tc_advance(TcCur& c, const TcItem* items, uint32_t full_base) {
     c.k0 += kTcKC;
     if (c.k0 >= c.kend) {
-        c.t += gridDim.x;
-        tc_cursor_item(A, B, c);
+        ++c.i;
+        tc_enter(c, items, full_base);
     }
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A, BigArgs B,
                                                                     const float* __restrict__ g_scale,
-                                                                    const double* __restrict__ g_alpha) {
+                                                                    const double* __restrict__ g_alpha, int dbg) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    __shared__ float s_scale[65];
+    __shared__ __align__(16) float s_scale[68];
     __shared__ double s_alpha[65];
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(8) unsigned long long bar_full_st[kTcStages], bar_empty_st[kTcStages];
+    __shared__ uint32_t exc_any[kTcExcSlots];  // item had an exception row (the epilogue scans its masks)
+    __shared__ __align__(8) unsigned long long bar_item_full[kTcItems], bar_item_empty[kTcItems],
+        bar_item_done[kTcItems];
     __shared__ __align__(8) unsigned long long bar_full_tl[2], bar_empty_tl[2];
-    __shared__ __align__(8) unsigned long long bar_tmem_full, bar_tmem_empty, bar_item[kTcSlots];
+    __shared__ __align__(8) unsigned long long bar_tmem_full, bar_tmem_empty;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nf = A.nf, gs = nf + 1;
     const bool want_rss = A.rss_rows != nullptr;
+    // tracing (tc_debug 3): CTA 0 of the first launch after the buffer was cleared
+    const bool trace = dbg == 8 && blockIdx.x == 0 && A.stats != nullptr && A.stats[49150] == A.stats[49149];
     const uint32_t sbase = tc::smem_addr(smem);
     unsigned char* digits = smem + TcSmem::digits;
     double* xchg = reinterpret_cast<double*>(smem + TcSmem::xchg);
     float* exc_x = reinterpret_cast<float*>(smem + TcSmem::exc_x);
     uint32_t* exc_mask = reinterpret_cast<uint32_t*>(smem + TcSmem::exc_mask);  // [slot][chunk][2]
+    TcItem* items = reinterpret_cast<TcItem*>(smem + TcSmem::items);
     double* rss_part = reinterpret_cast<double*>(smem + TcSmem::rss);
-    uint64_t* fin_T = reinterpret_cast<uint64_t*>(smem + TcSmem::fin_T);
+    const uint32_t full_base = smem_u32(&bar_item_full[0]);
 
-    // ---- setup (every thread), then the roles never meet at a block barrier again
+    // ---- setup, then the roles never meet at a block barrier again
     for (int e = tid; e < 2 * kTcDigitBuf / 16; e += blockDim.x)
         reinterpret_cast<uint4*>(digits)[e] = make_uint4(0u, 0u, 0u, 0u);  // padding bytes stay zero
-    for (int e = tid; e < kTcSlots * kTcMaxChunks * 2; e += blockDim.x) exc_mask[e] = 0u;
+    for (int e = tid; e < kTcExcSlots * kTcMaxChunks * 2; e += blockDim.x) exc_mask[e] = 0u;
+    for (int e = tid; e < kTcStages * kTcStageX / 16; e += blockDim.x)
+        reinterpret_cast<uint4*>(smem + TcSmem::stage_x)[e] = make_uint4(0u, 0u, 0u, 0u);  // padding columns stay 0
+    if (tid < kTcExcSlots) exc_any[tid] = 0u;
+    if (tid < 68) s_scale[tid] = tid < 65 ? g_scale[tid] : 0.f;
     if (tid < 65) {
-        s_scale[tid] = g_scale[tid];
         s_alpha[tid] = g_alpha[tid];
     }
     if (warp == 0) tc::tmem_alloc<512>(&s_tmem);
     if (tid == 0) {
-        for (int s = 0; s < kTcStages; ++s) {
-            mbar_init(smem_u32(&bar_full_st[s]), 1);
-            mbar_init(smem_u32(&bar_empty_st[s]), kTcCW);
+        for (int s = 0; s < kTcItems; ++s) {
+            mbar_init(smem_u32(&bar_item_full[s]), 64);  // 32 lanes x (descriptor writes + their copies)
+            mbar_init(smem_u32(&bar_item_empty[s]), 1);
+            mbar_init(smem_u32(&bar_item_done[s]), kTcCW);
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(smem_u32(&bar_full_tl[s]), kTcCW);
@@ -214,7 +255,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
         }
         mbar_init(smem_u32(&bar_tmem_full), 1);
         mbar_init(smem_u32(&bar_tmem_empty), 1);
-        for (int s = 0; s < kTcSlots; ++s) mbar_init(smem_u32(&bar_item[s]), kTcCW);
     }
     tc::fence_smem_async();
     tc::fence_before();
@@ -222,301 +262,445 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
     tc::fence_after();
     const uint32_t tmem = s_tmem;
 
-    if (warp == kTcCW) {
-        // ================= control warp: producer of the staging ring + MMA issue =================
-        const uint32_t idesc = tc::idesc_i8(128, kTcN) | (1u << 15) | (1u << 16);  // MN-major A and B
-        const uint32_t rowbytes = 16u * (uint32_t)xs_chunks(nf);
-        TcCursor p{}, m{};
-        p.t = m.t = blockIdx.x;
-        tc_cursor_item(A, B, p);
-        m = p;
-        int64_t jp = 0, jm = 0, item = 0;
-        bool m_first = true;
-        while (m.t < B.n_tiles) {
-            // produce up to kTcStages chunks ahead of the MMAs
-            while (p.t < B.n_tiles && jp < jm + kTcStages) {
-                const int s = (int)(jp % kTcStages);
-                if (jp >= kTcStages) mbar_wait(smem_u32(&bar_empty_st[s]), (uint32_t)((jp / kTcStages - 1) & 1));
-                const int kn = min(kTcKC, p.kend - p.k0);
-                TcMeta* meta = reinterpret_cast<TcMeta*>(smem + TcSmem::meta) + s;
-                float* ys = reinterpret_cast<float*>(smem + TcSmem::stage_y) + s * kTcKC;
-                for (int c = lane; c < 64; c += 32) {
-                    meta->T[c] = c < nf ? B.thr[(size_t)p.r * nf + c] : ~0ull;
-                    meta->wold[c] = (want_rss && c < nf) ? A.tgt_old[(int64_t)p.row * A.ld_old + c] : 0.f;
+    if (warp == kTcSchedWarp) {
+        // ================= scheduler: work items -> ring (lane-parallel resolution) =================
+        // items are claimed kTcGrab at a time from one counter (longest first: rows are sorted by
+        // length), so CTAs that start late or draw long items simply claim fewer
+        int i = 0;
+        bool more = true;
+        while (more) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(B.item_ctr, kTcGrab);
+            base = __shfl_sync(CALS_FULL_MASK, base, 0);
+            const int64_t t = (int64_t)base + lane;
+            int r = 0, row = 0, n = 0, kbeg = 0, kend = 0;
+            int64_t lo = 0;
+            if (lane < kTcGrab && t < B.n_tiles) {
+                const int64_t T_abs = B.tile_base + t;
+                if (B.tile_row != nullptr) {
+                    r = (int)(__ldg(B.tile_row + T_abs) - B.row_base);
+                } else {
+                    int64_t a = 0, b = B.n_big - 1;
+                    while (a < b) {
+                        const int64_t mid = (a + b + 1) >> 1;
+                        if (B.tile_ptr[mid] <= T_abs) a = mid; else b = mid - 1;
+                    }
+                    r = (int)a;
                 }
-                for (int k = lane; k < kTcKC; k += 32) ys[k] = k < kn ? __ldg(A.val + p.lo + p.k0 + k) : 0.f;
-                __syncwarp();
-                const uint32_t fb = smem_u32(&bar_full_st[s]);
-                if (lane == 0) mbar_expect_tx(fb, (uint32_t)kn * rowbytes);
-                const uint32_t sx = sbase + TcSmem::stage_x + (uint32_t)s * (kTcKC * kTcSX * 4u);
-                for (int k = lane; k < kn; k += 32)
-                    bulk_g2s(sx + (uint32_t)k * (kTcSX * 4u),
-                             A.src + (int64_t)__ldg(A.idx + p.lo + p.k0 + k) * A.ld_src, rowbytes, fb);
-                tc_cursor_next(A, B, p);
-                ++jp;
+                row = B.rows[r];
+                lo = A.ptr[row];
+                n = (int)(A.ptr[row + 1] - lo);
+                kbeg = (int)(T_abs - B.tile_ptr[r]) * B.item_rows;
+                kend = min(n, kbeg + B.item_rows);
             }
-            // MMAs of chunk jm
-            const int db = (int)(jm & 1);
-            const int kn = min(kTcKC, m.kend - m.k0);
-            const bool last = m.k0 + kTcKC >= m.kend;
-            if (lane == 0) {
-                mbar_wait(smem_u32(&bar_full_tl[db]), (uint32_t)((jm >> 1) & 1));
-                if (m_first && item > 0) mbar_wait(smem_u32(&bar_tmem_empty), (uint32_t)((item - 1) & 1));
-                tc::fence_after();
-                const int nks = (kn + 31) >> 5;
-                for (int ks = 0; ks < nks; ++ks) {
-                    const uint32_t base = sbase + TcSmem::digits + (uint32_t)(db * kTcDigitBuf + ks * kTcKStepBytes);
-                    const uint64_t a12 = tc::sdesc(base, 128, 512), a34 = tc::sdesc(base + kTcATile, 128, 512);
-                    const uint64_t b12 = tc::sdesc(base + 2 * kTcATile, 128, 512);
-                    const uint64_t b34 = tc::sdesc(base + 2 * kTcATile + kTcBTile, 128, 512);
-                    const uint32_t acc = (m_first && ks == 0) ? 0u : 1u;
-                    tc::mma_i8_ss(tmem, a12, b12, idesc, acc);
-                    tc::mma_i8_ss(tmem + kTcAccB, a12, b34, idesc, acc);
-                    tc::mma_i8_ss(tmem + kTcAccB, a34, b12, idesc, 1u);
+            for (int l = 0; l < kTcGrab && more; ++l, ++i) {
+                const int64_t tl = __shfl_sync(CALS_FULL_MASK, t, l);
+                const bool valid = tl < B.n_tiles;
+                const int rl = __shfl_sync(CALS_FULL_MASK, r, l), rowl = __shfl_sync(CALS_FULL_MASK, row, l);
+                const int nl = __shfl_sync(CALS_FULL_MASK, n, l), kbl = __shfl_sync(CALS_FULL_MASK, kbeg, l);
+                const int kel = __shfl_sync(CALS_FULL_MASK, kend, l);
+                const int64_t lol = __shfl_sync(CALS_FULL_MASK, lo, l);
+                const int sl = i % kTcItems;
+                if (i >= kTcItems) mbar_wait_backoff(smem_u32(&bar_item_empty[sl]), (uint32_t)(((i / kTcItems) - 1) & 1));
+                TcItem& d = items[sl];
+                if (lane == 0) {
+                    d.t = valid ? tl : -1;
+                    d.lo = lol;
+                    d.n = nl;
+                    d.kbeg = kbl;
+                    d.kend = kel;
+                    d.r = rl;
+                    d.row = rowl;
                 }
-                tc::commit(smem_u32(&bar_empty_tl[db]));
-                if (last) tc::commit(smem_u32(&bar_tmem_full));
+                if (valid) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int c = lane + 32 * h;
+                        if (c < nf) cp_async8(smem_u32(&d.T[tperm(c)]), B.thr + (size_t)rl * nf + c);
+                        else d.T[tperm(c)] = ~0ull;
+                        if (want_rss && c < nf) cp_async4(smem_u32(&d.wold[c]), A.tgt_old + (int64_t)rowl * A.ld_old + c);
+                        else d.wold[c] = 0.f;
+                    }
+                }
+                const uint32_t fb = smem_u32(&bar_item_full[sl]);
+                TC_TRACE(40960 + i, lane == 0 && i < 8192);
+                mbar_arrive(fb);           // this lane's descriptor / padding writes
+                cp_async_mbar_arrive(fb);  // and, asynchronously, its copies
+                more = valid;
             }
-            __syncwarp();
-            if (last) ++item;
-            m_first = last;
-            tc_cursor_next(A, B, m);
-            ++jm;
+        }
+    } else if (warp == kTcMmaWarp) {
+        // ================= MMA issue (one thread) =================
+        if (lane == 0) {
+            const uint32_t idesc = tc::idesc_i8(128, kTcN) | (1u << 15) | (1u << 16);  // MN-major A and B
+            int64_t j = 0;
+            for (int i = 0;; ++i) {
+                const int sl = i % kTcItems;
+                mbar_wait(full_base + 8u * (uint32_t)sl, (uint32_t)((i / kTcItems) & 1));
+                const TcItem& d = items[sl];
+                if (d.t < 0) break;
+                const int kbeg = d.kbeg, kend = d.kend;
+                for (int k0 = kbeg; k0 < kend; k0 += kTcKC, ++j) {
+                    const int db = (int)(j & 1);
+                    if (dbg & 16) mbar_wait_hint(smem_u32(&bar_full_tl[db]), (uint32_t)((j >> 1) & 1));
+                    else if (dbg & 64) {
+                        while (!mbar_test(smem_u32(&bar_full_tl[db]), (uint32_t)((j >> 1) & 1))) __nanosleep(20);
+                    } else mbar_wait(smem_u32(&bar_full_tl[db]), (uint32_t)((j >> 1) & 1));
+                    TC_TRACE(j * 8 + 4, j < 4096);
+                    if (k0 == kbeg && i > 0) mbar_wait(smem_u32(&bar_tmem_empty), (uint32_t)((i - 1) & 1));
+                    TC_TRACE(j * 8 + 5, j < 4096);
+                    if (trace && j < 4096) A.stats[j * 8 + 6] = (unsigned long long)i;
+                    tc::fence_after();
+                    const int nks = (min(kTcKC, kend - k0) + 31) >> 5;
+                    for (int ks = 0; ks < ((dbg & 1) ? 0 : nks); ++ks) {
+                        const uint32_t base = sbase + TcSmem::digits + (uint32_t)(db * kTcDigitBuf + ks * kTcKStepBytes);
+                        const uint64_t a12 = tc::sdesc(base, 128, 512), a34 = tc::sdesc(base + kTcATile, 128, 512);
+                        const uint64_t b12 = tc::sdesc(base + 2 * kTcATile, 128, 512);
+                        const uint64_t b34 = tc::sdesc(base + 2 * kTcATile + kTcBTile, 128, 512);
+                        const uint32_t acc = (k0 == kbeg && ks == 0) ? 0u : 1u;
+                        tc::mma_i8_ss(tmem, a12, b12, idesc, acc);
+                        tc::mma_i8_ss(tmem + kTcAccB, a12, b34, idesc, acc);
+                        tc::mma_i8_ss(tmem + kTcAccB, a34, b12, idesc, 1u);
+                    }
+                    tc::commit(smem_u32(&bar_empty_tl[db]));
+                    if (k0 + kTcKC >= kend) tc::commit(smem_u32(&bar_tmem_full));
+                }
+            }
+        }
+    } else if (warp >= kTcCW) {
+        // ================= epilogue (warps 8..11 = TMEM lane quarters 0..3) =================
+        const int ew = warp - kTcCW, et = tid - kTcCW * 32;
+        const uint32_t lrow = (uint32_t)(32 * ew) << 16;
+        for (int i = 0;; ++i) {
+            const int sl = i % kTcItems, xs = i % kTcExcSlots;
+            mbar_wait(full_base + 8u * (uint32_t)sl, (uint32_t)((i / kTcItems) & 1));
+            const TcItem& d = items[sl];
+            if (d.t < 0) break;
+            TC_TRACE(32768 + i * 8 + 0, et == 0 && i < 1024);
+            mbar_wait_backoff(smem_u32(&bar_item_done[sl]), (uint32_t)((i / kTcItems) & 1));
+            TC_TRACE(32768 + i * 8 + 1, et == 0 && i < 1024);
+            mbar_wait(smem_u32(&bar_tmem_full), (uint32_t)(i & 1));
+            TC_TRACE(32768 + i * 8 + 2, et == 0 && i < 1024);
+            tc::fence_after();
+            // per TMEM row (level h of column c) and column f, the four accumulators combine exactly
+            // in 64-bit integers: I = a0 2^24 + a1 2^16 + b0 2^8 + b1 (|a| < 2^29: |I| < 2^53, so its
+            // conversion to float64 is exact); G[c][f] = alpha_c alpha_f (2^-40 I_level1 + 2^-48 I_level2)
+            auto drain = [&](int f0, uint32_t (&a0)[8], uint32_t (&a1)[8], uint32_t (&b0)[8], uint32_t (&b1)[8]) {
+                tc::ld_32x32b_x8(tmem + lrow + f0, a0);
+                tc::ld_32x32b_x8(tmem + lrow + kTcLvl + f0, a1);
+                tc::ld_32x32b_x8(tmem + lrow + kTcAccB + f0, b0);
+                tc::ld_32x32b_x8(tmem + lrow + kTcAccB + kTcLvl + f0, b1);
+                tc::ld_wait();
+            };
+            auto combine = [](uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) {
+                const long long I = ((long long)(int)a0 << 24) + ((long long)(int)a1 << 16) +
+                                    ((long long)(int)b0 << 8) + (long long)(int)b1;
+                return (double)I;
+            };
+            if (ew >= 2) {  // level-2 rows first: their part into xchg
+                const int cr = 32 * (ew - 2) + lane;
+                for (int f0 = 0; f0 < kTcLvl; f0 += 8) {
+                    uint32_t a0[8], a1[8], b0[8], b1[8];
+                    drain(f0, a0, a1, b0, b1);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) xchg[cr * kTcLvl + f0 + q] = combine(a0[q], a1[q], b0[q], b1[q]);
+                }
+            }
+            named_bar(1, 128);
+            if (ew < 2) {
+                const int cr = 32 * ew + lane;
+                const double ac = s_alpha[cr];
+                for (int f0 = 0; f0 < kTcLvl; f0 += 8) {
+                    uint32_t a0[8], a1[8], b0[8], b1[8];
+                    drain(f0, a0, a1, b0, b1);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int f = f0 + q;
+                        const double p = fma(combine(a0[q], a1[q], b0[q], b1[q]), 0x1p-40,
+                                             xchg[cr * kTcLvl + f] * 0x1p-48);
+                        xchg[cr * kTcLvl + f] = ac * s_alpha[f <= 64 ? f : 64] * p;
+                    }
+                }
+            }
+            tc::fence_before();
+            named_bar(1, 128);
+            if (et == 0) mbar_arrive(smem_u32(&bar_tmem_empty));  // the next item's MMAs may start
+            TC_TRACE(32768 + i * 8 + 3, et == 0 && i < 1024);
+            // exception rows (a value past its column's digit range), chunk by chunk in slice
+            // order: their exact float64 contributions, G[c][:] += x_kc [x_k | y_k] if k is kept for c
+            const int nchunks = (d.kend - d.kbeg + kTcKC - 1) / kTcKC;
+            uint32_t* em = exc_mask + xs * kTcMaxChunks * 2;
+            const bool any_exc = exc_any[xs] != 0u;
+            for (int q = 0; q < (any_exc ? 2 * nchunks : 0); ++q) {  // 32-row halves of the chunks, in slice order
+                const uint32_t m = em[q];
+                if (m == 0u) continue;
+                named_bar(1, 128);  // exc_x free, mask read by every epilogue thread
+                if (et == 0) em[q] = 0u;
+                const int ne = __popc(m);
+                for (int e = et; e < ne * kTcLvl; e += 128) {
+                    const int ii = e / kTcLvl, f = e - ii * kTcLvl;
+                    const int k = d.kbeg + 32 * q + (int)__fns(m, 0, ii + 1);
+                    float v = 0.f;
+                    if (f < nf) v = __ldg(A.src + (int64_t)__ldg(A.idx + d.lo + k) * A.ld_src + f);
+                    else if (f == 64) v = __ldg(A.val + d.lo + k);
+                    else if (f == 65) v = __int_as_float(k);
+                    exc_x[ii * kTcLvl + f] = v;
+                }
+                named_bar(1, 128);
+                if (et < nf) {
+                    const int cr = et;
+                    const uint64_t T = d.T[tperm(cr)];
+                    const uint32_t Ta = (uint32_t)(T >> 32), Tk = 0xFFFFFFFFu - (uint32_t)T;
+                    for (int ii = 0; ii < ne; ++ii) {
+                        const float* xr = exc_x + ii * kTcLvl;
+                        const float xc = xr[cr];
+                        const uint32_t a = abs_bits(xc), kgl = (uint32_t)__float_as_int(xr[65]);
+                        if (!(a > Ta || (a == Ta && kgl <= Tk))) continue;
+                        const double xd = (double)xc;
+                        double* grow = xchg + cr * kTcLvl;
+                        for (int f = 0; f < nf; ++f) grow[f] = fma(xd, (double)xr[f], grow[f]);
+                        grow[64] = fma(xd, (double)xr[64], grow[64]);
+                    }
+                }
+            }
+            named_bar(1, 128);
+            if (et == 0) exc_any[xs] = 0u;
+            TC_TRACE(32768 + i * 8 + 4, et == 0 && i < 1024);
+            // the normal equations (+ lam*n on the diagonal of a finished row) and the residual
+            const bool direct = d.r >= B.n_multi;
+            double* out = direct ? A.gbuf + (size_t)d.r * nf * gs : B.part + (size_t)d.t * nf * gs;
+            const double lam_n = direct ? A.lam * (double)d.n : 0.0;
+            for (int cr = ew; cr < nf; cr += kTcEW) {  // a warp per row: coalesced, no division
+                double* orow = out + (size_t)cr * gs;
+                const double* xr = xchg + cr * kTcLvl;
+                for (int f = lane; f < nf; f += 32) orow[f] = xr[f] + (f == cr ? lam_n : 0.0);
+                if (lane == 0) orow[nf] = xr[64];
+            }
+            if (et == 0 && want_rss) {
+                double v = 0.0;
+                for (int w = 0; w < kTcCW; ++w) v += rss_part[sl * kTcCW + w];
+                if (direct) A.rss_rows[d.row] = v;
+                else B.rss_part[d.t] = v;
+            }
+            named_bar(1, 128);
+            TC_TRACE(32768 + i * 8 + 5, et == 0 && i < 1024);
+            if (et == 0) mbar_arrive(smem_u32(&bar_item_empty[sl]));
         }
     } else {
-        // ================= compute warps: digits (+ finalize on warps 0..3) =================
-        TcCursor c{};
-        c.t = blockIdx.x;
-        tc_cursor_item(A, B, c);
-        const int kl = lane >> 2, fql = lane & 3;
-        const int krel = 8 * warp + kl;  // slice row of this lane within the chunk
-        int64_t j = 0, item = 0;
+        // ================= digit pass (warps 0..15): gather, select, split =================
+        // lane (kl, fql): slice row kRW * warp + kl of the chunk, columns 4 (kLPR g + fql) + 0..3
+        const int kl = lane / kTcLPR, fql = lane % kTcLPR;
+        const int krel = kTcRW * warp + kl;  // slice row of this lane within the chunk
+        // row-major staging (256 bytes per slice row): the 8 lanes of a row copy and read one
+        // contiguous 128-byte segment per group (one shared-memory wavefront each way)
+        const uint32_t sx_lane = sbase + TcSmem::stage_x + (uint32_t)krel * 256u + 16u * (uint32_t)fql;
+        // index ring: the slice-row ids and ratings of chunk t in slot t % kTcRing, copied 2 kTcAhead
+        // chunks ahead by the row's first lane (so the gathers never wait on an index load)
+        const uint32_t ring_idx = sbase + TcSmem::ring + 4u * (uint32_t)krel;
+        const uint32_t ring_val = ring_idx + kTcRing * kTcKC * 4;
+        auto seg = [&](int g) { return 128u * (uint32_t)g; };
+        // digit-store offsets of this lane within a tile set: K part (its slice row) + MN part
+        // (its first column, per stacked level half); group g adds 1024 bytes (32 columns)
+        const uint32_t kk = (uint32_t)(krel & 31);
+        const uint32_t dig_lane = sbase + TcSmem::digits + (uint32_t)(krel >> 5) * kTcKStepBytes + tc_mn_off(0u, kk);
+        auto mn_part = [](uint32_t mn) { return (mn >> 4) * 512u + (mn & 15u); };
+        const uint32_t off_a0 = mn_part(4u * fql), off_a1 = mn_part(64u + 4u * fql);
+        const uint32_t off_b0 = off_a0, off_b1 = mn_part(kTcLvl + 4u * fql);
+        const uint32_t off_y0 = mn_part(64u), off_y1 = mn_part(kTcLvl + 64u);
+        auto issue_idx = [&](const TcCur& q, int slot) {
+            if (fql == 0) {
+                const uint32_t o = (uint32_t)slot * (kTcKC * 4);
+                if (q.ok && q.k0 + krel < q.kend) {
+                    cp_async4(ring_idx + o, A.idx + q.lo + q.k0 + krel);
+                    cp_async4(ring_val + o, A.val + q.lo + q.k0 + krel);
+                } else {
+                    sts_u32(ring_idx + o, 0xFFFFFFFFu);  // -1: no row
+                }
+            }
+        };
+        auto issue_data = [&](int stage, int slot) {
+            const int idx = (int)lds_u32(ring_idx + (uint32_t)slot * (kTcKC * 4));
+            if (idx >= 0 && !(dbg & 128)) {
+                const float* srow = A.src + (int64_t)idx * A.ld_src;
+#pragma unroll
+                for (int g = 0; g < kTcNG; ++g) {
+                    const int c0 = 4 * (kTcLPR * g + fql);
+                    if (c0 < nf) cp_async16(sx_lane + (uint32_t)stage * kTcStageX + seg(g), srow + c0);
+                }
+            }
+        };
+        // group t (t >= -kTcAhead) = {indices of chunk t + 2 kTcAhead, rows of chunk t + kTcAhead}
+        TcCur q{};
+        q.i = 0;
+        tc_enter(q, items, full_base);
+        auto adv = [&](TcCur& x) {
+            if (x.ok) tc_advance(x, items, full_base);
+        };
+#pragma unroll 1
+        for (int t = 0; t < kTcAhead; ++t) {
+            issue_idx(q, t);
+            adv(q);
+            cp_async_commit();
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+#pragma unroll 1
+        for (int t = 0; t < kTcAhead; ++t) {
+            issue_idx(q, kTcAhead + t);
+            adv(q);
+            issue_data(t, t);
+            cp_async_commit();
+        }
+        TcCur c{};
+        c.i = 0;
+        tc_enter(c, items, full_base);
         double racc = 0.0;
-        while (c.t < B.n_tiles) {
-            const int s = (int)(j % kTcStages), db = (int)(j & 1), slot = (int)(item % kTcSlots);
+#pragma unroll 1
+        for (int64_t j = 0; c.ok; ++j) {
+            // group j - kTcAhead landed: the rows of chunk j and the indices of chunk j + kTcAhead
+            TC_TRACE(j * 8 + 0, warp == 0 && lane == 0 && j < 4096);
+            cp_async_wait<kTcAhead - 1>();
+            __syncwarp();
+            TC_TRACE(j * 8 + 1, warp == 0 && lane == 0 && j < 4096);
+            issue_idx(q, (int)((j + 2 * kTcAhead) % kTcRing));
+            adv(q);
+            issue_data((int)((j + kTcAhead) % kTcStages), (int)((j + kTcAhead) % kTcRing));
+            cp_async_commit();
+            TC_TRACE(j * 8 + 7, warp == 0 && lane == 0 && j < 4096);
+            const int s = (int)(j % kTcStages), db = (int)(j & 1);
+            const int sl = c.i % kTcItems;
+            const TcItem& it_d = items[sl];
             const int kn = min(kTcKC, c.kend - c.k0);
             const bool last = c.k0 + kTcKC >= c.kend;
             const int ci = (c.k0 - c.kbeg) / kTcKC;
-            mbar_wait(smem_u32(&bar_full_st[s]), (uint32_t)((j / kTcStages) & 1));
-            if (j >= 2) mbar_wait(smem_u32(&bar_empty_tl[db]), (uint32_t)(((j - 2) >> 1) & 1));
-            const float* Xs = reinterpret_cast<const float*>(smem + TcSmem::stage_x) + s * kTcKC * kTcSX;
-            const float* ys = reinterpret_cast<const float*>(smem + TcSmem::stage_y) + s * kTcKC;
-            const TcMeta* meta = reinterpret_cast<const TcMeta*>(smem + TcSmem::meta) + s;
             const bool krow = krel < kn;
             const uint32_t kg = (uint32_t)(c.k0 + krel);
-            // fixed point of the lane's 16 elements, kept bits, exception flag, residual dot
-            int X[16];
-            uint32_t keepm[4];
-            bool exc = false;
-            float pdot = 0.f;
-#pragma unroll
-            for (int it = 0; it < 4; ++it) {
-                const int c0 = 4 * (4 * it + fql);
-                float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (krow && c0 < nf) x = *reinterpret_cast<const float4*>(Xs + krel * kTcSX + c0);
-                const float xv[4] = {x.x, x.y, x.z, x.w};
-                uint32_t km = 0u;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int cc = c0 + e;
-                    const float v = cc < nf ? xv[e] : 0.f;
-                    const float t = v * s_scale[cc];
-                    exc |= fabsf(t) >= kTcLimit;
-                    X[4 * it + e] = __float2int_rn(t);
-                    if (want_rss) pdot = fmaf(v, meta->wold[cc], pdot);
-                    const uint64_t T = meta->T[cc];
-                    const uint32_t a = abs_bits(v), Ta = (uint32_t)(T >> 32), Tk = 0xFFFFFFFFu - (uint32_t)T;
-                    const bool keep = krow && cc < nf && (a > Ta || (a == Ta && kg <= Tk));
-                    km |= keep ? (0xFFu << (8 * e)) : 0u;
+            const uint32_t sx = sx_lane + (uint32_t)s * kTcStageX;
+            // the lane's 8 elements (2 groups of 4 consecutive columns): fixed point X = rint(x * 2^32 /
+            // alpha_c), its four signed digits all at once -- byte i of (X + 0x80808080) ^ 0x80 is the
+            // digit of weight 2^(8i) (the +0x80 per byte carries exactly the borrows of a signed-digit
+            // split) -- transposed into one word per level; kept bits from the 64-bit selection key
+            const uint32_t lo_key = 0xFFFFFFFFu - kg;
+            const uint32_t row_on = krow ? 0xFFFFFFFFu : 0u;
+            if (dbg & 2) {
+                if (j >= 2) mbar_wait(smem_u32(&bar_empty_tl[db]), (uint32_t)(((j - 2) >> 1) & 1));
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&bar_full_tl[db]));
+                if (last) {
+                    if (lane == 0) rss_part[sl * kTcCW + warp] = 0.0;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(smem_u32(&bar_item_done[sl]));
                 }
-                keepm[it] = km;
+                tc_advance(c, items, full_base);
+                continue;
+            }
+            uint32_t lev[kTcNG][4];  // [group][level 1..4]
+            uint32_t km[kTcNG];
+            float amax = 0.f, pdot = 0.f;
+#pragma unroll
+            for (int g = 0; g < kTcNG; ++g) {
+                const int c0 = 4 * (kTcLPR * g + fql);
+                const float4 x = lds_f128(sx + seg(g));  // zero in padding columns
+                const float4 sc = *reinterpret_cast<const float4*>(s_scale + c0);
+                const ulonglong2 t01 = *reinterpret_cast<const ulonglong2*>(&it_d.T[tperm(c0)]);
+                const ulonglong2 t23 = *reinterpret_cast<const ulonglong2*>(&it_d.T[tperm(c0 + 2)]);
+                const float t0 = x.x * sc.x, t1 = x.y * sc.y, t2 = x.z * sc.z, t3 = x.w * sc.w;
+                amax = fmaxf(amax, fmaxf(fmaxf(fabsf(t0), fabsf(t1)), fmaxf(fabsf(t2), fabsf(t3))));
+                const uint32_t z0 = (uint32_t)__float2int_rn(t0) + 0x80808080u;
+                const uint32_t z1 = (uint32_t)__float2int_rn(t1) + 0x80808080u;
+                const uint32_t z2 = (uint32_t)__float2int_rn(t2) + 0x80808080u;
+                const uint32_t z3 = (uint32_t)__float2int_rn(t3) + 0x80808080u;
+                const uint32_t lo01 = __byte_perm(z0, z1, 0x5140), hi01 = __byte_perm(z0, z1, 0x7362);
+                const uint32_t lo23 = __byte_perm(z2, z3, 0x5140), hi23 = __byte_perm(z2, z3, 0x7362);
+                lev[g][3] = __byte_perm(lo01, lo23, 0x5410) ^ 0x80808080u;  // level 4: weight 2^0
+                lev[g][2] = __byte_perm(lo01, lo23, 0x7632) ^ 0x80808080u;  // level 3
+                lev[g][1] = __byte_perm(hi01, hi23, 0x5410) ^ 0x80808080u;  // level 2
+                lev[g][0] = __byte_perm(hi01, hi23, 0x7632) ^ 0x80808080u;  // level 1: weight 2^24
+                const bool k0 = (((uint64_t)abs_bits(x.x) << 32) | lo_key) >= t01.x;
+                const bool k1 = (((uint64_t)abs_bits(x.y) << 32) | lo_key) >= t01.y;
+                const bool k2 = (((uint64_t)abs_bits(x.z) << 32) | lo_key) >= t23.x;
+                const bool k3 = (((uint64_t)abs_bits(x.w) << 32) | lo_key) >= t23.y;
+                km[g] = ((k0 ? 0xFFu : 0u) | (k1 ? 0xFF00u : 0u) | (k2 ? 0xFF0000u : 0u) | (k3 ? 0xFF000000u : 0u)) &
+                        row_on;
+                if (want_rss) {
+                    const float4 wo = *reinterpret_cast<const float4*>(&it_d.wold[c0]);
+                    pdot = fmaf(x.x, wo.x, pdot);
+                    pdot = fmaf(x.y, wo.y, pdot);
+                    pdot = fmaf(x.z, wo.z, pdot);
+                    pdot = fmaf(x.w, wo.w, pdot);
+                }
             }
             float yv = 0.f;
-            int Xy = 0;
+            uint32_t zy = 0x80808080u;
             if (fql == 0) {
-                yv = krow ? ys[krel] : 0.f;
+                yv = krow ? lds_f32(ring_val + (uint32_t)(j % kTcRing) * (kTcKC * 4)) : 0.f;
                 const float ty = yv * s_scale[64];
-                exc |= fabsf(ty) >= kTcLimit;
-                Xy = __float2int_rn(ty);
+                amax = fmaxf(amax, fabsf(ty));
+                zy = (uint32_t)__float2int_rn(ty) + 0x80808080u;
             }
-            // the row's flag and dot over its four lanes
-            exc = ((__ballot_sync(CALS_FULL_MASK, exc) >> (4 * kl)) & 0xFu) != 0u;
+            // the row's exception flag and dot over its lanes
+            const bool exc = ((__ballot_sync(CALS_FULL_MASK, amax >= kTcLimit) >> (kTcLPR * kl)) & ((1u << kTcLPR) - 1u)) != 0u;
             if (want_rss) {
-                pdot += __shfl_xor_sync(CALS_FULL_MASK, pdot, 1);
-                pdot += __shfl_xor_sync(CALS_FULL_MASK, pdot, 2);
+#pragma unroll
+                for (int o = 1; o < kTcLPR; o <<= 1) pdot += __shfl_xor_sync(CALS_FULL_MASK, pdot, o);
                 if (fql == 0 && krow) {
-                    const double d = (double)yv - (double)pdot;
-                    racc = fma(d, d, racc);
+                    const double dd = (double)yv - (double)pdot;
+                    racc = fma(dd, dd, racc);
                 }
             }
-            const uint32_t zero_row = exc ? 0u : 0xFFFFFFFFu;
-            unsigned char* dbuf = digits + db * kTcDigitBuf + (krel >> 5) * kTcKStepBytes;
-            const uint32_t kk = (uint32_t)(krel & 31);
+            const uint32_t zero_row = exc ? 0u : row_on;
+            TC_TRACE(j * 8 + 2, warp == 0 && lane == 0 && j < 4096);
+            if (j >= 2) {
+                if (dbg & 32) mbar_wait_hint(smem_u32(&bar_empty_tl[db]), (uint32_t)(((j - 2) >> 1) & 1));
+                else mbar_wait(smem_u32(&bar_empty_tl[db]), (uint32_t)(((j - 2) >> 1) & 1));
+            }
+            TC_TRACE(j * 8 + 3, warp == 0 && lane == 0 && j < 4096);
+            const uint32_t dbase = dig_lane + (uint32_t)db * kTcDigitBuf;
 #pragma unroll
-            for (int it = 0; it < 4; ++it) {
-                const int c0 = 4 * (4 * it + fql);
-                uint32_t Y[4][4];  // [element][Y0..Y3]: Y0 = X, Y_{i+1} = (Y_i + 128) >> 8; level L byte = Y[4 - L]
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int x0 = X[4 * it + e];
-                    const int y1 = (x0 + 128) >> 8, y2 = (y1 + 128) >> 8, y3 = (y2 + 128) >> 8;
-                    Y[e][0] = (uint32_t)x0;
-                    Y[e][1] = (uint32_t)y1;
-                    Y[e][2] = (uint32_t)y2;
-                    Y[e][3] = (uint32_t)y3;
-                }
+            for (int g = 0; g < ((dbg & 4) ? 0 : kTcNG); ++g) {
 #pragma unroll
                 for (int L = 1; L <= 4; ++L) {
-                    const uint32_t w = pack4(Y[0][4 - L], Y[1][4 - L], Y[2][4 - L], Y[3][4 - L]) & zero_row;
-                    const int pair = (L - 1) >> 1, half = (L - 1) & 1;
-                    *reinterpret_cast<uint32_t*>(dbuf + 2 * kTcATile + pair * kTcBTile +
-                                                 tc_mn_off((uint32_t)(half * kTcLvl + c0), kk)) = w;
-                    *reinterpret_cast<uint32_t*>(dbuf + pair * kTcATile + tc_mn_off((uint32_t)(half * 64 + c0), kk)) =
-                        w & keepm[it];
+                    const uint32_t w = lev[g][L - 1] & zero_row;
+                    const uint32_t pair = (uint32_t)((L - 1) >> 1), half = (uint32_t)((L - 1) & 1);
+                    const uint32_t gofs = 1024u * (uint32_t)g;  // 32 columns = 2 MN core groups
+                    sts_u32(dbase + 2 * kTcATile + pair * kTcBTile + (half ? off_b1 : off_b0) + gofs, w);
+                    sts_u32(dbase + pair * kTcATile + (half ? off_a1 : off_a0) + gofs, w & km[g]);
                 }
             }
             if (fql == 0) {
-                const int y1 = (Xy + 128) >> 8, y2 = (y1 + 128) >> 8, y3 = (y2 + 128) >> 8;
-                const uint32_t yl[4] = {(uint32_t)y3, (uint32_t)y2, (uint32_t)y1, (uint32_t)Xy};  // levels 1..4
+                // the rating's digits (level L = byte 4 - L), one byte per level word (the rest is padding)
 #pragma unroll
                 for (int L = 1; L <= 4; ++L) {
-                    const int pair = (L - 1) >> 1, half = (L - 1) & 1;
-                    *reinterpret_cast<uint32_t*>(dbuf + 2 * kTcATile + pair * kTcBTile +
-                                                 tc_mn_off((uint32_t)(half * kTcLvl + 64), kk)) = yl[L - 1] & 0xFFu & zero_row;
+                    const uint32_t pair = (uint32_t)((L - 1) >> 1), half = (uint32_t)((L - 1) & 1);
+                    const uint32_t yb = ((zy >> (8 * (4 - L))) & 0xFFu) ^ 0x80u;
+                    sts_u32(dbase + 2 * kTcATile + pair * kTcBTile + (half ? off_y1 : off_y0), yb & zero_row);
                 }
-                if (exc && krow) atomicOr(&exc_mask[(slot * kTcMaxChunks + ci) * 2 + (krel >> 5)], 1u << (krel & 31));
-            }
-            if (last && warp < 4) {
-                // the finalize reads the item's thresholds after this stage is recycled
-                for (int cc = lane + 32 * warp; cc < 64; cc += 128) fin_T[slot * 64 + cc] = meta->T[cc];
+                if (exc && krow) {
+                    atomicOr(&exc_mask[((c.i % kTcExcSlots) * kTcMaxChunks + ci) * 2 + (krel >> 5)], 1u << (krel & 31));
+                    exc_any[c.i % kTcExcSlots] = 1u;
+                }
             }
             tc::fence_smem_async();
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(smem_u32(&bar_empty_st[s]));
-                mbar_arrive(smem_u32(&bar_full_tl[db]));
-            }
+                        if (lane == 0) mbar_arrive(smem_u32(&bar_full_tl[db]));
             if (last) {
                 // per-warp residual partial, then this warp is done with the item
                 double v = racc;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(CALS_FULL_MASK, v, o);
-                if (lane == 0) rss_part[slot * kTcCW + warp] = v;
+                if (lane == 0) rss_part[sl * kTcCW + warp] = v;
                 racc = 0.0;
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&bar_item[slot]));
-                if (warp < 4) {
-                    // ===== finalize (warps 0..3 = the four TMEM lane quarters) =====
-                    mbar_wait(smem_u32(&bar_item[slot]), (uint32_t)((item / kTcSlots) & 1));
-                    mbar_wait(smem_u32(&bar_tmem_full), (uint32_t)(item & 1));
-                    tc::fence_after();
-                    const uint32_t lrow = (uint32_t)(32 * warp) << 16;
-                    if (warp >= 2) {
-                        // second stacked level (ra = 1): weights 2^-8(beta + 1 + rb), beta 2 / 4
-                        const int cr = 32 * (warp - 2) + lane;
-                        const double wA0 = ldexp(1.0, -24), wA1 = ldexp(1.0, -32), wB0 = ldexp(1.0, -40),
-                                     wB1 = ldexp(1.0, -48);
-                        for (int f0 = 0; f0 < kTcLvl; f0 += 8) {
-                            uint32_t a0[8], a1[8], b0[8], b1[8];
-                            tc::ld_32x32b_x8(tmem + lrow + f0, a0);
-                            tc::ld_32x32b_x8(tmem + lrow + kTcLvl + f0, a1);
-                            tc::ld_32x32b_x8(tmem + lrow + kTcAccB + f0, b0);
-                            tc::ld_32x32b_x8(tmem + lrow + kTcAccB + kTcLvl + f0, b1);
-                            tc::ld_wait();
-#pragma unroll
-                            for (int q = 0; q < 8; ++q)
-                                xchg[cr * kTcLvl + f0 + q] = wA0 * (double)(int)a0[q] + wA1 * (double)(int)a1[q] +
-                                                             wB0 * (double)(int)b0[q] + wB1 * (double)(int)b1[q];
-                        }
-                    }
-                    named_bar(1, 128);
-                    if (warp < 2) {
-                        const int cr = 32 * warp + lane;
-                        const double wA0 = ldexp(1.0, -16), wA1 = ldexp(1.0, -24), wB0 = ldexp(1.0, -32),
-                                     wB1 = ldexp(1.0, -40);
-                        for (int f0 = 0; f0 < kTcLvl; f0 += 8) {
-                            uint32_t a0[8], a1[8], b0[8], b1[8];
-                            tc::ld_32x32b_x8(tmem + lrow + f0, a0);
-                            tc::ld_32x32b_x8(tmem + lrow + kTcLvl + f0, a1);
-                            tc::ld_32x32b_x8(tmem + lrow + kTcAccB + f0, b0);
-                            tc::ld_32x32b_x8(tmem + lrow + kTcAccB + kTcLvl + f0, b1);
-                            tc::ld_wait();
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                const int f = f0 + q;
-                                const double p = wA0 * (double)(int)a0[q] + wA1 * (double)(int)a1[q] +
-                                                 wB0 * (double)(int)b0[q] + wB1 * (double)(int)b1[q];
-                                xchg[cr * kTcLvl + f] = s_alpha[cr] * s_alpha[f <= 64 ? f : 64] * (p + xchg[cr * kTcLvl + f]);
-                            }
-                        }
-                    }
-                    tc::fence_before();
-                    named_bar(1, 128);
-                    if (tid == 0) mbar_arrive(smem_u32(&bar_tmem_empty));  // the next item's MMAs may start
-                    // exception rows (a value past its column's digit range), chunk by chunk in slice
-                    // order: their exact float64 contributions, G[c][:] += x_kc [x_k | y_k] if k is kept for c
-                    const int nchunks = (c.kend - c.kbeg + kTcKC - 1) / kTcKC;
-                    uint32_t* em = exc_mask + slot * kTcMaxChunks * 2;
-                    for (int q = 0; q < nchunks; ++q) {
-                        const uint32_t m0 = em[2 * q], m1 = em[2 * q + 1];
-                        if ((m0 | m1) == 0u) continue;
-                        named_bar(1, 128);  // exc_x free, masks read by every finalize thread
-                        if (tid == 0) em[2 * q] = em[2 * q + 1] = 0u;
-                        const int n0 = __popc(m0), ne = n0 + __popc(m1);
-                        for (int e = tid; e < ne * kTcLvl; e += 128) {
-                            const int i = e / kTcLvl, f = e - i * kTcLvl;
-                            const uint32_t mm = i < n0 ? m0 : m1;
-                            const int bit = (int)__fns(mm, 0, (i < n0 ? i : i - n0) + 1);
-                            const int k = c.kbeg + q * kTcKC + (i < n0 ? 0 : 32) + bit;
-                            float v = 0.f;
-                            if (f < nf) v = __ldg(A.src + (int64_t)__ldg(A.idx + c.lo + k) * A.ld_src + f);
-                            else if (f == 64) v = __ldg(A.val + c.lo + k);
-                            else if (f == 65) v = __int_as_float(k);
-                            exc_x[i * kTcLvl + f] = v;
-                        }
-                        named_bar(1, 128);
-                        if (tid < nf) {
-                            const int cr = tid;
-                            const uint64_t T = fin_T[slot * 64 + cr];
-                            const uint32_t Ta = (uint32_t)(T >> 32), Tk = 0xFFFFFFFFu - (uint32_t)T;
-                            for (int i = 0; i < ne; ++i) {
-                                const float* xr = exc_x + i * kTcLvl;
-                                const float xc = xr[cr];
-                                const uint32_t a = abs_bits(xc), kgl = (uint32_t)__float_as_int(xr[65]);
-                                if (!(a > Ta || (a == Ta && kgl <= Tk))) continue;
-                                const double xd = (double)xc;
-                                double* grow = xchg + cr * kTcLvl;
-                                for (int f = 0; f < nf; ++f) grow[f] = fma(xd, (double)xr[f], grow[f]);
-                                grow[64] = fma(xd, (double)xr[64], grow[64]);
-                            }
-                        }
-                    }
-                    named_bar(1, 128);
-                    // write the normal equations (+ lam*n on the diagonal of a finished row) and the residual
-                    const bool direct = c.r >= B.n_multi;
-                    double* out = direct ? A.gbuf + (size_t)c.r * nf * gs : B.part + (size_t)c.t * nf * gs;
-                    const double lam_n = direct ? A.lam * (double)c.n : 0.0;
-                    for (int e = tid; e < nf * gs; e += 128) {
-                        const int cr = e / gs, f = e - cr * gs;
-                        out[e] = f == nf ? xchg[cr * kTcLvl + 64] : xchg[cr * kTcLvl + f] + (f == cr ? lam_n : 0.0);
-                    }
-                    if (tid == 0 && want_rss) {
-                        double v = 0.0;
-                        for (int w = 0; w < kTcCW; ++w) v += rss_part[slot * kTcCW + w];
-                        if (direct) A.rss_rows[c.row] = v;
-                        else B.rss_part[c.t] = v;
-                    }
-                    named_bar(1, 128);
-                }
-                ++item;
+                if (lane == 0) mbar_arrive(smem_u32(&bar_item_done[sl]));
             }
-            tc_cursor_next(A, B, c);
-            ++j;
+            tc_advance(c, items, full_base);
         }
+        cp_async_wait<0>();
     }
     tc::fence_before();
     __syncthreads();
     if (warp == 0) tc::tmem_free<512>(tmem);
+    if (dbg == 8 && blockIdx.x == 0 && tid == 0 && A.stats != nullptr) A.stats[49150] += 1ull;
 }
 
 }  // namespace cals

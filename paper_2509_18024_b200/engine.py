@@ -43,6 +43,13 @@ class DeviceSide:
     """One side of the rating matrix (CSR over users or CSC over items) on the
     device, with its static schedule (budgets, tiers) and workspace."""
 
+    def complete_row(self, row):
+        """Whether row's sketch is complete (s_i == n_i: the exact SPD row, core.py:206-207),
+        from the unsharded count -- budget_host is zero outside this rank's shard."""
+        if self.fast:
+            return int(self.budget_host[row]) == int(self.counts[row])
+        return _budget(int(self.counts[row]), self.rate) == int(self.counts[row])
+
     def __init__(self, ptr, idx, val, n_src, n_f, rate, device, row_begin=0, row_end=None, fast=False, ptr_dev=None):
         torch = _lib.require_cuda()
         L = _lib.load()
@@ -53,6 +60,7 @@ class DeviceSide:
         self.n_rows = n_rows
         self.n_src = int(n_src)
         self.n_f = int(n_f)
+        self.rate = float(rate)
         self.device = device
         counts = np.diff(ptr).astype(np.int64)
         if row_end is None:
