@@ -48,7 +48,7 @@
 namespace cals {
 
 constexpr int kTcKC = 64;                       // slice rows per chunk (two K-steps of 32)
-constexpr int kTcCW = 16;                       // digit-pass warps
+constexpr int kTcCW = 8;                        // digit-pass warps
 constexpr int kTcRW = kTcKC / kTcCW;            // slice rows per digit-pass warp per chunk (4)
 constexpr int kTcLPR = 32 / kTcRW;              // lanes per slice row (8)
 constexpr int kTcNG = 64 / (4 * kTcLPR);        // groups of 4 columns per lane (2)
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
     const int nf = A.nf, gs = nf + 1;
     const bool want_rss = A.rss_rows != nullptr;
     // tracing (tc_debug 3): CTA 0 of the first launch after the buffer was cleared
-    const bool trace = dbg == 8 && blockIdx.x == 0 && A.stats != nullptr && A.stats[49150] == A.stats[49149];
+    const bool trace = (dbg & 8) && blockIdx.x == 0 && A.stats != nullptr && A.stats[49150] == A.stats[49149];
     const uint32_t sbase = tc::smem_addr(smem);
     unsigned char* digits = smem + TcSmem::digits;
     double* xchg = reinterpret_cast<double*>(smem + TcSmem::xchg);
@@ -493,12 +493,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
         const int krel = kTcRW * warp + kl;  // slice row of this lane within the chunk
         // row-major staging (256 bytes per slice row): the 8 lanes of a row copy and read one
         // contiguous 128-byte segment per group (one shared-memory wavefront each way)
-        const uint32_t sx_lane = sbase + TcSmem::stage_x + (uint32_t)krel * 256u + 16u * (uint32_t)fql;
+        const uint32_t sx_lane = sbase + TcSmem::stage_x + (uint32_t)krel * 256u;
         // index ring: the slice-row ids and ratings of chunk t in slot t % kTcRing, copied 2 kTcAhead
         // chunks ahead by the row's first lane (so the gathers never wait on an index load)
         const uint32_t ring_idx = sbase + TcSmem::ring + 4u * (uint32_t)krel;
         const uint32_t ring_val = ring_idx + kTcRing * kTcKC * 4;
-        auto seg = [&](int g) { return 128u * (uint32_t)g; };
+        // 16-byte segment (kLPR g + fql) of the row; with fewer than 8 lanes per row, odd rows
+        // swap 64-byte halves so the rows sharing a quarter-warp phase hit different banks
+        auto seg = [&](int g) {
+            const uint32_t sg = (uint32_t)(kTcLPR * g + fql) ^ (kTcLPR < 8 ? (uint32_t)(krel & 1) * 4u : 0u);
+            return 16u * sg;
+        };
         // digit-store offsets of this lane within a tile set: K part (its slice row) + MN part
         // (its first column, per stacked level half); group g adds 1024 bytes (32 columns)
         const uint32_t kk = (uint32_t)(krel & 31);
@@ -662,7 +667,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
                 for (int L = 1; L <= 4; ++L) {
                     const uint32_t w = lev[g][L - 1] & zero_row;
                     const uint32_t pair = (uint32_t)((L - 1) >> 1), half = (uint32_t)((L - 1) & 1);
-                    const uint32_t gofs = 1024u * (uint32_t)g;  // 32 columns = 2 MN core groups
+                    const uint32_t gofs = 128u * kTcLPR * (uint32_t)g;  // 4 kLPR columns further
                     sts_u32(dbase + 2 * kTcATile + pair * kTcBTile + (half ? off_b1 : off_b0) + gofs, w);
                     sts_u32(dbase + pair * kTcATile + (half ? off_a1 : off_a0) + gofs, w & km[g]);
                 }
@@ -700,7 +705,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
     tc::fence_before();
     __syncthreads();
     if (warp == 0) tc::tmem_free<512>(tmem);
-    if (dbg == 8 && blockIdx.x == 0 && tid == 0 && A.stats != nullptr) A.stats[49150] += 1ull;
+    if ((dbg & 8) && blockIdx.x == 0 && tid == 0 && A.stats != nullptr) A.stats[49150] += 1ull;
 }
 
 }  // namespace cals

@@ -26,7 +26,7 @@ buf = torch.zeros(49152, dtype=torch.int64, device="cuda")
 L = _lib.load()
 buf[49149] = launch
 L.cals_debug_stats(buf.data_ptr())
-_lib.set_tuning(tc_debug=8, serial_tiers=1)
+_lib.set_tuning(tc_debug=8 | int(os.environ.get("TC_DBG", "0")), serial_tiers=1)
 eng.half(side)
 torch.cuda.synchronize()
 L.cals_debug_stats(None)
