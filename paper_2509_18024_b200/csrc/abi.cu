@@ -116,6 +116,13 @@ size_t big_gram_smem(int nf, int chunk, int gwords = 0) {
            align16((size_t)nf * (chunk / 32) * 4 + lists + (size_t)chunk * gwords * 4) + g64;
 }
 
+// rows per staging buffer of the pipelined scan (two buffers; each thread counts <= 32 rows)
+// (one row per thread and copy: at most kThreads rows)
+int scan_chunk(int nf) {
+    const int ch = big_chunk(nf);
+    return std::min(kThreads, nf >= 32 ? std::max(32, ch / 2) : ch);
+}
+
 size_t big_scan_smem(int nf, int chunk) {
     return align16((size_t)chunk * xs_stride(nf) * 4) + align16((size_t)nf * kHB * 4);
 }
@@ -277,7 +284,8 @@ struct Work {
     uint64_t* thr_all;  // [n_rows][nf] selection thresholds (when the caller asks for none)
     float* tc_scale;    // [65] tensor-core Gram digit scales 2^(32 - E) (64 columns + ratings)
     double* tc_alpha;   // [65] 2^E
-    int* item_ctr;      // big_gram_tc work-item counter
+    int* item_ctr;      // big_gram_tc / big_scan2 work-item counter
+    int* icnt;          // [tiles][nf] per-item in-bracket counts (big_scan2)
     int* rf_cnt;        // [4]: per stream, rows deferred to the float64 refinement from the stored
     int64_t* rf_list;   // equations [2][gbuf_rows] (row << 32 | slot), and from the slice:
     int32_t* rs_list;   // [2][n_rows] rows
@@ -298,6 +306,7 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
     w.part = c.take<double>((size_t)bb.max_tiles * nf * (nf + 1));
     w.rss_part = c.take<double>((size_t)bb.max_tiles);
     w.hist = c.take<int>((size_t)bb.max_rows * nf * kHB);
+    w.icnt = c.take<int>((size_t)std::max<int64_t>(bb.max_tiles, 1) * nf);
     w.brk = c.take<uint32_t>((size_t)std::max<int64_t>(P->n_big, 1) * nf);  // all big rows (one calibration pass)
     w.fcnt = c.take<int>((size_t)bb.max_rows * nf);                      // fast_core: kept counts (multi-item rows)
     w.famax = c.take<unsigned long long>((size_t)bb.max_rows * nf);      // fast_core: fallback keys
@@ -607,6 +616,7 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
         B.part = w.part;
         B.rss_part = w.rss_part;
         B.hist = w.hist;
+        B.icnt = w.icnt;
         B.brk = w.brk + (size_t)r0 * nf;
         B.tile_row = P->big_tile_row;
         B.row_base = r0;
@@ -619,11 +629,24 @@ int launch_big(const SweepArgs& A, const cals_plan* P, const Work& w, cudaStream
             while (n_calib < B.n_big && tp[r0 + n_calib + 1] - tp[r0 + n_calib] >= 2) ++n_calib;
         B.n_multi = tp ? n_calib : B.n_big;  // without host offsets every row takes the partial path
         cudaMemsetAsync(w.hist, 0, sizeof(int) * (size_t)B.n_big * nf * kHB, st);
-        const size_t scan_smem = big_scan_smem(nf, B.chunk);
-        allow_smem(big_scan_kernel);
         {
-            ProfScope ps("big_scan_kernel", st);
-            big_scan_kernel<<<grid_for(big_scan_kernel, scan_smem, B.n_tiles), kThreads, scan_smem, st>>>(A, B);
+            // pipelined scan: two staging buffers of scan_chunk rows, items claimed from a counter
+            BigArgs S = B;
+            S.chunk = scan_chunk(nf);
+            S.item_ctr = w.item_ctr;
+            S.icnt = w.icnt;
+            cudaMemsetAsync(w.item_ctr, 0, sizeof(int), st);
+            const size_t scan_smem = 2 * align16((size_t)S.chunk * xs_stride(nf) * 4) + align16((size_t)nf * kHB * 4);
+            ProfScope ps("big_scan2_kernel", st);
+            if (nf == 64 && S.chunk == 64 && xs_stride(nf) == 68) {
+                allow_smem(big_scan2_kernel<4, 68, 64>);
+                big_scan2_kernel<4, 68, 64><<<grid_for(big_scan2_kernel<4, 68, 64>, scan_smem, B.n_tiles), kThreads,
+                                               scan_smem, st>>>(A, S);
+            } else {
+                allow_smem(big_scan2_kernel<0, 0, 0>);
+                big_scan2_kernel<0, 0, 0><<<grid_for(big_scan2_kernel<0, 0, 0>, scan_smem, B.n_tiles), kThreads,
+                                             scan_smem, st>>>(A, S);
+            }
         }
         {
             const int64_t warps = B.n_big * nf;

@@ -4,9 +4,9 @@
 //
 // A big row is cut into work items of `item_rows` slice rows, processed in
 // shared-memory chunks.  Per half-sweep:
-//   big_scan     counts per column above / inside the table bracket, a
+//   big_scan2    counts per column above / inside the table bracket, a
 //                32-bucket histogram of the bracket, and appends the
-//                bracket's keys to a per-(row, column) list
+//                bracket's keys to a per-(row, column) list (one share per item)
 //   big_resolve  one warp per (row, column): the histogram names the bucket
 //                holding the target rank, one filtering pass keeps its keys,
 //                a warp select finishes (or an exact whole-column search if
@@ -111,23 +111,55 @@ __global__ void __launch_bounds__(kThreads) big_calib_kernel(SweepArgs A, BigArg
     }
 }
 
-__global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs B) {
+// Tiled tier pass 1, pipelined: persistent CTAs claim work items from a counter
+// (B.item_ctr, zeroed before the launch; longest rows first), each item's slice is
+// streamed in chunks of B.chunk rows through two shared-memory buffers (the bulk
+// copies of chunk i+1 are in flight while chunk i is counted; slice-row ids are loaded
+// a chunk earlier still), and the count pass is compiled for the headline shape (PER
+// threads per column, row stride SXT floats, KCT-row chunks) without bounds checks on
+// full chunks.  An item writes its in-bracket keys into its own equal share of the
+// row's column region (cand_item_cap), reserving positions with shared-memory
+// counters: no global atomics per chunk and one block barrier per chunk.  Per (row,
+// column) outputs: count above the bracket, the in-bracket
+// histogram and total, and per item its in-bracket count (B.icnt; a share that
+// overflowed sends that column to big_resolve's exact search).
+template <int PER, int SXT, int KCT>
+__global__ void __launch_bounds__(kThreads) big_scan2_kernel(SweepArgs A, BigArgs B) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ int s_above[CALS_MAX_NF_DEV], s_base[CALS_MAX_NF_DEV], s_slot[CALS_MAX_NF_DEV];
+    __shared__ int s_above[CALS_MAX_NF_DEV], s_pos[CALS_MAX_NF_DEV];
     __shared__ uint32_t s_hib[CALS_MAX_NF_DEV], s_lob[CALS_MAX_NF_DEV];
-    __shared__ __align__(8) unsigned long long s_mbar;
-    const uint32_t mbar = smem_u32(&s_mbar);
-    uint32_t phase = 0;
-    if (threadIdx.x == 0) mbar_init(mbar, 1);
-    __syncthreads();
+    __shared__ __align__(8) unsigned long long s_mbar[2];
+    __shared__ int s_item;
     const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x;
-    const int sx = xs_stride(nf);
-    float* Xs = reinterpret_cast<float*>(smem);
-    int* s_hist = reinterpret_cast<int*>(smem + align16((size_t)B.chunk * sx * 4));  // [nf][kHB]
-    const uint32_t s_xs = smem_u32(Xs);
+    const int sx = SXT > 0 ? SXT : xs_stride(nf);
+    const int per = PER > 0 ? PER : nt / nf;  // threads per column
+    const int KC = KCT > 0 ? KCT : B.chunk;   // staged slice rows per buffer (<= blockDim.x)
     const uint32_t rowb = 4u * (uint32_t)sx;
-    const FastDiv fq((uint32_t)xs_chunks(nf));
-    for (int64_t t = blockIdx.x; t < B.n_tiles; t += gridDim.x) {
+    const uint32_t bufb = (uint32_t)align16((size_t)KC * sx * 4);
+    const uint32_t s_xs = smem_u32(smem);
+    int* s_hist = reinterpret_cast<int*>(smem + 2 * (size_t)bufb);  // [nf][kHB]
+    const uint32_t rowbytes = 16u * (uint32_t)xs_chunks(nf);
+    if (tid == 0) {
+        mbar_init(smem_u32(&s_mbar[0]), 1);
+        mbar_init(smem_u32(&s_mbar[1]), 1);
+    }
+    __syncthreads();
+    uint32_t phases = 0u;  // bit b: parity of buffer b's barrier
+    const int c = tid % nf, j = tid / nf;
+    const bool col_thread = tid < per * nf;
+    // chunk rows into buffer b: every thread copies its row (id in `rid`)
+    auto stage = [&](int b, int kn, int rid) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // prior generic reads of the buffer
+        if (tid == 0) mbar_expect_tx(smem_u32(&s_mbar[b]), (uint32_t)kn * rowbytes);
+        if (tid < kn) bulk_g2s(s_xs + (uint32_t)b * bufb + (uint32_t)tid * rowb, A.src + (int64_t)rid * A.ld_src,
+                               rowbytes, smem_u32(&s_mbar[b]));
+    };
+    for (;;) {
+        __syncthreads();  // previous item done with s_item, buffers, counters, histogram
+        if (tid == 0) s_item = atomicAdd(B.item_ctr, 1);
+        __syncthreads();
+        const int64_t t = s_item;
+        if (t >= B.n_tiles) break;
         const int64_t T_abs = B.tile_base + t;
         const int r = B.tile_row != nullptr ? (int)(__ldg(B.tile_row + T_abs) - B.row_base)
                                             : find_row(B.tile_ptr, B.n_big, T_abs);
@@ -136,76 +168,95 @@ __global__ void __launch_bounds__(kThreads) big_scan_kernel(SweepArgs A, BigArgs
         const int n = (int)(A.ptr[row + 1] - lo);
         const int s = A.budget[row];
         if (s >= n) continue;  // complete sketch: nothing to select (uniform per block)
-        const int kbeg = (int)(T_abs - B.tile_ptr[r]) * B.item_rows;
+        const int t_loc = (int)(T_abs - B.tile_ptr[r]);
+        const int kbeg = t_loc * B.item_rows;
         const int kend = min(n, kbeg + B.item_rows);
-        __syncthreads();
+        const int32_t* idx = A.idx + lo;
+        const int kn0 = min(KC, kend - kbeg);
+        const int rid0 = tid < kn0 ? __ldg(idx + kbeg + tid) : 0;
         if (tid < nf) {
             uint32_t hib, lob;
             big_bracket(A, B, r, tid, n, s, hib, lob);
             s_hib[tid] = hib;
             s_lob[tid] = lob;
             s_above[tid] = 0;
+            s_pos[tid] = 0;
         }
         for (int e = tid; e < nf * kHB; e += nt) s_hist[e] = 0;
-        const int64_t cbase = B.cand_ptr[r] - B.cand_base;
         const int capB = (int)((B.cand_ptr[r + 1] - B.cand_ptr[r]) / nf);
-        for (int k0 = kbeg; k0 < kend; k0 += B.chunk) {
-            const int kn = min(B.chunk, kend - k0);
-            __syncthreads();
-            if (xs_chunks(nf) >= 16) stage_slice_bulk(A, lo, k0, kn, s_xs, nullptr, mbar, phase);
-            else stage_slice(A, lo, k0, kn, Xs, nullptr, fq);
-            if (tid < nf) s_slot[tid] = 0;
-            __syncthreads();
-            const int per = nt / nf;  // threads per column; each scans <= 32 rows (big_chunk)
-            int my_in = 0, my_above = 0;
-            uint32_t inmask = 0;      // bit i: row j + i * per is inside the bracket
-            const int c = tid % nf, j = tid / nf;
-            if (tid < per * nf) {
+        const int capI = cand_item_cap(capB, (int)(B.tile_ptr[r + 1] - B.tile_ptr[r]));
+        uint64_t* cl = B.cand + (B.cand_ptr[r] - B.cand_base) + (int64_t)c * capB + (int64_t)t_loc * capI;
+        stage(0, kn0, rid0);
+        const int kn1_0 = kbeg + KC < kend ? min(KC, kend - kbeg - KC) : 0;
+        int rid_next = tid < kn1_0 ? __ldg(idx + kbeg + KC + tid) : 0;  // chunk 1's row
+        int my_above = 0;
+        int ci = 0;
+        for (int k0 = kbeg; k0 < kend; k0 += KC, ++ci) {
+            const int b = ci & 1;
+            const int kn = min(KC, kend - k0);
+            const int k1 = k0 + KC, kn1 = k1 < kend ? min(KC, kend - k1) : 0;
+            const int k2 = k1 + KC, kn2 = k2 < kend ? min(KC, kend - k2) : 0;
+            const int rid2 = tid < kn2 ? __ldg(idx + k2 + tid) : 0;  // two chunks ahead
+            mbar_wait(smem_u32(&s_mbar[b]), (phases >> b) & 1u);
+            phases ^= 1u << b;
+            __syncthreads();  // chunk ci landed for every thread; buffer b^1 free (chunk ci-1 emitted)
+            if (kn1 > 0) stage(b ^ 1, kn1, rid_next);
+            rid_next = rid2;
+            const uint32_t xb = s_xs + (uint32_t)b * bufb;
+            uint32_t inmask = 0;  // bit i: row j + i * per is inside the bracket
+            if (col_thread) {
                 const uint32_t hib = s_hib[c], lob = s_lob[c], span = hib - lob;
-                const uint32_t colb = s_xs + 4u * (uint32_t)c + (uint32_t)j * rowb, stepb = (uint32_t)per * rowb;
-                // branchless count pass (a warp spans 32 columns: any per-element branch
-                // would be taken by some lane almost always)
+                const uint32_t colb = xb + 4u * (uint32_t)c + (uint32_t)j * rowb;
+                if (KCT > 0 && kn == KCT) {
+                    // full chunk, compile-time row stride: immediate-offset loads, no bounds checks
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int k = j + i * per;
-                    const uint32_t a = k < kn ? abs_bits(lds_f32(colb + (uint32_t)i * stepb)) : 0u;
-                    my_above += (k < kn && a >= hib) ? 1 : 0;
-                    inmask |= (k < kn && a - lob < span) ? (1u << i) : 0u;
+                    for (int i = 0; i < KCT / PER; ++i) {
+                        const uint32_t a = abs_bits(lds_f32(colb + (uint32_t)(i * PER * SXT * 4)));
+                        my_above += a >= hib ? 1 : 0;
+                        inmask |= (a - lob < span) ? (1u << i) : 0u;
+                    }
+                } else {
+                    const int rows_t = (KC + per - 1) / per;
+                    const uint32_t stepb = (uint32_t)per * rowb;
+#pragma unroll 8
+                    for (int i = 0; i < rows_t; ++i) {
+                        const int k = j + i * per;
+                        const uint32_t a = k < kn ? abs_bits(lds_f32(colb + (uint32_t)i * stepb)) : 0u;
+                        my_above += (k < kn && a >= hib) ? 1 : 0;
+                        inmask |= (k < kn && a - lob < span) ? (1u << i) : 0u;
+                    }
                 }
-                my_in = __popc(inmask);
-                atomicAdd(&s_above[c], my_above);
-                if (my_in) atomicAdd(&s_slot[c], my_in);
-            }
-            __syncthreads();
-            if (tid < nf) {
-                const int cnt_c = s_slot[tid];
-                s_base[tid] = cnt_c ? atomicAdd(&B.cnt[((size_t)r * nf + tid) * 2 + 1], cnt_c) : 0;
-                s_slot[tid] = 0;
-            }
-            __syncthreads();
-            if (tid < per * nf && my_in) {
-                // one slot reservation per thread, then its keys in a contiguous run
-                uint64_t* cl = B.cand + cbase + (int64_t)c * capB;
-                int pos = s_base[c] + atomicAdd(&s_slot[c], my_in);
-                const uint32_t lob = s_lob[c];
-                const int sh = hb_shift(s_hib[c] - lob);
-                while (inmask) {
-                    const int i = __ffs(inmask) - 1;
-                    inmask &= inmask - 1;
-                    const int k = j + i * per;
-                    const float x = lds_f32(s_xs + (uint32_t)k * rowb + 4u * c);
-                    atomicAdd(&s_hist[c * kHB + (int)((abs_bits(x) - lob) >> sh)], 1);
-                    if (pos < capB) cl[pos] = make_key(x, (uint32_t)(k0 + k));
-                    ++pos;
+                const int my_in = __popc(inmask);
+                if (my_in) {
+                    // a contiguous run in the item's share of the column region
+                    int pos = atomicAdd(&s_pos[c], my_in);
+                    const uint32_t lob2 = lob;
+                    const int sh = hb_shift(span);
+                    while (inmask) {
+                        const int i = __ffs(inmask) - 1;
+                        inmask &= inmask - 1;
+                        const int k = j + i * per;
+                        const float x = lds_f32(xb + (uint32_t)k * rowb + 4u * c);
+                        atomicAdd(&s_hist[c * kHB + (int)((abs_bits(x) - lob2) >> sh)], 1);
+                        if (pos < capI) cl[pos] = make_key(x, (uint32_t)(k0 + k));
+                        ++pos;
+                    }
                 }
             }
         }
+        if (col_thread && my_above) atomicAdd(&s_above[c], my_above);
         __syncthreads();
-        if (tid < nf && s_above[tid]) atomicAdd(&B.cnt[((size_t)r * nf + tid) * 2], s_above[tid]);
+        if (tid < nf) {
+            if (s_above[tid]) atomicAdd(&B.cnt[((size_t)r * nf + tid) * 2], s_above[tid]);
+            if (s_pos[tid]) atomicAdd(&B.cnt[((size_t)r * nf + tid) * 2 + 1], s_pos[tid]);
+            B.icnt[(size_t)t * nf + tid] = s_pos[tid];
+        }
         for (int e = tid; e < nf * kHB; e += nt)
             if (s_hist[e]) atomicAdd(&B.hist[(size_t)r * nf * kHB + e], s_hist[e]);
     }
 }
+template __global__ void big_scan2_kernel<4, 68, 64>(SweepArgs, BigArgs);
+template __global__ void big_scan2_kernel<0, 0, 0>(SweepArgs, BigArgs);
 
 __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigArgs B) {
     const int nf = A.nf;
@@ -249,7 +300,15 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
             uint32_t hib, lob;
             big_bracket(A, B, r, c, n, s, hib, lob);
             const uint64_t hik = hi_key_of(hib), lok = (uint64_t)lob << 32;
-            if (above < s && s <= above + in && in <= capB && lok < hik) {
+            // the column's keys: one contiguous list, or (scan2, multi-item rows) one share per item
+            const int n_items = (int)(B.tile_ptr[r + 1] - B.tile_ptr[r]);
+            const int capI = B.icnt != nullptr ? cand_item_cap(capB, n_items) : capB;
+            const int64_t t0 = B.tile_ptr[r] - B.tile_base;  // batch-relative first item of the row
+            const int nseg = B.icnt != nullptr ? n_items : 1;
+            bool seg_over = false;
+            if (B.icnt != nullptr)
+                for (int q = 0; q < nseg; ++q) seg_over |= B.icnt[(size_t)(t0 + q) * nf + c] > capI;
+            if (above < s && s <= above + in && in <= capB && !seg_over && lok < hik) {
                 // bucket holding the target rank: inclusive scan of the histogram from the top
                 const int need = s - above;
                 const int bl = kHB - 1 - lane;  // lane 0 = highest bucket
@@ -273,17 +332,20 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
                 int m = 0;
                 bool spill = false;
                 uint64_t v = 0ull;
-                for (int i0 = 0; i0 < in; i0 += 128) {
+                for (int q = 0; q < nseg; ++q) {
+                const int cnt_q = B.icnt != nullptr ? B.icnt[(size_t)(t0 + q) * nf + c] : in;
+                const uint64_t* sl = cl + (int64_t)q * capI;
+                for (int i0 = 0; i0 < cnt_q; i0 += 128) {
                     uint64_t kk[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int i = i0 + 32 * u + lane;
-                        kk[u] = i < in ? cl[i] : 0ull;
+                        kk[u] = i < cnt_q ? sl[i] : 0ull;
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int i = i0 + 32 * u + lane;
-                        const bool keep = i < in && kk[u] >= blo && kk[u] < bhi;
+                        const bool keep = i < cnt_q && kk[u] >= blo && kk[u] < bhi;
                         const uint32_t bal = __ballot_sync(CALS_FULL_MASK, keep);
                         const int cnt = __popc(bal);
                         if (!spill && m + cnt <= 32) {
@@ -302,6 +364,7 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
                         }
                         m += cnt;
                     }
+                }
                 }
                 __syncwarp();
                 if (lane == 0) stat_add(A, kStBigColumns, 1);

@@ -101,8 +101,14 @@ struct BigArgs {
     float calib_z;
     int* fcnt;                // [n_big][nf] kept slice rows per column (multi-item rows)
     unsigned long long* famax;  // [n_big][nf] max key (abs_bits << 32 | ~k) per column (fallback row)
-    int* item_ctr;            // big_gram_tc: next unclaimed work item (zeroed before the launch)
+    int* item_ctr;            // big_gram_tc / big_scan2: next unclaimed work item (zeroed before the launch)
+    int* icnt;                // [n_tiles][nf] in-bracket keys of each work item (big_scan2): a multi-item
+                              // row's column region is split into equal per-item sub-regions
 };
+
+// Candidate sub-region of work item t_local (0-based within its row) of a row with
+// n_items items, in a column region of capB keys.
+__host__ __device__ inline int cand_item_cap(int capB, int n_items) { return capB / max(n_items, 1); }
 
 constexpr int kHB = 32;  // sub-buckets of a big row's bracket (linear in abs-bit space)
 
