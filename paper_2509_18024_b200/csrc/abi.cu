@@ -337,13 +337,17 @@ void launch_refine(const SweepArgs& A, cudaStream_t st, bool from_slice) {
     const int* cnt = from_slice ? A.rs_cnt : A.rf_cnt;
     const void* list = from_slice ? static_cast<const void*>(A.rs_list) : static_cast<const void*>(A.rf_list);
     // the per-batch list is usually empty (long rows rarely defer): one CTA per SM keeps that launch cheap
-    const int per_sm = from_slice ? (refine_threads(A.nf) == 256 ? 4 : 2) : 1;
-    if (refine_threads(A.nf) == 256) {
-        allow_smem(refine_kernel<256>);
-        refine_kernel<256><<<dev().sms * per_sm, 256, sm, st>>>(A, cnt, list, from_slice ? 1 : 0);
+    const int fs = from_slice ? 1 : 0;
+    if (A.nf > 64) {  // every system: register-blocked elimination (one 256-thread CTA per SM)
+        allow_smem(refine_rb_kernel<128>);
+        refine_rb_kernel<128><<<dev().sms, 256, sm, st>>>(A, cnt, list, fs);
+    } else if (A.nf > 32) {
+        allow_smem(refine_rb_kernel<64>);
+        refine_rb_kernel<64><<<dev().sms * (from_slice ? 2 : 1), 256, sm, st>>>(A, cnt, list, fs);
     } else {
-        allow_smem(refine_kernel<512>);
-        refine_kernel<512><<<dev().sms * per_sm, 512, sm, st>>>(A, cnt, list, from_slice ? 1 : 0);
+        const int per_sm = from_slice ? 4 : 1;
+        allow_smem(refine_kernel<256>);
+        refine_kernel<256><<<dev().sms * per_sm, 256, sm, st>>>(A, cnt, list, fs);
     }
     cudaMemsetAsync(const_cast<int*>(cnt), 0, sizeof(int), st);
 }

@@ -11,6 +11,16 @@ reason = sys.argv[2] if len(sys.argv) > 2 else "stall_long_sb"
 ntop = int(sys.argv[3]) if len(sys.argv) > 3 else 12
 det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(det)))
+# the longest captured launch
+dur = {}
+for r in rows[1:]:
+    d0 = dict(zip(rows[0], r))
+    if d0.get("Metric Name") == "Duration":
+        v = float(d0["Metric Value"].replace(",", ""))
+        dur[d0["ID"]] = v * (1000.0 if d0["Metric Unit"] == "ms" else (1e-3 if d0["Metric Unit"] == "ns" else 1.0))
+LID = max(dur, key=dur.get) if dur else "0"
+print("launch", LID, "of", len(dur))
+rows = [rows[0]] + [r for r in rows[1:] if dict(zip(rows[0], r)).get("ID") == LID]
 want = ["Duration", "DRAM Throughput", "L2 Cache Throughput", "Issue Slots Busy", "Executed Instructions", "L2 Hit Rate",
         "No Eligible", "Elapsed Cycles", "Achieved Active Warps Per SM", "Registers Per Thread"]
 h = rows[0]
@@ -20,12 +30,15 @@ for r in rows[1:]:
         print(f"{d['Metric Name']:<30} {d['Metric Value']} {d['Metric Unit']}")
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(io.StringIO(raw)))
-d = dict(zip(rr[0], rr[2] if len(rr) > 2 else rr[1]))
+idx = [i for i, r in enumerate(rr) if i >= 2 and dict(zip(rr[0], r)).get("ID") == LID] or [2 if len(rr) > 2 else 1]
+d = dict(zip(rr[0], rr[idx[0]]))
 st = [(k.replace("smsp__pcsamp_warps_issue_stalled_", ""), float(v.replace(",", "") or 0)) for k, v in d.items()
       if "pcsamp_warps_issue_stalled" in k and not k.endswith("not_issued")]
 tot = sum(v for _, v in st) or 1
 print("stalls:", ", ".join(f"{k} {v / tot * 100:.0f}%" for k, v in sorted(st, key=lambda kv: -kv[1])[:9]))
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"], capture_output=True,
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass",
+                      "--launch-skip", LID, "--launch-count", "1"] if False else
+                     ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"], capture_output=True,
                      text=True).stdout
 fname, hdr = None, None
 agg, txt, allagg = collections.Counter(), {}, collections.Counter()
