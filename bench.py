@@ -128,50 +128,146 @@ def tier_bytes(side, n_f):
     return small, big
 
 
-def cpu_baseline_port(data_host, spec, M0, seconds):
-    """The float64 C oracle (a restatement of the reference algorithm) on ONE
-    host core: a row sample of one user half-sweep + one item half-sweep."""
+def measured_compute_peaks():
+    """Microbenchmarked compute peaks of this pool's B200s (tools/peaks.cu ->
+    profiles/r02_peaks.json): FFMA2 fp32, DFMA fp64, tcgen05 kind::i8."""
+    p = os.path.join(ROOT, "profiles", "r02_peaks.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as fh:
+        d = json.load(fh)
+    return {"ffma2_tflops": d.get("ffma2_tflops"), "dfma_tflops": d.get("dfma_tflops"),
+            "i8_tops": (d.get("i8_ss_m128_n256") or {}).get("tops")}
+
+
+def compute_terms(core, n_f, prof, steps):
+    """Pipe utilisation of the contraction kernels next to the HBM term: the
+    tensor-core Gram's executed int8 MMA work (3 MMAs of M=128 N=144 K=32 per 32
+    slice rows of the tiled tier) and its algorithmic Gram flops (2 n_f (n_f + 1)
+    s_i per row), and the solve's LU flops (2/3 n_f^3 per row) on FFMA."""
+    peaks = measured_compute_peaks()
+    out = {"peaks_measured": peaks}
+    ks, alg = 0, 0.0
+    n_sys = 0
+    for side in (core.user, core.item):
+        c = side.counts
+        big = side.big_host
+        if big.size:
+            ks += int(((c[big] + 31) // 32).sum())
+            b = side.budget_host[big].astype(np.float64)
+            alg += float((2.0 * n_f * (n_f + 1) * b).sum())
+        n_sys += int((c > 0).sum())
+    tc = prof.get("big_gram_tc_kernel")
+    if tc and tc[1] > 0 and ks:
+        ops = ks * 3 * 2 * 128 * 144 * 32 * steps
+        t = tc[1] / 1e3
+        out["big_gram_tc_kernel"] = {
+            "pipe": "tensor (tcgen05 kind::i8)", "executed_tops": ops / t / 1e12,
+            "peak_tops": peaks.get("i8_tops"),
+            "frac": (ops / t / 1e12 / peaks["i8_tops"]) if peaks.get("i8_tops") else None,
+            "algorithmic_tflops": alg * steps / t / 1e12,
+            "note": "dense digit MMAs (1/rate x the sketched work, 4 int8 levels); algorithmic = sparse float64 Gram"}
+    sv = prof.get("solve_kernel")
+    if sv and sv[1] > 0:
+        fl = n_sys * (2.0 / 3.0 * n_f ** 3 + 2.0 * n_f ** 2) * steps
+        out["solve_kernel"] = {"pipe": "fp32 FMA (SIMT)", "achieved_tflops": fl / (sv[1] / 1e3) / 1e12,
+                               "peak_tflops": peaks.get("ffma2_tflops"),
+                               "frac": (fl / (sv[1] / 1e3) / 1e12 / peaks["ffma2_tflops"])
+                               if peaks.get("ffma2_tflops") else None}
+    return out
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def stratified_cpu_rate(R, spec, M0, threads, seconds, seed=0, n_strata=8):
+    """Time the reference algorithm's CPU path (the float64 C oracle port) on a bounded
+    sample of one full iteration and extrapolate to the whole workload.
+
+    Per side, rows (n > 0) are ordered by length and cut into n_strata strata holding
+    equal shares of the ratings; each stratum gets an equal slice of the time budget,
+    its largest rows first (so every side's giant rows are in the sample: one per
+    thread in stratum 0) and then random rows of the stratum.  The side's time is
+    sum_s nnz_s * (t_s / sampled_nnz_s).  Returns (ratings/s/iter, details)."""
     import oracle
 
     n_f, lam, rate = spec["n_f"], spec["lam"], spec["rate"]
-    R = data_host
-    rng = np.random.default_rng(0)
-    U = np.zeros((R.n_users, n_f))
+    rng = np.random.default_rng(seed)
+    # the item half-sweep's source: user rows as a user half-sweep leaves them (nonzero; an
+    # all-zero source would make every key tie and the reference's quickselect quadratic)
+    U = np.random.default_rng(12345).normal(0.0, 0.3, (R.n_users, n_f)).astype(np.float32).astype(np.float64)
     M = M0.astype(np.float64)
-    done_ratings, t_used = 0, 0.0
-    for side, ptr, idx, val, src, tgt in (("user", R.row_ptr, R.row_items, R.row_vals, M, U),
-                                          ("item", R.col_ptr, R.col_users, R.col_vals, None, None)):
-        if side == "item":
-            src, tgt = U, M.copy()
+    est_s, wall, sampled = 0.0, 0.0, 0
+    per_stratum = seconds / (2.0 * n_strata)
+    for side in ("user", "item"):
+        ptr, idx, val = (R.row_ptr, R.row_items, R.row_vals) if side == "user" else (R.col_ptr, R.col_users, R.col_vals)
+        src, tgt = (M, U.copy()) if side == "user" else (U, M.copy())
         counts = np.diff(ptr)
-        rows = rng.permutation(np.flatnonzero(counts > 0)).astype(np.int32)
-        budget = seconds / 2.0
-        pos = 0
-        t0 = time.perf_counter()
-        chunk = 64
-        while pos < rows.size and time.perf_counter() - t0 < budget:
-            sl = rows[pos:pos + chunk]
-            oracle.core_half_sweep(ptr, idx, val, src, n_f, lam, rate, tgt, want_rss=(side == "item"), rows=sl,
-                                   threads=1)
-            done_ratings += int(counts[sl].sum())
-            pos += sl.size
-            chunk = min(chunk * 2, 4096)
-        t_used += time.perf_counter() - t0
-    return {"value": done_ratings / t_used / 2.0 if t_used > 0 else 0.0, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"random row sample of one user + one item half-sweep ({done_ratings} slice ratings, "
-                      f"{t_used:.1f} s), float64 C oracle port, 1 thread; ratings/s/iter = sampled ratings / "
-                      f"time / 2 sides"}
+        order = np.argsort(-counts, kind="stable")
+        order = order[counts[order] > 0].astype(np.int32)
+        cum = np.cumsum(counts[order])
+        total = int(cum[-1]) if cum.size else 0
+        cuts = np.searchsorted(cum, np.linspace(0, total, n_strata + 1)[1:-1], side="right")
+        bounds = [0, *[int(c) for c in cuts], order.size]
+        for s in range(n_strata):
+            lo, hi = bounds[s], bounds[s + 1]
+            if hi <= lo:
+                continue
+            rows_s = order[lo:hi]
+            head = rows_s[:threads]
+            tail = rng.permutation(rows_s[threads:])
+            seq = np.concatenate([head, tail])
+            nnz_s = int(counts[rows_s].sum())
+            done, t_s, pos = 0, 0.0, 0
+            chunk = max(threads, 1)
+            while pos < seq.size and (t_s < per_stratum or done == 0):
+                sl = seq[pos:pos + chunk]
+                t0 = time.perf_counter()
+                oracle.core_half_sweep(ptr, idx, val, src, n_f, lam, rate, tgt, want_rss=(side == "item"), rows=sl,
+                                       threads=threads)
+                t_s += time.perf_counter() - t0
+                done += int(counts[sl].sum())
+                pos += sl.size
+                chunk = min(chunk * 2, 64 * max(threads, 1))
+            est_s += nnz_s * (t_s / done)
+            print(f"  [cpu sample] {side} stratum {s}: {done} of {nnz_s} ratings in {t_s:.2f} s", file=sys.stderr,
+                  flush=True)
+            wall += t_s
+            sampled += done
+    value = float(len(R.row_vals)) / est_s if est_s > 0 else 0.0
+    return value, {"estimated_s_per_iter": est_s, "sample_wall_s": wall, "sampled_ratings": sampled,
+                   "strata": n_strata}
+
+
+def cpu_baseline_port(data_host, spec, M0, seconds):
+    """The float64 C oracle (a restatement of the reference algorithm) on ONE host core,
+    on a stratified sample of one iteration (stratified_cpu_rate)."""
+    value, det = stratified_cpu_rate(data_host, spec, M0, 1, seconds)
+    return {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "cpu_model": cpu_model(),
+            "sample": (f"nnz-stratified row sample of one user + one item half-sweep (8 strata per side, largest rows "
+                       f"first), {det['sampled_ratings']} slice ratings in {det['sample_wall_s']:.1f} s measured; "
+                       f"float64 C oracle port, 1 thread; extrapolated {det['estimated_s_per_iter']:.0f} s per "
+                       f"iteration")}
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm's CPU path (oracle port) with
-    all host threads, each step = one bounded row sample of a full iteration."""
+    """--impl reference: the reference algorithm's CPU path (the float64 C oracle port; the
+    reference itself is Python+numba and does not travel to the GPU box) with all host
+    threads; each step is a bounded nnz-stratified sample of one full iteration
+    (stratified_cpu_rate), extrapolated to the whole workload (labelled as such)."""
     import torch
 
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import oracle
     from paper_2509_18024_b200 import synth
 
     spec = dict(synth.CONFIGS[args.config])
@@ -180,42 +276,40 @@ def run_reference(args):
     M0 = synth.init_m(R.n_items, spec["n_f"]).astype(np.float64)
     threads = os.cpu_count() or 1
     n_f, lam, rate = spec["n_f"], spec["lam"], spec["rate"]
-    rng = np.random.default_rng(1)
-    budget = max(5.0, 60.0 / max(args.steps + args.warmup, 1))
-    U = np.zeros((R.n_users, n_f))
-    M = M0.copy()
-    rates = []
+    budget = max(8.0, 120.0 / max(args.steps + args.warmup, 1))
+    rates, walls, ests, sampled = [], [], [], []
     for step in range(args.warmup + args.steps):
-        done, t_used = 0, 0.0
-        for side in ("user", "item"):
-            ptr, idx, val = (R.row_ptr, R.row_items, R.row_vals) if side == "user" else (R.col_ptr, R.col_users, R.col_vals)
-            src, tgt = (M, U) if side == "user" else (U, M)
-            counts = np.diff(ptr)
-            rows = rng.permutation(np.flatnonzero(counts > 0)).astype(np.int32)
-            pos, chunk = 0, 256 * threads
-            t0 = time.perf_counter()
-            while pos < rows.size and time.perf_counter() - t0 < budget / 2:
-                sl = rows[pos:pos + chunk]
-                oracle.core_half_sweep(ptr, idx, val, src, n_f, lam, rate, tgt, want_rss=(side == "item"), rows=sl,
-                                       threads=threads)
-                done += int(counts[sl].sum())
-                pos += sl.size
-            t_used += time.perf_counter() - t0
+        v, det = stratified_cpu_rate(R, spec, M0, threads, budget, seed=step)
         if step >= args.warmup:
-            rates.append(done / t_used / 2.0)
+            rates.append(v)
+            walls.append(det["sample_wall_s"])
+            ests.append(det["estimated_s_per_iter"])
+            sampled.append(det["sampled_ratings"])
     value = float(np.median(rates))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": data.nnz / value * 1e3,
+        "ms_per_step_is": "extrapolated from the stratified sample (see cpu_baseline)",
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "nnz": data.nnz, "n_users": R.n_users, "n_items": R.n_items,
                    "n_f": n_f, "lam": lam, "rate": rate},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"per step a random row sample of both half-sweeps, {budget:.0f} s of "
-                                   f"{threads}-thread float64 C oracle work; ms_per_step extrapolated to all rows"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+                         "sample": (f"per step an nnz-stratified row sample of both half-sweeps (8 strata per side, "
+                                    f"largest rows first), {budget:.0f} s budget of {threads}-thread float64 C "
+                                    f"oracle work; measured sample wall {np.median(walls):.1f} s over "
+                                    f"{int(np.median(sampled))} ratings per step, extrapolated "
+                                    f"{np.median(ests):.1f} s per full iteration")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+T_START = time.perf_counter()
+
+
+def phase(msg):
+    """Progress on stderr (the JSON line stays the only stdout)."""
+    print(f"[bench {time.perf_counter() - T_START:7.1f}s] {msg}", file=sys.stderr, flush=True)
 
 
 def main():
@@ -250,7 +344,9 @@ def main():
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t_gen
     M0 = synth.init_m(data.n_items, n_f)
+    phase(f"generated {args.config}")
     index_line = device_index_check(data, dev)
+    phase("device index checked")
     eff_rate = 1.0 if args.method == "full" else rate  # full ALS = complete budgets on every row
     eng = (ShardedEngine(data, n_f, eff_rate, lam, rank, world, device=dev, fast=args.method == "fast_core")
            if world > 1 else CoreEngine(data, n_f, eff_rate, lam, device=dev, fast=args.method == "fast_core"))
@@ -293,7 +389,9 @@ def main():
     e2e_line = None
     if not args.no_e2e:
         # a whole fit of the workload as its config states it (large: 10 iterations), from host arrays
+        phase("timed steps done; e2e fit")
         e2e_line = e2e(data, spec, M0, spec["iters"], rank, world, args.method)
+        phase("e2e done")
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -305,7 +403,8 @@ def main():
     sb_u, bb_u = tier_bytes(core.user, n_f)
     sb_i, bb_i = tier_bytes(core.item, n_f)
     kbytes = {"small_gram_kernel": (sb_u + sb_i) * args.steps, "big_gram_kernel": (bb_u + bb_i) * args.steps,
-              "big_scan_kernel": (bb_u + bb_i) * args.steps, "fast_gram_kernel": (bb_u + bb_i) * args.steps}
+              "big_gram_tc_kernel": (bb_u + bb_i) * args.steps, "big_scan2_kernel": (bb_u + bb_i) * args.steps,
+              "fast_gram_kernel": (bb_u + bb_i) * args.steps}
     dom = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (0, 0.0))
     dom_name, (dom_cnt, dom_ms) = dom
     dom_bytes = kbytes.get(dom_name)
@@ -313,6 +412,7 @@ def main():
     b_iter = algorithmic_bytes(np.diff(data.row_ptr.cpu().numpy()), n_f) + algorithmic_bytes(
         np.diff(data.col_ptr.cpu().numpy()), n_f)
     gpu_launches = sum(c for c, _ in prof.values())
+    compute = compute_terms(core, n_f, prof, args.steps)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -333,7 +433,8 @@ def main():
                      "peak_kind": peak_kind,
                      "launches": dom_cnt, "kernel_ms_total": dom_ms,
                      "step_alg_bytes": b_iter,
-                     "step_frac": (b_iter / (hbm * 1e9)) / (total_ms / 1e3 / args.steps)},
+                     "step_frac": (b_iter / (hbm * 1e9)) / (total_ms / 1e3 / args.steps),
+                     "compute": compute},
         "kernels": {k: {"launches": c, "ms": ms} for k, (c, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
         "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
@@ -343,7 +444,9 @@ def main():
     }
     if not args.no_cpu and world == 1:
         R_host = data.rating_matrix()
+        phase("cpu baseline")
         line["cpu_baseline"] = cpu_baseline_port(R_host, spec, M0, args.cpu_seconds)
+        phase("cpu baseline done")
     else:
         line["cpu_baseline"] = None
     if e2e_line is not None:

@@ -232,6 +232,8 @@ int cals_csr_to_csc(const int64_t* ptr, const int32_t* idx, const float* val, in
  * (for bench.py's roofline numbers).  collect() synchronises on the recorded
  * events, writes "name launches total_ms" lines into buf, and resets. */
 void cals_profile_enable(int on);
+/* 1 while per-kernel event timing is enabled (cals_profile_enable). */
+int cals_profile_enabled(void);
 /* Debug: point the sweep kernels at 16 device uint64 counters (NULL = off):
  * [0] table-resolved columns, [1] bracket fallbacks, [2] bracket candidates,
  * [3] candidates after pre-narrowing, [4] extra select rounds, [5] rows. */

@@ -83,6 +83,7 @@ SIGNATURES = {
     "cals_coo_to_csr": (i32, [P, P, P, i64, i64, i64, P, P, P, P, P, sz, P]),
     "cals_csr_to_csc": (i32, [P, P, P, i64, i64, i64, P, P, P, P, sz, P]),
     "cals_profile_enable": (None, [i32]),
+    "cals_profile_enabled": (i32, []),
     "cals_debug_stats": (None, [P]),
     "cals_debug_big_batch": (None, [ctypes.c_int64, ctypes.c_int64]),
     "cals_set_tuning": (None, [P]),
@@ -122,6 +123,16 @@ def check(rc: int, what: str) -> None:
 
 def profile_enable(on: bool) -> None:
     load().cals_profile_enable(1 if on else 0)
+
+
+def profile_enabled() -> bool:
+    return bool(load().cals_profile_enabled())
+
+
+# the standalone selection kernels of a half-sweep (FitReport.sketch_time); the staged
+# tier selects inside its Gram kernel and is not separable
+SELECTION_KERNELS = ("quantile_table_kernel", "big_calib_kernel", "big_scan2_kernel", "big_resolve_kernel",
+                     "tc_scales_kernel", "fast_sketch_kernels")
 
 
 def profile_collect() -> dict:

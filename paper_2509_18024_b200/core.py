@@ -276,6 +276,12 @@ def _fit_gpu(R, cfg, rate, init_u, init_m, items_first, engine):
         prev[0] = obj
         return done
 
+    # selection time (core.py:193-195,208-219): event time of the standalone selection
+    # kernels, collected through the native per-kernel timer unless the caller runs it
+    own_timer = not _lib.profile_enabled()
+    if own_timer:
+        _lib.profile_enable(True)
+        _lib.profile_collect()
     t0 = time.perf_counter()
     for it in range(cfg.max_iters):
         eng.step(first)  # iteration it; its first half also yields the residual of it-1
@@ -288,6 +294,11 @@ def _fit_gpu(R, cfg, rate, init_u, init_m, items_first, engine):
         converged = consume(eng.iters_done - 1)
     torch.cuda.current_stream().synchronize()
     t_loop = time.perf_counter() - t0
+    sketch_s = 0.0
+    if own_timer:
+        prof = _lib.profile_collect()
+        _lib.profile_enable(False)
+        sketch_s = sum(ms for k, (_, ms) in prof.items() if k in _lib.SELECTION_KERNELS) / 1e3
     iters = eng.iters_done
     U, M = eng.factors_host()
     report = FitReport(
@@ -296,8 +307,8 @@ def _fit_gpu(R, cfg, rate, init_u, init_m, items_first, engine):
         rmse_trace=np.asarray(rmse_trace),
         iters_run=iters,
         wall_clock_total=time.perf_counter() - start,
-        sketch_time=0.0,  # selection is fused into the half-sweep kernels (no separable phase)
-        solve_time=t_loop,
+        sketch_time=sketch_s,
+        solve_time=max(t_loop - sketch_s, 0.0),  # iteration wall - sketch time (als.py:294-298)
         converged=converged,
         skipped_users=skipped_u,
         skipped_items=skipped_m,

@@ -1092,6 +1092,11 @@ void cals_profile_enable(int on) {
     std::lock_guard<std::mutex> lk(P.mu);
     P.on = on != 0;
 }
+int cals_profile_enabled(void) {
+    Prof& P = prof();
+    std::lock_guard<std::mutex> lk(P.mu);
+    return P.on ? 1 : 0;
+}
 
 int cals_profile_collect(char* buf, size_t len) {
     Prof& P = prof();

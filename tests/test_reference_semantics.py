@@ -220,3 +220,29 @@ def test_imaging_rows_shorter_than_n_f(acc):
     assert np.isfinite(out).all() and out.min() >= 0.0 and out.max() <= 1.0
     np.testing.assert_allclose(rep.objective_trace, acc["img96_obj"], rtol=1e-3)
     assert rel_err_rows(F.user_factors, acc["img96_U"]) <= 1e-3
+
+
+def test_report_sketch_time_is_the_selection_phase():
+    """FitReport.sketch_time = time in selection (core.py:193-195,208-219), solve_time =
+    loop wall - sketch time (als.py:294-298): measured from the selection kernels' events,
+    positive when rows are long enough for the tiled tier's standalone selection kernels."""
+    rng = np.random.default_rng(5)
+    n_u, n_i = 4000, 60
+    mask = rng.random((n_u, n_i)) < 0.5  # items of ~2000 ratings: the tiled tier selects
+    u, i = np.nonzero(mask)
+    v = rng.normal(size=u.size).astype(np.float32).astype(np.float64)
+    R = cb.RatingMatrix(u, i, v, n_users=n_u, n_items=n_i)
+    cfg = cb.SolverConfig(method="core", n_f=16, lam=0.05, rate=0.1, max_iters=3, tol=1e-15)
+    F, rep = quiet(cb.fit_core, R, cfg)
+    assert rep.sketch_time > 0.0
+    assert rep.solve_time >= 0.0
+    assert rep.sketch_time + rep.solve_time <= rep.wall_clock_total + 1e-6
+    # the caller's own profiling session is left alone (no timing taken from it)
+    from paper_2509_18024_b200 import _lib
+    _lib.profile_enable(True)
+    try:
+        F2, rep2 = quiet(cb.fit_core, R, cfg)
+        assert rep2.sketch_time == 0.0 and _lib.profile_enabled()
+    finally:
+        _lib.profile_enable(False)
+        _lib.profile_collect()
