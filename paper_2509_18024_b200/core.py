@@ -283,16 +283,22 @@ def _fit_gpu(R, cfg, rate, init_u, init_m, items_first, engine):
         _lib.profile_enable(True)
         _lib.profile_collect()
     t0 = time.perf_counter()
-    for it in range(cfg.max_iters):
-        eng.step(first)  # iteration it; its first half also yields the residual of it-1
-        if it >= 1 and consume(it - 1):
-            converged = True
-            eng.rewind()  # the factors of iteration it-1 are the result
-            break
-    if not converged and eng.iters_done > 0:
-        eng.finish(first)
-        converged = consume(eng.iters_done - 1)
-    torch.cuda.current_stream().synchronize()
+    try:
+        for it in range(cfg.max_iters):
+            eng.step(first)  # iteration it; its first half also yields the residual of it-1
+            if it >= 1 and consume(it - 1):
+                converged = True
+                eng.rewind()  # the factors of iteration it-1 are the result
+                break
+        if not converged and eng.iters_done > 0:
+            eng.finish(first)
+            converged = consume(eng.iters_done - 1)
+        torch.cuda.current_stream().synchronize()
+    except BaseException:
+        if own_timer:  # (a NumericalError mid-fit must not leave the timer running)
+            _lib.profile_enable(False)
+            _lib.profile_collect()
+        raise
     t_loop = time.perf_counter() - t0
     sketch_s = 0.0
     if own_timer:

@@ -44,11 +44,12 @@ class DeviceSide:
     device, with its static schedule (budgets, tiers) and workspace."""
 
     def complete_row(self, row):
-        """Whether row's sketch is complete (s_i == n_i: the exact SPD row, core.py:206-207),
-        from the unsharded count -- budget_host is zero outside this rank's shard."""
+        """Whether (global) row's sketch is complete (s_i == n_i: the exact SPD row,
+        core.py:206-207)."""
+        loc = int(row) - self.row0
         if self.fast:
-            return int(self.budget_host[row]) == int(self.counts[row])
-        return _budget(int(self.counts[row]), self.rate) == int(self.counts[row])
+            return int(self.budget_host[loc]) == int(self.counts[loc])
+        return _budget(int(self.counts[loc]), self.rate) == int(self.counts[loc])
 
     def __init__(self, ptr, idx, val, n_src, n_f, rate, device, row_begin=0, row_end=None, fast=False, ptr_dev=None):
         torch = _lib.require_cuda()
@@ -56,6 +57,23 @@ class DeviceSide:
         if ptr_dev is None and torch.is_tensor(ptr):
             ptr_dev = ptr
         ptr = np.ascontiguousarray(ptr.cpu().numpy() if torch.is_tensor(ptr) else ptr, dtype=np.int64)
+        n_all = ptr.size - 1
+        if row_end is None:
+            row_end = n_all
+        row_begin, row_end = int(row_begin), int(row_end)
+        # a shard: only rows [row_begin, row_end) and their ratings live on this
+        # device -- a rebased pointer block and views of the index / value arrays; the kernels
+        # see a side of row_end - row_begin rows, and every per-row output pointer (target
+        # rows, thresholds) is offset by row_begin, so results land at the global rows
+        self.row0 = row_begin
+        if (row_begin, row_end) != (0, n_all):
+            base, end = int(ptr[row_begin]), int(ptr[row_end])
+            idx = idx[base:end]
+            val = val[base:end]
+            if ptr_dev is not None:
+                ptr_dev = (ptr_dev[row_begin:row_end + 1] - base).contiguous()
+            ptr = ptr[row_begin:row_end + 1] - base
+            row_begin, row_end = 0, ptr.size - 1
         n_rows = ptr.size - 1
         self.n_rows = n_rows
         self.n_src = int(n_src)
@@ -151,34 +169,49 @@ class DeviceSide:
                                               self.fast_ws.numel(), stream), "cals_fast_sketch")
             _lib.check(L.cals_fast_half_sweep(
                 ctypes.byref(self.side), ctypes.byref(self.plan), source.data_ptr(), source.shape[0], source.stride(0),
-                self.n_f, float(lam), self.gmask.data_ptr(), target.data_ptr(), target.stride(0),
-                target_old.data_ptr() if target_old is not None else None,
+                self.n_f, float(lam), self.gmask.data_ptr(), self._rows_ptr(target), target.stride(0),
+                self._rows_ptr(target_old) if target_old is not None else None,
                 target_old.stride(0) if target_old is not None else 0,
                 self.rss_rows.data_ptr() if want_rss else None,
                 self.pen_rows.data_ptr(), self.status.data_ptr(), self.summary.data_ptr(), self.ws.data_ptr(),
                 self.ws.numel(), stream), "cals_fast_half_sweep")
+            self._globalize_summary(stream)
             return
         rc = L.cals_core_half_sweep(
             ctypes.byref(self.side), ctypes.byref(self.plan), source.data_ptr(), source.shape[0],
-            source.stride(0), self.n_f, float(lam), target.data_ptr(), target.stride(0),
-            target_old.data_ptr() if target_old is not None else None,
+            source.stride(0), self.n_f, float(lam), self._rows_ptr(target), target.stride(0),
+            self._rows_ptr(target_old) if target_old is not None else None,
             target_old.stride(0) if target_old is not None else 0,
             self.rss_rows.data_ptr() if want_rss else None, self.pen_rows.data_ptr(),
-            thr_keys.data_ptr() if thr_keys is not None else None,
+            self._rows_ptr(thr_keys) if thr_keys is not None else None,
             self.status.data_ptr(), self.summary.data_ptr(), self.ws.data_ptr(), self.ws.numel(), stream)
         _lib.check(rc, "cals_core_half_sweep")
+        self._globalize_summary(stream)
+
+    def index_bytes(self):
+        """Device bytes of this side's index (pointers, row ids, ratings)."""
+        return int(self.ptr.numel() * 8 + self.idx.numel() * 4 + self.val.numel() * 4)
+
+    def _rows_ptr(self, t):
+        """Address of global row row0 of a per-row array (a shard's first row)."""
+        return t.data_ptr() + self.row0 * t.stride(0) * t.element_size()
+
+    def _globalize_summary(self, stream):
+        """The status word names a shard-local row: make it the global row (word - row0:
+        the low half stores 0xFFFFFFFF - row), so ranks' words compare under MAX."""
+        if self.row0:
+            torch = _lib.require_cuda()
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                self.summary.sub_((self.summary != 0).to(torch.int64) * self.row0)
 
     def residual(self, source, rows_w, stream=None):
         torch = _lib.require_cuda()
         if stream is None:
             stream = torch.cuda.current_stream(self.device).cuda_stream
-        # this shard's rows only: a view of the side starting at row_begin
-        r0, r1 = self.row_range
-        view = _lib.cals_side(self.ptr.data_ptr() + 8 * r0, self.idx.data_ptr(), self.val.data_ptr(), r1 - r0,
-                              self.side.nnz)
-        _lib.check(_lib.load().cals_residual(ctypes.byref(view), source.data_ptr(), source.stride(0), self.n_f,
-                                             rows_w[r0:].data_ptr(), rows_w.stride(0),
-                                             self.rss_rows[r0:].data_ptr(), stream),
+        # this side's rows (a shard holds only its own), against their global target rows
+        _lib.check(_lib.load().cals_residual(ctypes.byref(self.side), source.data_ptr(), source.stride(0), self.n_f,
+                                             self._rows_ptr(rows_w), rows_w.stride(0), self.rss_rows.data_ptr(),
+                                             stream),
                    "cals_residual")
 
 
@@ -231,7 +264,9 @@ class CoreEngine:
         self._sides = {}
         # a host matrix ships its CSR only: the CSC (item side) is built from the
         # device CSR (csrc/index.cu) on a side stream, beside the first half-sweep
-        self._csc_on_device = not torch.is_tensor(R.col_ptr)
+        # (a shard holds a CSR row block only, so its CSC block comes from the host index)
+        self._csc_on_device = not torch.is_tensor(R.col_ptr) and tuple(ir) == (0, self.n_items) and \
+            tuple(ur) == (0, self.n_users)
         self._user_ready = None
         # factor rows padded to a multiple of 4 floats (16-byte gathers); padding stays zero
         self.ld = (self.n_f + 3) // 4 * 4

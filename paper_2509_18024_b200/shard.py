@@ -5,11 +5,13 @@ Rows of a half-sweep are independent given a read-only source snapshot
 rows of each side against its full replica of the source factors, then the
 updated blocks are all-gathered (one collective per half-sweep) so every rank
 again holds the full target matrix.  The fused residual is a scalar
-all-reduce.  Ratings never move: a rank only needs its CSR row block and CSC
-column block (it keeps the whole index here for simplicity of the planner).
+all-reduce.  Ratings never move: a rank only holds its CSR row block and CSC
+column block.
 
 The exchange helpers are backend-agnostic (NCCL on GPUs, gloo on CPU for the
-host-logic tests).
+host-logic tests).  Each rank's DeviceSide holds only its CSR row block and CSC
+column block (rebased pointers, views of the rating arrays), plus full fp32
+replicas of both factor matrices (the gathers touch arbitrary source rows).
 """
 
 from __future__ import annotations
@@ -37,32 +39,36 @@ def nnz_balanced_ranges(ptr, world):
 
 
 def allgather_rows(F, ranges, rank, group=None, scratch=None):
-    """All-gather-v of row blocks: after the call every rank's F holds every
-    rank's rows F[r0:r1].  Blocks are padded to the largest one so a single
-    all_gather_into_tensor moves everything."""
+    """All-gather-v of row blocks: after the call every rank's F holds every rank's
+    rows F[r0:r1].
+
+    Every block is broadcast by its owner straight into the block's own rows of F
+    on every rank (rows are contiguous in the row-major factor matrix), so no rank
+    stages a send buffer or scatters a receive buffer; NCCL runs the broadcasts
+    back to back on its stream over NVLink.  CUDA tensors under a host backend
+    (gloo: several ranks on one device, functional tests only) go through one
+    host copy."""
     world = len(ranges)
     if world == 1:
         return F
-    maxr = max(r1 - r0 for r0, r1 in ranges)
-    nf = F.shape[1]
-    if scratch is None or scratch.numel() < (world + 1) * maxr * nf:
-        scratch = torch.empty((world + 1) * maxr * nf, dtype=F.dtype, device=F.device)
-    send = scratch[:maxr * nf].view(maxr, nf)
-    recv = scratch[maxr * nf:(world + 1) * maxr * nf].view(world, maxr, nf)
-    r0, r1 = ranges[rank]
-    send[:r1 - r0].copy_(F[r0:r1])
-    if F.is_cuda and dist.get_backend(group) != "nccl":
-        # host-staged exchange for CPU backends (gloo): functional tests of the
-        # sharded engine with several ranks on one device
-        rc = recv.cpu()
-        dist.all_gather_into_tensor(rc.view(-1), send.cpu().view(-1), group=group)
-        recv.copy_(rc)
-    else:
-        dist.all_gather_into_tensor(recv.view(-1), send.view(-1), group=group)
-    for q, (q0, q1) in enumerate(ranges):
-        if q != rank and q1 > q0:
-            F[q0:q1].copy_(recv[q, :q1 - q0])
+    backend = dist.get_backend(group)
+    if F.is_cuda and backend != "nccl":
+        host = F.cpu()
+        _broadcast_blocks(host, ranges, group)
+        F.copy_(host)
+        return scratch
+    _broadcast_blocks(F, ranges, group)
     return scratch
+
+
+def _broadcast_blocks(F, ranges, group):
+    works = []
+    for q, (q0, q1) in enumerate(ranges):
+        if q1 > q0:
+            src = q if group is None else dist.get_global_rank(group, q)
+            works.append(dist.broadcast(F[q0:q1], src=src, group=group, async_op=True))
+    for w in works:
+        w.wait()
 
 
 class ShardedEngine:

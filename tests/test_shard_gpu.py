@@ -1,8 +1,9 @@
-"""The sharded engine end to end on real kernels: two ranks (gloo, host-staged
+"""The sharded engine end to end on real kernels: 2 and 3 ranks (gloo, host-staged
 exchange) sharing cuda:0 run full iterations of ShardedEngine; the gathered
 factors must equal a single-process CoreEngine run bit for bit (rows are
-independent within a half-sweep, each computed by the same kernels) and the
-all-reduced objective terms must agree to fp64 rounding."""
+independent within a half-sweep, each computed by the same kernels), the
+all-reduced objective terms must agree to fp64 rounding, and each rank must hold
+only its shard of the index (~1/N of the CSR and CSC bytes)."""
 
 import os
 import socket
@@ -34,7 +35,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_path):
+def _worker(rank, world, port, out_path, bytes_path):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
@@ -46,6 +47,7 @@ def _worker(rank, world, port, out_path):
     eng = ShardedEngine(R, 32, 0.2, 0.05, rank, world, device=torch.device("cuda", 0))
     eng.set_factors(np.zeros((n_u, 32)), M0)
     terms = [eng.iterate() for _ in range(2)]
+    np.save(bytes_path.format(rank), np.array([eng.user.index_bytes(), eng.item.index_bytes()]))
     if rank == 0:
         U, M = eng.factors_host()
         np.savez(out_path, U=U, M=M, rss=[t.rss for t in terms], pen=[t.pen for t in terms])
@@ -53,13 +55,15 @@ def _worker(rank, world, port, out_path):
     dist.destroy_process_group()
 
 
-def test_two_rank_sharded_engine_matches_single_process(tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_engine_matches_single_process(tmp_path, world):
     import paper_2509_18024_b200 as cb
     from paper_2509_18024_b200.engine import CoreEngine
     out = str(tmp_path / "rank0.npz")
+    bpath = str(tmp_path / "bytes{}.npy")
     ctx = mp.get_context("spawn")
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, out)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, out, bpath)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
@@ -77,3 +81,8 @@ def test_two_rank_sharded_engine_matches_single_process(tmp_path):
     np.testing.assert_array_equal(got["M"], M)
     np.testing.assert_allclose(got["rss"], [t.rss for t in terms], rtol=1e-12)
     np.testing.assert_allclose(got["pen"], [t.pen for t in terms], rtol=1e-12)
+    # per-rank index: its shard only (nnz-balanced blocks; pointers add one entry per row)
+    full = np.array([eng.user.index_bytes(), eng.item.index_bytes()], dtype=np.float64)
+    per_rank = np.array([np.load(bpath.format(r)) for r in range(world)], dtype=np.float64)
+    assert np.allclose(per_rank.sum(axis=0), full, rtol=0.01)
+    assert (per_rank / full <= 1.0 / world + 0.1).all(), per_rank / full
