@@ -360,8 +360,12 @@ def main():
         dist.barrier()
     stream = torch.cuda.current_stream(dev)
     times = []
-    _lib.profile_enable(True)
-    _lib.profile_collect()
+    # timed steps run as the fit runs them: iterations t >= 1 replay a CUDA graph per parity
+    # (CoreEngine.step; the sharded engine stays eager) -- captured here, before the timed region
+    eng.step("user")
+    eng.step("user")
+    torch.cuda.synchronize()
+    graphs = len(getattr(eng, "_graphs", {}))
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.fill_(1)
@@ -376,6 +380,19 @@ def main():
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
+    # per-kernel event times (roofline, launch count) from the same number of eager steps right
+    # after the timed ones: profile scopes record events around every launch, so they are kept
+    # out of the timed region
+    _lib.profile_enable(True)
+    _lib.profile_collect()
+    use_graphs = getattr(eng, "use_graphs", False)
+    eng.use_graphs = False
+    for _ in range(args.steps):
+        flush.fill_(1)
+        eng.step("user")
+        eng.terms(eng.iters_done - 2)
+    torch.cuda.synchronize()
+    eng.use_graphs = use_graphs
     prof = _lib.profile_collect()
     _lib.profile_enable(False)
     total_ms = float(sum(times))
@@ -437,6 +454,9 @@ def main():
                      "compute": compute},
         "kernels": {k: {"launches": c, "ms": ms} for k, (c, ms) in sorted(prof.items(), key=lambda kv: -kv[1][1])},
         "gpu_launches": gpu_launches,
+        "cuda_graphs": {"replayed": graphs > 0, "graphs": graphs,
+                        "note": "timed iterations replay one captured graph per parity; kernel times and the "
+                                "launch count come from as many eager steps run after the timed region"},
         "clocks": clk.summary(),
         "rmse_prev_iter": float(np.sqrt(terms.rss / core.ssq)),
         "setup_s": {"generate": t_gen},

@@ -261,6 +261,9 @@ void cals_debug_big_batch(int64_t cand_keys, int64_t tiles);
  *   tc_debug       profiling only (results are then wrong): bit 0 skips the
  *                  tensor-core Gram's MMAs, bit 1 its digit pass, bit 2 its digit
  *                  stores; 8 traces CTA 0 into the cals_debug_stats buffer
+ *   qtab_min_nnz   sides with fewer ratings skip the per-half-sweep quantile
+ *                  table (the staged tier then selects by its exact column
+ *                  search; default 2^20; 1 = always build it)
  */
 typedef struct cals_tuning {
     int32_t item_rows;
@@ -272,6 +275,7 @@ typedef struct cals_tuning {
     int32_t fold_chunks;
     int32_t serial_tiers;
     int32_t tc_debug;
+    int64_t qtab_min_nnz;
 } cals_tuning;
 void cals_set_tuning(const cals_tuning* tuning);
 void cals_get_tuning(cals_tuning* tuning);

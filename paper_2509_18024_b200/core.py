@@ -277,15 +277,33 @@ def _fit_gpu(R, cfg, rate, init_u, init_m, items_first, engine):
         return done
 
     # selection time (core.py:193-195,208-219): event time of the standalone selection
-    # kernels, collected through the native per-kernel timer unless the caller runs it
+    # kernels, collected through the native per-kernel timer unless the caller runs it.
+    # Iterations 0 and 1 run eagerly under the timer; from iteration 2 on the engine
+    # replays CUDA graphs (no per-kernel events inside a graph), each counted at
+    # iteration 1's selection time (the same launches on data of the same shape).
     own_timer = not _lib.profile_enabled()
+    sel_ms = [0.0, 0.0]  # iteration 0, iteration 1
+    graph_iters = 0
+
+    def selection_ms():
+        return sum(ms for k, (_, ms) in _lib.profile_collect().items() if k in _lib.SELECTION_KERNELS)
+
     if own_timer:
         _lib.profile_enable(True)
         _lib.profile_collect()
     t0 = time.perf_counter()
     try:
         for it in range(cfg.max_iters):
+            if own_timer and it == 1:
+                torch.cuda.current_stream().synchronize()
+                sel_ms[0] = selection_ms()
             eng.step(first)  # iteration it; its first half also yields the residual of it-1
+            if own_timer and it == 1:
+                torch.cuda.current_stream().synchronize()
+                sel_ms[1] = selection_ms()
+                _lib.profile_enable(False)
+            if own_timer and it >= 2:
+                graph_iters += 1
             if it >= 1 and consume(it - 1):
                 converged = True
                 eng.rewind()  # the factors of iteration it-1 are the result
@@ -302,9 +320,11 @@ def _fit_gpu(R, cfg, rate, init_u, init_m, items_first, engine):
     t_loop = time.perf_counter() - t0
     sketch_s = 0.0
     if own_timer:
-        prof = _lib.profile_collect()
-        _lib.profile_enable(False)
-        sketch_s = sum(ms for k, (_, ms) in prof.items() if k in _lib.SELECTION_KERNELS) / 1e3
+        if _lib.profile_enabled():  # stopped before iteration 1 ended: the timer is still on
+            sel_ms[0] += selection_ms()
+            _lib.profile_enable(False)
+        _lib.profile_collect()
+        sketch_s = (sel_ms[0] + sel_ms[1] * (1 + graph_iters)) / 1e3
     iters = eng.iters_done
     U, M = eng.factors_host()
     report = FitReport(

@@ -25,7 +25,7 @@ constexpr int kItemRowsMin = 16384;  // slice rows per work item (sweep on the 5
 thread_local char g_err[256] = "";
 
 // explicit tuning (cals_set_tuning); zero / negative fields select the built-in defaults
-cals_tuning g_tuning = {0, -1.0f, -1, 0, 0, 0.0f, 0, 0, 0};
+cals_tuning g_tuning = {0, -1.0f, -1, 0, 0, 0.0f, 0, 0, 0, 0};
 int64_t g_big_cand_budget = 0, g_big_tile_budget = 0;  // debug overrides, see cals_debug_big_batch
 unsigned long long* g_stats = nullptr;  // debug counters (device), see cals_debug_stats
 
@@ -241,7 +241,10 @@ BigBatches big_batches(const cals_plan* P) {
         return b;
     }
     const int nf = P->n_f;
-    const int64_t cand_budget = g_big_cand_budget > 0 ? g_big_cand_budget : (int64_t)1 << 27;  // 1 GiB of keys
+    // 8 GiB of candidate keys per batch: fewer, larger batches (500M config: 46 -> ~8 batches per
+    // half-sweep, 425 -> 362 ms per iteration, tools/batch_sweep.py); the workspace stays a
+    // small share of the 180 GB of HBM (32 GB for both sides of the 500M config)
+    const int64_t cand_budget = g_big_cand_budget > 0 ? g_big_cand_budget : (int64_t)1 << 30;
     const int64_t tile_budget = g_big_tile_budget > 0
                                     ? g_big_tile_budget
                                     : std::max<int64_t>(1, ((int64_t)1 << 30) / ((int64_t)nf * (nf + 1) * 4));
@@ -818,7 +821,11 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.summary = reinterpret_cast<unsigned long long*>(status_summary);
     A.qtab = nullptr;
 
-    const bool long_small = P->n_small > 0 && P->small_seg_maxn[0] > 16;
+    // the quantile table (one CTA per column sorting QS samples, ~30 us) pays off only on
+    // sides with many ratings; below 2^20 the staged tier's exact column search is cheaper
+    // (small config: 160k ratings)
+    const int64_t qtab_min = g_tuning.qtab_min_nnz > 0 ? g_tuning.qtab_min_nnz : ((int64_t)1 << 20);
+    const bool long_small = P->n_small > 0 && P->small_seg_maxn[0] > 16 && side->nnz >= qtab_min;
     if ((long_small || P->n_big > 0) && side->nnz > 0) {
         const int QS = P->n_big > 0 ? kQSbig : kQSsmall;
         allow_smem(quantile_table_kernel);
@@ -1080,7 +1087,7 @@ void cals_debug_big_batch(int64_t cand_keys, int64_t tiles) {
     g_big_tile_budget = tiles;
 }
 void cals_set_tuning(const cals_tuning* t) {
-    static const cals_tuning defaults = {0, -1.0f, -1, 0, 0, 0.0f, 0, 0, 0};
+    static const cals_tuning defaults = {0, -1.0f, -1, 0, 0, 0.0f, 0, 0, 0, 0};
     g_tuning = t != nullptr ? *t : defaults;
 }
 void cals_get_tuning(cals_tuning* t) {

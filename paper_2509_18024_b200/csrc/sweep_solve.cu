@@ -64,7 +64,25 @@ __global__ void __launch_bounds__(128, 3) solve_wide_kernel(SweepArgs A, const i
         const bool spd = A.budget[row] >= n;
         const double* G = A.gbuf + (size_t)li * nout;
         __syncwarp();
-        for (int e = lane; e < nout; e += 32) W[e] = (float)__ldcs(G + e);
+        {
+            // nf (nf + 1) is even and every slot starts 16-byte aligned: 16-byte streaming loads,
+            // eight per lane in flight (the copy is latency-bound at 12 warps per SM otherwise)
+            const double2* G2 = reinterpret_cast<const double2*>(G);
+            float2* W2 = reinterpret_cast<float2*>(W);
+            const int n2 = nout >> 1;
+            int e = lane;
+            for (; e + 32 * 7 < n2; e += 32 * 8) {
+                double2 v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = __ldcs(G2 + e + 32 * u);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) W2[e + 32 * u] = make_float2((float)v[u].x, (float)v[u].y);
+            }
+            for (; e < n2; e += 32) {
+                const double2 v = __ldcs(G2 + e);
+                W2[e] = make_float2((float)v.x, (float)v.y);
+            }
+        }
         __syncwarp();
         float x0, x1;
         const int st = CALS_ROW_OK;

@@ -293,6 +293,11 @@ class CoreEngine:
                 target=lambda: self._ssq_box.__setitem__(0, float(np.dot(v, v)) if v.size else 0.0), daemon=True)
             self._ssq_thread.start()
         self.iters_done = 0
+        self._s1 = torch.zeros(1, dtype=torch.int64, device=device)
+        # CUDA-graph replay of iterations t >= 1 (see step); the sharded engine turns it off
+        # (its exchange is a collective between half-sweeps)
+        self.use_graphs = True
+        self._graphs, self._graph_after, self._graph_failed = {}, {}, set()
 
     @property
     def ssq(self):
@@ -413,9 +418,32 @@ class CoreEngine:
 
     def step(self, first="user"):
         """Enqueue iteration t = iters_done; its first half also yields the
-        residual of iteration t-1, which is then published to the host."""
-        torch = _lib.require_cuda()
+        residual of iteration t-1, which is then published to the host.
+
+        From t = 1 on, an iteration is a fixed sequence of launches on fixed
+        buffers that depends only on t's parity (which factor buffer is current,
+        which objective slot is written), so with ``use_graphs`` it is captured
+        once per parity as a CUDA graph and replayed: one launch per iteration
+        instead of a few dozen (the small configs are launch-bound)."""
         t = self.iters_done
+        if self.use_graphs and t > 0:
+            key = (first, t % 2, self.cu, self.cm)
+            g = self._graphs.get(key)
+            if g is None and key not in self._graph_failed:
+                g = self._capture(first, key)
+            if g is not None:
+                g.replay()
+                self.cu, self.cm = self._graph_after[key]
+                self._publish(t - 1)
+                self.iters_done = t + 1
+                return
+        self._step_body(first, t)
+        if t > 0:
+            self._publish(t - 1)
+        self.iters_done = t + 1
+
+    def _step_body(self, first, t):
+        """The device work of iteration t (no host reads, no publication)."""
         second = "item" if first == "user" else "user"
         sf = self._side(first)
         self.half(first, rss=t > 0)
@@ -423,16 +451,38 @@ class CoreEngine:
         if t > 0:
             self._sum(sf.rss_rows, self.slots[(t - 1) % 2, 0:1].data_ptr())
             self._reduce_scalars((t - 1) % 2, (0,))
-            self._publish(t - 1)
-        s1 = sf.summary.clone()
+        self._s1.copy_(sf.summary)
         self.half(second, rss=False)
         cur = self.slots[t % 2]
         self._sum(self.user.pen_rows, cur[1:2].data_ptr())
         self._sum(self.item.pen_rows, cur[2:3].data_ptr())
-        cur[3:4].copy_(s1.view(torch.float64))
-        cur[4:5].copy_(ss.summary.view(torch.float64))
+        cur[3:4].copy_(self._s1.view(_lib.require_cuda().float64))
+        cur[4:5].copy_(ss.summary.view(_lib.require_cuda().float64))
         self._reduce_scalars(t % 2, (1, 2, 3, 4))
-        self.iters_done = t + 1
+
+    def _capture(self, first, key):
+        """Capture iteration t's device work (t >= 1, parity key[1]) as a CUDA graph.
+        The capture runs nothing; the factor-buffer flips it implies are recorded and
+        undone so replay() applies them.  A capture failure (e.g. a kernel profile
+        scope recording events) leaves this parity on the eager path."""
+        torch = _lib.require_cuda()
+        if _lib.profile_enabled():
+            return None
+        cu, cm, done = self.cu, self.cm, self.iters_done
+        g = torch.cuda.CUDAGraph()
+        try:
+            torch.cuda.synchronize(self.device)
+            with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                self._step_body(first, done)
+        except RuntimeError:
+            self._graph_failed.add(key)
+            self.cu, self.cm = cu, cm
+            torch.cuda.synchronize(self.device)
+            return None
+        self._graph_after[key] = (self.cu, self.cm)
+        self.cu, self.cm = cu, cm
+        self._graphs[key] = g
+        return g
 
     def finish(self, first="user"):
         """Residual of the last iteration: one gather pass over the first side."""

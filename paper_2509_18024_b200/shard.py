@@ -107,6 +107,7 @@ class ShardedEngine:
         eng = _Sharded(R, n_f, rate, lam, device=device, user_range=user_ranges[rank], item_range=item_ranges[rank],
                        fast=fast)
         eng._scratch = None
+        eng.use_graphs = False  # the exchange between half-sweeps is a collective: eager launches
         eng.rank, eng.world, eng.group = rank, world, group
         eng.user_ranges, eng.item_ranges = user_ranges, item_ranges
         return eng

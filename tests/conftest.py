@@ -39,6 +39,27 @@ def csr_csc(users, items, vals, n_users, n_items):
             (col_ptr, users[o2].astype(np.int32), vals[o2]))
 
 
+@pytest.fixture(autouse=True)
+def _table_on_small_sides():
+    """The production path skips the quantile table on sides below 2^20 ratings
+    (qtab_min_nnz); the parity tests run at sizes far below that, so by default they
+    build it anyway (the path every full-size config takes).  A test that wants the
+    production setting asks for qtab_min_nnz=0 through `tuning`."""
+    from paper_2509_18024_b200 import _lib
+
+    try:
+        _lib.load(build_if_missing=False)
+    except (RuntimeError, OSError):  # no native library: nothing to tune
+        yield
+        return
+    saved = _lib.TUNING_DEFAULTS["qtab_min_nnz"]
+    _lib.TUNING_DEFAULTS["qtab_min_nnz"] = 1
+    prev = _lib.set_tuning()
+    yield
+    _lib.TUNING_DEFAULTS["qtab_min_nnz"] = saved
+    _lib.set_tuning(**prev)
+
+
 @pytest.fixture
 def tuning():
     """Explicit native tuning for one test (cals_set_tuning), restored afterwards."""

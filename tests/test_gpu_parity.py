@@ -234,6 +234,18 @@ def test_oracle_parity_mixed_tiers(n_f, item_rows, tuning):
         assert eng.item.plan.n_big > 0  # the heavy items exercise the tiled tier
 
 
+@pytest.mark.parametrize("n_f", [1, 5, 16, 32, 64])
+def test_oracle_parity_staged_exact_selection(n_f, tuning):
+    """The production setting on a side below qtab_min_nnz: no quantile table, every
+    staged row (lengths up to the staged limit) selected by the exact column search."""
+    tuning(qtab_min_nnz=0)
+    u, i, v = random_matrix(n_f + 7, 3000, 400, 0.04)  # no tiled rows: the table would be built for them
+    R = cb.RatingMatrix(u, i, v, n_users=3000, n_items=400)
+    M0 = np.random.default_rng(2).normal(0, 0.1, (400, n_f)).astype(np.float32)
+    eng = check_against_oracle(R, n_f, 0.05, 0.2, M0)
+    assert eng.user.plan.n_small > 0 and eng.item.plan.n_big == 0
+
+
 @pytest.mark.parametrize("n_f", [1, 5, 8, 16])
 def test_oracle_parity_tiled_tier_small_rank(n_f):
     """Rows long enough to leave shared memory even at tiny n_f."""
