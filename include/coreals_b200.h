@@ -255,7 +255,8 @@ void cals_debug_big_batch(int64_t cand_keys, int64_t tiles);
  *                  (tcgen05 kind::i8, csrc/sweep_tc.cu), 1 the float64 SIMT
  *                  accumulate it replaced (comparison); both float64-quality
  *   calib_samples, calib_z   long-row bracket calibration (defaults 4096, 5.5)
- *   fold_chunks    fp32 Gram (n_f > 64): staged chunks summed before a float64 fold (4)
+ *   fold_chunks    fp32 tiled Gram (n_f <= 32, and method fast_core): staged chunks summed
+ *                  before a float64 fold (4); above n_f = 32 the tiled Gram sums in float64
  *   serial_tiers   1: the staged tier runs on the caller's stream before the tiled
  *                  tier instead of beside it on a second stream (profiling)
  *   tc_debug       profiling only (results are then wrong): bit 0 skips the

@@ -487,13 +487,14 @@ int launch_small(SweepArgs A, const cals_plan* P, const Work& w, cudaStream_t st
 template <int CPL, bool FAST = false>
 void launch_big_gram(const SweepArgs& A, const BigArgs& B, size_t smem, cudaStream_t st) {
     constexpr int threads = big_gram_threads(CPL);
-    if constexpr (CPL == 4 && !FAST) {
-        // float64 accumulation of the SIMT tiled Gram: long rows of later iterations reach cond ~1e6,
-        // where fp32 partial sums miss the 1e-4 contract (the tensor-core Gram is the default here)
+    if constexpr (CPL >= 4 && !FAST) {
+        // float64 accumulation of the SIMT tiled Gram (n_f > 32): long rows of later iterations reach
+        // cond ~1e6, where fp32 partial sums miss the 1e-4 contract (at 32 < n_f <= 64 the tensor-core
+        // Gram is the default; above 64 this is the tiled Gram)
         {
-            allow_smem(big_gram_kernel<4, false, true>);
-            big_gram_kernel<4, false, true>
-                <<<grid_for(big_gram_kernel<4, false, true>, smem, B.n_tiles, 8, threads), threads, smem, st>>>(A, B);
+            allow_smem(big_gram_kernel<CPL, false, true>);
+            big_gram_kernel<CPL, false, true>
+                <<<grid_for(big_gram_kernel<CPL, false, true>, smem, B.n_tiles, 8, threads), threads, smem, st>>>(A, B);
             return;
         }
     }

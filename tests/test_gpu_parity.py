@@ -445,12 +445,19 @@ def test_oracle_parity_ill_conditioned(n_f, item_rows, tuning):
     assert int(stats[15]) > 0  # the float64 path was exercised
 
 
-@pytest.mark.parametrize("n_f", [16, 64])
-def test_later_iteration_half_sweep_matches_oracle(n_f):
+@pytest.mark.parametrize("n_f,tune", [(16, None), (64, None), (64, dict(gram_path=1)),
+                                        (128, dict(item_rows=1024, rf_slice_max=512))])
+def test_later_iteration_half_sweep_matches_oracle(n_f, tune, tuning):
     """After several iterations the factors are large and the sketched systems
     ill-conditioned (the regime where an all-fp32 pipeline drifted from the
     float64 reference): one more half-sweep from the GPU's own state
-    still matches the oracle fed the same state -- keys exactly, rows to 1e-4."""
+    still matches the oracle fed the same state -- keys exactly, rows to 1e-4.
+    n_f = 64 runs on the tensor-core Gram and (gram_path=1) on the float64 SIMT
+    Gram; n_f = 128 with multi-item rows whose float64 re-solve starts from the
+    STORED tiled equations (rows above rf_slice_max), i.e. from the float64
+    accumulation of big_gram_kernel<8>."""
+    if tune:
+        tuning(**tune)
     u, i, v = random_matrix(n_f + 7, 3000, 400, 0.05, heavy_items=8, heavy_density=0.9)
     R = cb.RatingMatrix(u, i, v, n_users=3000, n_items=400)
     M0 = np.random.default_rng(2).normal(0, 0.1, (400, n_f)).astype(np.float32)

@@ -27,5 +27,5 @@ for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 1):
         torch.cuda.synchronize()
         prof = _lib.profile_collect()
         print(it, side, round(e0.elapsed_time(e1), 2), "ms", {k: (c, round(v, 2)) for k, (c, v) in
-                                                           sorted(prof.items(), key=lambda kv: -kv[1][1])[:6]},
+                                                           sorted(prof.items(), key=lambda kv: -kv[1][1])[:12]},
               flush=True)
