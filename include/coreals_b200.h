@@ -265,6 +265,10 @@ void cals_debug_big_batch(int64_t cand_keys, int64_t tiles);
  *   qtab_min_nnz   sides with fewer ratings skip the per-half-sweep quantile
  *                  table (the staged tier then selects by its exact column
  *                  search; default 2^20; 1 = always build it)
+ *   staged_max_rows  rows up to this many ratings take the staged tier (whole slice in one
+ *                  CTA's shared memory); longer rows the tiled tier.  0 = the longest row
+ *                  whose staged layout fits the tier's shared-memory budget (384 at
+ *                  n_f = 64, rate 0.1); values above that are clamped to it
  */
 typedef struct cals_tuning {
     int32_t item_rows;
@@ -277,6 +281,7 @@ typedef struct cals_tuning {
     int32_t serial_tiers;
     int32_t tc_debug;
     int64_t qtab_min_nnz;
+    int32_t staged_max_rows;
 } cals_tuning;
 void cals_set_tuning(const cals_tuning* tuning);
 void cals_get_tuning(cals_tuning* tuning);

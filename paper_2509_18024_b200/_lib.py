@@ -39,11 +39,11 @@ class cals_tuning(ctypes.Structure):
     _fields_ = [("item_rows", ctypes.c_int32), ("ill_ratio", ctypes.c_float), ("rf_slice_max", ctypes.c_int32),
                 ("gram_path", ctypes.c_int32), ("calib_samples", ctypes.c_int32), ("calib_z", ctypes.c_float),
                 ("fold_chunks", ctypes.c_int32), ("serial_tiers", ctypes.c_int32),
-                ("tc_debug", ctypes.c_int32), ("qtab_min_nnz", ctypes.c_int64)]
+                ("tc_debug", ctypes.c_int32), ("qtab_min_nnz", ctypes.c_int64), ("staged_max_rows", ctypes.c_int32)]
 
 
 TUNING_DEFAULTS = dict(item_rows=0, ill_ratio=-1.0, rf_slice_max=-1, gram_path=0, calib_samples=0, calib_z=0.0,
-                       fold_chunks=0, serial_tiers=0, tc_debug=0, qtab_min_nnz=0)
+                       fold_chunks=0, serial_tiers=0, tc_debug=0, qtab_min_nnz=0, staged_max_rows=0)
 
 
 def set_tuning(**fields):

@@ -720,7 +720,8 @@ int cals_plan_build(const int64_t* counts, int64_t n_rows, int n_f, double rate,
     std::memset(meta, 0, sizeof(*meta));
     meta->n_f = n_f;
     meta->n_rows = n_rows;
-    const int nmax = small_nmax(n_f, rate);
+    int nmax = small_nmax(n_f, rate);
+    if (g_tuning.staged_max_rows > 0) nmax = std::min(nmax, g_tuning.staged_max_rows);
     std::vector<int32_t> small, big;
     for (int64_t i = 0; i < n_rows; ++i) {
         if (counts[i] <= 0) continue;
@@ -1088,7 +1089,7 @@ void cals_debug_big_batch(int64_t cand_keys, int64_t tiles) {
     g_big_tile_budget = tiles;
 }
 void cals_set_tuning(const cals_tuning* t) {
-    static const cals_tuning defaults = {0, -1.0f, -1, 0, 0, 0.0f, 0, 0, 0, 0};
+    static const cals_tuning defaults = {0, -1.0f, -1, 0, 0, 0.0f, 0, 0, 0, 0, 0};
     g_tuning = t != nullptr ? *t : defaults;
 }
 void cals_get_tuning(cals_tuning* t) {

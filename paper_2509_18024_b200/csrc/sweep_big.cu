@@ -259,8 +259,13 @@ template __global__ void big_scan2_kernel<4, 68, 64>(SweepArgs, BigArgs);
 template __global__ void big_scan2_kernel<0, 0, 0>(SweepArgs, BigArgs);
 
 __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigArgs B) {
+    // per warp: the target bucket's keys while they number <= 32 (each keeping lane stores its key
+    // at its rank; lane p then picks up key p -- a find-nth-set-bit + shuffle per lane and round
+    // cost 29 % of this kernel's instructions)
+    __shared__ uint64_t s_keep[kThreads / 32][32];
     const int nf = A.nf;
     const int lane = threadIdx.x & 31;
+    uint64_t* keep_w = s_keep[threadIdx.x >> 5];
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwork = B.n_big * nf;
     const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -349,14 +354,11 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
                         const uint32_t bal = __ballot_sync(CALS_FULL_MASK, keep);
                         const int cnt = __popc(bal);
                         if (!spill && m + cnt <= 32) {
-                            const int p = lane - m;
-                            const bool mine = p >= 0 && p < cnt;
-                            const uint64_t got = __shfl_sync(CALS_FULL_MASK, kk[u], mine ? (int)__fns(bal, 0, p + 1) : 0);
-                            if (mine) v = got;
+                            if (keep) keep_w[m + __popc(bal & lanemask_lt())] = kk[u];
                         } else {
                             if (!spill) {
                                 __syncwarp();
-                                if (lane < m) cl[lane] = v;
+                                if (lane < m) cl[lane] = keep_w[lane];
                                 spill = true;
                             }
                             __syncwarp();
@@ -368,8 +370,17 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
                 }
                 __syncwarp();
                 if (lane == 0) stat_add(A, kStBigColumns, 1);
-                T = spill ? warp_select_keys(KeyList{cl}, m, need - before, blo, bhi, lane)
-                          : warp_kth_desc(v, m, need - before, lane);
+                if (spill) {
+                    T = warp_select_keys(KeyList{cl}, m, need - before, blo, bhi, lane);
+                } else {
+                    // rank of the lane's key among the m kept keys (broadcast reads of the list)
+                    v = lane < m ? keep_w[lane] : 0ull;
+                    int gt = 0;
+                    for (int j = 0; j < m; ++j) gt += (keep_w[j] > v) ? 1 : 0;
+                    const uint32_t hit = __ballot_sync(CALS_FULL_MASK, lane < m && gt == need - before - 1);
+                    T = __shfl_sync(CALS_FULL_MASK, v, __ffs(hit) - 1);
+                    __syncwarp();  // keep_w is free for the warp's next column
+                }
             } else {
                 if (lane == 0) {
                     stat_add(A, kStBigFallback, 1);

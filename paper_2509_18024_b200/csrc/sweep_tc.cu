@@ -177,6 +177,17 @@ __global__ void __launch_bounds__(256) tc_scales_kernel(const uint32_t* __restri
         if (CALS_TC_TRACE && trace && (cond)) A.stats[(slot)] = (unsigned long long)clock64(); \
     } while (0)
 
+// Long waits of the role warps (a whole work item).  A try_wait loop is the default: each
+// attempt blocks the warp for a few tens of cycles in hardware, so a waiting warp issues ~0.1
+// instructions per cycle; the nanosleep(128) poll it replaces returned at once and its four
+// epilogue warps + scheduler took ~45 % of the kernel's issue slots (ncu, r02).  tc_debug
+// 256: try_wait with a suspend-time hint; 512: the old test + nanosleep poll.
+__device__ __forceinline__ void tc_long_wait(uint32_t mbar, uint32_t phase, int dbg) {
+    if (dbg & 256) mbar_wait_hint(mbar, phase);
+    else if (dbg & 512) mbar_wait_backoff(mbar, phase);
+    else mbar_wait(mbar, phase);
+}
+
 // Work-item cursor of the digit-pass warps (item ring position + chunk start).
 struct TcCur {
     int i;       // item sequence number (ring slot i % kTcItems)
@@ -301,7 +312,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
                 const int kel = __shfl_sync(CALS_FULL_MASK, kend, l);
                 const int64_t lol = __shfl_sync(CALS_FULL_MASK, lo, l);
                 const int sl = i % kTcItems;
-                if (i >= kTcItems) mbar_wait_backoff(smem_u32(&bar_item_empty[sl]), (uint32_t)(((i / kTcItems) - 1) & 1));
+                if (i >= kTcItems) tc_long_wait(smem_u32(&bar_item_empty[sl]), (uint32_t)(((i / kTcItems) - 1) & 1), dbg);
                 TcItem& d = items[sl];
                 if (lane == 0) {
                     d.t = valid ? tl : -1;
@@ -377,7 +388,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
             const TcItem& d = items[sl];
             if (d.t < 0) break;
             TC_TRACE(32768 + i * 8 + 0, et == 0 && i < 1024);
-            mbar_wait_backoff(smem_u32(&bar_item_done[sl]), (uint32_t)((i / kTcItems) & 1));
+            tc_long_wait(smem_u32(&bar_item_done[sl]), (uint32_t)((i / kTcItems) & 1), dbg);
             TC_TRACE(32768 + i * 8 + 1, et == 0 && i < 1024);
             mbar_wait(smem_u32(&bar_tmem_full), (uint32_t)(i & 1));
             TC_TRACE(32768 + i * 8 + 2, et == 0 && i < 1024);
