@@ -174,6 +174,27 @@ int cals_predict_entries(const float* U, const float* M, int n_f, int ld_u, int 
  * metrics.py:64-160). */
 int cals_predict_entries_f64(const double* U, const double* M, int n_f, int ld_u, int ld_m, const int64_t* users,
                              const int64_t* items, int64_t n, double* out, void* stream);
+/* predict_full (als.py:155-157): out[u * ld_out + i] = U[u] . M[i] for every (u, i), float64
+ * (a register-tiled 64 x 64 output tile per CTA). */
+int cals_predict_full_f64(const double* U, const double* M, int64_t n_users, int64_t n_items, int n_f, int ld_u,
+                          int ld_m, double* out, int64_t ld_out, void* stream);
+/*
+ * Ranking metrics per user (metrics.py:89-147: hit@k and score-gain NDCG@k), one warp per user
+ * segment of the held-out entries.  seg_ptr int64[n_seg+1] groups the entries by user with items
+ * ascending inside a segment (the device index of the held-out triplets); perm[e] is the
+ * original position of grouped entry e, truths / scores are in original order.  An entry's
+ * predicted rank counts the entries of its user with a larger score, or an equal score and a
+ * smaller item (the reference's lexsort((item, -score))); its ideal rank orders by truth.
+ * Per user (float64, 0/1 flags as 0.0/1.0; users without entries get zeros):
+ *   qual[u]  any entry with truth >= threshold          (hit@k qualifies, metrics.py:113-116)
+ *   hit[u]   qual and such an entry at predicted rank < k_hit
+ *   used[u]  ideal DCG@k_ndcg > 0                        (metrics.py:142-143)
+ *   ratio[u] DCG@k_ndcg / ideal DCG@k_ndcg if used, else 0
+ * The caller reduces them (cals_sum_f64: fixed-order sums).
+ */
+int cals_rank_metrics(const int64_t* seg_ptr, int64_t n_seg, const int32_t* perm, const double* truths,
+                      const double* scores, int k_hit, double threshold, int k_ndcg, double* qual, double* hit,
+                      double* ratio, double* used, void* stream);
 
 /*
  * Method 'fast_core' (core.py:255-298): ONE sketch of the whole source per

@@ -79,6 +79,8 @@ SIGNATURES = {
     "cals_update_core": (i32, [P, i64, i32, P, P, P, f64, i32, P, P, P]),
     "cals_predict_entries": (i32, [P, P, i32, i32, i32, P, P, i64, P, P]),
     "cals_predict_entries_f64": (i32, [P, P, i32, i32, i32, P, P, i64, P, P]),
+    "cals_predict_full_f64": (i32, [P, P, i64, i64, i32, i32, i32, P, i64, P]),
+    "cals_rank_metrics": (i32, [P, i64, P, P, P, i32, f64, i32, P, P, P, P, P]),
     "cals_index_workspace_bytes": (sz, [i64, i64, i64]),
     "cals_coo_to_csr": (i32, [P, P, P, i64, i64, i64, P, P, P, P, P, sz, P]),
     "cals_csr_to_csc": (i32, [P, P, P, i64, i64, i64, P, P, P, P, sz, P]),

@@ -120,26 +120,29 @@ def predict(F, i, j):
     return float(F.user_factors[i] @ F.item_factors[j])
 
 
-def predict_entries(F, users, items, chunk=1 << 18):
-    """Predicted ratings for parallel index arrays (als.py:143-152), evaluated on
-    the GPU by the float64 gather-dot kernel (cals_predict_entries_f64) on the
-    FactorPair's float64 rows, so scores match the reference's einsum up to the
-    summation order (rankings in the evaluation metrics depend on them)."""
+def _device_factors(F):
+    """FactorPair rows as float64 CUDA tensors (the reference's precision, als.py:40-49)."""
     from . import _lib
     torch = _lib.require_cuda()
+    dev = torch.device("cuda")
+    U = torch.from_numpy(np.ascontiguousarray(F.user_factors, dtype=np.float64)).to(dev)
+    M = torch.from_numpy(np.ascontiguousarray(F.item_factors, dtype=np.float64)).to(dev)
+    return torch, dev, U, M
+
+
+def predict_entries_device(F, users, items):
+    """predict_entries with the scores left on the device (float64 CUDA tensor, flat);
+    the evaluation metrics rank them there (metrics.py)."""
+    from . import _lib
     users = np.asarray(users, dtype=np.int64)
     items = np.asarray(items, dtype=np.int64)
     if users.shape != items.shape:
         raise ValueError("users and items must have the same shape")
+    torch, dev, U, M = _device_factors(F)
     if users.size == 0:
-        return np.empty(0, dtype=np.float64)
-    U_h = np.ascontiguousarray(F.user_factors, dtype=np.float64)
-    M_h = np.ascontiguousarray(F.item_factors, dtype=np.float64)
-    if users.min() < 0 or users.max() >= U_h.shape[0] or items.min() < 0 or items.max() >= M_h.shape[0]:
+        return torch.empty(0, dtype=torch.float64, device=dev)
+    if users.min() < 0 or users.max() >= U.shape[0] or items.min() < 0 or items.max() >= M.shape[0]:
         raise IndexError("entry index out of range")
-    dev = torch.device("cuda")
-    U = torch.from_numpy(U_h).to(dev)
-    M = torch.from_numpy(M_h).to(dev)
     uu = torch.from_numpy(users.reshape(-1)).to(dev)
     ii = torch.from_numpy(items.reshape(-1)).to(dev)
     out = torch.empty(users.size, dtype=torch.float64, device=dev)
@@ -148,9 +151,38 @@ def predict_entries(F, users, items, chunk=1 << 18):
     _lib.check(_lib.load().cals_predict_entries_f64(U.data_ptr(), M.data_ptr(), nf, nf, nf, uu.data_ptr(),
                                                     ii.data_ptr(), users.size, out.data_ptr(), st),
                "cals_predict_entries_f64")
-    return out.cpu().numpy().reshape(users.shape)
+    return out
 
 
-def predict_full(F):
-    """Dense reconstruction U @ M^T (als.py:155-157); a plain GEMM (library call)."""
-    return F.user_factors @ F.item_factors.T
+def predict_entries(F, users, items, chunk=1 << 18):
+    """Predicted ratings for parallel index arrays (als.py:143-152), evaluated on
+    the GPU by the float64 gather-dot kernel (cals_predict_entries_f64) on the
+    FactorPair's float64 rows, so scores match the reference's einsum up to the
+    summation order (rankings in the evaluation metrics depend on them)."""
+    users = np.asarray(users, dtype=np.int64)
+    if users.size == 0:
+        if users.shape != np.asarray(items).shape:
+            raise ValueError("users and items must have the same shape")
+        return np.empty(0, dtype=np.float64)
+    return predict_entries_device(F, users, items).cpu().numpy().reshape(users.shape)
+
+
+def predict_full(F, block_rows=1 << 16):
+    """Dense reconstruction U @ M^T (als.py:155-157) in float64 on the GPU
+    (cals_predict_full_f64, a register-tiled kernel), in blocks of user rows so the
+    device holds at most block_rows x n_items outputs at a time."""
+    from . import _lib
+    torch, dev, U, M = _device_factors(F)
+    n_u, n_i, nf = U.shape[0], M.shape[0], F.n_f
+    out = np.empty((n_u, n_i), dtype=np.float64)
+    if n_u == 0 or n_i == 0:
+        return out
+    st = torch.cuda.current_stream().cuda_stream
+    L = _lib.load()
+    for r0 in range(0, n_u, block_rows):
+        r1 = min(n_u, r0 + block_rows)
+        blk = torch.empty((r1 - r0, n_i), dtype=torch.float64, device=dev)
+        _lib.check(L.cals_predict_full_f64(U[r0:r1].data_ptr(), M.data_ptr(), r1 - r0, n_i, nf, nf, nf,
+                                           blk.data_ptr(), n_i, st), "cals_predict_full_f64")
+        out[r0:r1] = blk.cpu().numpy()
+    return out

@@ -1083,6 +1083,29 @@ int cals_predict_entries_f64(const double* U, const double* M, int n_f, int ld_u
     return cuda_status("cals_predict_entries_f64");
 }
 
+int cals_predict_full_f64(const double* U, const double* M, int64_t n_users, int64_t n_items, int n_f, int ld_u,
+                          int ld_m, double* out, int64_t ld_out, void* stream) {
+    if (!U || !M || !out || n_f < 1 || ld_u < n_f || ld_m < n_f || n_users < 0 || n_items < 0 || ld_out < n_items)
+        return CALS_ERR_ARG;
+    if (n_users == 0 || n_items == 0) return CALS_OK;
+    const int64_t gx = (n_items + 63) / 64, gy = (n_users + 63) / 64;
+    if (gy > 65535) return CALS_ERR_UNSUPPORTED;  // > 4M users: call it per block of rows
+    predict_full_f64_kernel<<<dim3((unsigned)gx, (unsigned)gy), 256, 0, (cudaStream_t)stream>>>(
+        U, M, n_users, n_items, n_f, ld_u, ld_m, out, ld_out);
+    return cuda_status("cals_predict_full_f64");
+}
+
+int cals_rank_metrics(const int64_t* seg_ptr, int64_t n_seg, const int32_t* perm, const double* truths,
+                      const double* scores, int k_hit, double threshold, int k_ndcg, double* qual, double* hit,
+                      double* ratio, double* used, void* stream) {
+    if (!seg_ptr || !perm || !truths || !scores || !qual || !hit || !ratio || !used || n_seg < 0) return CALS_ERR_ARG;
+    if (n_seg == 0) return CALS_OK;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((n_seg + 7) / 8, (int64_t)dev().sms * 8));
+    rank_metrics_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(seg_ptr, n_seg, perm, truths, scores, k_hit,
+                                                                      threshold, k_ndcg, qual, hit, ratio, used);
+    return cuda_status("cals_rank_metrics");
+}
+
 void cals_debug_stats(void* device_counters) { g_stats = (unsigned long long*)device_counters; }
 void cals_debug_big_batch(int64_t cand_keys, int64_t tiles) {
     g_big_cand_budget = cand_keys;

@@ -265,4 +265,96 @@ __global__ void __launch_bounds__(256) predict_entries_f64_kernel(const double* 
     }
 }
 
+// ---- predict_full (als.py:155-157): out = U M^T, float64 -------------------
+// 16 x 16 threads, a 64 x 64 output tile per CTA (4 x 4 per thread), K in steps of 16
+// through shared memory (transposed tiles: conflict-free reads along the output rows).
+__global__ void __launch_bounds__(256) predict_full_f64_kernel(const double* __restrict__ U, const double* __restrict__ M,
+                                                               int64_t nu, int64_t ni, int nf, int ldu, int ldm,
+                                                               double* __restrict__ out, int64_t ldo) {
+    __shared__ double su[16][65], sm[16][65];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t u0 = (int64_t)blockIdx.y * 64, i0 = (int64_t)blockIdx.x * 64;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int k0 = 0; k0 < nf; k0 += 16) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < 64 * 16; e += 256) {
+            const int r = e >> 4, k = e & 15;
+            su[k][r] = (u0 + r < nu && k0 + k < nf) ? U[(u0 + r) * ldu + k0 + k] : 0.0;
+            sm[k][r] = (i0 + r < ni && k0 + k < nf) ? M[(i0 + r) * ldm + k0 + k] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            double a[4], b[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a[q] = su[k][ty + 16 * q];
+                b[q] = sm[k][tx + 16 * q];
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int w = 0; w < 4; ++w) acc[q][w] = fma(a[q], b[w], acc[q][w]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int64_t u = u0 + ty + 16 * q, i = i0 + tx + 16 * w;
+            if (u < nu && i < ni) out[u * ldo + i] = acc[q][w];
+        }
+}
+
+// ---- ranking metrics per user (metrics.py:89-147) --------------------------
+// One warp per user segment; entry i's predicted rank = entries of the segment with a larger
+// score, or an equal score and an earlier position (items ascend inside a segment, so that
+// is the reference's smaller-item tie rule); ideal rank likewise by truth.
+__global__ void __launch_bounds__(256) rank_metrics_kernel(const int64_t* __restrict__ seg, int64_t n_seg,
+                                                           const int32_t* __restrict__ perm,
+                                                           const double* __restrict__ truths,
+                                                           const double* __restrict__ scores, int k_hit, double thr,
+                                                           int k_ndcg, double* __restrict__ qual,
+                                                           double* __restrict__ hit, double* __restrict__ ratio,
+                                                           double* __restrict__ used) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t u = w0; u < n_seg; u += nw) {
+        const int64_t lo = seg[u], hi = seg[u + 1];
+        double dcg = 0.0, idcg = 0.0;
+        bool rel_any = false, hit_any = false;
+        for (int64_t i = lo + lane; i < hi; i += 32) {
+            const int32_t pi = perm[i];
+            const double si = scores[pi], ti = truths[pi];
+            int rs = 0, rt = 0;
+            for (int64_t j = lo; j < hi; ++j) {
+                const int32_t pj = perm[j];
+                const double sj = scores[pj], tj = truths[pj];
+                rs += (sj > si || (sj == si && j < i)) ? 1 : 0;
+                rt += (tj > ti || (tj == ti && j < i)) ? 1 : 0;
+            }
+            if (rs < k_ndcg) dcg += ti * (1.0 / log2((double)(rs + 2)));
+            if (rt < k_ndcg) idcg += ti * (1.0 / log2((double)(rt + 2)));
+            const bool rel = ti >= thr;
+            rel_any |= rel;
+            hit_any |= rel && rs < k_hit;
+        }
+        dcg = warp_sum_d(dcg);
+        idcg = warp_sum_d(idcg);
+        const bool q = __any_sync(CALS_FULL_MASK, rel_any), h = __any_sync(CALS_FULL_MASK, hit_any);
+        if (lane == 0) {
+            const bool us = idcg > 0.0;
+            qual[u] = q ? 1.0 : 0.0;
+            hit[u] = (q && h) ? 1.0 : 0.0;
+            used[u] = us ? 1.0 : 0.0;
+            ratio[u] = us ? dcg / idcg : 0.0;
+        }
+    }
+}
+
 }  // namespace cals

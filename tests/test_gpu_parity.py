@@ -364,6 +364,64 @@ def test_predict_entries_and_full():
     assert cb.predict(F, 3, 4) == pytest.approx(float(F.user_factors[3] @ F.item_factors[4]))
     with pytest.raises(IndexError):
         cb.predict_entries(F, [50], [0])
+    # predict_full (als.py:155-157) on the device, float64: ragged tile edges and row blocks
+    for nu, ni, nf in [(50, 40, 7), (130, 65, 64), (64, 129, 128), (1, 1, 1)]:
+        Fp = cb.FactorPair(rng.normal(size=(nu, nf)), rng.normal(size=(ni, nf)))
+        np.testing.assert_allclose(cb.predict_full(Fp), Fp.user_factors @ Fp.item_factors.T, rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(cb.predict_full(Fp, block_rows=33), Fp.user_factors @ Fp.item_factors.T,
+                                   rtol=1e-12, atol=1e-12)
+
+
+def _reference_rank_metrics(users, items, truths, scores, k_hit, thr, k_ndcg):
+    """Per-user loop with the reference's ordering rules (metrics.py:89-147), numpy."""
+    hits = n_qual = n_used = 0
+    total = 0.0
+    for u in np.unique(users):
+        sel = users == u
+        it, tr, sc = items[sel], truths[sel], scores[sel]
+        rank = np.lexsort((it, -sc))
+        tr_r = tr[rank]
+        rel = tr_r >= thr
+        if rel.any():
+            n_qual += 1
+            hits += bool(rel[:k_hit].any())
+        kk = min(k_ndcg, tr.size)
+        disc = 1.0 / np.log2(np.arange(2, kk + 2))
+        idcg = float(np.sort(tr)[::-1][:kk] @ disc)
+        if idcg > 0.0:
+            total += float(tr_r[:kk] @ disc) / idcg
+            n_used += 1
+    return hits, n_qual, total, n_used
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_device_ranking_metrics_ties_and_empty_users(seed):
+    """hit@k / ndcg@k ranked on the device (cals_rank_metrics): equal scores (duplicated
+    item factor rows) resolve to the smaller item, equal and negative truths, users without
+    held-out entries, one very long user segment."""
+    rng = np.random.default_rng(seed)
+    n_u, n_i, nf = 300, 120, 6
+    M = rng.normal(size=(n_i, nf))
+    M[1::3] = M[0:-1:3][: M[1::3].shape[0]]  # pairs of identical items: tied scores
+    F = cb.FactorPair(rng.normal(size=(n_u, nf)), M)
+    mask = rng.random((n_u, n_i)) < 0.08
+    mask[7] = True          # a long segment
+    mask[10:40] = False     # users without entries
+    hu, hi = np.nonzero(mask)
+    o = rng.permutation(hu.size)  # the held-out set arrives unordered
+    hu, hi = hu[o], hi[o]
+    hr = np.round(rng.normal(0.5, 1.0, hu.size), 1)  # many equal truths, some negative
+    sc = np.einsum("ef,ef->e", F.user_factors[hu], F.item_factors[hi])
+    for k_hit, thr, k_ndcg in [(1, 1.5, 1), (3, 0.7, 5), (10, 2.0, 200)]:
+        hits, n_qual, total, n_used = _reference_rank_metrics(hu, hi, hr, sc, k_hit, thr, k_ndcg)
+        assert cb.hit_at_k((hu, hi, hr), F, k_hit, threshold=thr) == hits / n_qual
+        assert cb.ndcg_at_k((hu, hi, hr), F, k_ndcg) == pytest.approx(total / n_used, rel=1e-12)
+    with pytest.raises(cb.DataError):
+        cb.hit_at_k((hu, hi, hr), F, 3, threshold=1e9)  # nobody qualifies
+    with pytest.raises(cb.DataError):
+        cb.ndcg_at_k((hu, hi, -np.abs(hr) - 1.0), F, 3)  # nonpositive ideal DCG everywhere
+    with pytest.raises(cb.DataError):
+        cb.ndcg_at_k((np.r_[hu, hu[:1]], np.r_[hi, hi[:1]], np.r_[hr, hr[:1]]), F, 3)  # duplicated pair
 
 
 def test_singular_row_raises_with_reference_context():
