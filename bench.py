@@ -44,7 +44,9 @@ UNIT = "ratings/s/iter"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 5 for large, more on the small configs so the timed region "
+                         "lasts long enough for the clock sampler: DEFAULT_STEPS)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
@@ -53,7 +55,15 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.steps is None:  # the CPU arm's steps are bounded samples of seconds each: 5 everywhere
+        args.steps = DEFAULT_STEPS.get(args.config, 5) if args.impl == "ours" else 5
+    return args
+
+
+# default timed steps per workload: the small configs take 0.2-20 ms per iteration, and nvidia-smi
+# delivers a sample every ~20 ms, so their timed region is stretched to ~1 s of iterations
+DEFAULT_STEPS = {"small": 2000, "medium": 300, "powerlaw": 50, "large": 5, "wide": 2}
 
 
 def measured_peaks():
@@ -84,6 +94,10 @@ class ClockSampler:
                  "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.perf_counter()  # nvidia-smi needs a few hundred ms to deliver its first sample
+            while not self.samples and time.perf_counter() - t0 < 3.0:
+                time.sleep(0.01)
+            self.samples.clear()  # keep only samples taken while the timed region runs
         except OSError:
             self.proc = None
         return self
