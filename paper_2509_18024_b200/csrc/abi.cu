@@ -25,7 +25,7 @@ constexpr int kItemRowsMin = 16384;  // slice rows per work item (sweep on the 5
 thread_local char g_err[256] = "";
 
 // explicit tuning (cals_set_tuning); zero / negative fields select the built-in defaults
-cals_tuning g_tuning = {0, -1.0f, -1, 0, 0, 0.0f, 0, 0, 0, 0};
+cals_tuning g_tuning = {0, -1.0f, -1, 0, 0, 0.0f, 0, 0, 0, 0, 0};
 int64_t g_big_cand_budget = 0, g_big_tile_budget = 0;  // debug overrides, see cals_debug_big_batch
 unsigned long long* g_stats = nullptr;  // debug counters (device), see cals_debug_stats
 
@@ -358,9 +358,14 @@ void launch_refine(const SweepArgs& A, cudaStream_t st, bool from_slice) {
 template <int NFP>
 void launch_solve(const SweepArgs& A, const int32_t* rows, int64_t count, cudaStream_t st) {
     if (count <= 0) return;
-    if (A.nf > 64) {
+    if (A.nf > 64 && A.ill_ratio == 0.f) {  // every system straight to the float64 elimination (comparison)
         ProfScope ps("solve_kernel", st);
         defer_all_kernel<<<(int)std::min<int64_t>((count + 255) / 256, (int64_t)dev().sms * 8), 256, 0, st>>>(
+            A, rows, count);
+    } else if (A.nf > 64) {  // fp32 register LU + float64 iterative refinement (sweep_solve_ir.cu)
+        ProfScope ps("solve_kernel", st);
+        allow_smem(solve_ir_kernel);
+        solve_ir_kernel<<<(int)std::min<int64_t>(count, (int64_t)dev().sms * 3), kIrN, solve_ir_smem(), st>>>(
             A, rows, count);
     } else {
         launch_solve_fp32<NFP>(A, rows, count, st);
@@ -722,6 +727,8 @@ int cals_plan_build(const int64_t* counts, int64_t n_rows, int n_f, double rate,
     meta->n_rows = n_rows;
     int nmax = small_nmax(n_f, rate);
     if (g_tuning.staged_max_rows > 0) nmax = std::min(nmax, g_tuning.staged_max_rows);
+    // above n_f = 64 the solve forms a staged row's residual from its slice (sweep_solve_ir.cu)
+    if (n_f > 64) nmax = std::min(nmax, kIrSliceN);
     std::vector<int32_t> small, big;
     for (int64_t i = 0; i < n_rows; ++i) {
         if (counts[i] <= 0) continue;

@@ -39,6 +39,10 @@ CONFIGS = {
                   sigma=1.0, min_count=1, rank=64, noise=0.3, n_f=64, lam=0.02, rate=0.1, iters=10),
     "wide": dict(n_users=10_000_000, n_items=1_000_000, kind="powerlaw", nnz=2_000_000_000, zipf=1.0, mu=4.5,
                  sigma=1.3, min_count=1, rank=128, noise=0.3, n_f=128, lam=0.01, rate=0.05, iters=5),
+    # wide at 1/100 scale (same row-length distributions and rank): profiling and parity runs of the
+    # n_f = 128 path that finish in seconds
+    "wide_s": dict(n_users=100_000, n_items=10_000, kind="powerlaw", nnz=20_000_000, zipf=1.0, mu=4.5,
+                   sigma=1.3, min_count=1, rank=128, noise=0.3, n_f=128, lam=0.01, rate=0.05, iters=5),
 }
 
 

@@ -500,7 +500,31 @@ def test_oracle_parity_ill_conditioned(n_f, item_rows, tuning):
         check_against_oracle(R, n_f, 0.01, 0.1, M0)
     finally:
         _lib.load().cals_debug_stats(None)
-    assert int(stats[15]) > 0  # the float64 path was exercised
+    if n_f <= 64:
+        assert int(stats[15]) > 0  # the float64 path was exercised
+    # above n_f = 64 the fp32 LU + float64 iterative refinement (sweep_solve_ir.cu) holds these
+    # systems itself; test_float64_elimination_above_64 sends them through the float64 elimination
+
+
+@pytest.mark.parametrize("n_f", [80, 128])
+def test_float64_elimination_above_64(n_f, tuning):
+    """ill_ratio = 0 sends every system above n_f = 64 straight to the float64 elimination
+    (refine_rb_kernel: the path the mixed-precision solve falls back to): same 1e-4 contract on
+    the ill-conditioned matrix, and every system is counted as refined."""
+    from paper_2509_18024_b200 import _lib
+    tuning(ill_ratio=0.0)
+    u, i, v = random_matrix(n_f + 50, 1500, 300, 0.05, heavy_items=6, heavy_density=0.9)
+    R = cb.RatingMatrix(u, i, v, n_users=1500, n_items=300)
+    rng = np.random.default_rng(3)
+    base = rng.normal(0.0, 3.0, (300, 1))
+    M0 = (base + 0.05 * rng.normal(0.0, 3.0, (300, n_f))).astype(np.float32)
+    stats = torch.zeros(16, dtype=torch.int64, device="cuda")
+    _lib.load().cals_debug_stats(stats.data_ptr())
+    try:
+        check_against_oracle(R, n_f, 0.01, 0.1, M0)
+    finally:
+        _lib.load().cals_debug_stats(None)
+    assert int(stats[15]) >= int((np.diff(R.row_ptr) > 0).sum())
 
 
 @pytest.mark.parametrize("n_f,tune", [(16, None), (64, None), (64, dict(gram_path=1)),
