@@ -291,6 +291,7 @@ struct Work {
     int* icnt;          // [tiles][nf] per-item in-bracket counts (big_scan2)
     int* rf_cnt;        // [4]: per stream, rows deferred to the float64 refinement from the stored
     int64_t* rf_list;   // equations [2][gbuf_rows] (row << 32 | slot), and from the slice:
+    int64_t* ir_list;   // [2][gbuf_rows]: systems handed to the mixed-precision solve (counters rf_cnt[4..5])
     int32_t* rs_list;   // [2][n_rows] rows
 };
 
@@ -322,8 +323,9 @@ Work carve(const cals_plan* P, void* ws, size_t* total) {
     w.tc_scale = c.take<float>(65);
     w.tc_alpha = c.take<double>(65);
     w.item_ctr = c.take<int>(1);
-    w.rf_cnt = c.take<int>(4);
+    w.rf_cnt = c.take<int>(8);
     w.rf_list = c.take<int64_t>((size_t)2 * w.gbuf_rows);
+    w.ir_list = c.take<int64_t>((size_t)2 * w.gbuf_rows);
     w.rs_list = c.take<int32_t>((size_t)2 * std::max<int64_t>(P->n_rows, 1));
     *total = c.off + 256;
     return w;
@@ -364,11 +366,18 @@ void launch_solve(const SweepArgs& A, const int32_t* rows, int64_t count, cudaSt
             A, rows, count);
     } else if (A.nf > 64) {  // fp32 register LU + float64 iterative refinement (sweep_solve_ir.cu)
         ProfScope ps("solve_kernel", st);
-        allow_smem(solve_ir_kernel);
-        solve_ir_kernel<<<(int)std::min<int64_t>(count, (int64_t)dev().sms * 3), kIrN, solve_ir_smem(), st>>>(
+        allow_smem(solve_ir_kernel<128>);
+        solve_ir_kernel<128><<<(int)std::min<int64_t>(count, (int64_t)dev().sms * 3), 128, solve_ir_smem(128), st>>>(
             A, rows, count);
     } else {
         launch_solve_fp32<NFP>(A, rows, count, st);
+        if (A.ir_list != nullptr) {  // 32 < n_f <= 64: its ill-conditioned systems, mixed precision
+            ProfScope ps("solve_ir_kernel", st);
+            allow_smem(solve_ir_kernel<64>);
+            solve_ir_kernel<64><<<(int)std::min<int64_t>(count, (int64_t)dev().sms * 8), 64, solve_ir_smem(64), st>>>(
+                A, nullptr, 0);
+            cudaMemsetAsync(A.ir_cnt, 0, sizeof(int), st);
+        }
     }
     launch_refine(A, st, false);  // systems that need this batch's stored equations
 }
@@ -822,8 +831,10 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.rf_list = w.rf_list;
     A.rs_cnt = w.rf_cnt + 2;
     A.rs_list = w.rs_list;
+    A.ir_cnt = w.rf_cnt + 4;
+    A.ir_list = (n_f > 32 && n_f <= 64 && A.ill_ratio != 0.f) ? w.ir_list : nullptr;
     A.rf_slice_max = g_tuning.rf_slice_max >= 0 ? g_tuning.rf_slice_max : kRfSliceMax;
-    cudaMemsetAsync(w.rf_cnt, 0, 4 * sizeof(int), st);
+    cudaMemsetAsync(w.rf_cnt, 0, 8 * sizeof(int), st);
     A.gbuf = w.gbuf;
     A.stats = g_stats;
     A.status = row_status;
@@ -860,6 +871,8 @@ int cals_core_half_sweep(const cals_side* side, const cals_plan* P, const float*
         As.rf_list = w.rf_list + w.gbuf_rows;
         As.rs_cnt = w.rf_cnt + 3;
         As.rs_list = w.rs_list + std::max<int64_t>(P->n_rows, 1);
+        As.ir_cnt = w.rf_cnt + 5;
+        if (As.ir_list != nullptr) As.ir_list = w.ir_list + w.gbuf_rows;
         ss = dev().side;
         cudaEventRecord(dev().fork, st);
         cudaStreamWaitEvent(ss, dev().fork, 0);
@@ -986,8 +999,10 @@ int cals_fast_half_sweep(const cals_side* side, const cals_plan* P, const float*
     A.rf_list = w.rf_list;
     A.rs_cnt = w.rf_cnt + 2;
     A.rs_list = w.rs_list;
+    A.ir_cnt = w.rf_cnt + 4;
+    A.ir_list = (n_f > 32 && n_f <= 64 && A.ill_ratio != 0.f) ? w.ir_list : nullptr;
     A.rf_slice_max = 0;  // fast_core rows keep their stored equations (whole-source sketch)
-    cudaMemsetAsync(w.rf_cnt, 0, 4 * sizeof(int), st);
+    cudaMemsetAsync(w.rf_cnt, 0, 8 * sizeof(int), st);
     A.gbuf = w.gbuf;
     A.stats = g_stats;
     A.status = row_status;

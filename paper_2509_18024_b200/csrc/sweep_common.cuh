@@ -42,6 +42,8 @@ struct SweepArgs {
     int* rs_cnt;                  // rows deferred that rebuild their Gram from the slice: refined once
     int32_t* rs_list;             // after the tier's last batch (one launch, no per-batch latency)
     int rf_slice_max;             // rows up to this length rebuild from the slice (0: none)
+    int* ir_cnt;                  // 32 < n_f <= 64: systems the fp32 solve hands to the mixed-precision
+    int64_t* ir_list;             // solve (sweep_solve_ir.cu), (row << 32 | slot), per batch
     float ill_ratio;              // pivot-magnitude spread that defers a system (ill_ratio_for)
 };
 
@@ -54,6 +56,12 @@ __device__ __forceinline__ void defer_refine(const SweepArgs& A, int row, int64_
         const int at = atomicAdd(A.rf_cnt, 1);
         A.rf_list[at] = ((int64_t)row << 32) | (int64_t)(uint32_t)slot;
     }
+}
+
+// 32 < n_f <= 64: an ill-conditioned system first goes to the fp32 LU + float64 iterative
+// refinement (which defers to the float64 elimination what it cannot hold).
+__device__ __forceinline__ void defer_ir(const SweepArgs& A, int row, int64_t slot) {
+    A.ir_list[atomicAdd(A.ir_cnt, 1)] = ((int64_t)row << 32) | (int64_t)(uint32_t)slot;
 }
 
 // Debug counters (only when A.stats != nullptr): see cals_debug_stats.

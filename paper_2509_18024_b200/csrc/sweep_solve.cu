@@ -87,7 +87,10 @@ __global__ void __launch_bounds__(128, 3) solve_wide_kernel(SweepArgs A, const i
         float x0, x1;
         const int st = CALS_ROW_OK;
         if (wide_lu_solve<NF>(W, nf, spd, A.ill_ratio, x0, x1, lane)) {  // the float64 refinement owns the row
-            if (lane == 0) defer_refine(A, row, li);
+            if (lane == 0) {
+                if (A.ir_list != nullptr) defer_ir(A, row, li);  // mixed-precision solve first (sweep_solve_ir.cu)
+                else defer_refine(A, row, li);
+            }
             continue;
         }
         float* out = A.tgt + (int64_t)row * A.ld_tgt;

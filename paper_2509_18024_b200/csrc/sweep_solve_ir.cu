@@ -1,9 +1,10 @@
-// sweep_solve_ir.cu -- phase B above n_f = 64: mixed-precision solve of the
-// sketched normal equations (core.py:120-131, _kernels.py:233-236: LAPACK gesv
+// sweep_solve_ir.cu -- mixed-precision solve of the sketched normal equations:
+// every system above n_f = 64, and at 32 < n_f <= 64 the systems the fp32 warp
+// LU (solve_wide_kernel) found ill-conditioned (core.py:120-131, _kernels.py:233-236: LAPACK gesv
 // on the float64 system).
 //
-// The float64 system stays in the batch buffer; a CTA of 128 threads factors
-// its fp32 rounding with a register-resident LU (thread r owns row r, 128
+// The float64 system stays in the batch buffer; a CTA of N = 64 / 128 threads factors
+// its fp32 rounding with a register-resident LU (thread r owns row r, N
 // columns in registers, partial pivoting without row swaps: the pivot row of a
 // step is published through shared memory and every unused row eliminates
 // against it), then refines the solution against the float64 system:
@@ -31,32 +32,32 @@
 // ever reports CALS_ROW_OK.  A complete sketch (s == n, als.py:184-205)
 // eliminates without pivoting and defers on a non-positive pivot.
 //
-// Three CTAs per SM (66 KB of shared memory each: the fp32 copy of the system,
-// then the packed factors in pivot order for the triangular solves).
+// N = 128: three CTAs per SM (66 KB of shared memory each: the fp32 copy of the
+// system, then the packed factors for the triangular solves); N = 64: eight.
 #include "solve.cuh"
 #include "sweep_common.cuh"
 
 namespace cals {
 
-constexpr int kIrN = 128;          // padded order: thread r owns row r
-constexpr int kIrLd = kIrN + 1;    // shared-memory row stride (conflict-free column walks)
+constexpr int kIrN = 128;          // largest padded order (thread r owns row r); the kernel is built for 64 and 128
 constexpr int kIrMaxIt = 6;        // corrections before the float64 pass takes over
 constexpr int kIrSliceN = 448;     // rows up to this length (and rf_slice_max) take the slice residual; the staged
                                    // tier holds no longer row above n_f = 64 (cals_plan_build)
 constexpr float kIrTol = 1e-6f;    // rho * |d| <= kIrTol * |x|
 constexpr float kIrRhoMax = 0.5f;  // slowest accepted contraction
 
-__host__ __device__ inline size_t solve_ir_smem() { return (size_t)kIrN * kIrLd * sizeof(float); }
+__host__ __device__ inline size_t solve_ir_smem(int N) { return (size_t)N * (N + 1) * sizeof(float); }
 
+template <int N>
 struct IrShared {
-    float prow[2][kIrN + 8];  // pivot row of the step: columns, [128] rhs, [129] the pivot itself
-    uint32_t key[2][4];       // per-warp pivot candidates
-    double xd[kIrN];          // the solution, float64
-    float rhs[kIrN];          // right-hand side in pivot order
-    float xs[kIrN];           // solved block values of the triangular solves
-    float dinv[kIrN];         // 1 / U_tt
-    int perm[kIrN];           // equation e was the pivot row of step perm[e]
-    int inv[kIrN];            // ... and step t pivoted on equation inv[t]
+    float prow[2][N + 8];  // pivot row of the step: columns, [128] rhs, [129] the pivot itself
+    uint32_t key[2][4];       // per-warp pivot candidates (N / 32 used)
+    double xd[N];          // the solution, float64
+    float rhs[N];          // right-hand side in pivot order
+    float xs[N];           // solved block values of the triangular solves
+    float dinv[N];         // 1 / U_tt
+    int perm[N];           // equation e was the pivot row of step perm[e]
+    int inv[N];            // ... and step t pivoted on equation inv[t]
     float red[4];
     double pen[4];
     double t[kIrSliceN];      // slice residual: y_k - x_k . x
@@ -73,8 +74,8 @@ __device__ __forceinline__ void ffma2_sv(float& d0, float& d1, unsigned long lon
 }
 
 // a[B0 + i] for a CTA-uniform runtime i in [0, 16): a jump table instead of a 16-way select chain
-template <int B0>
-__device__ __forceinline__ float ir_pick(const float (&a)[kIrN], int i) {
+template <int N, int B0>
+__device__ __forceinline__ float ir_pick(const float (&a)[N], int i) {
     switch (i) {
         case 0: return a[B0 + 0];
         case 1: return a[B0 + 1];
@@ -99,14 +100,14 @@ __device__ __forceinline__ float ir_pick(const float (&a)[kIrN], int i) {
 // the thread's row comes from a 16-way register select; the update sweeps columns
 // j >= B0, the pivot row publishing zeros at j <= K so the multipliers stored left of
 // K survive.
-template <int B0>
-__device__ __forceinline__ bool ir_block(float (&a)[kIrN], float& rhs, bool& used, int& ord, float& diag, IrShared& S,
+template <int N, int B0>
+__device__ __forceinline__ bool ir_block(float (&a)[N], float& rhs, bool& used, int& ord, float& diag, IrShared<N>& S,
                                          float* __restrict__ Lrow, int nf, bool spd, int r, int lane, int warp) {
 #pragma unroll 1
     for (int K = B0; K < B0 + 16; ++K) {
         if (K >= nf) return false;
         const int par = K & 1;
-        const float ck = ir_pick<B0>(a, K - B0);
+        const float ck = ir_pick<N, B0>(a, K - B0);
         int p = K;
         if (!spd) {
             // largest |a[r][K]| over the unused rows, ties (to 2^-16 relative) to the smallest row:
@@ -115,8 +116,9 @@ __device__ __forceinline__ bool ir_block(float (&a)[kIrN], float& rhs, bool& use
             const uint32_t wbest = __reduce_max_sync(CALS_FULL_MASK, mine);
             if (lane == 0) S.key[par][warp] = wbest;
             __syncthreads();
-            const uint4 k4 = *reinterpret_cast<const uint4*>(S.key[par]);
-            const uint32_t best = max(max(k4.x, k4.y), max(k4.z, k4.w));
+            uint32_t best = S.key[par][0];
+#pragma unroll
+            for (int w = 1; w < N / 32; ++w) best = max(best, S.key[par][w]);
             if ((best >> 7) == 0u) return true;  // no nonzero finite candidate (NaN keys are caught below)
             p = 127 - (int)(best & 127u);
         }
@@ -130,14 +132,14 @@ __device__ __forceinline__ bool ir_block(float (&a)[kIrN], float& rhs, bool& use
                 *reinterpret_cast<float4*>(pr + j) = make_float4(j + 0 > K ? a[j + 0] : 0.f, j + 1 > K ? a[j + 1] : 0.f,
                                                                  j + 2 > K ? a[j + 2] : 0.f, j + 3 > K ? a[j + 3] : 0.f);
 #pragma unroll
-            for (int j = B0 + 16; j < kIrN; j += 4)
+            for (int j = B0 + 16; j < N; j += 4)
                 *reinterpret_cast<float4*>(pr + j) = make_float4(a[j], a[j + 1], a[j + 2], a[j + 3]);
-            pr[kIrN] = rhs;
-            pr[kIrN + 1] = ck;
+            pr[N] = rhs;
+            pr[N + 1] = ck;
         }
         __syncthreads();
         const float* pr = S.prow[par];
-        const float d = pr[kIrN + 1];
+        const float d = pr[N + 1];
         if (spd ? !(d > 0.f) : !(fabsf(d) <= 3.0e38f)) return true;  // breakdown: uniform (every thread reads d)
         const float f = used ? 0.f : ck * __frcp_rn(d);
         if (!used) Lrow[K] = f;  // the multiplier (L entry) goes straight to the packed factors
@@ -145,35 +147,36 @@ __device__ __forceinline__ bool ir_block(float (&a)[kIrN], float& rhs, bool& use
         unsigned long long nf2;
         asm("mov.b64 %0, {%1, %1};" : "=l"(nf2) : "f"(nf1));
 #pragma unroll
-        for (int j = B0; j < kIrN; j += 4) {
+        for (int j = B0; j < N; j += 4) {
             const float4 v = *reinterpret_cast<const float4*>(pr + j);
             ffma2_sv(a[j + 0], a[j + 1], nf2, v.x, v.y);
             ffma2_sv(a[j + 2], a[j + 3], nf2, v.z, v.w);
         }
-        rhs = fmaf(nf1, pr[kIrN], rhs);
+        rhs = fmaf(nf1, pr[N], rhs);
     }
     return false;
 }
 
-template <int... Q>
-__device__ __forceinline__ bool ir_eliminate(float (&a)[kIrN], float& rhs, bool& used, int& ord, float& diag,
-                                             IrShared& S, float* __restrict__ Lrow, int nf, bool spd, int r, int lane,
+template <int N, int... Q>
+__device__ __forceinline__ bool ir_eliminate(float (&a)[N], float& rhs, bool& used, int& ord, float& diag,
+                                             IrShared<N>& S, float* __restrict__ Lrow, int nf, bool spd, int r, int lane,
                                              int warp, std::integer_sequence<int, Q...>) {
     bool fail = false;
-    ((fail = fail || ir_block<16 * Q>(a, rhs, used, ord, diag, S, Lrow, nf, spd, r, lane, warp)), ...);
+    ((fail = fail || ir_block<N, 16 * Q>(a, rhs, used, ord, diag, S, Lrow, nf, spd, r, lane, warp)), ...);
     return fail;
 }
 
 // U x = rhs over the packed factors (pivot-order row t = stored row S.inv[t]: L left of column t, U
 // from it); thread t owns pivot-order row t.  Blocks of 32: the owning warp solves its diagonal block by
 // shuffles, the rows above subtract the block's contribution.
-__device__ __forceinline__ float ir_solve_upper(const float* __restrict__ LU, IrShared& S, float rhs, int t, int lane,
+template <int N>
+__device__ __forceinline__ float ir_solve_upper(const float* __restrict__ LU, IrShared<N>& S, float rhs, int t, int lane,
                                                 int warp) {
-    const float* row = LU + S.inv[t] * kIrLd;
+    const float* row = LU + S.inv[t] * (N + 1);
     const float di = S.dinv[t];
     float x = 0.f;
 #pragma unroll
-    for (int B = 3; B >= 0; --B) {
+    for (int B = N / 32 - 1; B >= 0; --B) {
         if (warp == B) {
 #pragma unroll
             for (int k = 31; k >= 0; --k) {
@@ -201,11 +204,12 @@ __device__ __forceinline__ float ir_solve_upper(const float* __restrict__ LU, Ir
 }
 
 // L y = rhs (unit diagonal), same blocking, forward.
-__device__ __forceinline__ float ir_solve_lower(const float* __restrict__ LU, IrShared& S, float rhs, int t, int lane,
+template <int N>
+__device__ __forceinline__ float ir_solve_lower(const float* __restrict__ LU, IrShared<N>& S, float rhs, int t, int lane,
                                                 int warp) {
-    const float* row = LU + S.inv[t] * kIrLd;
+    const float* row = LU + S.inv[t] * (N + 1);
 #pragma unroll
-    for (int B = 0; B < 4; ++B) {
+    for (int B = 0; B < N / 32; ++B) {
         if (warp == B) {
 #pragma unroll
             for (int k = 0; k < 31; ++k) {
@@ -214,7 +218,7 @@ __device__ __forceinline__ float ir_solve_lower(const float* __restrict__ LU, Ir
             }
             S.xs[t] = rhs;
         }
-        if (B < 3) {
+        if (B < N / 32 - 1) {
             __syncthreads();
             if (warp > B) {
 #pragma unroll
@@ -232,95 +236,109 @@ __device__ __forceinline__ float ir_solve_lower(const float* __restrict__ LU, Ir
 }
 
 // max over the CTA of a non-negative float (uniform result)
-__device__ __forceinline__ float ir_block_max(float v, IrShared& S, int lane, int warp) {
+template <int N>
+__device__ __forceinline__ float ir_block_max(float v, IrShared<N>& S, int lane, int warp) {
     const uint32_t w = __reduce_max_sync(CALS_FULL_MASK, __float_as_uint(v));
     __syncthreads();
     if (lane == 0) S.red[warp] = __uint_as_float(w);
     __syncthreads();
-    return fmaxf(fmaxf(S.red[0], S.red[1]), fmaxf(S.red[2], S.red[3]));
+    float m = S.red[0];
+#pragma unroll
+    for (int w = 1; w < N / 32; ++w) m = fmaxf(m, S.red[w]);
+    return m;
 }
 
-__global__ void __launch_bounds__(kIrN, 3) solve_ir_kernel(SweepArgs A, const int32_t* __restrict__ rows,
-                                                           int64_t n_list) {
+// rows != nullptr: the batch's systems rows[li], equations in slot li (n_f > 64: every system).
+// rows == nullptr: the systems the fp32 solve deferred, (row << 32 | slot) entries of A.ir_list
+// (32 < n_f <= 64).
+template <int N>
+__global__ void __launch_bounds__(N, N == 128 ? 3 : 8) solve_ir_kernel(SweepArgs A, const int32_t* __restrict__ rows,
+                                                                        int64_t n_rows) {
+    constexpr int LD = N + 1;  // shared-memory row stride (conflict-free column walks)
+    constexpr int NW = N / 32;
+    constexpr int MC = N / 32 + 1;  // 32-column groups of an augmented row
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ __align__(16) IrShared S;
+    __shared__ __align__(16) IrShared<N> S;
     float* LU = reinterpret_cast<float*>(smem);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nf = A.nf, gs = nf + 1;
+    const int64_t n_list = rows != nullptr ? n_rows : (int64_t)*A.ir_cnt;
     for (int64_t li = blockIdx.x; li < n_list; li += gridDim.x) {
-        const int row = rows[li];
+        const int64_t ent = rows != nullptr ? (((int64_t)rows[li] << 32) | li) : A.ir_list[li];
+        const int row = (int)(ent >> 32);
+        const int64_t slot = (int64_t)(uint32_t)ent;
         const int n = (int)(A.ptr[row + 1] - A.ptr[row]);
         const bool spd = A.budget[row] >= n;
-        const double* __restrict__ G = A.gbuf + (size_t)li * nf * gs;
+        const double* __restrict__ G = A.gbuf + (size_t)slot * nf * gs;
         const int64_t lo = A.ptr[row];
         // short rows (fp32-summed equations): the residual comes from the slice
         const bool slice = n <= kIrSliceN && n <= A.rf_slice_max;
         const uint64_t thr = (slice && tid < nf) ? A.thr_keys[(int64_t)row * nf + tid] : 0ull;
         __syncthreads();  // the previous system's factors are consumed
         if (slice)
-            for (int k = tid; k < n; k += kIrN) S.idx[k] = __ldg(A.idx + lo + k);
+            for (int k = tid; k < n; k += N) S.idx[k] = __ldg(A.idx + lo + k);
         // ---- the system, rounded to fp32, into shared memory (warp per row, coalesced) ----
-        for (int i0 = warp; i0 < nf; i0 += 16) {
-            double v[4][5];
+        for (int i0 = warp; i0 < nf; i0 += 4 * NW) {
+            double v[4][MC];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int i = i0 + 4 * u;
+                const int i = i0 + NW * u;
 #pragma unroll
-                for (int m = 0; m < 5; ++m) {
+                for (int m = 0; m < MC; ++m) {
                     const int j = lane + 32 * m;
                     v[u][m] = (i < nf && j < gs) ? __ldcs(G + (size_t)i * gs + j) : 0.0;
                 }
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int i = i0 + 4 * u;
+                const int i = i0 + NW * u;
 #pragma unroll
-                for (int m = 0; m < 5; ++m) {
+                for (int m = 0; m < MC; ++m) {
                     const int j = lane + 32 * m;
-                    if (i < nf && j < gs) LU[i * kIrLd + j] = (float)v[u][m];
+                    if (i < nf && j < gs) LU[i * LD + j] = (float)v[u][m];
                 }
             }
         }
         __syncthreads();
-        if (li + gridDim.x < n_list) {  // the CTA's next system on its way into L2 meanwhile
+        if (rows != nullptr && li + gridDim.x < n_list) {  // the CTA's next system on its way into L2 meanwhile
             const char* nx = reinterpret_cast<const char*>(A.gbuf + (size_t)(li + gridDim.x) * nf * gs);
-            for (int off = tid * 128; off < nf * gs * 8; off += kIrN * 128)
+            for (int off = tid * 128; off < nf * gs * 8; off += N * 128)
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + off));
         }
         // ---- thread r takes row r; rows / columns beyond nf are identity padding ----
-        float a[kIrN];
+        float a[N];
         float rhs = 0.f;
         const int r = tid;
         if (r < nf) {
 #pragma unroll
-            for (int j = 0; j < kIrN; ++j) a[j] = j < nf ? LU[r * kIrLd + j] : 0.f;
-            rhs = LU[r * kIrLd + nf];
+            for (int j = 0; j < N; ++j) a[j] = j < nf ? LU[r * LD + j] : 0.f;
+            rhs = LU[r * LD + nf];
         } else {
 #pragma unroll
-            for (int j = 0; j < kIrN; ++j) a[j] = j == r ? 1.f : 0.f;
+            for (int j = 0; j < N; ++j) a[j] = j == r ? 1.f : 0.f;
         }
         bool used = r >= nf;  // padding rows never pivot: they keep step r
         int ord = r;
         float diag = 1.f;
-        bool fail = ir_eliminate(a, rhs, used, ord, diag, S, LU + r * kIrLd, nf, spd, r, lane, warp,
-                                 std::make_integer_sequence<int, kIrN / 16>{});
+        bool fail = ir_eliminate<N>(a, rhs, used, ord, diag, S, LU + r * LD, nf, spd, r, lane, warp,
+                                    std::make_integer_sequence<int, N / 16>{});
         fail = fail || __syncthreads_or(!used);  // every row pivoted (uniform)
         int st = -1;                            // -1: deferred to the float64 pass
         if (!fail) {
             // ---- the U part of the row joins its multipliers in shared memory (row r stays row r;
             // the triangular solves walk the rows in pivot order through S.inv) ----
 #pragma unroll
-            for (int j = 0; j < kIrN; ++j)
-                if (j >= ord) LU[r * kIrLd + j] = a[j];
+            for (int j = 0; j < N; ++j)
+                if (j >= ord) LU[r * LD + j] = a[j];
             S.dinv[ord] = __frcp_rn(diag);
             S.rhs[ord] = rhs;
             S.perm[r] = ord;
             S.inv[ord] = r;
             __syncthreads();
             const int t = tid;
-            float x0 = ir_solve_upper(LU, S, S.rhs[t], t, lane, warp);
+            float x0 = ir_solve_upper<N>(LU, S, S.rhs[t], t, lane, warp);
             double x = (double)x0;
-            float prev = ir_block_max(fabsf(x0), S, lane, warp);  // |x0|: the "correction" before the first
+            float prev = ir_block_max<N>(fabsf(x0), S, lane, warp);  // |x0|: the "correction" before the first
             if (!(prev <= 3.0e38f)) fail = true;
             for (int it = 0; it < kIrMaxIt && !fail && st < 0; ++it) {
                 S.xd[t] = x;
@@ -331,18 +349,18 @@ __global__ void __launch_bounds__(kIrN, 3) solve_ir_kernel(SweepArgs A, const in
                     double xq[4];
 #pragma unroll
                     for (int q = 0; q < 4; ++q) xq[q] = 4 * lane + q < nf ? S.xd[4 * lane + q] : 0.0;
-                    for (int k0 = warp; k0 < n; k0 += 16) {
+                    for (int k0 = warp; k0 < n; k0 += 4 * NW) {
                         float4 v[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            const int k = k0 + 4 * u;
+                            const int k = k0 + NW * u;
                             v[u] = (k < n && 4 * lane < nf)
                                        ? __ldg(reinterpret_cast<const float4*>(A.src + (int64_t)S.idx[k] * A.ld_src) + lane)
                                        : make_float4(0.f, 0.f, 0.f, 0.f);
                         }
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            const int k = k0 + 4 * u;
+                            const int k = k0 + NW * u;
                             double p = (double)v[u].x * xq[0];
                             p = fma((double)v[u].y, xq[1], p);
                             p = fma((double)v[u].z, xq[2], p);
@@ -372,37 +390,37 @@ __global__ void __launch_bounds__(kIrN, 3) solve_ir_kernel(SweepArgs A, const in
                         S.rhs[S.perm[t]] = (float)(acc - A.lam * (double)n * x);
                     }
                 } else {
-                // r = b - G x in float64 from the stored equations: warp per equation, lanes over columns
-                for (int e0 = warp; e0 < nf; e0 += 16) {
-                    double acc[4];
+                    // r = b - G x in float64 from the stored equations: warp per equation, lanes over columns
+                    for (int e0 = warp; e0 < nf; e0 += 4 * NW) {
+                        double acc[4];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int e = e0 + 4 * u;
-                        acc[u] = 0.0;
-                        if (e < nf) {
-                            const double* g = G + (size_t)e * gs;
+                        for (int u = 0; u < 4; ++u) {
+                            const int e = e0 + NW * u;
+                            acc[u] = 0.0;
+                            if (e < nf) {
+                                const double* g = G + (size_t)e * gs;
 #pragma unroll
-                            for (int m = 0; m < 4; ++m) {
-                                const int j = lane + 32 * m;
-                                if (j < nf) acc[u] = fma(__ldg(g + j), S.xd[j], acc[u]);
+                                for (int m = 0; m < NW; ++m) {
+                                    const int j = lane + 32 * m;
+                                    if (j < nf) acc[u] = fma(__ldg(g + j), S.xd[j], acc[u]);
+                                }
                             }
                         }
-                    }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int e = e0 + 4 * u;
-                        const double s = warp_sum_d(acc[u]);
-                        if (lane == 0 && e < nf) S.rhs[S.perm[e]] = (float)(__ldg(G + (size_t)e * gs + nf) - s);
+                        for (int u = 0; u < 4; ++u) {
+                            const int e = e0 + NW * u;
+                            const double sm = warp_sum_d(acc[u]);
+                            if (lane == 0 && e < nf) S.rhs[S.perm[e]] = (float)(__ldg(G + (size_t)e * gs + nf) - sm);
+                        }
                     }
-                }
                 }
                 __syncthreads();
-                const float y = ir_solve_lower(LU, S, S.rhs[t], t, lane, warp);
+                const float y = ir_solve_lower<N>(LU, S, S.rhs[t], t, lane, warp);
                 __syncthreads();  // the lower solve's last block values are read before the upper solve rewrites them
-                const float d = ir_solve_upper(LU, S, y, t, lane, warp);
+                const float d = ir_solve_upper<N>(LU, S, y, t, lane, warp);
                 x += (double)d;
-                const float dn = ir_block_max(fabsf(d), S, lane, warp);
-                const float xn = ir_block_max(fabsf((float)x), S, lane, warp);
+                const float dn = ir_block_max<N>(fabsf(d), S, lane, warp);
+                const float xn = ir_block_max<N>(fabsf((float)x), S, lane, warp);
                 if (!(dn <= 3.0e38f)) { fail = true; break; }
                 // contraction measured between two corrections (the first one is compared with |x0|, which
                 // only bounds it: x0 also carries the fp32 rounding of the equations, so the first
@@ -419,7 +437,12 @@ __global__ void __launch_bounds__(kIrN, 3) solve_ir_kernel(SweepArgs A, const in
                     const double p = warp_sum_d(t < nf ? (double)xf * (double)xf : 0.0);
                     if (lane == 0) S.pen[warp] = p;
                     __syncthreads();
-                    if (tid == 0) A.pen_rows[row] = (double)n * (((S.pen[0] + S.pen[1]) + S.pen[2]) + S.pen[3]);
+                    if (tid == 0) {
+                        double ps = S.pen[0];
+#pragma unroll
+                        for (int w = 1; w < NW; ++w) ps += S.pen[w];
+                        A.pen_rows[row] = (double)n * ps;
+                    }
                 }
                 if (tid == 0) {
                     A.status[row] = CALS_ROW_OK;
@@ -427,8 +450,10 @@ __global__ void __launch_bounds__(kIrN, 3) solve_ir_kernel(SweepArgs A, const in
                 }
             }
         }
-        if (st < 0 && tid == 0) defer_refine(A, row, li);  // the float64 elimination owns the row
+        if (st < 0 && tid == 0) defer_refine(A, row, slot);  // the float64 elimination owns the row
     }
 }
+template __global__ void solve_ir_kernel<64>(SweepArgs, const int32_t*, int64_t);
+template __global__ void solve_ir_kernel<128>(SweepArgs, const int32_t*, int64_t);
 
 }  // namespace cals

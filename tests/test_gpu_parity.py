@@ -500,15 +500,15 @@ def test_oracle_parity_ill_conditioned(n_f, item_rows, tuning):
         check_against_oracle(R, n_f, 0.01, 0.1, M0)
     finally:
         _lib.load().cals_debug_stats(None)
-    if n_f <= 64:
+    if n_f <= 32:
         assert int(stats[15]) > 0  # the float64 path was exercised
-    # above n_f = 64 the fp32 LU + float64 iterative refinement (sweep_solve_ir.cu) holds these
-    # systems itself; test_float64_elimination_above_64 sends them through the float64 elimination
+    # above n_f = 32 the fp32 LU + float64 iterative refinement (sweep_solve_ir.cu) holds most of
+    # these systems itself; test_float64_elimination sends them through the float64 elimination
 
 
-@pytest.mark.parametrize("n_f", [80, 128])
-def test_float64_elimination_above_64(n_f, tuning):
-    """ill_ratio = 0 sends every system above n_f = 64 straight to the float64 elimination
+@pytest.mark.parametrize("n_f", [48, 64, 80, 128])
+def test_float64_elimination(n_f, tuning):
+    """ill_ratio = 0 sends every system above n_f = 32 straight to the float64 elimination
     (refine_rb_kernel: the path the mixed-precision solve falls back to): same 1e-4 contract on
     the ill-conditioned matrix, and every system is counted as refined."""
     from paper_2509_18024_b200 import _lib

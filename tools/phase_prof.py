@@ -1,6 +1,6 @@
 """Per-kernel event-timed breakdown of full iterations of a config under several
 tuning variants (one process, one dataset):  python tools/phase_prof.py large
-"default" "serial_tiers=1" "cand=29" ...   Each variant: 2 warm-up + 2 timed iterations."""
+"default" "serial_tiers=1" "cand=29" ...   Each variant: 2 (or $WARM) warm-up + 2 timed iterations."""
 import json
 import os
 import sys
@@ -33,9 +33,12 @@ for var in sys.argv[2:]:
     L.cals_debug_big_batch(cand, 0)
     eng = CoreEngine(d, spec["n_f"], spec["rate"], spec["lam"])
     eng.set_factors(np.zeros((d.n_users, spec["n_f"]), np.float32), M0)
-    for _ in range(2):
+    eng.use_graphs = False  # eager launches: the event profile needs them
+    for _ in range(int(os.environ.get("WARM", "2"))):  # WARM=8: factors of a later iteration
         eng.step("user")
     torch.cuda.synchronize()
+    stats = torch.zeros(16, dtype=torch.int64, device="cuda")
+    L.cals_debug_stats(stats.data_ptr())
     _lib.profile_enable(True)
     _lib.profile_collect()
     t0 = time.perf_counter()
@@ -47,6 +50,8 @@ for var in sys.argv[2:]:
     torch.cuda.synchronize()
     prof = _lib.profile_collect()
     _lib.profile_enable(False)
+    L.cals_debug_stats(None)
+    print("float64-pass systems per iteration:", int(stats[15]) // 2, flush=True)
     ms = e0.elapsed_time(e1) / 2
     ks = {k: (c // 2, round(v / 2, 2)) for k, (c, v) in sorted(prof.items(), key=lambda kv: -kv[1][1])}
     print(json.dumps({"variant": var, "ms_per_iter": round(ms, 2), "kernels(launches, ms per iter)": ks}), flush=True)
