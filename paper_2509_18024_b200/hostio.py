@@ -54,12 +54,42 @@ def upload(a, dtype, device):
 
 
 def download_f64(t):
-    """Device tensor -> float64 numpy array (widened on the device, copied into
-    pinned memory that the returned array owns)."""
+    """Device tensor -> float64 numpy array: widened on the device, copied out in chunks
+    through two pinned staging buffers (torch's host allocator caches them across calls;
+    pinning a result-sized buffer per call costs more than the copy itself: 0.31 s for the
+    614 MB of the 500M config's factors) into an ordinary numpy array, the host copy of
+    one chunk overlapping the device read of the next."""
     import torch
 
-    d = t.to(torch.float64).contiguous()
-    host = torch.empty(d.shape, dtype=torch.float64, pin_memory=True)
-    host.copy_(d, non_blocking=True)
-    torch.cuda.current_stream(d.device).synchronize()
-    return host.numpy()
+    d = t.to(torch.float64).contiguous().reshape(-1)
+    n = d.numel()
+    out = np.empty(tuple(t.shape), dtype=np.float64)
+    if n == 0:
+        return out
+    dst = torch.from_numpy(out).reshape(-1)
+    chunk = max(1, _CHUNK_BYTES // 8)
+    if n <= chunk:
+        dst.copy_(d)
+        return out
+    bufs = [torch.empty(chunk, dtype=torch.float64, pin_memory=True) for _ in range(2)]
+    cur = torch.cuda.current_stream(d.device)
+    cs = torch.cuda.Stream(d.device)
+    cs.wait_stream(cur)  # `d` was produced on the current stream
+    spans = [(lo, min(n, lo + chunk)) for lo in range(0, n, chunk)]
+    evs = [None, None]
+
+    def start(i):
+        lo, hi = spans[i]
+        with torch.cuda.stream(cs):
+            bufs[i & 1][:hi - lo].copy_(d[lo:hi], non_blocking=True)
+            evs[i & 1] = torch.cuda.Event()
+            evs[i & 1].record(cs)
+
+    start(0)
+    for i, (lo, hi) in enumerate(spans):
+        evs[i & 1].synchronize()
+        if i + 1 < len(spans):
+            start(i + 1)  # the other buffer: its previous host copy finished in the last round
+        dst[lo:hi].copy_(bufs[i & 1][:hi - lo])
+    cur.wait_stream(cs)  # `d` is released on the current stream only after the reads
+    return out
