@@ -26,8 +26,9 @@
 // second correction on, rho / (1 - rho) * |d| <= 1e-6 |x| (max norms; the
 // factor contract is 1e-4 per row), and hands the system to the
 // float64 elimination (sweep_refine.cu) when the fp32 factorisation breaks
-// down or the refinement contracts slower than 0.5 per step or has not
-// converged after kIrMaxIt corrections (cond * 1e-6 >~ 0.5).  That float64
+// down or the refinement contracts slower than 0.7 per step or has not
+// converged after kIrMaxIt = 12 corrections (cond * 1e-6 >~ 0.7; a correction costs ~1/12 of
+// the float64 elimination, so the budget is where the two break even).  That float64
 // pass owns the reference's singular / jitter semantics, so this kernel only
 // ever reports CALS_ROW_OK.  A complete sketch (s == n, als.py:184-205)
 // eliminates without pivoting and defers on a non-positive pivot.
@@ -40,11 +41,11 @@
 namespace cals {
 
 constexpr int kIrN = 128;          // largest padded order (thread r owns row r); the kernel is built for 64 and 128
-constexpr int kIrMaxIt = 6;        // corrections before the float64 pass takes over
+constexpr int kIrMaxIt = 12;       // corrections before the float64 pass takes over (N = 128; 6 at N = 64)
 constexpr int kIrSliceN = 448;     // rows up to this length (and rf_slice_max) take the slice residual; the staged
                                    // tier holds no longer row above n_f = 64 (cals_plan_build)
 constexpr float kIrTol = 1e-6f;    // rho * |d| <= kIrTol * |x|
-constexpr float kIrRhoMax = 0.5f;  // slowest accepted contraction
+constexpr float kIrRhoMax = 0.7f;  // slowest accepted contraction (N = 128; 0.5 at N = 64)
 
 __host__ __device__ inline size_t solve_ir_smem(int N) { return (size_t)N * (N + 1) * sizeof(float); }
 
@@ -257,6 +258,10 @@ __global__ void __launch_bounds__(N, N == 128 ? 3 : 8) solve_ir_kernel(SweepArgs
     constexpr int LD = N + 1;  // shared-memory row stride (conflict-free column walks)
     constexpr int NW = N / 32;
     constexpr int MC = N / 32 + 1;  // 32-column groups of an augmented row
+    // the correction budget sits where a correction and the float64 elimination break even: the
+    // 64-wide elimination is cheap (measured on the 500M config: 6 / 0.5 beats 12 / 0.7 by 1 ms)
+    constexpr int max_it = N == 128 ? kIrMaxIt : 6;
+    constexpr float rho_max = N == 128 ? kIrRhoMax : 0.5f;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ __align__(16) IrShared<N> S;
     float* LU = reinterpret_cast<float*>(smem);
@@ -340,7 +345,7 @@ __global__ void __launch_bounds__(N, N == 128 ? 3 : 8) solve_ir_kernel(SweepArgs
             double x = (double)x0;
             float prev = ir_block_max<N>(fabsf(x0), S, lane, warp);  // |x0|: the "correction" before the first
             if (!(prev <= 3.0e38f)) fail = true;
-            for (int it = 0; it < kIrMaxIt && !fail && st < 0; ++it) {
+            for (int it = 0; it < max_it && !fail && st < 0; ++it) {
                 S.xd[t] = x;
                 if (t >= nf) S.rhs[t] = 0.f;
                 __syncthreads();
@@ -426,8 +431,8 @@ __global__ void __launch_bounds__(N, N == 128 ? 3 : 8) solve_ir_kernel(SweepArgs
                 // only bounds it: x0 also carries the fp32 rounding of the equations, so the first
                 // correction ends the iteration only when it is itself negligible)
                 const float rho = prev > 0.f ? dn / prev : 0.f;
-                if (dn <= kIrTol * xn || (it > 0 && rho <= kIrRhoMax && rho * dn <= (1.f - rho) * kIrTol * xn)) st = CALS_ROW_OK;
-                else if (rho > kIrRhoMax) fail = true;
+                if (dn <= kIrTol * xn || (it > 0 && rho <= rho_max && rho * dn <= (1.f - rho) * kIrTol * xn)) st = CALS_ROW_OK;
+                else if (rho > rho_max) fail = true;
                 prev = dn;
             }
             if (st == CALS_ROW_OK) {
