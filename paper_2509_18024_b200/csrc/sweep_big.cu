@@ -111,6 +111,74 @@ __global__ void __launch_bounds__(kThreads) big_calib_kernel(SweepArgs A, BigArg
     }
 }
 
+// Threshold of one column whose bracket held the target rank (above < s <= above + in, the
+// in-bracket keys complete in one contiguous list cl[0, in)): the sub-bucket of the target rank
+// from the histogram (cnt_b: the calling lane's bucket, lane 0 = highest), that bucket's keys
+// kept in the warp's shared-memory list while they number <= 32, else compacted in place in
+// cl, and the need-th largest of them.  Used by big_scan2_kernel for single-item rows, right
+// after their only item: the keys are still in L2 and the counts in shared memory
+// (big_resolve_kernel keeps the per-item-share form for multi-item rows).
+__device__ __forceinline__ uint64_t resolve_one_list(uint64_t* __restrict__ cl, int in, int need, int cnt_b, uint32_t hib,
+                                                     uint32_t lob, uint64_t* __restrict__ keep_w, int lane) {
+    const uint64_t hik = hi_key_of(hib);
+    int incl = cnt_b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t2 = __shfl_up_sync(CALS_FULL_MASK, incl, o);
+        if (lane >= o) incl += t2;
+    }
+    const uint32_t hit = __ballot_sync(CALS_FULL_MASK, incl >= need);
+    const int L = __ffs(hit) - 1;  // first lane whose prefix reaches need
+    const int before = __shfl_sync(CALS_FULL_MASK, incl - cnt_b, L);
+    const int bT = kHB - 1 - L;
+    const int sh = hb_shift(hib - lob);
+    const uint64_t blo = hb_lower_key(bT, lob, sh);
+    const uint64_t bhi = min(hb_lower_key(bT + 1, lob, sh), hik);
+    int m = 0;
+    bool spill = false;
+    for (int i0 = 0; i0 < in; i0 += 128) {
+        uint64_t kk[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + 32 * u + lane;
+            kk[u] = i < in ? cl[i] : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + 32 * u + lane;
+            const bool keep = i < in && kk[u] >= blo && kk[u] < bhi;
+            const uint32_t bal = __ballot_sync(CALS_FULL_MASK, keep);
+            const int cnt = __popc(bal);
+            if (!spill && m + cnt <= 32) {
+                if (keep) keep_w[m + __popc(bal & lanemask_lt())] = kk[u];
+            } else {
+                if (!spill) {
+                    __syncwarp();
+                    if (lane < m) cl[lane] = keep_w[lane];
+                    spill = true;
+                }
+                __syncwarp();
+                if (keep) cl[m + __popc(bal & lanemask_lt())] = kk[u];
+            }
+            m += cnt;
+        }
+    }
+    __syncwarp();
+    uint64_t T;
+    if (spill) {
+        T = warp_select_keys(KeyList{cl}, m, need - before, blo, bhi, lane);
+    } else {
+        // rank of the lane's key among the m kept keys (broadcast reads of the list)
+        const uint64_t v = lane < m ? keep_w[lane] : 0ull;
+        int gt = 0;
+        for (int jj = 0; jj < m; ++jj) gt += (keep_w[jj] > v) ? 1 : 0;
+        const uint32_t hit2 = __ballot_sync(CALS_FULL_MASK, lane < m && gt == need - before - 1);
+        T = __shfl_sync(CALS_FULL_MASK, v, __ffs(hit2) - 1);
+        __syncwarp();  // keep_w is free for the warp's next column
+    }
+    return T;
+}
+
 // Tiled tier pass 1, pipelined: persistent CTAs claim work items from a counter
 // (B.item_ctr, zeroed before the launch; longest rows first), each item's slice is
 // streamed in chunks of B.chunk rows through two shared-memory buffers (the bulk
@@ -124,12 +192,14 @@ __global__ void __launch_bounds__(kThreads) big_calib_kernel(SweepArgs A, BigArg
 // histogram and total, and per item its in-bracket count (B.icnt; a share that
 // overflowed sends that column to big_resolve's exact search).
 template <int PER, int SXT, int KCT>
-__global__ void __launch_bounds__(kThreads) big_scan2_kernel(SweepArgs A, BigArgs B) {
+__global__ void __launch_bounds__(kThreads, 4) big_scan2_kernel(SweepArgs A, BigArgs B) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_above[CALS_MAX_NF_DEV], s_pos[CALS_MAX_NF_DEV];
     __shared__ uint32_t s_hib[CALS_MAX_NF_DEV], s_lob[CALS_MAX_NF_DEV];
     __shared__ __align__(8) unsigned long long s_mbar[2];
     __shared__ int s_item;
+    __shared__ uint64_t s_keep[kThreads / 32][32];  // fused resolve of single-item rows (resolve_one_list)
+    __shared__ unsigned char s_done[CALS_MAX_NF_DEV];
     const int nf = A.nf, tid = threadIdx.x, nt = blockDim.x;
     const int sx = SXT > 0 ? SXT : xs_stride(nf);
     const int per = PER > 0 ? PER : nt / nf;  // threads per column
@@ -246,13 +316,42 @@ __global__ void __launch_bounds__(kThreads) big_scan2_kernel(SweepArgs A, BigArg
         }
         if (col_thread && my_above) atomicAdd(&s_above[c], my_above);
         __syncthreads();
+        // A single-item row is resolved right here: its counts and histogram are in shared memory and
+        // its in-bracket keys (written by this CTA a moment ago) in L2, so the columns whose bracket held
+        // the target rank get their threshold without the round trip through big_resolve_kernel (which
+        // skips them: in-count -1) -- no dependent header loads, no second pass over the keys from HBM.
+        const bool single = B.tile_ptr[r + 1] - B.tile_ptr[r] == 1;
+        if (single) {
+            const int warp = tid >> 5, lane = tid & 31;
+            uint64_t* cl0 = B.cand + (B.cand_ptr[r] - B.cand_base);
+            for (int c2 = warp; c2 < nf; c2 += nt >> 5) {
+                const int above = s_above[c2], in = s_pos[c2];
+                const uint32_t hib = s_hib[c2], lob = s_lob[c2];
+                const bool ok = above < s && s <= above + in && in <= capB && ((uint64_t)lob << 32) < hi_key_of(hib);
+                if (ok) {
+                    const uint64_t T = resolve_one_list(cl0 + (int64_t)c2 * capB, in, s - above,
+                                                        s_hist[c2 * kHB + (kHB - 1 - lane)], hib, lob, s_keep[warp], lane);
+                    if (lane == 0) {
+                        stat_add(A, kStBigColumns, 1);
+                        B.thr[(size_t)r * nf + c2] = T;
+                        if (A.thr_keys != nullptr) A.thr_keys[(int64_t)row * nf + c2] = T;
+                    }
+                }
+                if (lane == 0) s_done[c2] = ok ? 1 : 0;
+            }
+            __syncthreads();
+        }
         if (tid < nf) {
-            if (s_above[tid]) atomicAdd(&B.cnt[((size_t)r * nf + tid) * 2], s_above[tid]);
-            if (s_pos[tid]) atomicAdd(&B.cnt[((size_t)r * nf + tid) * 2 + 1], s_pos[tid]);
+            if (single && s_done[tid]) {
+                B.cnt[((size_t)r * nf + tid) * 2 + 1] = -1;  // resolved: big_resolve_kernel skips the column
+            } else {
+                if (s_above[tid]) atomicAdd(&B.cnt[((size_t)r * nf + tid) * 2], s_above[tid]);
+                if (s_pos[tid]) atomicAdd(&B.cnt[((size_t)r * nf + tid) * 2 + 1], s_pos[tid]);
+            }
             B.icnt[(size_t)t * nf + tid] = s_pos[tid];
         }
         for (int e = tid; e < nf * kHB; e += nt)
-            if (s_hist[e]) atomicAdd(&B.hist[(size_t)r * nf * kHB + e], s_hist[e]);
+            if (s_hist[e] && !(single && s_done[e / kHB])) atomicAdd(&B.hist[(size_t)r * nf * kHB + e], s_hist[e]);
     }
 }
 template __global__ void big_scan2_kernel<4, 68, 64>(SweepArgs, BigArgs);
@@ -271,6 +370,7 @@ __global__ void __launch_bounds__(kThreads) big_resolve_kernel(SweepArgs A, BigA
     const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t w = gw; w < nwork; w += wstride) {
         const int r = (int)(w / nf), c = (int)(w % nf);
+        if (B.cnt[((size_t)r * nf + c) * 2 + 1] < 0) continue;  // resolved by big_scan2_kernel (single-item row)
         const int row = B.rows[r];
         const int64_t lo = A.ptr[row];
         const int n = (int)(A.ptr[row + 1] - lo);

@@ -13,6 +13,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2509_18024_b200 import _lib, synth  # noqa: E402
 from paper_2509_18024_b200.engine import CoreEngine  # noqa: E402
 
+if os.environ.get("CALS_LIB"):  # A/B runs: another build of the library (tool only)
+    _lib.LIB_PATH = os.path.abspath(os.environ["CALS_LIB"])
 cfg = sys.argv[1]
 spec = synth.CONFIGS[cfg]
 d = synth.generate(cfg, device="cuda")
