@@ -571,6 +571,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
         c.i = 0;
         tc_enter(c, items, full_base);
         double racc = 0.0;
+        // loop-invariant operands in registers: the lane's column scales for the whole launch, its
+        // 8 selection thresholds for as long as the work item lasts (reloaded when c.i changes)
+        float4 scr[kTcNG];
+#pragma unroll
+        for (int g = 0; g < kTcNG; ++g) scr[g] = *reinterpret_cast<const float4*>(s_scale + 4 * (kTcLPR * g + fql));
+        const float sc_y = s_scale[64];
+        ulonglong2 thr01[kTcNG], thr23[kTcNG];
+        float4 wold_r[kTcNG];
+        int thr_item = -1;
 #pragma unroll 1
         for (int64_t j = 0; c.ok; ++j) {
             // group j - kTcAhead landed: the rows of chunk j and the indices of chunk j + kTcAhead
@@ -610,6 +619,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
                 tc_advance(c, items, full_base);
                 continue;
             }
+            if (c.i != thr_item) {
+                thr_item = c.i;
+#pragma unroll
+                for (int g = 0; g < kTcNG; ++g) {
+                    const int c0 = 4 * (kTcLPR * g + fql);
+                    thr01[g] = *reinterpret_cast<const ulonglong2*>(&it_d.T[tperm(c0)]);
+                    thr23[g] = *reinterpret_cast<const ulonglong2*>(&it_d.T[tperm(c0 + 2)]);
+                    if (want_rss) wold_r[g] = *reinterpret_cast<const float4*>(&it_d.wold[c0]);
+                }
+            }
             uint32_t lev[kTcNG][4];  // [group][level 1..4]
             uint32_t km[kTcNG];
             float amax = 0.f, pdot = 0.f;
@@ -617,9 +636,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
             for (int g = 0; g < kTcNG; ++g) {
                 const int c0 = 4 * (kTcLPR * g + fql);
                 const float4 x = lds_f128(sx + seg(g));  // zero in padding columns
-                const float4 sc = *reinterpret_cast<const float4*>(s_scale + c0);
-                const ulonglong2 t01 = *reinterpret_cast<const ulonglong2*>(&it_d.T[tperm(c0)]);
-                const ulonglong2 t23 = *reinterpret_cast<const ulonglong2*>(&it_d.T[tperm(c0 + 2)]);
+                const float4 sc = scr[g];
+                const ulonglong2 t01 = thr01[g], t23 = thr23[g];
                 const float t0 = x.x * sc.x, t1 = x.y * sc.y, t2 = x.z * sc.z, t3 = x.w * sc.w;
                 amax = fmaxf(amax, fmaxf(fmaxf(fabsf(t0), fabsf(t1)), fmaxf(fabsf(t2), fabsf(t3))));
                 const uint32_t z0 = (uint32_t)__float2int_rn(t0) + 0x80808080u;
@@ -639,7 +657,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
                 km[g] = ((k0 ? 0xFFu : 0u) | (k1 ? 0xFF00u : 0u) | (k2 ? 0xFF0000u : 0u) | (k3 ? 0xFF000000u : 0u)) &
                         row_on;
                 if (want_rss) {
-                    const float4 wo = *reinterpret_cast<const float4*>(&it_d.wold[c0]);
+                    const float4 wo = wold_r[g];
                     pdot = fmaf(x.x, wo.x, pdot);
                     pdot = fmaf(x.y, wo.y, pdot);
                     pdot = fmaf(x.z, wo.z, pdot);
@@ -650,7 +668,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
             uint32_t zy = 0x80808080u;
             if (fql == 0) {
                 yv = krow ? lds_f32(ring_val + (uint32_t)(j % kTcRing) * (kTcKC * 4)) : 0.f;
-                const float ty = yv * s_scale[64];
+                const float ty = yv * sc_y;
                 amax = fmaxf(amax, fabsf(ty));
                 zy = (uint32_t)__float2int_rn(ty) + 0x80808080u;
             }
