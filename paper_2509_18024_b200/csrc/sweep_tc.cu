@@ -223,10 +223,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
     __shared__ double s_alpha[65];
     __shared__ uint32_t s_tmem;
     __shared__ uint32_t exc_any[kTcExcSlots];  // item had an exception row (the epilogue scans its masks)
-    __shared__ __align__(8) unsigned long long bar_item_full[kTcItems], bar_item_empty[kTcItems],
-        bar_item_done[kTcItems];
-    __shared__ __align__(8) unsigned long long bar_full_tl[2], bar_empty_tl[2];
-    __shared__ __align__(8) unsigned long long bar_tmem_full, bar_tmem_empty;
+    // every mbarrier in one array, addressed as full_base + a compile-time offset (separate arrays cost a
+    // generic-to-shared conversion per use inside the role loops): item_full[kTcItems], item_empty[kTcItems],
+    // item_done[kTcItems], full_tl[2], empty_tl[2], tmem_full, tmem_empty
+    __shared__ __align__(8) unsigned long long bars[3 * kTcItems + 6];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nf = A.nf, gs = nf + 1;
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
     uint32_t* exc_mask = reinterpret_cast<uint32_t*>(smem + TcSmem::exc_mask);  // [slot][chunk][2]
     TcItem* items = reinterpret_cast<TcItem*>(smem + TcSmem::items);
     double* rss_part = reinterpret_cast<double*>(smem + TcSmem::rss);
-    const uint32_t full_base = smem_u32(&bar_item_full[0]);
+    const uint32_t full_base = smem_u32(&bars[0]);
 
     // ---- setup, then the roles never meet at a block barrier again
     for (int e = tid; e < 2 * kTcDigitBuf / 16; e += blockDim.x)
@@ -256,16 +256,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
     if (warp == 0) tc::tmem_alloc<512>(&s_tmem);
     if (tid == 0) {
         for (int s = 0; s < kTcItems; ++s) {
-            mbar_init(smem_u32(&bar_item_full[s]), 64);  // 32 lanes x (descriptor writes + their copies)
-            mbar_init(smem_u32(&bar_item_empty[s]), 1);
-            mbar_init(smem_u32(&bar_item_done[s]), kTcCW);
+            mbar_init((full_base + 8u * (uint32_t)(0 + (s))), 64);  // 32 lanes x (descriptor writes + their copies)
+            mbar_init((full_base + 8u * (uint32_t)(kTcItems + (s))), 1);
+            mbar_init((full_base + 8u * (uint32_t)(2 * kTcItems + (s))), kTcCW);
         }
         for (int s = 0; s < 2; ++s) {
-            mbar_init(smem_u32(&bar_full_tl[s]), kTcCW);
-            mbar_init(smem_u32(&bar_empty_tl[s]), 1);
+            mbar_init((full_base + 8u * (uint32_t)(3 * kTcItems + (s))), kTcCW);
+            mbar_init((full_base + 8u * (uint32_t)(3 * kTcItems + 2 + (s))), 1);
         }
-        mbar_init(smem_u32(&bar_tmem_full), 1);
-        mbar_init(smem_u32(&bar_tmem_empty), 1);
+        mbar_init((full_base + 8u * (uint32_t)(3 * kTcItems + 4)), 1);
+        mbar_init((full_base + 8u * (uint32_t)(3 * kTcItems + 5)), 1);
     }
     tc::fence_smem_async();
     tc::fence_before();
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
                 const int kel = __shfl_sync(CALS_FULL_MASK, kend, l);
                 const int64_t lol = __shfl_sync(CALS_FULL_MASK, lo, l);
                 const int sl = i % kTcItems;
-                if (i >= kTcItems) tc_long_wait(smem_u32(&bar_item_empty[sl]), (uint32_t)(((i / kTcItems) - 1) & 1), dbg);
+                if (i >= kTcItems) tc_long_wait((full_base + 8u * (uint32_t)(kTcItems + (sl))), (uint32_t)(((i / kTcItems) - 1) & 1), dbg);
                 TcItem& d = items[sl];
                 if (lane == 0) {
                     d.t = valid ? tl : -1;
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
                         else d.wold[c] = 0.f;
                     }
                 }
-                const uint32_t fb = smem_u32(&bar_item_full[sl]);
+                const uint32_t fb = (full_base + 8u * (uint32_t)(0 + (sl)));
                 TC_TRACE(40960 + i, lane == 0 && i < 8192);
                 mbar_arrive(fb);           // this lane's descriptor / padding writes
                 cp_async_mbar_arrive(fb);  // and, asynchronously, its copies
@@ -353,12 +353,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
                 const int kbeg = d.kbeg, kend = d.kend;
                 for (int k0 = kbeg; k0 < kend; k0 += kTcKC, ++j) {
                     const int db = (int)(j & 1);
-                    if (dbg & 16) mbar_wait_hint(smem_u32(&bar_full_tl[db]), (uint32_t)((j >> 1) & 1));
+                    if (dbg & 16) mbar_wait_hint((full_base + 8u * (uint32_t)(3 * kTcItems + (db))), (uint32_t)((j >> 1) & 1));
                     else if (dbg & 64) {
-                        while (!mbar_test(smem_u32(&bar_full_tl[db]), (uint32_t)((j >> 1) & 1))) __nanosleep(20);
-                    } else mbar_wait(smem_u32(&bar_full_tl[db]), (uint32_t)((j >> 1) & 1));
+                        while (!mbar_test((full_base + 8u * (uint32_t)(3 * kTcItems + (db))), (uint32_t)((j >> 1) & 1))) __nanosleep(20);
+                    } else mbar_wait((full_base + 8u * (uint32_t)(3 * kTcItems + (db))), (uint32_t)((j >> 1) & 1));
                     TC_TRACE(j * 8 + 4, j < 4096);
-                    if (k0 == kbeg && i > 0) mbar_wait(smem_u32(&bar_tmem_empty), (uint32_t)((i - 1) & 1));
+                    if (k0 == kbeg && i > 0) mbar_wait((full_base + 8u * (uint32_t)(3 * kTcItems + 5)), (uint32_t)((i - 1) & 1));
                     TC_TRACE(j * 8 + 5, j < 4096);
                     if (trace && j < 4096) A.stats[j * 8 + 6] = (unsigned long long)i;
                     tc::fence_after();
@@ -373,8 +373,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
                         tc::mma_i8_ss(tmem + kTcAccB, a12, b34, idesc, acc);
                         tc::mma_i8_ss(tmem + kTcAccB, a34, b12, idesc, 1u);
                     }
-                    tc::commit(smem_u32(&bar_empty_tl[db]));
-                    if (k0 + kTcKC >= kend) tc::commit(smem_u32(&bar_tmem_full));
+                    tc::commit((full_base + 8u * (uint32_t)(3 * kTcItems + 2 + (db))));
+                    if (k0 + kTcKC >= kend) tc::commit((full_base + 8u * (uint32_t)(3 * kTcItems + 4)));
                 }
             }
         }
@@ -388,9 +388,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
             const TcItem& d = items[sl];
             if (d.t < 0) break;
             TC_TRACE(32768 + i * 8 + 0, et == 0 && i < 1024);
-            tc_long_wait(smem_u32(&bar_item_done[sl]), (uint32_t)((i / kTcItems) & 1), dbg);
+            tc_long_wait((full_base + 8u * (uint32_t)(2 * kTcItems + (sl))), (uint32_t)((i / kTcItems) & 1), dbg);
             TC_TRACE(32768 + i * 8 + 1, et == 0 && i < 1024);
-            mbar_wait(smem_u32(&bar_tmem_full), (uint32_t)(i & 1));
+            mbar_wait((full_base + 8u * (uint32_t)(3 * kTcItems + 4)), (uint32_t)(i & 1));
             TC_TRACE(32768 + i * 8 + 2, et == 0 && i < 1024);
             tc::fence_after();
             // per TMEM row (level h of column c) and column f, the four accumulators combine exactly
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
             }
             tc::fence_before();
             named_bar(1, 128);
-            if (et == 0) mbar_arrive(smem_u32(&bar_tmem_empty));  // the next item's MMAs may start
+            if (et == 0) mbar_arrive((full_base + 8u * (uint32_t)(3 * kTcItems + 5)));  // the next item's MMAs may start
             TC_TRACE(32768 + i * 8 + 3, et == 0 && i < 1024);
             // exception rows (a value past its column's digit range), chunk by chunk in slice
             // order: their exact float64 contributions, G[c][:] += x_kc [x_k | y_k] if k is kept for c
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
             }
             named_bar(1, 128);
             TC_TRACE(32768 + i * 8 + 5, et == 0 && i < 1024);
-            if (et == 0) mbar_arrive(smem_u32(&bar_item_empty[sl]));
+            if (et == 0) mbar_arrive((full_base + 8u * (uint32_t)(kTcItems + (sl))));
         }
     } else {
         // ================= digit pass (warps 0..15): gather, select, split =================
@@ -611,13 +611,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
             const uint32_t lo_key = 0xFFFFFFFFu - kg;
             const uint32_t row_on = krow ? 0xFFFFFFFFu : 0u;
             if (dbg & 2) {
-                if (j >= 2) mbar_wait(smem_u32(&bar_empty_tl[db]), (uint32_t)(((j - 2) >> 1) & 1));
+                if (j >= 2) mbar_wait((full_base + 8u * (uint32_t)(3 * kTcItems + 2 + (db))), (uint32_t)(((j - 2) >> 1) & 1));
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&bar_full_tl[db]));
+                if (lane == 0) mbar_arrive((full_base + 8u * (uint32_t)(3 * kTcItems + (db))));
                 if (last) {
                     if (lane == 0) rss_part[sl * kTcCW + warp] = 0.0;
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(smem_u32(&bar_item_done[sl]));
+                    if (lane == 0) mbar_arrive((full_base + 8u * (uint32_t)(2 * kTcItems + (sl))));
                 }
                 tc_advance(c, items, full_base);
                 continue;
@@ -648,16 +648,15 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
                 const uint32_t z3 = (uint32_t)__float2int_rn(t3) + 0x80808080u;
                 const uint32_t lo01 = __byte_perm(z0, z1, 0x5140), hi01 = __byte_perm(z0, z1, 0x7362);
                 const uint32_t lo23 = __byte_perm(z2, z3, 0x5140), hi23 = __byte_perm(z2, z3, 0x7362);
-                lev[g][3] = __byte_perm(lo01, lo23, 0x5410) ^ 0x80808080u;  // level 4: weight 2^0
-                lev[g][2] = __byte_perm(lo01, lo23, 0x7632) ^ 0x80808080u;  // level 3
-                lev[g][1] = __byte_perm(hi01, hi23, 0x5410) ^ 0x80808080u;  // level 2
-                lev[g][0] = __byte_perm(hi01, hi23, 0x7632) ^ 0x80808080u;  // level 1: weight 2^24
+                lev[g][3] = __byte_perm(lo01, lo23, 0x5410);  // level 4: weight 2^0
+                lev[g][2] = __byte_perm(lo01, lo23, 0x7632);  // level 3
+                lev[g][1] = __byte_perm(hi01, hi23, 0x5410);  // level 2
+                lev[g][0] = __byte_perm(hi01, hi23, 0x7632);  // level 1: weight 2^24
                 const bool k0 = (((uint64_t)abs_bits(x.x) << 32) | lo_key) >= t01.x;
                 const bool k1 = (((uint64_t)abs_bits(x.y) << 32) | lo_key) >= t01.y;
                 const bool k2 = (((uint64_t)abs_bits(x.z) << 32) | lo_key) >= t23.x;
                 const bool k3 = (((uint64_t)abs_bits(x.w) << 32) | lo_key) >= t23.y;
-                km[g] = ((k0 ? 0xFFu : 0u) | (k1 ? 0xFF00u : 0u) | (k2 ? 0xFF0000u : 0u) | (k3 ? 0xFF000000u : 0u)) &
-                        row_on;
+                km[g] = (k0 ? 0xFFu : 0u) | (k1 ? 0xFF00u : 0u) | (k2 ? 0xFF0000u : 0u) | (k3 ? 0xFF000000u : 0u);  // & zero_row below
                 if (want_rss) {
                     const float4 wo = *reinterpret_cast<const float4*>(&it_d.wold[c0]);  // in registers too: spills
                     pdot = fmaf(x.x, wo.x, pdot);
@@ -687,20 +686,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
             const uint32_t zero_row = exc ? 0u : row_on;
             TC_TRACE(j * 8 + 2, warp == 0 && lane == 0 && j < 4096);
             if (j >= 2) {
-                if (dbg & 32) mbar_wait_hint(smem_u32(&bar_empty_tl[db]), (uint32_t)(((j - 2) >> 1) & 1));
-                else mbar_wait(smem_u32(&bar_empty_tl[db]), (uint32_t)(((j - 2) >> 1) & 1));
+                if (dbg & 32) mbar_wait_hint((full_base + 8u * (uint32_t)(3 * kTcItems + 2 + (db))), (uint32_t)(((j - 2) >> 1) & 1));
+                else mbar_wait((full_base + 8u * (uint32_t)(3 * kTcItems + 2 + (db))), (uint32_t)(((j - 2) >> 1) & 1));
             }
             TC_TRACE(j * 8 + 3, warp == 0 && lane == 0 && j < 4096);
             const uint32_t dbase = dig_lane + (uint32_t)db * kTcDigitBuf;
+            uint32_t kmz[kTcNG];
+#pragma unroll
+            for (int g = 0; g < kTcNG; ++g) kmz[g] = km[g] & zero_row;
 #pragma unroll
             for (int g = 0; g < ((dbg & 4) ? 0 : kTcNG); ++g) {
 #pragma unroll
                 for (int L = 1; L <= 4; ++L) {
-                    const uint32_t w = lev[g][L - 1] & zero_row;
+                    // un-bias (^ 0x80 per byte) and mask in one LOP3 per stored word
+                    const uint32_t w = (lev[g][L - 1] ^ 0x80808080u) & zero_row;
                     const uint32_t pair = (uint32_t)((L - 1) >> 1), half = (uint32_t)((L - 1) & 1);
                     const uint32_t gofs = 128u * kTcLPR * (uint32_t)g;  // 4 kLPR columns further
                     sts_u32(dbase + 2 * kTcATile + pair * kTcBTile + (half ? off_b1 : off_b0) + gofs, w);
-                    sts_u32(dbase + pair * kTcATile + (half ? off_a1 : off_a0) + gofs, w & km[g]);
+                    sts_u32(dbase + pair * kTcATile + (half ? off_a1 : off_a0) + gofs,
+                            (lev[g][L - 1] ^ 0x80808080u) & kmz[g]);
                 }
             }
             if (fql == 0) {
@@ -718,7 +722,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
             }
             tc::fence_smem_async();
             __syncwarp();
-                        if (lane == 0) mbar_arrive(smem_u32(&bar_full_tl[db]));
+                        if (lane == 0) mbar_arrive((full_base + 8u * (uint32_t)(3 * kTcItems + (db))));
             if (last) {
                 // per-warp residual partial, then this warp is done with the item
                 double v = racc;
@@ -727,7 +731,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
                 if (lane == 0) rss_part[sl * kTcCW + warp] = v;
                 racc = 0.0;
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&bar_item_done[sl]));
+                if (lane == 0) mbar_arrive((full_base + 8u * (uint32_t)(2 * kTcItems + (sl))));
             }
             tc_advance(c, items, full_base);
         }
