@@ -408,27 +408,31 @@ __global__ void __launch_bounds__(kTcThreads, 1) big_gram_tc_kernel(SweepArgs A,
                                     ((long long)(int)b0 << 8) + (long long)(int)b1;
                 return (double)I;
             };
-            if (ew >= 2) {  // level-2 rows first: their part into xchg
-                const int cr = 32 * (ew - 2) + lane;
-                for (int f0 = 0; f0 < kTcLvl; f0 += 8) {
+            // both warp pairs drain at once, on opposite column halves: level-1 warps (TMEM rows 0..63) take
+            // columns [0, 40) first, level-2 warps (rows 64..127) [40, 72); after the barrier they swap.  The
+            // first visitor of (c, f) leaves its exact scaled integer, the second adds its own with one
+            // rounding and applies alpha_c alpha_f -- the same value in either order -- so TMEM is held for
+            // 5 + 5 column blocks instead of 9 + 9 (the next item's MMAs wait on this drain)
+            {
+                const bool lvl2 = ew >= 2;
+                const int cr = 32 * (ew & 1) + lane;
+                const double ac = s_alpha[cr];
+                const double wscale = lvl2 ? 0x1p-48 : 0x1p-40;
+                for (int f0 = lvl2 ? 40 : 0; f0 < (lvl2 ? kTcLvl : 40); f0 += 8) {
                     uint32_t a0[8], a1[8], b0[8], b1[8];
                     drain(f0, a0, a1, b0, b1);
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) xchg[cr * kTcLvl + f0 + q] = combine(a0[q], a1[q], b0[q], b1[q]);
+                    for (int q = 0; q < 8; ++q)
+                        xchg[cr * kTcLvl + f0 + q] = combine(a0[q], a1[q], b0[q], b1[q]) * wscale;  // exact
                 }
-            }
-            named_bar(1, 128);
-            if (ew < 2) {
-                const int cr = 32 * ew + lane;
-                const double ac = s_alpha[cr];
-                for (int f0 = 0; f0 < kTcLvl; f0 += 8) {
+                named_bar(1, 128);
+                for (int f0 = lvl2 ? 0 : 40; f0 < (lvl2 ? 40 : kTcLvl); f0 += 8) {
                     uint32_t a0[8], a1[8], b0[8], b1[8];
                     drain(f0, a0, a1, b0, b1);
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         const int f = f0 + q;
-                        const double p = fma(combine(a0[q], a1[q], b0[q], b1[q]), 0x1p-40,
-                                             xchg[cr * kTcLvl + f] * 0x1p-48);
+                        const double p = fma(combine(a0[q], a1[q], b0[q], b1[q]), wscale, xchg[cr * kTcLvl + f]);
                         xchg[cr * kTcLvl + f] = ac * s_alpha[f <= 64 ? f : 64] * p;
                     }
                 }
